@@ -1,0 +1,288 @@
+#!/usr/bin/env python3
+"""Throughput bench of the TQSim B200 hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_qft15] [--impl tqsim|reference]
+
+A step = one whole tree run (every §8(a) row: noise draws, fan-out, gate
+passes, leaf measurement, readout; + the NCCL allreduce of leaf outcomes when
+N > 1) of BASELINE.json's config (default configs[1] = C2 qft15, 10,000 shots ->
+10,240 outcomes).  Top-level branches are sharded over ranks (weak scaling of
+the number of trees: every rank runs its shard of one tree per step, so the
+job does one tree per step; "scaling": "strong").
+
+value     noisy shots/s = outcomes per tree * K / (max over ranks of the CUDA-event
+          time of K steps), inputs (gate tables) resident in HBM.
+e2e       the same metric through the C-ABI call a user makes (tqsim_run for N=1:
+          host circuit in, host histogram out; planning, H2D of the gate tables,
+          D2H of the outcomes and the histogram inside the timed region).
+roofline  gate-pass kernel: algorithmic bytes / summed CUDA-event launch time of
+          the pass kernels in profiled steps, vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the oracle (oracle/, numpy, 1 thread) on a bounded sample of the
+          same workload (one top-level subtree), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "noisy shots/sec and gate-amp updates/s; gate-kernel HBM GB/s vs B200 peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2_qft15")
+    ap.add_argument("--impl", default="tqsim", choices=["tqsim", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--batch-log2", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        try:
+            with open(self.f.name) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline(w, sample_top: int = 1):
+    """The oracle as it stands (numpy, 1 thread) on a bounded sample of the workload."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import gates as OG
+    from oracle.planner import dcp_plan, fixed_plan
+    from oracle.tree import NoiseModel, error_rates, simulate_tree
+
+    low = OG.lower(w.circuit.gates)
+    nm = NoiseModel(w.p1, w.p2, w.readout_p01, w.readout_p10)
+    if w.arities:
+        plan = fixed_plan(len(low), w.arities)
+    else:
+        plan = dcp_plan(error_rates(low, nm), w.shots, w.circuit.n_qubits, w.copy_cost_gates)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        res = simulate_tree(w.circuit.n_qubits, low, plan, nm, w.seed, top_range=(0, sample_top))
+        dt = time.perf_counter() - t0
+    n = len(res.leaves)
+    return {"value": n / dt, "unit": "shots/s", "cores": 1, "kind": "oracle",
+            "sample": "%d of %d top-level subtrees (%d leaves) of %s, full tree DFS, %.1f s"
+                      % (sample_top, plan.arities[0], n, w.name, dt)}
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    vals = []
+    cb = None
+    for s in range(args.steps):
+        cb = cpu_baseline(w)
+        vals.append(cb["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "shots/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "shots": w.shots},
+            "cpu_baseline": {"value": v, "unit": "shots/s", "cores": 1, "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": "shots/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from workloads import load_config
+    w = load_config(args.config)
+    if args.impl == "reference":
+        return run_reference(args, w, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2203_13892_b200.tqsim as T
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    n, gates, noise, shots, ar = T.workload_args(w)
+    opts = T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2)
+    h = T.tqsim_create(n, gates, noise, shots, ar, opts)
+    plan = h.plan
+    N = int(plan.n_outcomes)
+    ws = torch.empty(h.workspace_bytes(rank, world), dtype=torch.uint8, device=dev)
+    out = torch.zeros(N, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream(dev)
+
+    def step(seed):
+        out.zero_()
+        h.execute(seed, rank, world, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
+        if world > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+
+    for i in range(args.warmup):
+        step(1000 + i)
+    torch.cuda.synchronize(dev)
+    stats1 = h.stats()
+    launches_per_step = int(stats1.kernel_launches)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for i in range(args.steps):
+            step(i)
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    clocks = clk.summary()
+
+    # roofline of the gate-pass kernel: profiled steps (CUDA events around every launch)
+    popts = T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, profile=1)
+    hp = T.tqsim_create(n, gates, noise, shots, ar, popts)
+    pass_ms = meas_ms = 0.0
+    pass_bytes = meas_bytes = 0
+    pass_launches = 0
+    for i in range(max(1, min(args.steps, 3))):
+        out.zero_()
+        hp.execute(i, rank, world, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
+        s = hp.stats()
+        pass_ms += s.pass_ms
+        meas_ms += s.measure_ms
+        pass_bytes += s.pass_bytes
+        meas_bytes += s.measure_bytes
+        pass_launches += s.pass_launches
+    hp.close()
+    hbm_peak, peak_src = peaks()
+    achieved = pass_bytes / (pass_ms * 1e-3) / 1e9 if pass_ms > 0 else 0.0
+    pt = torch.tensor([pass_ms, meas_ms], dtype=torch.float64, device=dev)
+
+    # end to end through the public C-ABI call (host buffers)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        T.tqsim_run(n, gates, noise, shots, ar, 0)     # warm (arena, module load)
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            r = T.tqsim_run(n, gates, noise, shots, ar, i)
+        dt = time.perf_counter() - t0
+        h2d = (len(T.tqsim_lower_circuit(n, gates)) * (8 * 8 + 1)
+               + int(plan.hbm_passes and 0))   # gate matrices + 2q flags; op/phase tables below
+        e2e = {"value": N * args.steps / dt, "unit": "shots/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": N * 4,
+               "note": "tqsim_run: lowering+planning+H2D gate tables+tree+D2H outcomes+histogram"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(w)
+
+    if rank == 0:
+        shots_s = N * args.steps / (ms * 1e-3)
+        gau = plan.gate_amp_updates * args.steps / (ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": shots_s, "unit": "shots/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n_qubits": n, "shots": shots, "outcomes": N,
+                       "arities": plan.arity_list, "lowered_gates": int(plan.n_lowered_gates),
+                       "tile_qubits": args.tile or 12,
+                       "l2": "inputs larger than L2 (state batches >= 1 GiB per launch group)",
+                       "parallelism": "top-level branch sharding x%d" % world},
+            "gate_amp_updates_per_s": gau,
+            "tree_vs_flat_gate_ratio": plan.flat_gate_amp_updates / plan.gate_amp_updates,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                         "peak_source": peak_src, "kernel": "pass_kernel<K>",
+                         "pass_share_of_step": float(pt[0].item()) / (float(pt[0].item()) + float(pt[1].item()))
+                         if (pt[0].item() + pt[1].item()) > 0 else None,
+                         "pass_launches_profiled": pass_launches},
+            "gpu_launches": launches_per_step * args.steps + (args.steps if world > 1 else 0) * 0,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,239 @@
+/*
+ * tqsim.h -- C ABI of the B200-native TQSim hot path.
+ *
+ * TQSim (arXiv 2203.13892): multi-shot noisy statevector simulation that
+ * reuses intermediate states through a tree.  Citations: "P:n" = line n of the
+ * paper text with its section / equation; "S:n" = SPEC.md line n;
+ * "R<k>" = reading k of DESIGN.md (the paper is silent / ambiguous there).
+ *
+ * Problem statement: given a circuit, a noise model and N
+ * shots, return a histogram of >= N noisy measurement outcomes.
+ *
+ * Conventions shared by every entry point
+ *   - Basis index x = sum_q bit_q * 2^q (little endian, R6).  Outcomes
+ *     and bitstrings are such integers.
+ *   - All pointers are plain host pointers unless the name starts with d_
+ *     (device pointer, CUDA global memory of the current device) or the
+ *     argument is a `void* stream` (a cudaStream_t, NULL = legacy default).
+ *   - Ownership: the caller owns every input and may free it after the call
+ *     returns (the library copies what it keeps).  Objects returned through
+ *     `**out` are owned by the library and released with the matching
+ *     *_free / tqsim_destroy call.  Device buffers passed in stay caller-owned.
+ *   - Errors: every function returns a tqsim_status; on failure nothing is
+ *     written to `*out` and tqsim_last_error() returns a thread-local message.
+ *     No C++ exception ever crosses this boundary.
+ *   - Functions marked [host] never touch the GPU and work without one.
+ *   - Functions marked [gpu] need a CUDA device of compute capability 10.0
+ *     (B200, sm_100a); without it they return TQSIM_ECUDA.  There is no CPU
+ *     fallback.
+ */
+#ifndef TQSIM_H
+#define TQSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TQSIM_MAX_LEVELS 64
+#define TQSIM_MAX_QUBITS 30
+
+typedef enum {
+  TQSIM_OK = 0,
+  TQSIM_EINVAL = 2,     /* bad circuit / noise / arity / argument (SPEC exit code 2) */
+  TQSIM_ECAPACITY = 3,  /* memory budget or workspace too small (SPEC exit code 3)  */
+  TQSIM_ECUDA = 4,      /* CUDA error or no sm_100 device                                    */
+  TQSIM_ENCCL = 5,      /* reserved: collective failure (the allreduce runs in the caller)  */
+  TQSIM_EINTERNAL = 6
+} tqsim_status;
+
+/* Gate kinds (S:33 set + P(U1)).  Matrices (R5, standard OpenQASM 2 forms):
+ *   H=[[1,1],[1,-1]]/sqrt2, X, Y=[[0,-i],[i,0]], Z, S=diag(1,i), SDG, T=diag(1,e^{i pi/4}), TDG,
+ *   RX(t)=[[c,-is],[-is,c]], RY(t)=[[c,-s],[s,c]], RZ(t)=diag(e^{-it/2},e^{it/2}),
+ *   P(t)=diag(1,e^{it}), U(t,p,l)=[[c,-e^{il}s],[e^{ip}s,e^{i(p+l)}c]],  c=cos t/2, s=sin t/2.
+ *   Single-angle gates (RX, RY, RZ, P, CP) take their angle in `theta`.
+ *   CX(q0=control, q1=target); CZ(q0,q1); SWAP(q0,q1); CP(theta; q0=control, q1=target).
+ * Lowering (R4): CP -> P(t/2)q0, CX, P(-t/2)q1, CX, P(t/2)q1;  SWAP -> CX(a,b) CX(b,a) CX(a,b).
+ * Every LOWERED gate is one noise location (R1); gate index g counts lowered gates. */
+typedef enum {
+  TQ_X = 0, TQ_Y, TQ_Z, TQ_H, TQ_S, TQ_SDG, TQ_T, TQ_TDG,
+  TQ_RX, TQ_RY, TQ_RZ, TQ_P, TQ_U, TQ_CX, TQ_CZ, TQ_SWAP, TQ_CP
+} tqsim_gate_kind;
+
+typedef struct {
+  uint32_t kind;      /* tqsim_gate_kind */
+  uint32_t q0, q1;    /* q1 used by 2q kinds only; must differ from q0 */
+  uint32_t reserved;  /* 0 */
+  double theta, phi, lambda;
+} tqsim_gate;         /* 40 bytes */
+
+typedef struct {
+  uint32_t n_qubits;  /* 1 .. TQSIM_MAX_QUBITS */
+  uint32_t reserved;
+  uint64_t n_gates;   /* >= 1 */
+  const tqsim_gate* gates;
+} tqsim_circuit;
+
+/* Depolarizing noise (R1/R2): after every lowered 1q gate, with
+ * probability p1 one of X,Y,Z uniformly; after every 2q gate, with probability
+ * p2 one of the 15 non-II Pauli pairs uniformly.  Readout error (R11):
+ * each measured bit flips 0->1 with readout_p01 and 1->0 with readout_p10.
+ * All in [0, 1]. */
+typedef struct {
+  double p1, p2, readout_p01, readout_p10;
+} tqsim_noise_model;
+
+typedef struct {
+  double copy_cost_gates;     /* first-slice length m = round(.) (R14); default 10 */
+  double z;                   /* Eq.4 z-score (R12); default 1.96 */
+  double eps;                 /* Eq.4 margin of error; default 0.05 */
+  uint64_t mem_budget_bytes;  /* HBM budget for states (P:310 memory limit, R25); default 180e9 */
+  uint32_t topup;             /* 0 = A_0 <- max(A_0, ceil(N/A_r^k)) (R18, default); 1 = round robin */
+  uint32_t tile_qubits;       /* HBM-pass tile width K (4..13); 0 = auto (12) */
+  uint32_t batch_log2_amps;   /* target amplitudes per level batch = 2^v; 0 = auto (26) */
+  uint32_t profile;           /* 1 = time every kernel launch with CUDA events (tqsim_stats) */
+} tqsim_options;
+
+/* The tree plan (§3.1): level d executes lowered gates
+ * [boundaries[d], boundaries[d+1]) (subcircuit d) and has
+ * instances_d = prod_{i<=d} arities[i] nodes (Eq.2).  n_outcomes = prod arities >= n_shots. */
+typedef struct {
+  uint32_t n_levels;
+  uint32_t n_qubits;
+  uint32_t arities[TQSIM_MAX_LEVELS];
+  uint64_t boundaries[TQSIM_MAX_LEVELS + 1];
+  double first_error_rate;          /* Eq.3 p_hat (0 for fixed / flat plans) */
+  double predicted_speedup_nodes;   /* node ratio vs (N,1,..,1) (Table 3) */
+  double predicted_speedup_gates;   /* flat gate-apps / tree gate-apps */
+  uint64_t n_lowered_gates;
+  uint64_t n_outcomes;
+  uint64_t node_executions;         /* sum_d instances_d */
+  uint64_t gate_amp_updates;        /* sum_d instances_d * |slice_d| * 2^n */
+  uint64_t flat_gate_amp_updates;   /* n_outcomes * n_lowered_gates * 2^n */
+  uint64_t hbm_passes;              /* sum_d instances_d * passes(slice d) */
+} tqsim_plan;
+
+/* Execution statistics of the last tqsim_execute on a handle. */
+typedef struct {
+  uint64_t kernel_launches;         /* every kernel this library launched */
+  uint64_t pass_launches;           /* gate-pass kernels (the hot loop) */
+  uint64_t measure_launches;
+  uint64_t node_executions;
+  uint64_t gate_amp_updates;
+  uint64_t pass_bytes;              /* algorithmic HBM bytes of gate passes: states*2^n*32 (16 if root-synthesized read) */
+  uint64_t measure_bytes;           /* algorithmic HBM bytes of leaf measurement */
+  double pass_ms;                   /* sum of gate-pass launch durations (profile=1 only) */
+  double measure_ms;                /* sum of measurement launch durations (profile=1 only) */
+  uint64_t leaves;                  /* leaves sampled by this shard */
+} tqsim_stats;
+
+typedef struct {
+  tqsim_plan plan;
+  uint64_t n_distinct;
+  uint64_t* bitstrings;             /* ascending, length n_distinct */
+  uint64_t* counts;                 /* sum = plan.n_outcomes */
+  uint32_t* leaf_outcomes;          /* length plan.n_outcomes, leaf order */
+  double wall_s;
+  tqsim_stats stats;
+} tqsim_result;
+
+/* Optional state dumps for parity tests: the state of node (level, instance)
+ * after its subcircuit (after the last gate and its Pauli, before measurement)
+ * is copied to dump_host + i * 2 * 2^n doubles (interleaved re, im). */
+typedef struct {
+  uint32_t n_dumps;
+  uint32_t reserved;
+  const uint32_t* dump_levels;
+  const uint64_t* dump_instances;
+  double* dump_host;
+} tqsim_debug;
+
+/* Operation record of the pass plan (for host-side invariant tests). */
+typedef struct {
+  uint32_t level, pass, phase, gate;   /* gate = lowered gate index g */
+  uint64_t tile_qubit_mask;            /* global qubits staged by the pass's tiles */
+  uint64_t reg_qubit_mask;             /* global qubits held in registers in the phase */
+} tqsim_op_record;
+
+typedef struct tqsim_handle tqsim_handle;
+
+/* [host] */
+void tqsim_default_options(tqsim_options* opts);
+const char* tqsim_last_error(void);
+const char* tqsim_version(void);
+
+/* [host] Lower a circuit (R4).  Writes up to `cap` gates; *n_out = lowered count. */
+tqsim_status tqsim_lower_circuit(const tqsim_circuit* circuit, tqsim_gate* out, uint64_t cap,
+                                 uint64_t* n_out);
+
+/* [host] Plan the tree: DCP (§3.2, Eqs.3-5, R12-R18) when arities ==
+ * NULL, else the fixed-arity override split into n_levels near-equal slices
+ * (R20; requires prod arities >= n_shots, every arity >= 1,
+ * n_levels <= lowered gate count).  opts NULL = defaults. */
+tqsim_status tqsim_plan_circuit(const tqsim_circuit* circuit, const tqsim_noise_model* noise,
+                                uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                                const tqsim_options* opts, tqsim_plan* out);
+
+/* [host] The pass plan as op records (one per lowered gate). */
+tqsim_status tqsim_describe_passes(const tqsim_circuit* circuit, const tqsim_noise_model* noise,
+                                   uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                                   const tqsim_options* opts, tqsim_op_record* out, uint64_t cap,
+                                   uint64_t* n_out);
+
+/* [host] Shard of rank/world: level-0 instances
+ * [top_begin, top_end) = [floor(A0*r/W), floor(A0*(r+1)/W)), whose leaves are
+ * the contiguous range [leaf_begin, leaf_end). */
+tqsim_status tqsim_shard_range(const tqsim_plan* plan, uint32_t rank, uint32_t world,
+                               uint64_t* top_begin, uint64_t* top_end, uint64_t* leaf_begin,
+                               uint64_t* leaf_end);
+
+/* [gpu] Create an execution handle on the current device: lowering, plan,
+ * pass plan, gate tables uploaded to HBM. */
+tqsim_status tqsim_create(const tqsim_circuit* circuit, const tqsim_noise_model* noise,
+                          uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                          const tqsim_options* opts, tqsim_handle** out);
+tqsim_status tqsim_get_plan(const tqsim_handle* h, tqsim_plan* out);
+tqsim_status tqsim_get_stats(const tqsim_handle* h, tqsim_stats* out);
+void tqsim_destroy(tqsim_handle* h);
+
+/* [host] Device workspace a shard needs (state batches of every level + leaf scratch). */
+tqsim_status tqsim_workspace_bytes(const tqsim_handle* h, uint32_t rank, uint32_t world,
+                                   uint64_t* bytes);
+
+/* [gpu] Run the shard (rank, world) of the tree asynchronously on `stream`:
+ * every leaf l of the shard gets d_leaf_outcomes[l] = its measured bitstring;
+ * other entries are not touched (zero the array and allreduce(SUM) across
+ * ranks to combine).  d_workspace: >= tqsim_workspace_bytes,
+ * 256-byte aligned.  d_leaf_outcomes: plan.n_outcomes uint32.  The call
+ * returns once all work is enqueued (profile=1: once it has finished). */
+tqsim_status tqsim_execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world,
+                           void* stream, void* d_workspace, uint64_t workspace_bytes,
+                           uint32_t* d_leaf_outcomes);
+
+/* [gpu] The north_star call: host circuit in, host histogram out (allocates
+ * its own workspace, synchronous).  tree_arities NULL = auto (DCP). */
+tqsim_status tqsim_run(const tqsim_circuit* circuit, const tqsim_noise_model* noise,
+                       uint64_t n_shots, const uint32_t* tree_arities, uint32_t n_levels,
+                       uint64_t seed, tqsim_result** out);
+
+/* [gpu] tqsim_run with options and optional state dumps (debug may be NULL). */
+tqsim_status tqsim_run_ex(const tqsim_circuit* circuit, const tqsim_noise_model* noise,
+                          uint64_t n_shots, const uint32_t* tree_arities, uint32_t n_levels,
+                          uint64_t seed, const tqsim_options* opts, const tqsim_debug* debug,
+                          tqsim_result** out);
+void tqsim_result_free(tqsim_result* r);
+
+/* [gpu] Debug / parity hooks running the SAME device functions as the hot path.
+ * Philox4x32-10 on n counters: in = n x {c0,c1,c2,c3,k0,k1}, out = n x 4 words. */
+tqsim_status tqsim_debug_philox(const uint32_t* in, uint64_t n, uint32_t* out);
+/* Noise codes of level `level`, instances [inst_begin, inst_begin+count):
+ * out[i * slice_len + t] = code of gate boundaries[level]+t (0 none, 1..3 / 1..15). */
+tqsim_status tqsim_debug_noise_table(tqsim_handle* h, uint64_t seed, uint32_t level,
+                                     uint64_t inst_begin, uint64_t count, uint8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQSIM_H */

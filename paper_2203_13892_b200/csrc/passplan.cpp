@@ -1,0 +1,160 @@
+// Pass planner: slice -> HBM passes -> register phases.
+//
+// Not in the paper (its underlying simulator is Qulacs); this is the
+// B200 design of DESIGN.md §"Kernels".  Every HBM pass stages tiles of 2^K
+// amplitudes spanning the K tile qubits {0..4} ∪ H (qubits 0..4 give 512-byte
+// contiguous segments) in shared memory; inside a tile each thread holds 16
+// amplitudes spanning RBITS = 4 tile positions in registers ("phase"), applies
+// every consecutive gate on those positions, then the tile is re-shuffled
+// through shared memory for the next phase.
+//
+// Gate order is preserved except that a gate may move ahead of earlier gates
+// with which it shares no qubit (they commute); the Pauli error of a gate is
+// applied together with the gate, so "noise after its gate" holds.
+#include <algorithm>
+
+#include "tq_internal.h"
+
+namespace tq {
+
+namespace {
+
+inline uint64_t qmask(const LGate& g) { return (1ull << g.q0) | (1ull << g.q1); }
+inline int popc(uint64_t v) { return __builtin_popcountll(v); }
+
+// Greedy in-order grouping with commuting look-ahead.  `cost_mask(g)` is the
+// set of resources gate g needs beyond the always-present ones; `cap` bounds
+// the resources of one group.  Returns groups of gate indices.
+template <class MaskFn>
+std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
+    const std::vector<uint32_t>& order, const std::vector<LGate>& gates, MaskFn need_mask,
+    int cap) {
+  std::vector<std::pair<std::vector<uint32_t>, uint64_t>> groups;
+  std::vector<uint32_t> remaining = order;
+  while (!remaining.empty()) {
+    uint64_t used = 0, blocked = 0;
+    std::vector<uint32_t> in, deferred;
+    for (uint32_t g : remaining) {
+      const uint64_t qm = qmask(gates[g]);
+      if (qm & blocked) {
+        deferred.push_back(g);
+        blocked |= qm;
+        continue;
+      }
+      const uint64_t need = need_mask(g);
+      if (popc(used | need) <= cap) {
+        used |= need;
+        in.push_back(g);
+      } else {
+        deferred.push_back(g);
+        blocked |= qm;
+      }
+    }
+    if (in.empty()) throw Error{TQSIM_EINTERNAL, "pass planner made no progress"};
+    groups.emplace_back(std::move(in), used);
+    remaining.swap(deferred);
+  }
+  return groups;
+}
+
+}  // namespace
+
+uint64_t PassPlan::passes_total(const std::vector<uint64_t>& inst) const {
+  uint64_t t = 0;
+  for (size_t d = 0; d < levels.size(); ++d) t += inst[d] * levels[d].size();
+  return t;
+}
+
+PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan,
+                        const Options& o) {
+  PassPlan pp;
+  const int n = std::max<int>((int)n_qubits, RBITS);
+  pp.n_sim = n;
+  int K = o.tile_qubits ? (int)o.tile_qubits : 12;
+  K = std::max(K, std::min(n, LOW_Q + 2));   // >= 2 free high slots so any 2q gate fits
+  K = std::min(K, n);
+  const int low = std::min(LOW_Q, K);
+  const uint64_t low_mask = (1ull << low) - 1;
+  const int hcap = K - low;
+
+  for (size_t d = 0; d + 1 < plan.bounds.size(); ++d) {
+    std::vector<uint32_t> order;
+    for (uint64_t g = plan.bounds[d]; g < plan.bounds[d + 1]; ++g) order.push_back((uint32_t)g);
+    auto passes = group_gates(order, gates,
+                              [&](uint32_t g) { return qmask(gates[g]) & ~low_mask; }, hcap);
+    std::vector<PassDesc> lvl;
+    for (size_t pi = 0; pi < passes.size(); ++pi) {
+      uint64_t H = passes[pi].second;
+      for (int q = low; q < n && popc(H) < hcap; ++q)   // pad with the lowest unused high qubits
+        if (!(H >> q & 1)) H |= 1ull << q;
+      PassDesc pd;
+      pd.K = K;
+      int pos = 0;
+      int qpos[64];
+      for (int q = 0; q < 64; ++q) qpos[q] = -1;
+      for (int q = 0; q < low; ++q) { pd.tile_q[pos] = (uint8_t)q; qpos[q] = pos++; }
+      for (int q = low; q < n; ++q)
+        if (H >> q & 1) { pd.tile_q[pos] = (uint8_t)q; qpos[q] = pos++; }
+      pd.tile_mask = low_mask | H;
+      pd.n_out = 0;
+      for (int q = 0; q < n; ++q)
+        if (!(pd.tile_mask >> q & 1)) pd.out_q[pd.n_out++] = (uint8_t)q;
+      // phases over tile positions
+      auto pos_mask = [&](uint32_t g) {
+        return (1ull << qpos[gates[g].q0]) | (1ull << qpos[gates[g].q1]);
+      };
+      auto phases = group_gates(passes[pi].first, gates, pos_mask, RBITS);
+      pd.phase_begin = (uint32_t)pp.phases.size();
+      pd.op_begin = (uint32_t)pp.ops.size();
+      for (size_t ph = 0; ph < phases.size(); ++ph) {
+        uint64_t R = phases[ph].second;
+        for (int p = K - 1; p >= 0 && popc(R) < RBITS; --p)   // pad with high positions
+          if (!(R >> p & 1) && p >= low) R |= 1ull << p;
+        for (int p = 0; p < K && popc(R) < RBITS; ++p)
+          if (!(R >> p & 1)) R |= 1ull << p;
+        PhaseDesc pdsc{};
+        int rb = 0, rbit_of_pos[MAX_K];
+        for (int p = 0; p < K; ++p)
+          if (R >> p & 1) { pdsc.rpos[rb] = (uint8_t)p; rbit_of_pos[p] = rb++; }
+        // thread-bit -> position map
+        std::vector<int> nonr;
+        for (int p = 0; p < K; ++p)
+          if (!(R >> p & 1)) nonr.push_back(p);
+        const bool global_phase = ph == 0 || ph + 1 == phases.size();
+        std::vector<int> tmap;
+        if (!global_phase && nonr.size() >= 3) {
+          // lanes 0..2 on positions of distinct residue mod 3 -> conflict-free 16-byte
+          // shared-memory accesses under the XOR swizzle of kernels.cu
+          std::vector<int> rest = nonr;
+          for (int r = 0; r < 3; ++r)
+            for (size_t i = 0; i < rest.size(); ++i)
+              if (rest[i] % 3 == r) { tmap.push_back(rest[i]); rest.erase(rest.begin() + i); break; }
+          tmap.insert(tmap.end(), rest.begin(), rest.end());
+        } else {
+          tmap = nonr;
+        }
+        for (size_t m = 0; m < tmap.size(); ++m) pdsc.tpos[m] = (uint8_t)tmap[m];
+        pdsc.op_begin = (uint32_t)pp.ops.size();
+        for (uint32_t g : phases[ph].first) {
+          const LGate& lg = gates[g];
+          OpDesc od{};
+          od.type = lg.op;
+          od.two = lg.two ? 1 : 0;
+          od.gate = g;
+          od.ra = (uint8_t)rbit_of_pos[qpos[lg.q0]];
+          od.rb = lg.two ? (uint8_t)rbit_of_pos[qpos[lg.q1]] : od.ra;
+          pp.ops.push_back(od);
+        }
+        pdsc.op_end = (uint32_t)pp.ops.size();
+        pp.phases.push_back(pdsc);
+      }
+      pd.phase_end = (uint32_t)pp.phases.size();
+      pd.op_end = (uint32_t)pp.ops.size();
+      lvl.push_back(pd);
+    }
+    pp.levels.push_back(std::move(lvl));
+  }
+  return pp;
+}
+
+}  // namespace tq

@@ -1,0 +1,593 @@
+// Tree scheduler, workspace layout and the C ABI (SURVEY §8(a) rows a4, a7,
+// a8; §8(b)).
+//
+// The tree (§3, §3.1) is walked level by level in batches:
+// run_level(d, [i0, i1)) runs subcircuit d on a batch of <= cap[d] level-d
+// instances (fan-out fused into the first pass: every child reads its parent's
+// state from the level d-1 batch, "state copy"), then recurses into the
+// children of that batch.  Live states are sum_d cap[d], bounded by
+// options.mem_budget_bytes (180 GB by default, R25; the paper's "memory
+// capacity limit").  Leaves are measured right after their last pass.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "tq_internal.h"
+
+struct tqsim_handle {
+  uint32_t n_user = 0;
+  int n_sim = 0;
+  tq::Options opts;
+  tqsim_noise_model noise{};
+  std::vector<tq::LGate> gates;
+  tq::Plan plan;
+  tq::PassPlan pp;
+  tqsim_plan cplan{};
+  std::vector<uint64_t> inst;
+  tq::DeviceTables dt;
+  void* d_ops = nullptr;
+  void* d_phases = nullptr;
+  void* d_mats = nullptr;
+  uint8_t* d_two = nullptr;
+  tqsim_stats stats{};
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> ev_marks;   // (kind 0 pass / 1 measure, event index)
+  const tqsim_debug* debug = nullptr;
+  cudaStream_t debug_stream = nullptr;
+};
+
+namespace tq {
+
+namespace {
+thread_local std::string g_last_error;
+
+struct CudaFail {
+  int code;
+  const char* what;
+};
+
+inline void ck(int code, const char* what) {
+  if (code != 0) throw CudaFail{code, what};
+}
+inline void ckc(cudaError_t e, const char* what) { ck((int)e, what); }
+
+template <class F>
+tqsim_status guarded(F&& f) {
+  try {
+    f();
+    return TQSIM_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.status;
+  } catch (const CudaFail& e) {
+    g_last_error = std::string(e.what) + ": " + cuda_error_string(e.code);
+    return TQSIM_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return TQSIM_ECAPACITY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TQSIM_EINTERNAL;
+  } catch (...) {
+    g_last_error = "unknown internal error";
+    return TQSIM_EINTERNAL;
+  }
+}
+
+void validate_noise(const tqsim_noise_model* nm) {
+  if (!nm) throw Error{TQSIM_EINVAL, "noise model is NULL"};
+  const double v[4] = {nm->p1, nm->p2, nm->readout_p01, nm->readout_p10};
+  for (double p : v)
+    if (!(p >= 0.0 && p <= 1.0)) throw Error{TQSIM_EINVAL, "probabilities must be in [0, 1]"};
+}
+
+void require_device() {
+  int dev = 0, count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw Error{TQSIM_ECUDA, "no CUDA device (this library has no CPU fallback)"};
+  ckc(cudaGetDevice(&dev), "cudaGetDevice");
+  int major = 0;
+  ckc(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev), "cc");
+  if (major != 10) throw Error{TQSIM_ECUDA, "needs an sm_100 (B200) device"};
+}
+
+struct Layout {
+  std::vector<uint64_t> cap;       // states per level batch
+  std::vector<uint64_t> off;       // byte offset of level buffer
+  uint64_t sums_off = 0, total = 0;
+  int chunk_log2 = 0;
+};
+
+constexpr uint64_t ALIGN = 256;
+inline uint64_t align_up(uint64_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
+
+void shard(const tqsim_plan& p, uint32_t rank, uint32_t world, uint64_t& t0, uint64_t& t1) {
+  if (world < 1 || rank >= world) throw Error{TQSIM_EINVAL, "rank must be < world, world >= 1"};
+  const uint64_t a0 = p.arities[0];
+  t0 = a0 * rank / world;
+  t1 = a0 * (rank + 1) / world;
+}
+
+Layout layout(const tqsim_handle* h, uint64_t top_count) {
+  Layout L;
+  const int n = h->n_sim;
+  const uint64_t S = 16ull << n;
+  const int tl = h->opts.batch_log2_amps ? (int)h->opts.batch_log2_amps : 26;
+  const uint64_t target = tl >= n ? (1ull << (tl - n)) : 1ull;
+  const size_t levels = h->plan.arities.size();
+  uint64_t per = std::max<uint64_t>(top_count, 1);
+  for (size_t d = 0; d < levels; ++d) {
+    if (d > 0) per *= h->plan.arities[d];
+    L.cap.push_back(std::max<uint64_t>(1, std::min(per, target)));
+  }
+  L.chunk_log2 = std::min(n, 12);
+  auto total_of = [&](Layout& l) {
+    uint64_t off = 0;
+    l.off.clear();
+    for (size_t d = 0; d < levels; ++d) {
+      l.off.push_back(off);
+      off = align_up(off + l.cap[d] * S);
+    }
+    l.sums_off = off;
+    off = align_up(off + l.cap.back() * (8ull << (n - l.chunk_log2)));
+    l.total = off;
+    return off;
+  };
+  while (total_of(L) > h->opts.mem_budget) {
+    auto it = std::max_element(L.cap.begin(), L.cap.end());
+    if (*it <= 1) throw Error{TQSIM_ECAPACITY, "memory budget too small for one state per level"};
+    *it = (*it + 1) / 2;
+  }
+  return L;
+}
+
+// ---------------------------------------------------------------- global arena for tqsim_run
+std::mutex g_arena_mu;
+void* g_arena = nullptr;
+size_t g_arena_size = 0;
+
+void* arena_get(size_t bytes) {
+  if (g_arena_size >= bytes) return g_arena;
+  if (g_arena) cudaFree(g_arena);
+  g_arena = nullptr;
+  g_arena_size = 0;
+  ckc(cudaMalloc(&g_arena, bytes), "cudaMalloc workspace");
+  g_arena_size = bytes;
+  return g_arena;
+}
+
+// ---------------------------------------------------------------- scheduler
+struct Exec {
+  tqsim_handle* h;
+  uint64_t seed;
+  cudaStream_t st;
+  char* ws;
+  Layout L;
+  uint32_t* d_out;
+};
+
+cudaEvent_t next_event(tqsim_handle* h) {
+  if (h->ev_used == h->ev_pool.size()) {
+    cudaEvent_t e;
+    ckc(cudaEventCreate(&e), "cudaEventCreate");
+    h->ev_pool.push_back(e);
+  }
+  return h->ev_pool[h->ev_used++];
+}
+
+void mark(Exec& x, int kind) {
+  if (!x.h->opts.profile) return;
+  cudaEvent_t e = next_event(x.h);
+  ckc(cudaEventRecord(e, x.st), "cudaEventRecord");
+  x.h->ev_marks.push_back({kind, x.h->ev_used - 1});
+}
+
+void dump_if_requested(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, const char* level_buf) {
+  const tqsim_debug* dbg = x.h->debug;
+  if (!dbg || !dbg->n_dumps) return;
+  const uint64_t amps_user = 1ull << x.h->n_user;
+  for (uint32_t i = 0; i < dbg->n_dumps; ++i) {
+    if (dbg->dump_levels[i] != d) continue;
+    const uint64_t j = dbg->dump_instances[i];
+    if (j < b || j >= b + cnt) continue;
+    ckc(cudaMemcpyAsync(dbg->dump_host + 2 * amps_user * i,
+                        level_buf + ((j - b) << (x.h->n_sim + 4)), 16 * amps_user,
+                        cudaMemcpyDeviceToHost, x.st),
+        "dump copy");
+    ckc(cudaStreamSynchronize(x.st), "dump sync");
+  }
+}
+
+void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_first) {
+  tqsim_handle* h = x.h;
+  const int n = h->n_sim;
+  const uint32_t levels = (uint32_t)h->plan.arities.size();
+  const uint64_t cap = x.L.cap[d];
+  char* buf = x.ws + x.L.off[d];
+  const char* pbuf = d > 0 ? x.ws + x.L.off[d - 1] : nullptr;
+  const auto& passes = h->pp.levels[d];
+  for (uint64_t b = i0; b < i1; b += cap) {
+    const uint64_t cnt = std::min(cap, i1 - b);
+    for (size_t p = 0; p < passes.size(); ++p) {
+      PassLaunch pl{};
+      pl.src_mode = p > 0 ? 2u : (d == 0 ? 0u : 1u);
+      pl.src = pbuf;
+      pl.dst = buf;
+      pl.child_first = b;
+      pl.parent_first = parent_first;
+      pl.arity = h->plan.arities[d];
+      pl.batch = (uint32_t)cnt;
+      pl.seed = x.seed;
+      pl.p1 = h->noise.p1;
+      pl.p2 = h->noise.p2;
+      mark(x, 0);
+      ck(launch_pass(passes[p], n, h->dt, pl, x.st), "gate pass launch");
+      mark(x, 0);
+      h->stats.kernel_launches++;
+      h->stats.pass_launches++;
+      const uint64_t amps = cnt << n;
+      uint64_t bytes = amps * 16;   // write
+      if (pl.src_mode == 2) bytes += amps * 16;
+      else if (pl.src_mode == 1) {
+        const uint64_t A = pl.arity;
+        const uint64_t parents = (b + cnt - 1) / A - b / A + 1;
+        bytes += (parents << n) * 16;
+      }
+      h->stats.pass_bytes += bytes;
+    }
+    h->stats.node_executions += cnt;
+    h->stats.gate_amp_updates += (cnt * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
+    dump_if_requested(x, d, b, cnt, buf);
+    if (d + 1 == levels) {
+      double* sums = reinterpret_cast<double*>(x.ws + x.L.sums_off);
+      mark(x, 1);
+      ck(launch_chunk_sums(buf, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
+      ck(launch_sample(buf, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, x.seed,
+                       h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
+         "sample launch");
+      mark(x, 1);
+      h->stats.kernel_launches += 2;
+      h->stats.measure_launches += 2;
+      h->stats.measure_bytes += (cnt << n) * 16 + (cnt << x.L.chunk_log2) * 16;
+      h->stats.leaves += cnt;
+    } else {
+      const uint64_t A = h->plan.arities[d + 1];
+      run_level(x, d + 1, b * A, (b + cnt) * A, b);
+    }
+  }
+}
+
+tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,
+                            const uint32_t* arities, uint32_t n_levels, const tqsim_options* o,
+                            bool need_gpu) {
+  validate_noise(nm);
+  Options opts = options_from(o);
+  auto* h = new tqsim_handle();
+  try {
+    h->n_user = c ? c->n_qubits : 0;
+    h->gates = lower(c);
+    h->opts = opts;
+    h->noise = *nm;
+    h->plan = make_plan(h->gates, c->n_qubits, nm, n_shots, arities, n_levels, opts);
+    h->pp = make_pass_plan(h->gates, c->n_qubits, h->plan, opts);
+    h->n_sim = h->pp.n_sim;
+    h->inst = instances(h->plan);
+    fill_plan(h->plan, c->n_qubits, h->gates.size(), h->pp.passes_total(h->inst), &h->cplan);
+    if (need_gpu) {
+      require_device();
+      std::vector<double> mats(h->gates.size() * 8);
+      std::vector<uint8_t> two(h->gates.size());
+      for (size_t g = 0; g < h->gates.size(); ++g) {
+        std::memcpy(&mats[g * 8], h->gates[g].m, 8 * sizeof(double));
+        two[g] = h->gates[g].two ? 1 : 0;
+      }
+      const size_t ob = h->pp.ops.size() * sizeof(OpDesc);
+      const size_t pb = h->pp.phases.size() * sizeof(PhaseDesc);
+      ckc(cudaMalloc(&h->d_ops, std::max<size_t>(ob, 16)), "cudaMalloc ops");
+      ckc(cudaMalloc(&h->d_phases, std::max<size_t>(pb, 16)), "cudaMalloc phases");
+      ckc(cudaMalloc(&h->d_mats, mats.size() * sizeof(double)), "cudaMalloc mats");
+      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_two), two.size()), "cudaMalloc two");
+      ckc(cudaMemcpy(h->d_ops, h->pp.ops.data(), ob, cudaMemcpyHostToDevice), "upload ops");
+      ckc(cudaMemcpy(h->d_phases, h->pp.phases.data(), pb, cudaMemcpyHostToDevice), "upload phases");
+      ckc(cudaMemcpy(h->d_mats, mats.data(), mats.size() * sizeof(double), cudaMemcpyHostToDevice),
+          "upload mats");
+      ckc(cudaMemcpy(h->d_two, two.data(), two.size(), cudaMemcpyHostToDevice), "upload two");
+      h->dt.ops = static_cast<const OpDesc*>(h->d_ops);
+      h->dt.phases = static_cast<const PhaseDesc*>(h->d_phases);
+      h->dt.mats = static_cast<const double*>(h->d_mats);
+    }
+  } catch (...) {
+    tqsim_destroy(h);
+    throw;
+  }
+  return h;
+}
+
+void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cudaStream_t st,
+             void* ws, uint64_t ws_bytes, uint32_t* d_out) {
+  if (!h) throw Error{TQSIM_EINVAL, "handle is NULL"};
+  if (!d_out) throw Error{TQSIM_EINVAL, "d_leaf_outcomes is NULL"};
+  uint64_t t0, t1;
+  shard(h->cplan, rank, world, t0, t1);
+  Exec x{h, seed, st, static_cast<char*>(ws), layout(h, t1 - t0), d_out};
+  if (!ws || ws_bytes < x.L.total) throw Error{TQSIM_ECAPACITY, "workspace too small"};
+  if (reinterpret_cast<uintptr_t>(ws) % ALIGN) throw Error{TQSIM_EINVAL, "workspace not 256-byte aligned"};
+  h->stats = tqsim_stats{};
+  h->ev_used = 0;
+  h->ev_marks.clear();
+  if (t1 > t0) run_level(x, 0, t0, t1, 0);
+  if (h->opts.profile) {
+    ckc(cudaStreamSynchronize(st), "profile sync");
+    for (size_t i = 0; i + 1 < h->ev_marks.size(); i += 2) {
+      float ms = 0.f;
+      ckc(cudaEventElapsedTime(&ms, h->ev_pool[h->ev_marks[i].second],
+                               h->ev_pool[h->ev_marks[i + 1].second]),
+          "cudaEventElapsedTime");
+      if (h->ev_marks[i].first == 0) h->stats.pass_ms += ms;
+      else h->stats.measure_ms += ms;
+    }
+  }
+}
+
+void build_result(tqsim_handle* h, const std::vector<uint32_t>& outs, double wall, tqsim_result** out) {
+  auto* r = static_cast<tqsim_result*>(std::calloc(1, sizeof(tqsim_result)));
+  if (!r) throw std::bad_alloc();
+  r->plan = h->cplan;
+  r->stats = h->stats;
+  r->wall_s = wall;
+  std::vector<uint32_t> sorted = outs;
+  std::sort(sorted.begin(), sorted.end());
+  std::vector<uint64_t> bits, counts;
+  for (size_t i = 0; i < sorted.size();) {
+    size_t j = i;
+    while (j < sorted.size() && sorted[j] == sorted[i]) ++j;
+    bits.push_back(sorted[i]);
+    counts.push_back(j - i);
+    i = j;
+  }
+  r->n_distinct = bits.size();
+  r->bitstrings = static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, bits.size()) * 8));
+  r->counts = static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, counts.size()) * 8));
+  r->leaf_outcomes = static_cast<uint32_t*>(std::malloc(std::max<size_t>(1, outs.size()) * 4));
+  if (!r->bitstrings || !r->counts || !r->leaf_outcomes) {
+    tqsim_result_free(r);
+    throw std::bad_alloc();
+  }
+  std::memcpy(r->bitstrings, bits.data(), bits.size() * 8);
+  std::memcpy(r->counts, counts.data(), counts.size() * 8);
+  std::memcpy(r->leaf_outcomes, outs.data(), outs.size() * 4);
+  *out = r;
+}
+
+}  // namespace
+}  // namespace tq
+
+using namespace tq;
+
+extern "C" {
+
+void tqsim_default_options(tqsim_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->copy_cost_gates = 10.0;
+  o->z = 1.96;
+  o->eps = 0.05;
+  o->mem_budget_bytes = 180000000000ull;
+}
+
+const char* tqsim_last_error(void) { return g_last_error.c_str(); }
+const char* tqsim_version(void) { return "tqsim-b200 0.1 (sm_100a)"; }
+
+tqsim_status tqsim_lower_circuit(const tqsim_circuit* c, tqsim_gate* out, uint64_t cap,
+                                 uint64_t* n_out) {
+  return guarded([&] {
+    std::vector<LGate> g = lower(c);
+    if (!n_out) throw Error{TQSIM_EINVAL, "n_out is NULL"};
+    *n_out = g.size();
+    for (uint64_t i = 0; i < g.size() && i < cap && out; ++i) {
+      out[i] = tqsim_gate{};
+      out[i].kind = g[i].kind;
+      out[i].q0 = g[i].q0;
+      out[i].q1 = g[i].two ? g[i].q1 : 0;
+    }
+  });
+}
+
+tqsim_status tqsim_plan_circuit(const tqsim_circuit* c, const tqsim_noise_model* nm,
+                                uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                                const tqsim_options* o, tqsim_plan* out) {
+  return guarded([&] {
+    if (!out) throw Error{TQSIM_EINVAL, "out is NULL"};
+    tqsim_handle* h = create_handle(c, nm, n_shots, arities, n_levels, o, false);
+    *out = h->cplan;
+    tqsim_destroy(h);
+  });
+}
+
+tqsim_status tqsim_describe_passes(const tqsim_circuit* c, const tqsim_noise_model* nm,
+                                   uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                                   const tqsim_options* o, tqsim_op_record* out, uint64_t cap,
+                                   uint64_t* n_out) {
+  return guarded([&] {
+    if (!n_out) throw Error{TQSIM_EINVAL, "n_out is NULL"};
+    tqsim_handle* h = create_handle(c, nm, n_shots, arities, n_levels, o, false);
+    uint64_t k = 0;
+    for (size_t d = 0; d < h->pp.levels.size(); ++d)
+      for (size_t p = 0; p < h->pp.levels[d].size(); ++p) {
+        const PassDesc& pd = h->pp.levels[d][p];
+        for (uint32_t ph = pd.phase_begin; ph < pd.phase_end; ++ph) {
+          const PhaseDesc& P = h->pp.phases[ph];
+          uint64_t rmask = 0;
+          for (int b = 0; b < RBITS; ++b) rmask |= 1ull << pd.tile_q[P.rpos[b]];
+          for (uint32_t i = P.op_begin; i < P.op_end; ++i, ++k)
+            if (out && k < cap)
+              out[k] = tqsim_op_record{(uint32_t)d, (uint32_t)p, ph - pd.phase_begin,
+                                       h->pp.ops[i].gate, pd.tile_mask, rmask};
+        }
+      }
+    *n_out = k;
+    tqsim_destroy(h);
+  });
+}
+
+tqsim_status tqsim_shard_range(const tqsim_plan* p, uint32_t rank, uint32_t world,
+                               uint64_t* top_begin, uint64_t* top_end, uint64_t* leaf_begin,
+                               uint64_t* leaf_end) {
+  return guarded([&] {
+    if (!p || p->n_levels < 1) throw Error{TQSIM_EINVAL, "plan is NULL or empty"};
+    uint64_t t0, t1;
+    shard(*p, rank, world, t0, t1);
+    uint64_t below = 1;
+    for (uint32_t d = 1; d < p->n_levels; ++d) below *= p->arities[d];
+    if (top_begin) *top_begin = t0;
+    if (top_end) *top_end = t1;
+    if (leaf_begin) *leaf_begin = t0 * below;
+    if (leaf_end) *leaf_end = t1 * below;
+  });
+}
+
+tqsim_status tqsim_create(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,
+                          const uint32_t* arities, uint32_t n_levels, const tqsim_options* o,
+                          tqsim_handle** out) {
+  return guarded([&] {
+    if (!out) throw Error{TQSIM_EINVAL, "out is NULL"};
+    *out = create_handle(c, nm, n_shots, arities, n_levels, o, true);
+  });
+}
+
+tqsim_status tqsim_get_plan(const tqsim_handle* h, tqsim_plan* out) {
+  return guarded([&] {
+    if (!h || !out) throw Error{TQSIM_EINVAL, "NULL argument"};
+    *out = h->cplan;
+  });
+}
+
+tqsim_status tqsim_get_stats(const tqsim_handle* h, tqsim_stats* out) {
+  return guarded([&] {
+    if (!h || !out) throw Error{TQSIM_EINVAL, "NULL argument"};
+    *out = h->stats;
+  });
+}
+
+void tqsim_destroy(tqsim_handle* h) {
+  if (!h) return;
+  if (h->d_ops) cudaFree(h->d_ops);
+  if (h->d_phases) cudaFree(h->d_phases);
+  if (h->d_mats) cudaFree(h->d_mats);
+  if (h->d_two) cudaFree(h->d_two);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  delete h;
+}
+
+tqsim_status tqsim_workspace_bytes(const tqsim_handle* h, uint32_t rank, uint32_t world,
+                                   uint64_t* bytes) {
+  return guarded([&] {
+    if (!h || !bytes) throw Error{TQSIM_EINVAL, "NULL argument"};
+    uint64_t t0, t1;
+    shard(h->cplan, rank, world, t0, t1);
+    *bytes = layout(h, t1 - t0).total;
+  });
+}
+
+tqsim_status tqsim_execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world,
+                           void* stream, void* d_workspace, uint64_t workspace_bytes,
+                           uint32_t* d_leaf_outcomes) {
+  return guarded([&] {
+    execute(h, seed, rank, world, static_cast<cudaStream_t>(stream), d_workspace, workspace_bytes,
+            d_leaf_outcomes);
+  });
+}
+
+tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,
+                          const uint32_t* arities, uint32_t n_levels, uint64_t seed,
+                          const tqsim_options* o, const tqsim_debug* debug, tqsim_result** out) {
+  return guarded([&] {
+    if (!out) throw Error{TQSIM_EINVAL, "out is NULL"};
+    const auto t_start = std::chrono::steady_clock::now();
+    tqsim_handle* h = create_handle(c, nm, n_shots, arities, n_levels, o, true);
+    cudaStream_t st = nullptr;
+    try {
+      std::lock_guard<std::mutex> lock(g_arena_mu);
+      h->debug = debug;
+      uint64_t t0, t1;
+      shard(h->cplan, 0, 1, t0, t1);
+      const uint64_t ws = layout(h, t1 - t0).total;
+      const uint64_t nout = h->cplan.n_outcomes;
+      const uint64_t out_off = align_up(ws);
+      char* base = static_cast<char*>(arena_get(out_off + nout * 4));
+      ckc(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+      uint32_t* d_out = reinterpret_cast<uint32_t*>(base + out_off);
+      ckc(cudaMemsetAsync(d_out, 0, nout * 4, st), "memset outcomes");
+      execute(h, seed, 0, 1, st, base, ws, d_out);
+      std::vector<uint32_t> outs(nout);
+      ckc(cudaMemcpyAsync(outs.data(), d_out, nout * 4, cudaMemcpyDeviceToHost, st), "D2H outcomes");
+      ckc(cudaStreamSynchronize(st), "stream sync");
+      cudaStreamDestroy(st);
+      st = nullptr;
+      const double wall =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      build_result(h, outs, wall, out);
+    } catch (...) {
+      if (st) cudaStreamDestroy(st);
+      tqsim_destroy(h);
+      throw;
+    }
+    tqsim_destroy(h);
+  });
+}
+
+tqsim_status tqsim_run(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,
+                       const uint32_t* tree_arities, uint32_t n_levels, uint64_t seed,
+                       tqsim_result** out) {
+  return tqsim_run_ex(c, nm, n_shots, tree_arities, n_levels, seed, nullptr, nullptr, out);
+}
+
+void tqsim_result_free(tqsim_result* r) {
+  if (!r) return;
+  std::free(r->bitstrings);
+  std::free(r->counts);
+  std::free(r->leaf_outcomes);
+  std::free(r);
+}
+
+tqsim_status tqsim_debug_philox(const uint32_t* in, uint64_t n, uint32_t* out) {
+  return guarded([&] {
+    if (!in || !out) throw Error{TQSIM_EINVAL, "NULL argument"};
+    require_device();
+    uint32_t *di = nullptr, *dout = nullptr;
+    ckc(cudaMalloc(&di, std::max<uint64_t>(1, n) * 24), "cudaMalloc");
+    ckc(cudaMalloc(&dout, std::max<uint64_t>(1, n) * 16), "cudaMalloc");
+    cudaMemcpy(di, in, n * 24, cudaMemcpyHostToDevice);
+    int e = launch_philox_debug(di, n, dout);
+    if (e == 0) e = (int)cudaMemcpy(out, dout, n * 16, cudaMemcpyDeviceToHost);
+    cudaFree(di);
+    cudaFree(dout);
+    ck(e, "philox debug");
+  });
+}
+
+tqsim_status tqsim_debug_noise_table(tqsim_handle* h, uint64_t seed, uint32_t level,
+                                     uint64_t inst_begin, uint64_t count, uint8_t* out) {
+  return guarded([&] {
+    if (!h || !out) throw Error{TQSIM_EINVAL, "NULL argument"};
+    if (level >= h->plan.arities.size()) throw Error{TQSIM_EINVAL, "level out of range"};
+    const uint32_t b0 = (uint32_t)h->plan.bounds[level];
+    const uint32_t len = (uint32_t)(h->plan.bounds[level + 1] - b0);
+    uint8_t* d = nullptr;
+    const uint64_t bytes = std::max<uint64_t>(1, count * len);
+    ckc(cudaMalloc(&d, bytes), "cudaMalloc");
+    int e = launch_noise_table(h->d_two + b0, b0, len, inst_begin, count, seed, h->noise.p1,
+                               h->noise.p2, d);
+    if (e == 0) e = (int)cudaMemcpy(out, d, count * len, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    ck(e, "noise table");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// Internal declarations of the TQSim B200 runtime (not part of the C ABI).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tqsim.h"
+
+namespace tq {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+  tqsim_status status;
+  std::string msg;
+};
+
+// ---------------------------------------------------------------- IR
+enum OpType : uint8_t { OP_GEN = 0, OP_DIAG = 1, OP_CX = 2, OP_CZ = 3 };
+
+struct LGate {              // one lowered gate = one noise location (R1)
+  uint32_t kind;            // tqsim_gate_kind of the primitive (1q kinds, CX, CZ)
+  uint32_t q0, q1;          // q1 = q0 for 1q
+  bool two;
+  uint8_t op;               // OpType
+  double m[8];              // 2x2 complex, row major (re,im) pairs: m00 m01 m10 m11
+};
+
+// Validates and lowers (R4).  Throws Error{TQSIM_EINVAL}.
+std::vector<LGate> lower(const tqsim_circuit* c);
+
+// ---------------------------------------------------------------- planner
+struct Options {
+  double copy_cost_gates = 10.0, z = 1.96, eps = 0.05;
+  uint64_t mem_budget = 180000000000ull;
+  uint32_t topup = 0, tile_qubits = 0, batch_log2_amps = 0, profile = 0;
+};
+Options options_from(const tqsim_options* o);
+
+struct Plan {
+  std::vector<uint32_t> arities;
+  std::vector<uint64_t> bounds;   // size L+1
+  double p_hat = 0.0;
+};
+
+Plan make_plan(const std::vector<LGate>& gates, uint32_t n_qubits, const tqsim_noise_model* nm,
+               uint64_t n_shots, const uint32_t* arities, uint32_t n_levels, const Options& o);
+void fill_plan(const Plan& p, uint32_t n_qubits, uint64_t n_gates, uint64_t hbm_passes,
+               tqsim_plan* out);
+std::vector<uint64_t> instances(const Plan& p);   // Eq.2, per level
+
+// ---------------------------------------------------------------- pass plan
+constexpr int RBITS = 4;        // amplitudes per thread = 2^RBITS (register-resident qubits)
+constexpr int MAX_K = 13;       // max tile qubits per HBM pass (2^13 * 16 B = 128 KiB smem)
+constexpr int LOW_Q = 5;        // qubits 0..4 are in every tile (512 B contiguous segments)
+
+struct OpDesc {                 // 8 bytes, device-readable
+  uint8_t type;                 // OpType
+  uint8_t ra, rb;               // register bit(s) 0..3 (rb = target for CX)
+  uint8_t two;                  // 2q noise location
+  uint32_t gate;                // lowered gate index g (noise key + matrix)
+};
+
+struct PhaseDesc {              // 32 bytes, device-readable
+  uint8_t rpos[RBITS];          // tile-local positions held in registers
+  uint8_t tpos[MAX_K - RBITS];  // thread-index bit m -> tile-local position
+  uint8_t pad[32 - RBITS - (MAX_K - RBITS) - 8];
+  uint32_t op_begin, op_end;    // global op indices
+};
+static_assert(sizeof(PhaseDesc) == 32, "PhaseDesc layout");
+
+struct PassDesc {
+  int K = 0;                    // tile qubits
+  uint8_t tile_q[MAX_K];        // tile-local position -> global qubit
+  int n_out = 0;
+  uint8_t out_q[32];            // non-tile qubits (ascending)
+  uint32_t phase_begin = 0, phase_end = 0;
+  uint32_t op_begin = 0, op_end = 0;
+  uint64_t tile_mask = 0;
+};
+
+struct PassPlan {
+  int n_sim = 0;                         // simulated width (>= RBITS)
+  std::vector<std::vector<PassDesc>> levels;   // per level, its passes
+  std::vector<PhaseDesc> phases;
+  std::vector<OpDesc> ops;
+  uint64_t passes_total(const std::vector<uint64_t>& inst) const;
+};
+
+PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan,
+                        const Options& o);
+
+// ---------------------------------------------------------------- kernels (kernels.cu)
+struct PassLaunch {
+  const void* src;              // double2*; root synthesized when src_mode == 0
+  void* dst;
+  uint32_t src_mode;            // 0 root |0..0>, 1 fan-out from parent batch, 2 in place
+  uint64_t child_first;         // global instance id of batch slot 0
+  uint64_t parent_first;        // global instance id of parent slot 0 (mode 1)
+  uint32_t arity;               // A_d (mode 1)
+  uint32_t batch;
+  uint64_t seed;
+  double p1, p2;
+};
+
+struct DeviceTables {
+  const OpDesc* ops = nullptr;
+  const PhaseDesc* phases = nullptr;
+  const double* mats = nullptr;  // 8 doubles per lowered gate
+};
+
+int launch_pass(const PassDesc& pd, int n_sim, const DeviceTables& t, const PassLaunch& L,
+                void* stream);
+int launch_chunk_sums(const void* states, uint32_t batch, int n_sim, int chunk_log2, double* sums,
+                      void* stream);
+int launch_sample(const void* states, const double* sums, uint32_t batch, int n_sim, int n_user,
+                  int chunk_log2, uint64_t leaf_first, uint64_t seed, double p01, double p10,
+                  uint32_t* d_out, void* stream);
+int launch_philox_debug(const uint32_t* d_in, uint64_t n, uint32_t* d_out);
+int launch_noise_table(const uint8_t* d_two, uint32_t slice_begin, uint32_t slice_len,
+                       uint64_t inst_begin, uint64_t count, uint64_t seed, double p1, double p2,
+                       uint8_t* d_out);
+const char* cuda_error_string(int code);
+
+}  // namespace tq

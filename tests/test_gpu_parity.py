@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Bars (BASELINE north_star): per-trajectory amplitudes max-abs <= 1e-10 (fp64);
+sampled outcomes bit-exact except draws the oracle flags as lying within 1e-9
+of a cumulative-probability boundary; histograms identical otherwise.
+"""
+import numpy as np
+import pytest
+
+import paper_2203_13892_b200.tqsim as T
+from oracle import gates as OG
+from oracle.noise import noise_codes_np
+from oracle.philox import philox4x32_10
+from oracle.planner import Plan, fixed_plan, dcp_plan
+from oracle.tree import (NoiseModel, error_rates, ideal_state, leaf_ancestors,
+                         simulate_leaf_flat, simulate_tree)
+from tq_testutil import golden_rows
+from workloads import basis_prep_gates, ghz_gates, load_config, qft_gates, random_circuit
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-10
+
+
+def oracle_plan_of(res_plan) -> Plan:
+    return Plan(res_plan.arity_list, res_plan.boundary_list)
+
+
+def assert_leaves_match(gpu_leaf, oracle_leaves, allow_flag=True):
+    flagged = 0
+    for l, r in oracle_leaves.items():
+        if r.flagged and allow_flag:
+            flagged += 1
+            continue
+        assert int(gpu_leaf[l]) == r.outcome, (l, int(gpu_leaf[l]), r.outcome, r.x)
+    return flagged
+
+
+def run_and_compare(n, gates, nm: NoiseModel, shots, arities, seed, opts=None, dumps=()):
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
+    res = T.tqsim_run_ex(n, gates, noise, shots, arities, seed, opts, dumps)
+    plan = oracle_plan_of(res.plan)
+    low = OG.lower(gates)
+    ref = simulate_tree(n, low, plan, nm, seed, dump=dumps)
+    assert res.leaf_outcomes.shape[0] == plan.n_outcomes
+    flagged = assert_leaves_match(res.leaf_outcomes, ref.leaves)
+    if flagged == 0:
+        want = {}
+        for r in ref.leaves.values():
+            want[r.outcome] = want.get(r.outcome, 0) + 1
+        assert res.counts == want
+    for i, key in enumerate(dumps):
+        err = np.max(np.abs(res.dumps[i] - ref.dumps[key]))
+        assert err <= AMP_TOL, (key, err)
+    return res, ref
+
+
+def test_device_philox_known_answers_and_oracle():
+    rows = golden_rows("philox_kat.txt")
+    words = np.array([[int(v, 16) for v in r[:6]] for r in rows], dtype=np.uint32)
+    out = T.tqsim_debug_philox(words)
+    for r, o in zip(rows, out):
+        assert tuple(int(v) for v in o) == tuple(int(v, 16) for v in r[6:10])
+    rng = np.random.default_rng(0)
+    words = rng.integers(0, 2 ** 32, size=(500, 6), dtype=np.uint64).astype(np.uint32)
+    out = T.tqsim_debug_philox(words)
+    for w, o in zip(words, out):
+        assert tuple(int(v) for v in o) == philox4x32_10(w[:4], w[4:6])
+
+
+def test_noise_tables_match_oracle():
+    w = load_config("c2_qft15")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    h = T.tqsim_create(n, gates, noise, shots, ar)
+    p = h.plan
+    low = OG.lower(gates)
+    for level in (0, p.n_levels - 1):
+        b0, b1 = p.boundaries[level], p.boundaries[level + 1]
+        count = 300
+        got = h.noise_table(5, level, 17, count)
+        g = np.arange(b0, b1)[None, :]
+        j = np.arange(17, 17 + count)[:, None]
+        two = np.array([OG.is_two_qubit(low[i]) for i in range(b0, b1)])[None, :]
+        want = noise_codes_np(g, j, 5, np.where(two, w.p2, w.p1), two)
+        assert np.array_equal(got, want)
+    h.close()
+
+
+def test_c1_qft5_full_tree():
+    w = load_config("c1_qft5")
+    nm = NoiseModel(w.p1, w.p2, w.readout_p01, w.readout_p10)
+    dumps = [(0, j) for j in range(10)] + [(1, j) for j in (0, 1, 99, 500, 999)]
+    res, ref = run_and_compare(5, w.circuit.gates, nm, w.shots, w.arities, w.seed, dumps=dumps)
+    assert res.plan.n_outcomes == 1000
+
+
+@pytest.mark.parametrize("tile", [0, 4, 7, 9, 10, 12, 13])
+def test_random_circuits_all_tiles(tile):
+    rng = np.random.default_rng(100 + tile)
+    for it in range(3):
+        n = int(rng.integers(4, 15))
+        gates = random_circuit(n, int(rng.integers(20, 80)), rng)
+        nm = NoiseModel(0.05, 0.1, 0.02, 0.03)          # many errors: every Pauli path
+        arities = [3, 2, 4] if it % 2 == 0 else None
+        shots = 24 if arities else 40
+        opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)  # ragged batches
+        dumps = [(0, 0), (0, 2)]
+        run_and_compare(n, gates, nm, shots, arities, 1234 + it, opts, dumps)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_tiny_widths(n):
+    rng = np.random.default_rng(n)
+    gates = random_circuit(n, 30, rng)
+    if not gates:
+        pytest.skip("no gates")
+    run_and_compare(n, gates, NoiseModel(0.1, 0.2, 0.05, 0.05), 30, [5, 6], 3,
+                    dumps=[(1, 0), (1, 29)])
+
+
+def test_qft_noise_free_equals_closed_form():
+    n = 13
+    x = 4321
+    gates = basis_prep_gates(x, n) + qft_gates(n)
+    res = T.tqsim_run_ex(n, gates, T.noise_arg(0, 0), 8, [2, 4], 0, None, [(1, 0), (1, 7)])
+    y = np.arange(2 ** n)
+    want = np.exp(2j * np.pi * x * y / 2 ** n) / np.sqrt(2 ** n)
+    for i in range(2):
+        assert np.max(np.abs(res.dumps[i] - want)) < 1e-12
+
+
+def test_ghz_two_peaks_and_outcomes():
+    n = 16
+    res = T.tqsim_run_ex(n, ghz_gates(n), T.noise_arg(0, 0), 2000, [2000], 0, None, [(0, 5)])
+    st = res.dumps[0]
+    assert abs(st[0] - 2 ** -0.5) < 1e-15 and abs(st[-1] - 2 ** -0.5) < 1e-15
+    assert set(res.counts) == {0, 2 ** n - 1}
+    assert abs(res.counts[0] - 1000) < 5 * np.sqrt(500)
+
+
+def test_arity_one_tree_equals_flat_on_gpu():
+    w = load_config("c1_qft5")
+    noise = T.noise_arg(0.02, 0.05, 0.01, 0.01)
+    flat = T.tqsim_run_ex(5, w.circuit.gates, noise, 300, [300], 9)
+    tree = T.tqsim_run_ex(5, w.circuit.gates, noise, 300, [300, 1, 1, 1], 9)
+    assert np.array_equal(flat.leaf_outcomes, tree.leaf_outcomes)
+
+
+def test_c2_qft15_full_config_leaf_subset():
+    w = load_config("c2_qft15")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    nm = NoiseModel(w.p1, w.p2, w.readout_p01, w.readout_p10)
+    plan0 = T.tqsim_plan_circuit(n, gates, noise, shots, ar)
+    L = plan0.n_levels
+    leaves = [0, 1, 777, 5119, 5120, 10239] + list(np.random.default_rng(0).integers(0, 10240, 6))
+    dumps = [(L - 1, int(l)) for l in leaves[:4]]
+    res = T.tqsim_run_ex(n, gates, noise, shots, ar, w.seed, None, dumps)
+    plan = oracle_plan_of(res.plan)
+    assert plan.arities == [20] + [2] * 9
+    low = OG.lower(gates)
+    for i, l in enumerate(leaves):
+        r, psi, _ = simulate_leaf_flat(n, low, plan, nm, w.seed, int(l), want_states=True)
+        if not r.flagged:
+            assert int(res.leaf_outcomes[l]) == r.outcome
+        if i < len(dumps):
+            assert np.max(np.abs(res.dumps[i] - psi)) <= AMP_TOL
+    assert sum(res.counts.values()) == 10240
+
+
+def test_serial_shards_equal_single_run():
+    torch = pytest.importorskip("torch")
+    w = load_config("c1_qft5")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    h = T.tqsim_create(n, gates, noise, shots, ar)
+    N = h.plan.n_outcomes
+    outs = []
+    for world in (1, 2, 3, 4):
+        acc = torch.zeros(N, dtype=torch.int64, device="cuda")
+        for r in range(world):
+            ws = torch.empty(h.workspace_bytes(r, world), dtype=torch.uint8, device="cuda")
+            o = torch.zeros(N, dtype=torch.int32, device="cuda")
+            h.execute(7, r, world, torch.cuda.current_stream().cuda_stream, ws.data_ptr(),
+                      ws.numel(), o.data_ptr())
+            acc += o.to(torch.int64)
+        outs.append(acc.cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    h.close()
+
+
+def test_device_philox_matches_curand():
+    import ctypes as C
+    import os
+    from tq_testutil import ROOT
+    so = os.path.join(ROOT, "tests", "_curand_ref.so")
+    ref = C.CDLL(so)
+    rng = np.random.default_rng(42)
+    words = rng.integers(0, 2 ** 32, size=(4096, 6), dtype=np.uint64).astype(np.uint32)
+    want = np.zeros((4096, 4), dtype=np.uint32)
+    assert ref.curand_philox_ref(words.ctypes.data_as(C.c_void_p), C.c_uint64(4096),
+                                 want.ctypes.data_as(C.c_void_p)) == 0
+    assert np.array_equal(T.tqsim_debug_philox(words), want)

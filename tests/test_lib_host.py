@@ -1,0 +1,186 @@
+"""Host-side tests of the C-ABI library (no GPU): it loads, exports every
+symbol of include/tqsim.h, and its host logic (lowering, DCP planner, pass
+planner, shard ranges) agrees with the oracle / invariants.  GPU entry points
+must fail loudly without a device (no CPU fallback)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2203_13892_b200.tqsim as T
+from oracle import gates as OG
+from oracle.planner import dcp_plan, fixed_plan
+from oracle.tree import NoiseModel, error_rates
+from tq_testutil import ROOT
+from workloads import config_names, load_config, random_circuit
+
+HAVE_GPU = False
+try:
+    import torch
+    HAVE_GPU = torch.cuda.is_available()
+except Exception:  # pragma: no cover
+    pass
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "tqsim.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tqsim_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = T.lib()
+    names = header_functions()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(T.EXPORTS)
+    assert "sm_100a" in T.tqsim_version()
+
+
+def test_lowering_matches_oracle():
+    for name in config_names():
+        w = load_config(name)
+        mine = T.tqsim_lower_circuit(w.circuit.n_qubits, w.circuit.gates)
+        ref = OG.lower(w.circuit.gates)
+        assert [(k, a, (b if b >= 0 else 0)) for (k, a, b, *_r) in ref] == \
+               [(k, a, (b if k in ("cx", "cz") else 0)) for (k, a, b) in mine]
+
+
+def _oracle_plan(w, arities=None, **kw):
+    low = OG.lower(w.circuit.gates)
+    if arities is not None:
+        return fixed_plan(len(low), arities)
+    rates = error_rates(low, NoiseModel(w.p1, w.p2))
+    return dcp_plan(rates, w.shots, w.circuit.n_qubits, w.copy_cost_gates, **kw)
+
+
+def test_plan_matches_oracle_on_configs():
+    for name in config_names():
+        w = load_config(name)
+        n, gates, noise, shots, ar = T.workload_args(w)
+        p = T.tqsim_plan_circuit(n, gates, noise, shots, ar)
+        o = _oracle_plan(w, ar)
+        assert p.arity_list == o.arities, name
+        assert p.boundary_list == o.boundaries, name
+        assert p.n_outcomes == o.n_outcomes
+        assert p.node_executions == sum(o.instances())
+        assert abs(p.predicted_speedup_nodes - o.node_ratio_speedup()) < 1e-12
+        assert abs(p.first_error_rate - o.first_error_rate) < 1e-15
+
+
+def test_plan_matches_oracle_random_sweep():
+    rng = np.random.default_rng(3)
+    for it in range(60):
+        n = int(rng.integers(1, 12))
+        G = int(rng.integers(1, 400))
+        gates = random_circuit(n, G, rng)
+        if not gates:
+            continue
+        p1 = float(rng.choice([0.0, 1e-4, 1e-3, 1e-2, 0.2]))
+        p2 = float(rng.choice([0.0, 1e-3, 1e-2, 0.3]))
+        shots = int(rng.integers(1, 40000))
+        cc = float(rng.choice([1, 3, 10, 20.4]))
+        topup = int(rng.integers(0, 2))
+        opts = T.default_options(copy_cost_gates=cc, topup=topup)
+        p = T.tqsim_plan_circuit(n, gates, T.noise_arg(p1, p2), shots, None, opts)
+        low = OG.lower(gates)
+        o = dcp_plan(error_rates(low, NoiseModel(p1, p2)), shots, n, cc, topup=topup)
+        assert p.arity_list == o.arities and p.boundary_list == o.boundaries
+
+
+def test_invalid_inputs_rejected():
+    noise = T.noise_arg(1e-3, 1e-2)
+    with pytest.raises(T.TqsimError) as e:
+        T.tqsim_plan_circuit(3, [("cx", 0, 0, 0, 0, 0)], noise, 10)
+    assert e.value.status == 2
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(3, [("h", 3, -1, 0, 0, 0)], noise, 10)
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(3, [("h", 0, -1, 0, 0, 0)], T.noise_arg(1.5, 0), 10)
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(3, [("h", 0, -1, 0, 0, 0)] * 4, noise, 100, arities=[5, 5])
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(3, [("h", 0, -1, 0, 0, 0)] * 2, noise, 8, arities=[2, 2, 2])
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(31, [("h", 0, -1, 0, 0, 0)], noise, 8)
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(3, [("h", 0, -1, 0, 0, 0)], noise, 0)
+    # memory budget too small for the DCP limit -> flat plan; for execution -> ECAPACITY
+    p = T.tqsim_plan_circuit(20, [("h", 0, -1, 0, 0, 0)] * 100, noise, 1000,
+                             options=T.default_options(mem_budget_bytes=16 << 20))
+    assert p.n_levels == 1
+
+
+def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
+    recs = T.tqsim_describe_passes(n, gates, noise, shots, arities, options)
+    plan = T.tqsim_plan_circuit(n, gates, noise, shots, arities, options)
+    low = OG.lower(gates)
+    assert sorted(r.gate for r in recs) == list(range(len(low)))     # every gate exactly once
+    pos = {}
+    for i, r in enumerate(recs):
+        b = plan.boundary_list
+        assert b[r.level] <= r.gate < b[r.level + 1]                 # in its own slice
+        k, a, c = low[r.gate][0], low[r.gate][1], low[r.gate][2]
+        qm = (1 << a) | ((1 << c) if c >= 0 else 0)
+        assert qm & ~r.reg_qubit_mask == 0                           # gate qubits in registers
+        assert r.reg_qubit_mask & ~r.tile_qubit_mask == 0            # registers within the tile
+        assert bin(r.reg_qubit_mask).count("1") == min(4, max(n, 4))
+        pos[r.gate] = (r.level, r.pass_, r.phase, i)
+    # order preserved between any two gates sharing a qubit
+    last = {}
+    for g, (k, a, c, *_r) in enumerate(low):
+        for q in (a, c):
+            if q < 0:
+                continue
+            if q in last:
+                assert pos[last[q]] < pos[g], (last[q], g)
+            last[q] = g
+    return recs, plan
+
+
+def test_pass_plan_invariants_configs():
+    for name in config_names():
+        w = load_config(name)
+        recs, plan = _check_pass_invariants(*T.workload_args(w))
+        assert plan.hbm_passes > 0
+
+
+def test_pass_plan_invariants_random():
+    rng = np.random.default_rng(9)
+    for it in range(40):
+        n = int(rng.integers(1, 22))
+        gates = random_circuit(n, int(rng.integers(1, 200)), rng)
+        if not gates:
+            continue
+        tq = int(rng.choice([0, 4, 7, 9, 12, 13]))
+        _check_pass_invariants(n, gates, T.noise_arg(1e-3, 1e-2), int(rng.integers(1, 3000)),
+                               None, T.default_options(tile_qubits=tq))
+
+
+def test_shard_ranges_partition():
+    w = load_config("c5_hea28")
+    plan = T.tqsim_plan_circuit(*T.workload_args(w))
+    for world in (1, 2, 3, 4, 8, 200):
+        leaves, tops = [], []
+        for r in range(world):
+            t0, t1, l0, l1 = T.tqsim_shard_range(plan, r, world)
+            tops.append((t0, t1))
+            leaves.append((l0, l1))
+        assert tops[0][0] == 0 and tops[-1][1] == plan.arities[0]
+        assert leaves[0][0] == 0 and leaves[-1][1] == plan.n_outcomes
+        assert all(a[1] == b[0] for a, b in zip(leaves, leaves[1:]))
+    with pytest.raises(T.TqsimError):
+        T.tqsim_shard_range(plan, 2, 2)
+
+
+@pytest.mark.skipif(HAVE_GPU, reason="checks the no-GPU failure mode")
+def test_gpu_entry_points_fail_loudly_without_device():
+    w = load_config("c1_qft5")
+    with pytest.raises(T.TqsimError) as e:
+        T.tqsim_create(*T.workload_args(w))
+    assert e.value.status == 4
+    with pytest.raises(T.TqsimError) as e:
+        T.tqsim_run(*T.workload_args(w))
+    assert e.value.status == 4
