@@ -182,6 +182,22 @@ tqsim_status tqsim_describe_passes(const tqsim_circuit* circuit, const tqsim_noi
                                    const tqsim_options* opts, tqsim_op_record* out, uint64_t cap,
                                    uint64_t* n_out);
 
+/* [host] Generate and compile (NVRTC, sm_100a; no GPU needed) every run-time
+ * specialized gate-pass kernel of the plan: one kernel per (level, pass) whose
+ * gate sequence, qubit positions and matrices are compile-time constants.
+ * Outputs may be NULL.  Compile errors -> TQSIM_EINTERNAL with the NVRTC log. */
+tqsim_status tqsim_compile_passes(const tqsim_circuit* circuit, const tqsim_noise_model* noise,
+                                  uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                                  const tqsim_options* opts, uint64_t* n_kernels,
+                                  uint64_t* cubin_bytes, double* seconds);
+
+/* [host] CUDA source of the specialized kernel of (level, pass): up to cap-1
+ * characters + NUL are written to out; *n_out = full length. */
+tqsim_status tqsim_pass_source(const tqsim_circuit* circuit, const tqsim_noise_model* noise,
+                               uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                               const tqsim_options* opts, uint32_t level, uint32_t pass, char* out,
+                               uint64_t cap, uint64_t* n_out);
+
 /* [host] Shard of rank/world: level-0 instances
  * [top_begin, top_end) = [floor(A0*r/W), floor(A0*(r+1)/W)), whose leaves are
  * the contiguous range [leaf_begin, leaf_end). */

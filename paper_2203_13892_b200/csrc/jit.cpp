@@ -1,0 +1,424 @@
+// Run-time specialization of the gate-pass kernels.
+//
+// Each HBM pass of the pass plan becomes one kernel whose gate sequence,
+// tile/register qubit positions and gate matrices are compile-time constants:
+//   * register tile of 16 complex128 amplitudes per thread in named registers;
+//   * CX, SWAP-parts and X gates are register RENAMINGS (no instructions);
+//   * diagonal gates touch only the amplitudes they change; zero matrix
+//     components are skipped (real matrices cost half the FMAs);
+//   * the keyed Pauli error of every gate (codes computed per CTA by the shared
+//     tq_noise_code) is applied right AFTER its gate on a rarely-taken branch
+//     ("noise operators ... after each of the gates");
+//   * the first pass of a node reads its PARENT's state (fused fan-out) or
+//     synthesizes |0..0> (root); passes with one phase need no shared memory.
+// Sources are compiled with NVRTC for sm_100a (one program per pass, in
+// parallel host threads) and cached in-process by source text.
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <unordered_map>
+
+#include "tq_internal.h"
+
+namespace tq {
+
+namespace {
+
+const char* kPrelude =
+#include "jit_prelude.inc"
+    ;
+
+const char* kJitTypes = R"TQ(
+struct __align__(16) tq_d2 { double x, y; };
+struct TqJitArgs {
+  const tq_d2* src; tq_d2* dst; tq_u64 seed; double p1, p2;
+  tq_u64 child_first, parent_first; tq_u32 arity, batch;
+};
+__device__ __forceinline__ void tq_pauli_rt(tq_d2& x, tq_d2& y, tq_u32 p) {
+  if (p == 1u) { const tq_d2 t = x; x = y; y = t; }
+  else if (p == 2u) { const tq_d2 t = x; x.x = y.y; x.y = -y.x; y.x = -t.y; y.y = t.x; }
+  else if (p == 3u) { y.x = -y.x; y.y = -y.y; }
+}
+)TQ";
+
+struct HostJitArgs {   // mirrors TqJitArgs
+  const void* src;
+  void* dst;
+  uint64_t seed;
+  double p1, p2;
+  uint64_t child_first, parent_first;
+  uint32_t arity, batch;
+};
+
+std::string hexd(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%a", v);
+  return b;
+}
+
+uint32_t host_swz(uint32_t i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9) ^ (i >> 12)) & 7u); }
+
+// re/im of  a*x + b*y  with a = (ar, ai), b = (br, bi); zero components skipped.
+std::string lin(double ar, double ai, const std::string& x, double br, double bi,
+                const std::string& y, bool imag) {
+  std::vector<std::pair<double, std::string>> t;
+  if (!imag) {
+    if (ar != 0) t.push_back({ar, x + ".x"});
+    if (ai != 0) t.push_back({-ai, x + ".y"});
+    if (br != 0) t.push_back({br, y + ".x"});
+    if (bi != 0) t.push_back({-bi, y + ".y"});
+  } else {
+    if (ar != 0) t.push_back({ar, x + ".y"});
+    if (ai != 0) t.push_back({ai, x + ".x"});
+    if (br != 0) t.push_back({br, y + ".y"});
+    if (bi != 0) t.push_back({bi, y + ".x"});
+  }
+  if (t.empty()) return "0.0";
+  std::string e = "(" + hexd(t.back().first) + " * " + t.back().second + ")";
+  for (int i = (int)t.size() - 2; i >= 0; --i)
+    e = "fma(" + hexd(t[i].first) + ", " + t[i].second + ", " + e + ")";
+  return e;
+}
+
+struct Gen {
+  std::ostringstream o;
+  int rm[16];   // logical register index -> slot
+  void reset_map() {
+    for (int k = 0; k < 16; ++k) rm[k] = k;
+  }
+  std::string r(int logical) { return "r" + std::to_string(rm[logical]); }
+};
+
+std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
+                     int n, int mode, const std::string& name, int& threads, size_t& smem) {
+  const int K = pd.K, T = 1 << (K - RBITS);
+  const int nph = (int)(pd.phase_end - pd.phase_begin);
+  const int nops = (int)(pd.op_end - pd.op_begin);
+  const bool use_smem = nph > 1;
+  threads = T;
+  smem = use_smem ? (size_t)16 << K : 0;
+  Gen g;
+  std::ostringstream& o = g.o;
+  o << "static __constant__ tq_u32 GIDX[" << std::max(nops, 1) << "] = {";
+  for (int i = 0; i < nops; ++i) o << (i ? "," : "") << pp.ops[pd.op_begin + i].gate << "u";
+  if (!nops) o << "0u";
+  o << "};\nstatic __constant__ unsigned char TWO[" << std::max(nops, 1) << "] = {";
+  for (int i = 0; i < nops; ++i) o << (i ? "," : "") << (int)pp.ops[pd.op_begin + i].two;
+  if (!nops) o << "0";
+  o << "};\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << (K <= 12 ? 2 : 1) << ") "
+    << name << "(const TqJitArgs a) {\n";
+  if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
+  o << "  __shared__ unsigned char codes[" << std::max(nops, 1) << "];\n";
+  o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
+  o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
+  o << "  const tq_u64 inst = a.child_first + s;\n  tq_u32 gtile = 0u;\n";
+  for (int i = 0; i < pd.n_out; ++i)
+    o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << ";\n";
+  o << "  for (tq_u32 i = tid; i < " << nops << "u; i += " << T << "u)\n"
+    << "    codes[i] = (unsigned char)tq_noise_code(GIDX[i], inst, a.seed, TWO[i] ? a.p2 : a.p1, TWO[i] != 0);\n";
+  o << "  tq_d2* __restrict__ dst = a.dst + ((tq_u64)s << " << n << ");\n";
+  if (mode == 1)
+    o << "  const tq_d2* __restrict__ src = a.src + ((inst / a.arity - a.parent_first) << " << n << ");\n";
+  else if (mode == 2)
+    o << "  const tq_d2* src = dst;\n";
+  o << "  tq_d2 r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, r10, r11, r12, r13, r14, r15;\n";
+  o << "  __syncthreads();\n";
+
+  for (int ph = 0; ph < nph; ++ph) {
+    const PhaseDesc& P = pp.phases[pd.phase_begin + ph];
+    const bool first = ph == 0, last = ph == nph - 1;
+    g.reset_map();
+    // thread-dependent part of the tile-local index and of the global index
+    std::ostringstream lb, gb;
+    lb << "0u";
+    gb << "gtile";
+    for (int m = 0; m < K - RBITS; ++m) {
+      lb << " | (((tid >> " << m << ") & 1u) << " << (int)P.tpos[m] << ")";
+      gb << " | (((tid >> " << m << ") & 1u) << " << (int)pd.tile_q[P.tpos[m]] << ")";
+    }
+    uint32_t goff[16], soff[16];
+    for (int k = 0; k < 16; ++k) {
+      uint32_t go = 0, lo = 0;
+      for (int b = 0; b < RBITS; ++b)
+        if (k >> b & 1) {
+          go |= 1u << pd.tile_q[P.rpos[b]];
+          lo |= 1u << P.rpos[b];
+        }
+      goff[k] = go;
+      soff[k] = host_swz(lo);
+    }
+    o << "  { // phase " << ph << "\n";
+    if (first) {
+      o << "    const tq_u32 gb = " << gb.str() << ";\n";
+      for (int k = 0; k < 16; ++k) {
+        if (mode == 0)
+          o << "    r" << k << ".x = (gb + " << goff[k] << "u == 0u) ? 1.0 : 0.0; r" << k << ".y = 0.0;\n";
+        else
+          o << "    r" << k << " = src[gb + " << goff[k] << "u];\n";
+      }
+    } else {
+      o << "    __syncthreads();\n    const tq_u32 sb = tq_swz(" << lb.str() << ");\n";
+      for (int k = 0; k < 16; ++k) o << "    r" << k << " = tile[sb ^ " << soff[k] << "u];\n";
+      o << "    __syncthreads();\n";
+    }
+    for (uint32_t oi = P.op_begin; oi < P.op_end; ++oi) {
+      const OpDesc& od = pp.ops[oi];
+      const LGate& lg = gates[od.gate];
+      const int ci = (int)(oi - pd.op_begin);
+      const int ba = od.ra, bb = od.rb;
+      o << "    // g" << od.gate << "\n";
+      if (od.type == OP_CX) {
+        for (int k = 0; k < 16; ++k)
+          if ((k >> ba & 1) && !(k >> bb & 1)) std::swap(g.rm[k], g.rm[k | 1 << bb]);
+      } else if (od.type == OP_CZ) {
+        for (int k = 0; k < 16; ++k)
+          if ((k >> ba & 1) && (k >> bb & 1))
+            o << "    " << g.r(k) << ".x = -" << g.r(k) << ".x; " << g.r(k) << ".y = -" << g.r(k) << ".y;\n";
+      } else {
+        const double* m = lg.m;
+        const bool is_x = m[0] == 0 && m[1] == 0 && m[2] == 1 && m[3] == 0 && m[4] == 1 && m[5] == 0 &&
+                          m[6] == 0 && m[7] == 0;
+        if (is_x) {
+          for (int k = 0; k < 16; ++k)
+            if (!(k >> ba & 1)) std::swap(g.rm[k], g.rm[k | 1 << ba]);
+        } else if (od.type == OP_DIAG) {
+          for (int k = 0; k < 16; ++k) {
+            const bool one = (k >> ba) & 1;
+            const double dr = one ? m[6] : m[0], di = one ? m[7] : m[1];
+            if (dr == 1.0 && di == 0.0) continue;
+            const std::string v = g.r(k);
+            o << "    { const tq_d2 x = " << v << "; " << v << ".x = " << lin(dr, di, "x", 0, 0, "x", false)
+              << "; " << v << ".y = " << lin(dr, di, "x", 0, 0, "x", true) << "; }\n";
+          }
+        } else {
+          for (int k = 0; k < 16; ++k) {
+            if (k >> ba & 1) continue;
+            const std::string va = g.r(k), vb = g.r(k | 1 << ba);
+            o << "    { const tq_d2 x = " << va << ", y = " << vb << ";\n";
+            o << "      " << va << ".x = " << lin(m[0], m[1], "x", m[2], m[3], "y", false) << ";\n";
+            o << "      " << va << ".y = " << lin(m[0], m[1], "x", m[2], m[3], "y", true) << ";\n";
+            o << "      " << vb << ".x = " << lin(m[4], m[5], "x", m[6], m[7], "y", false) << ";\n";
+            o << "      " << vb << ".y = " << lin(m[4], m[5], "x", m[6], m[7], "y", true) << "; }\n";
+          }
+        }
+      }
+      // keyed Pauli error after the gate (rare branch)
+      o << "    { const tq_u32 c = codes[" << ci << "];\n      if (__builtin_expect(c != 0u, 0)) {\n";
+      if (od.two) {
+        o << "        const tq_u32 pa = c >> 2, pb = c & 3u;\n";
+        for (int k = 0; k < 16; ++k)
+          if (!(k >> ba & 1)) o << "        tq_pauli_rt(" << g.r(k) << ", " << g.r(k | 1 << ba) << ", pa);\n";
+        for (int k = 0; k < 16; ++k)
+          if (!(k >> bb & 1)) o << "        tq_pauli_rt(" << g.r(k) << ", " << g.r(k | 1 << bb) << ", pb);\n";
+      } else {
+        for (int k = 0; k < 16; ++k)
+          if (!(k >> ba & 1)) o << "        tq_pauli_rt(" << g.r(k) << ", " << g.r(k | 1 << ba) << ", c);\n";
+      }
+      o << "      } }\n";
+    }
+    if (last) {
+      o << "    const tq_u32 gbs = " << gb.str() << ";\n";
+      for (int k = 0; k < 16; ++k) o << "    dst[gbs + " << goff[k] << "u] = " << g.r(k) << ";\n";
+    } else {
+      o << "    const tq_u32 sbs = tq_swz(" << lb.str() << ");\n";
+      for (int k = 0; k < 16; ++k) o << "    tile[sbs ^ " << soff[k] << "u] = " << g.r(k) << ";\n";
+    }
+    o << "  }\n";
+  }
+  o << "}\n";
+  return o.str();
+}
+
+struct CompiledKernel {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t fn = nullptr;
+};
+
+std::mutex g_cache_mu;
+std::unordered_map<std::string, CompiledKernel> g_cache;   // full source -> kernel
+std::atomic<uint64_t> g_compiles{0};
+
+std::string compile_to_cubin(const std::string& src, const std::string& name) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) !=
+      NVRTC_SUCCESS)
+    throw Error{TQSIM_EINTERNAL, "nvrtcCreateProgram failed"};
+  // TQSIM_JIT_LINEINFO=1 adds line info for ncu source views (slower compiles, bigger cubins)
+  static const bool lineinfo = [] {
+    const char* e = std::getenv("TQSIM_JIT_LINEINFO");
+    return e && e[0] == '1';
+  }();
+  const char* opts[] = {"-arch=sm_100a", "-default-device", "-std=c++17", "-lineinfo"};
+  const nvrtcResult r = nvrtcCompileProgram(prog, lineinfo ? 4 : 3, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t ls = 0;
+    nvrtcGetProgramLogSize(prog, &ls);
+    std::string log(ls, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    throw Error{TQSIM_EINTERNAL, "NVRTC failed for " + name + ": " + log.substr(0, 2000)};
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::string cubin(n, '\0');
+  nvrtcGetCUBIN(prog, &cubin[0]);
+  nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+}  // namespace
+
+std::string jit_source(const PassPlan& pp, const std::vector<LGate>& gates, size_t level,
+                       size_t pass, const std::string& name) {
+  int th;
+  size_t sm;
+  const int mode = pass > 0 ? 2 : (level == 0 ? 0 : 1);
+  return std::string(kPrelude) + kJitTypes +
+         gen_pass(pp.levels[level][pass], pp, gates, pp.n_sim, mode, name, th, sm);
+}
+
+uint64_t jit_compile_count() { return g_compiles.load(); }
+
+void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint64_t* n_kernels,
+                      uint64_t* cubin_bytes) {
+  std::vector<std::string> srcs, names;
+  for (size_t d = 0; d < pp.levels.size(); ++d)
+    for (size_t p = 0; p < pp.levels[d].size(); ++p) {
+      names.push_back("tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p));
+      srcs.push_back(jit_source(pp, gates, d, p, names.back()));
+    }
+  std::vector<std::string> errs(srcs.size());
+  std::vector<size_t> sizes(srcs.size(), 0);
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> pool;
+  const size_t nt = std::min<size_t>(srcs.size(), std::max(1u, std::thread::hardware_concurrency()));
+  for (size_t t = 0; t < nt; ++t)
+    pool.emplace_back([&] {
+      for (;;) {
+        const size_t i = next.fetch_add(1);
+        if (i >= srcs.size()) return;
+        try {
+          sizes[i] = compile_to_cubin(srcs[i], names[i]).size();
+        } catch (const Error& e) {
+          errs[i] = e.msg;
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  uint64_t tot = 0;
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    if (!errs[i].empty()) throw Error{TQSIM_EINTERNAL, errs[i]};
+    tot += sizes[i];
+  }
+  if (n_kernels) *n_kernels = srcs.size();
+  if (cubin_bytes) *cubin_bytes = tot;
+}
+
+std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vector<LGate>& gates,
+                                            double* compile_seconds) {
+  struct Job {
+    size_t d, p;
+    std::string name, src;
+    int threads;
+    size_t smem;
+    std::string cubin;
+    std::string err;
+  };
+  std::vector<Job> jobs;
+  std::vector<std::vector<JitPass>> out(pp.levels.size());
+  for (size_t d = 0; d < pp.levels.size(); ++d) {
+    out[d].resize(pp.levels[d].size());
+    for (size_t p = 0; p < pp.levels[d].size(); ++p) {
+      Job j;
+      j.d = d;
+      j.p = p;
+      j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p);
+      const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
+      std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
+                                  j.smem);
+      j.src = std::string(kPrelude) + kJitTypes + body;
+      jobs.push_back(std::move(j));
+    }
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<size_t> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (size_t i = 0; i < jobs.size(); ++i)
+      if (!g_cache.count(jobs[i].src)) todo.push_back(i);
+  }
+  if (!todo.empty()) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nthreads = std::min<size_t>(todo.size(), hw);
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> pool;
+    for (size_t t = 0; t < nthreads; ++t)
+      pool.emplace_back([&] {
+        for (;;) {
+          const size_t i = next.fetch_add(1);
+          if (i >= todo.size()) return;
+          Job& j = jobs[todo[i]];
+          try {
+            j.cubin = compile_to_cubin(j.src, j.name);
+          } catch (const Error& e) {
+            j.err = e.msg;
+          }
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (size_t i : todo)
+      if (!jobs[i].err.empty()) throw Error{TQSIM_EINTERNAL, jobs[i].err};
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (size_t i : todo) {
+      Job& j = jobs[i];
+      if (g_cache.count(j.src)) continue;
+      CompiledKernel ck;
+      cudaError_t e = cudaLibraryLoadData(&ck.lib, j.cubin.data(), nullptr, nullptr, 0, nullptr,
+                                          nullptr, 0);
+      if (e != cudaSuccess) throw Error{TQSIM_ECUDA, std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e)};
+      e = cudaLibraryGetKernel(&ck.fn, ck.lib, j.name.c_str());
+      if (e != cudaSuccess) throw Error{TQSIM_ECUDA, std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e)};
+      if (j.smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(reinterpret_cast<const void*>(ck.fn),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)j.smem);
+        if (e != cudaSuccess) throw Error{TQSIM_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)};
+      }
+      g_cache[j.src] = ck;
+      g_compiles++;
+    }
+  }
+  if (compile_seconds)
+    *compile_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (Job& j : jobs) {
+    const CompiledKernel& ck = g_cache.at(j.src);
+    out[j.d][j.p] = JitPass{reinterpret_cast<void*>(ck.fn), j.threads, j.smem};
+  }
+  return out;
+}
+
+
+
+int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
+  HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
+                L.arity ? L.arity : 1u, L.batch};
+  const uint64_t grid = (uint64_t)L.batch << pd.n_out;
+  if (grid == 0) return 0;
+  if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;
+  void* args[] = {&a};
+  return (int)cudaLaunchKernel(jp.kernel, dim3((unsigned)grid), dim3(jp.threads), args, jp.smem,
+                               static_cast<cudaStream_t>(stream));
+}
+
+}  // namespace tq

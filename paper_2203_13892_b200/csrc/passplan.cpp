@@ -28,7 +28,7 @@ inline int popc(uint64_t v) { return __builtin_popcountll(v); }
 template <class MaskFn>
 std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
     const std::vector<uint32_t>& order, const std::vector<LGate>& gates, MaskFn need_mask,
-    int cap) {
+    int cap, size_t max_items = ~size_t(0)) {
   std::vector<std::pair<std::vector<uint32_t>, uint64_t>> groups;
   std::vector<uint32_t> remaining = order;
   while (!remaining.empty()) {
@@ -36,7 +36,7 @@ std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
     std::vector<uint32_t> in, deferred;
     for (uint32_t g : remaining) {
       const uint64_t qm = qmask(gates[g]);
-      if (qm & blocked) {
+      if ((qm & blocked) || in.size() >= max_items) {
         deferred.push_back(g);
         blocked |= qm;
         continue;
@@ -81,7 +81,8 @@ PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, cons
     std::vector<uint32_t> order;
     for (uint64_t g = plan.bounds[d]; g < plan.bounds[d + 1]; ++g) order.push_back((uint32_t)g);
     auto passes = group_gates(order, gates,
-                              [&](uint32_t g) { return qmask(gates[g]) & ~low_mask; }, hcap);
+                              [&](uint32_t g) { return qmask(gates[g]) & ~low_mask; }, hcap,
+                              MAX_PASS_OPS);
     std::vector<PassDesc> lvl;
     for (size_t pi = 0; pi < passes.size(); ++pi) {
       uint64_t H = passes[pi].second;

@@ -28,10 +28,8 @@ struct tqsim_handle {
   tq::PassPlan pp;
   tqsim_plan cplan{};
   std::vector<uint64_t> inst;
-  tq::DeviceTables dt;
-  void* d_ops = nullptr;
-  void* d_phases = nullptr;
-  void* d_mats = nullptr;
+  std::vector<std::vector<tq::JitPass>> jit;   // specialized pass kernels [level][pass]
+  double compile_s = 0.0;
   uint8_t* d_two = nullptr;
   tqsim_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
@@ -227,7 +225,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       pl.p1 = h->noise.p1;
       pl.p2 = h->noise.p2;
       mark(x, 0);
-      ck(launch_pass(passes[p], n, h->dt, pl, x.st), "gate pass launch");
+      ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
       mark(x, 0);
       h->stats.kernel_launches++;
       h->stats.pass_launches++;
@@ -281,26 +279,12 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     fill_plan(h->plan, c->n_qubits, h->gates.size(), h->pp.passes_total(h->inst), &h->cplan);
     if (need_gpu) {
       require_device();
-      std::vector<double> mats(h->gates.size() * 8);
       std::vector<uint8_t> two(h->gates.size());
-      for (size_t g = 0; g < h->gates.size(); ++g) {
-        std::memcpy(&mats[g * 8], h->gates[g].m, 8 * sizeof(double));
-        two[g] = h->gates[g].two ? 1 : 0;
-      }
-      const size_t ob = h->pp.ops.size() * sizeof(OpDesc);
-      const size_t pb = h->pp.phases.size() * sizeof(PhaseDesc);
-      ckc(cudaMalloc(&h->d_ops, std::max<size_t>(ob, 16)), "cudaMalloc ops");
-      ckc(cudaMalloc(&h->d_phases, std::max<size_t>(pb, 16)), "cudaMalloc phases");
-      ckc(cudaMalloc(&h->d_mats, mats.size() * sizeof(double)), "cudaMalloc mats");
+      for (size_t g = 0; g < h->gates.size(); ++g) two[g] = h->gates[g].two ? 1 : 0;
       ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_two), two.size()), "cudaMalloc two");
-      ckc(cudaMemcpy(h->d_ops, h->pp.ops.data(), ob, cudaMemcpyHostToDevice), "upload ops");
-      ckc(cudaMemcpy(h->d_phases, h->pp.phases.data(), pb, cudaMemcpyHostToDevice), "upload phases");
-      ckc(cudaMemcpy(h->d_mats, mats.data(), mats.size() * sizeof(double), cudaMemcpyHostToDevice),
-          "upload mats");
       ckc(cudaMemcpy(h->d_two, two.data(), two.size(), cudaMemcpyHostToDevice), "upload two");
-      h->dt.ops = static_cast<const OpDesc*>(h->d_ops);
-      h->dt.phases = static_cast<const PhaseDesc*>(h->d_phases);
-      h->dt.mats = static_cast<const double*>(h->d_mats);
+      // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
+      h->jit = jit_build(h->pp, h->gates, &h->compile_s);
     }
   } catch (...) {
     tqsim_destroy(h);
@@ -436,6 +420,50 @@ tqsim_status tqsim_describe_passes(const tqsim_circuit* c, const tqsim_noise_mod
   });
 }
 
+tqsim_status tqsim_compile_passes(const tqsim_circuit* c, const tqsim_noise_model* nm,
+                                  uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                                  const tqsim_options* o, uint64_t* n_kernels,
+                                  uint64_t* cubin_bytes, double* seconds) {
+  return guarded([&] {
+    tqsim_handle* h = create_handle(c, nm, n_shots, arities, n_levels, o, false);
+    const auto t0 = std::chrono::steady_clock::now();
+    try {
+      jit_compile_only(h->pp, h->gates, n_kernels, cubin_bytes);
+    } catch (...) {
+      tqsim_destroy(h);
+      throw;
+    }
+    if (seconds)
+      *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    tqsim_destroy(h);
+  });
+}
+
+tqsim_status tqsim_pass_source(const tqsim_circuit* c, const tqsim_noise_model* nm,
+                               uint64_t n_shots, const uint32_t* arities, uint32_t n_levels,
+                               const tqsim_options* o, uint32_t level, uint32_t pass, char* out,
+                               uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    tqsim_handle* h = create_handle(c, nm, n_shots, arities, n_levels, o, false);
+    std::string s;
+    try {
+      if (level >= h->pp.levels.size() || pass >= h->pp.levels[level].size())
+        throw Error{TQSIM_EINVAL, "level/pass out of range"};
+      s = jit_source(h->pp, h->gates, level, pass, "tq_pass");
+    } catch (...) {
+      tqsim_destroy(h);
+      throw;
+    }
+    tqsim_destroy(h);
+    if (n_out) *n_out = s.size();
+    if (out && cap) {
+      const size_t k = std::min<size_t>(cap - 1, s.size());
+      std::memcpy(out, s.data(), k);
+      out[k] = '\0';
+    }
+  });
+}
+
 tqsim_status tqsim_shard_range(const tqsim_plan* p, uint32_t rank, uint32_t world,
                                uint64_t* top_begin, uint64_t* top_end, uint64_t* leaf_begin,
                                uint64_t* leaf_end) {
@@ -477,9 +505,6 @@ tqsim_status tqsim_get_stats(const tqsim_handle* h, tqsim_stats* out) {
 
 void tqsim_destroy(tqsim_handle* h) {
   if (!h) return;
-  if (h->d_ops) cudaFree(h->d_ops);
-  if (h->d_phases) cudaFree(h->d_phases);
-  if (h->d_mats) cudaFree(h->d_mats);
   if (h->d_two) cudaFree(h->d_two);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   delete h;

@@ -54,6 +54,7 @@ std::vector<uint64_t> instances(const Plan& p);   // Eq.2, per level
 constexpr int RBITS = 4;        // amplitudes per thread = 2^RBITS (register-resident qubits)
 constexpr int MAX_K = 13;       // max tile qubits per HBM pass (2^13 * 16 B = 128 KiB smem)
 constexpr int LOW_Q = 5;        // qubits 0..4 are in every tile (512 B contiguous segments)
+constexpr int MAX_PASS_OPS = 192; // gates per pass kernel (code size / shared codes bound)
 
 struct OpDesc {                 // 8 bytes, device-readable
   uint8_t type;                 // OpType
@@ -104,14 +105,6 @@ struct PassLaunch {
   double p1, p2;
 };
 
-struct DeviceTables {
-  const OpDesc* ops = nullptr;
-  const PhaseDesc* phases = nullptr;
-  const double* mats = nullptr;  // 8 doubles per lowered gate
-};
-
-int launch_pass(const PassDesc& pd, int n_sim, const DeviceTables& t, const PassLaunch& L,
-                void* stream);
 int launch_chunk_sums(const void* states, uint32_t batch, int n_sim, int chunk_log2, double* sums,
                       void* stream);
 int launch_sample(const void* states, const double* sums, uint32_t batch, int n_sim, int n_user,
@@ -122,5 +115,20 @@ int launch_noise_table(const uint8_t* d_two, uint32_t slice_begin, uint32_t slic
                        uint64_t inst_begin, uint64_t count, uint64_t seed, double p1, double p2,
                        uint8_t* d_out);
 const char* cuda_error_string(int code);
+
+// ---------------------------------------------------------------- JIT pass kernels (jit.cpp)
+struct JitPass {
+  void* kernel = nullptr;   // cudaKernel_t
+  int threads = 0;
+  size_t smem = 0;
+};
+std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vector<LGate>& gates,
+                                            double* compile_seconds);
+void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint64_t* n_kernels,
+                      uint64_t* cubin_bytes);
+std::string jit_source(const PassPlan& pp, const std::vector<LGate>& gates, size_t level,
+                       size_t pass, const std::string& name);
+uint64_t jit_compile_count();
+int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream);
 
 }  // namespace tq

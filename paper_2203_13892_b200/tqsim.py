@@ -111,6 +111,12 @@ _SIGS = {
     "tqsim_describe_passes": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
                                         _P(C.c_uint32), C.c_uint32, _P(tqsim_options),
                                         _P(tqsim_op_record), C.c_uint64, _P(C.c_uint64)]),
+    "tqsim_compile_passes": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
+                                       _P(C.c_uint32), C.c_uint32, _P(tqsim_options),
+                                       _P(C.c_uint64), _P(C.c_uint64), _P(C.c_double)]),
+    "tqsim_pass_source": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
+                                    _P(C.c_uint32), C.c_uint32, _P(tqsim_options), C.c_uint32,
+                                    C.c_uint32, C.c_char_p, C.c_uint64, _P(C.c_uint64)]),
     "tqsim_shard_range": (C.c_int, [_P(tqsim_plan), C.c_uint32, C.c_uint32, _P(C.c_uint64),
                                     _P(C.c_uint64), _P(C.c_uint64), _P(C.c_uint64)]),
     "tqsim_create": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
@@ -225,6 +231,31 @@ def tqsim_describe_passes(n_qubits, gates, noise, n_shots, arities=None, options
     _check(lib().tqsim_describe_passes(C.byref(ca.c), C.byref(noise), int(n_shots), a, L, opt,
                                        out, n.value, C.byref(n)))
     return [out[i] for i in range(n.value)]
+
+
+def tqsim_compile_passes(n_qubits, gates, noise, n_shots, arities=None, options=None):
+    """Compile every specialized pass kernel (host-only NVRTC): (kernels, cubin bytes, seconds)."""
+    ca = CircuitArg(n_qubits, gates)
+    a, L = _arities(arities)
+    k, b, s = C.c_uint64(), C.c_uint64(), C.c_double()
+    _check(lib().tqsim_compile_passes(C.byref(ca.c), C.byref(noise), int(n_shots), a, L,
+                                      C.byref(options) if options else None, C.byref(k),
+                                      C.byref(b), C.byref(s)))
+    return int(k.value), int(b.value), float(s.value)
+
+
+def tqsim_pass_source(n_qubits, gates, noise, n_shots, arities=None, options=None, level=0,
+                      pass_=0) -> str:
+    ca = CircuitArg(n_qubits, gates)
+    a, L = _arities(arities)
+    n = C.c_uint64()
+    opt = C.byref(options) if options else None
+    _check(lib().tqsim_pass_source(C.byref(ca.c), C.byref(noise), int(n_shots), a, L, opt, level,
+                                   pass_, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().tqsim_pass_source(C.byref(ca.c), C.byref(noise), int(n_shots), a, L, opt, level,
+                                   pass_, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
 
 
 def tqsim_shard_range(plan: tqsim_plan, rank: int, world: int) -> Tuple[int, int, int, int]:
