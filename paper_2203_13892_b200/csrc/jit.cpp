@@ -116,7 +116,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   for (int i = 0; i < nops; ++i) o << (i ? "," : "") << (int)pp.ops[pd.op_begin + i].two;
   if (!nops) o << "0";
   o << "};\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << (K <= 12 ? 2 : 1) << ") "
+  // 16 resident warps per SM (128 registers / thread), as many independent CTAs as fit
+  const int minb = K >= 13 ? 1
+                           : std::max(1, std::min(512 / T, (int)((227 * 1024) / ((16 << K) + 1024))));
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << std::min(minb, 32) << ") "
     << name << "(const TqJitArgs a) {\n";
   if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
   o << "  __shared__ unsigned char codes[" << std::max(nops, 1) << "];\n";
