@@ -137,7 +137,13 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const tq_d2* src = dst;\n";
   o << "  tq_d2 r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, r10, r11, r12, r13, r14, r15;\n";
   o << "  __syncthreads();\n";
-
+  // Error-free instances (the common case: no Pauli drawn for any gate of the
+  // pass) run a path without any per-gate error check; the others run the same
+  // pass with the keyed Pauli applied after its gate.  Uniform per CTA.
+  o << "  int any_err = 0;\n";
+  o << "  for (tq_u32 i = tid; i < " << nops << "u; i += " << T << "u) any_err |= codes[i] != 0;\n";
+  o << "  if (!__syncthreads_or(any_err)) {\n";
+  auto emit_phases = [&](bool with_errors) {
   for (int ph = 0; ph < nph; ++ph) {
     const PhaseDesc& P = pp.phases[pd.phase_begin + ph];
     const bool first = ph == 0, last = ph == nph - 1;
@@ -216,8 +222,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           }
         }
       }
+      if (!with_errors) continue;
       // keyed Pauli error after the gate (rare branch)
-      o << "    { const tq_u32 c = codes[" << ci << "];\n      if (__builtin_expect(c != 0u, 0)) {\n";
+      o << "    { const tq_u32 c = codes[" << ci << "];\n      if (c != 0u) {\n";
       if (od.two) {
         o << "        const tq_u32 pa = c >> 2, pb = c & 3u;\n";
         for (int k = 0; k < 16; ++k)
@@ -239,6 +246,11 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     }
     o << "  }\n";
   }
+  };
+  emit_phases(false);
+  o << "  } else {\n";
+  emit_phases(true);
+  o << "  }\n";
   o << "}\n";
   return o.str();
 }
