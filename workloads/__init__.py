@@ -9,5 +9,5 @@ consume these descriptions independently.
 from .generators import (  # noqa: F401
     GATE_KINDS, Circuit, Workload, qft_gates, basis_prep_gates, brickwork_gates,
     random_3_regular_edges, qaoa_gates, hea_gates, ghz_gates, load_config,
-    config_names, make_config, random_circuit,
+    config_names, make_config, make_variant, monomial_brickwork_gates, random_circuit,
 )

@@ -220,6 +220,46 @@ def make_config(name: str) -> Workload:
     raise KeyError(name)
 
 
+MONOMIAL_1Q = ("x", "y", "z", "s", "sdg", "t", "tdg", "p", "rz")
+
+
+def monomial_brickwork_gates(n: int, layers: int, rng: np.random.Generator) -> List[Gate]:
+    """C3-shaped brickwork whose 1q gates are monomial matrices (one non-zero per
+    row/column), so every noisy trajectory of |0..0> stays 1-sparse."""
+    out: List[Gate] = []
+    for layer in range(layers):
+        for q in range(n):
+            k = MONOMIAL_1Q[int(rng.integers(0, len(MONOMIAL_1Q)))]
+            out.append(g1(k, q, float(rng.uniform(0.0, 2 * math.pi))))
+        start = 0 if layer % 2 == 0 else 1
+        for a in range(start, n - 1, 2):
+            out.append(g2("cx", a, a + 1))
+    return out
+
+
+def make_variant(name: str) -> Workload:
+    """Structured full-size variants of C3/C4/C5 (SURVEY §8(c) "What pins each
+    part"): same widths, gate counts, noise and shots as the configs, with the
+    structure changed so the oracle can predict every leaf at full size."""
+    if name == "c3_brick20_monomial":
+        base = make_config("c3_brick20")
+        gates = monomial_brickwork_gates(20, 20, np.random.default_rng(1))
+        return Workload(name, Circuit(20, gates), base.p1, base.p2, base.readout_p01,
+                        base.readout_p10, base.shots, None, 0)
+    if name == "c4_qaoa24_beta0":
+        base = make_config("c4_qaoa24")
+        m = base.meta
+        gates = qaoa_gates(24, m["edges"], m["gammas"], [0.0, 0.0])
+        return Workload(name, Circuit(24, gates), base.p1, base.p2, 0.0, 0.0, base.shots, None, 0,
+                        meta={"edges": m["edges"], "gammas": m["gammas"], "betas": [0.0, 0.0]})
+    if name == "c5_hea28_ry0":
+        base = make_config("c5_hea28")
+        gates = hea_gates(28, 4, np.zeros((4, 28)))
+        return Workload(name, Circuit(28, gates), base.p1, base.p2, base.readout_p01,
+                        base.readout_p10, base.shots, None, 0)
+    raise KeyError(name)
+
+
 def config_names() -> List[str]:
     return ["c1_qft5", "c2_qft15", "c3_brick20", "c4_qaoa24", "c5_hea28"]
 
