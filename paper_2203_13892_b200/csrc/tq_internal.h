@@ -53,7 +53,7 @@ std::vector<uint64_t> instances(const Plan& p);   // Eq.2, per level
 // ---------------------------------------------------------------- pass plan
 constexpr int RBITS = 4;        // amplitudes per thread = 2^RBITS (register-resident qubits)
 constexpr int MAX_K = 13;       // max tile qubits per HBM pass (2^13 * 16 B = 128 KiB smem)
-constexpr int LOW_Q = 5;        // qubits 0..4 are in every tile (512 B contiguous segments)
+constexpr int LOW_Q = 3;        // qubits 0..4 are in every tile (512 B contiguous segments)
 constexpr int MAX_PASS_OPS = 192; // gates per pass kernel (code size / shared codes bound)
 
 struct OpDesc {                 // 8 bytes, device-readable
