@@ -43,6 +43,7 @@ struct __align__(16) tq_d2 { double x, y; };
 struct TqJitArgs {
   const tq_d2* src; tq_d2* dst; tq_u64 seed; double p1, p2;
   tq_u64 child_first, parent_first; tq_u32 arity, batch;
+  const double* __restrict__ cm;   // gate-matrix coefficients of this pass (run-time data)
 };
 __device__ __forceinline__ void tq_pauli_rt(tq_d2& x, tq_d2& y, tq_u32 p) {
   if (p == 1u) { const tq_d2 t = x; x = y; y = t; }
@@ -58,6 +59,7 @@ struct HostJitArgs {   // mirrors TqJitArgs
   double p1, p2;
   uint64_t child_first, parent_first;
   uint32_t arity, batch;
+  const double* cm;
 };
 
 std::string hexd(double v) {
@@ -67,6 +69,45 @@ std::string hexd(double v) {
 }
 
 uint32_t host_swz(uint32_t i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9) ^ (i >> 12)) & 7u); }
+
+// Gate-matrix coefficients are RUN-TIME data (a per-pass global table read once
+// per gate into registers with __ldg), so the generated source -- and the
+// compiled-kernel cache key -- depends only on the circuit's structure (gate
+// kinds, qubits, which matrix components are 0 or +-1), not on its angles.
+struct ConstPool {
+  std::vector<double> vals;
+  std::map<uint64_t, int> index;
+  std::map<uint64_t, std::string> local;   // per gate: value bits -> register name
+  std::ostringstream decl;
+  int nlocal = 0;
+  void begin_op() {
+    local.clear();
+    decl.str("");
+    nlocal = 0;
+  }
+  std::string ref(double v) {
+    if (v == 1.0) return "1.0";
+    if (v == -1.0) return "-1.0";
+    uint64_t bits;
+    std::memcpy(&bits, &v, 8);
+    auto lt = local.find(bits);
+    if (lt != local.end()) return lt->second;
+    auto it = index.find(bits);
+    int k;
+    if (it == index.end()) {
+      k = (int)vals.size();
+      vals.push_back(v);
+      index[bits] = k;
+    } else {
+      k = it->second;
+    }
+    const std::string name = "q" + std::to_string(nlocal++);
+    decl << "      const double " << name << " = __ldg(a.cm + " << k << ");\n";
+    local[bits] = name;
+    return name;
+  }
+};
+thread_local ConstPool* g_pool = nullptr;   // set while one kernel is generated
 
 // re/im of  a*x + b*y  with a = (ar, ai), b = (br, bi); zero components skipped.
 std::string lin(double ar, double ai, const std::string& x, double br, double bi,
@@ -84,9 +125,9 @@ std::string lin(double ar, double ai, const std::string& x, double br, double bi
     if (bi != 0) t.push_back({bi, y + ".x"});
   }
   if (t.empty()) return "0.0";
-  std::string e = "(" + hexd(t.back().first) + " * " + t.back().second + ")";
+  std::string e = "(" + g_pool->ref(t.back().first) + " * " + t.back().second + ")";
   for (int i = (int)t.size() - 2; i >= 0; --i)
-    e = "fma(" + hexd(t[i].first) + ", " + t[i].second + ", " + e + ")";
+    e = "fma(" + g_pool->ref(t[i].first) + ", " + t[i].second + ", " + e + ")";
   return e;
 }
 
@@ -100,7 +141,8 @@ struct Gen {
 };
 
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
-                     int n, int mode, const std::string& name, int& threads, size_t& smem) {
+                     int n, int mode, const std::string& name, int& threads, size_t& smem,
+                     std::vector<double>& coefs) {
   const int K = pd.K, T = 1 << (K - RBITS);
   const int nph = (int)(pd.phase_end - pd.phase_begin);
   const int nops = (int)(pd.op_end - pd.op_begin);
@@ -109,6 +151,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   smem = use_smem ? (size_t)16 << K : 0;
   Gen g;
   std::ostringstream& o = g.o;
+  ConstPool pool;
+  g_pool = &pool;
   o << "static __constant__ tq_u32 GIDX[" << std::max(nops, 1) << "] = {";
   for (int i = 0; i < nops; ++i) o << (i ? "," : "") << pp.ops[pd.op_begin + i].gate << "u";
   if (!nops) o << "0u";
@@ -202,24 +246,30 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           for (int k = 0; k < 16; ++k)
             if (!(k >> ba & 1)) std::swap(g.rm[k], g.rm[k | 1 << ba]);
         } else if (od.type == OP_DIAG) {
+          std::ostringstream oo;
+          pool.begin_op();
           for (int k = 0; k < 16; ++k) {
             const bool one = (k >> ba) & 1;
             const double dr = one ? m[6] : m[0], di = one ? m[7] : m[1];
             if (dr == 1.0 && di == 0.0) continue;
             const std::string v = g.r(k);
-            o << "    { const tq_d2 x = " << v << "; " << v << ".x = " << lin(dr, di, "x", 0, 0, "x", false)
-              << "; " << v << ".y = " << lin(dr, di, "x", 0, 0, "x", true) << "; }\n";
+            oo << "      { const tq_d2 x = " << v << "; " << v << ".x = " << lin(dr, di, "x", 0, 0, "x", false)
+               << "; " << v << ".y = " << lin(dr, di, "x", 0, 0, "x", true) << "; }\n";
           }
+          o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
         } else {
+          std::ostringstream oo;
+          pool.begin_op();
           for (int k = 0; k < 16; ++k) {
             if (k >> ba & 1) continue;
             const std::string va = g.r(k), vb = g.r(k | 1 << ba);
-            o << "    { const tq_d2 x = " << va << ", y = " << vb << ";\n";
-            o << "      " << va << ".x = " << lin(m[0], m[1], "x", m[2], m[3], "y", false) << ";\n";
-            o << "      " << va << ".y = " << lin(m[0], m[1], "x", m[2], m[3], "y", true) << ";\n";
-            o << "      " << vb << ".x = " << lin(m[4], m[5], "x", m[6], m[7], "y", false) << ";\n";
-            o << "      " << vb << ".y = " << lin(m[4], m[5], "x", m[6], m[7], "y", true) << "; }\n";
+            oo << "      { const tq_d2 x = " << va << ", y = " << vb << ";\n";
+            oo << "        " << va << ".x = " << lin(m[0], m[1], "x", m[2], m[3], "y", false) << ";\n";
+            oo << "        " << va << ".y = " << lin(m[0], m[1], "x", m[2], m[3], "y", true) << ";\n";
+            oo << "        " << vb << ".x = " << lin(m[4], m[5], "x", m[6], m[7], "y", false) << ";\n";
+            oo << "        " << vb << ".y = " << lin(m[4], m[5], "x", m[6], m[7], "y", true) << "; }\n";
           }
+          o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
         }
       }
       if (!with_errors) continue;
@@ -252,6 +302,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   emit_phases(true);
   o << "  }\n";
   o << "}\n";
+  g_pool = nullptr;
+  coefs = pool.vals;
   return o.str();
 }
 
@@ -298,9 +350,10 @@ std::string jit_source(const PassPlan& pp, const std::vector<LGate>& gates, size
                        size_t pass, const std::string& name) {
   int th;
   size_t sm;
+  std::vector<double> cf;
   const int mode = pass > 0 ? 2 : (level == 0 ? 0 : 1);
   return std::string(kPrelude) + kJitTypes +
-         gen_pass(pp.levels[level][pass], pp, gates, pp.n_sim, mode, name, th, sm);
+         gen_pass(pp.levels[level][pass], pp, gates, pp.n_sim, mode, name, th, sm, cf);
 }
 
 uint64_t jit_compile_count() { return g_compiles.load(); }
@@ -349,6 +402,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
     size_t smem;
     std::string cubin;
     std::string err;
+    std::vector<double> coefs;
   };
   std::vector<Job> jobs;
   std::vector<std::vector<JitPass>> out(pp.levels.size());
@@ -361,7 +415,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
       j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p);
       const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
       std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
-                                  j.smem);
+                                  j.smem, j.coefs);
       j.src = std::string(kPrelude) + kJitTypes + body;
       jobs.push_back(std::move(j));
     }
@@ -418,7 +472,12 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (Job& j : jobs) {
     const CompiledKernel& ck = g_cache.at(j.src);
-    out[j.d][j.p] = JitPass{reinterpret_cast<void*>(ck.fn), j.threads, j.smem};
+    JitPass jp;
+    jp.kernel = reinterpret_cast<void*>(ck.fn);
+    jp.threads = j.threads;
+    jp.smem = j.smem;
+    jp.coefs = j.coefs;
+    out[j.d][j.p] = jp;
   }
   return out;
 }
@@ -427,7 +486,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
-                L.arity ? L.arity : 1u, L.batch};
+                L.arity ? L.arity : 1u, L.batch, jp.d_cm};
   const uint64_t grid = (uint64_t)L.batch << pd.n_out;
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;
