@@ -43,7 +43,6 @@ struct __align__(16) tq_d2 { double x, y; };
 struct TqJitArgs {
   const tq_d2* src; tq_d2* dst; tq_u64 seed; double p1, p2;
   tq_u64 child_first, parent_first; tq_u32 arity, batch;
-  const double* __restrict__ cm;   // gate-matrix coefficients of this pass (run-time data)
 };
 __device__ __forceinline__ void tq_pauli_rt(tq_d2& x, tq_d2& y, tq_u32 p) {
   if (p == 1u) { const tq_d2 t = x; x = y; y = t; }
@@ -59,7 +58,6 @@ struct HostJitArgs {   // mirrors TqJitArgs
   double p1, p2;
   uint64_t child_first, parent_first;
   uint32_t arity, batch;
-  const double* cm;
 };
 
 std::string hexd(double v) {
@@ -70,10 +68,10 @@ std::string hexd(double v) {
 
 uint32_t host_swz(uint32_t i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9) ^ (i >> 12)) & 7u); }
 
-// Gate-matrix coefficients are RUN-TIME data (a per-pass global table read once
-// per gate into registers with __ldg), so the generated source -- and the
-// compiled-kernel cache key -- depends only on the circuit's structure (gate
-// kinds, qubits, which matrix components are 0 or +-1), not on its angles.
+// Gate-matrix coefficients: FP64 literals in the generated code (default), or --
+// TQSIM_JIT_COEF=0 -- a by-value kernel parameter table, which makes the source
+// (and the compiled-kernel cache key) depend only on the circuit's structure
+// (gate kinds, qubits, which components are 0 or +-1), not on its angles.
 struct ConstPool {
   std::vector<double> vals;
   std::map<uint64_t, int> index;
@@ -85,9 +83,13 @@ struct ConstPool {
     decl.str("");
     nlocal = 0;
   }
+  // 2 (default): FP64 literals -- fastest (the measured best on B200);
+  // 0: by-value kernel parameter -- source (and cache key) independent of angles
+  int mode = 2;
   std::string ref(double v) {
     if (v == 1.0) return "1.0";
     if (v == -1.0) return "-1.0";
+    if (mode == 2) return hexd(v);
     uint64_t bits;
     std::memcpy(&bits, &v, 8);
     auto lt = local.find(bits);
@@ -102,7 +104,7 @@ struct ConstPool {
       k = it->second;
     }
     const std::string name = "q" + std::to_string(nlocal++);
-    decl << "      const double " << name << " = __ldg(a.cm + " << k << ");\n";
+    decl << "      const double " << name << " = cf.v[" << k << "];\n";
     local[bits] = name;
     return name;
   }
@@ -152,6 +154,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   Gen g;
   std::ostringstream& o = g.o;
   ConstPool pool;
+  {
+    const char* e = std::getenv("TQSIM_JIT_COEF");   // "0" = parameter mode
+    pool.mode = (e && e[0] == '0') ? 0 : 2;
+  }
   g_pool = &pool;
   o << "static __constant__ tq_u32 GIDX[" << std::max(nops, 1) << "] = {";
   for (int i = 0; i < nops; ++i) o << (i ? "," : "") << pp.ops[pd.op_begin + i].gate << "u";
@@ -164,7 +170,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   const int minb = K >= 13 ? 1
                            : std::max(1, std::min(512 / T, (int)((227 * 1024) / ((16 << K) + 1024))));
   o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << std::min(minb, 32) << ") "
-    << name << "(const TqJitArgs a) {\n";
+    << name << "(const TqJitArgs a, const TqCoef cf) {\n";
   if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
   o << "  __shared__ unsigned char codes[" << std::max(nops, 1) << "];\n";
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
@@ -304,7 +310,11 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   o << "}\n";
   g_pool = nullptr;
   coefs = pool.vals;
-  return o.str();
+  // gate coefficients are a by-value kernel parameter (constant bank 0): run-time
+  // data, so the source depends only on the circuit's structure
+  std::string src = "struct TqCoef { double v[" + std::to_string(std::max<size_t>(coefs.size(), 1)) +
+                    "]; };\n" + o.str();
+  return src;
 }
 
 struct CompiledKernel {
@@ -486,11 +496,12 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
-                L.arity ? L.arity : 1u, L.batch, jp.d_cm};
+                L.arity ? L.arity : 1u, L.batch};
   const uint64_t grid = (uint64_t)L.batch << pd.n_out;
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;
-  void* args[] = {&a};
+  static const double zero = 0.0;
+  void* args[] = {&a, const_cast<double*>(jp.coefs.empty() ? &zero : jp.coefs.data())};
   return (int)cudaLaunchKernel(jp.kernel, dim3((unsigned)grid), dim3(jp.threads), args, jp.smem,
                                static_cast<cudaStream_t>(stream));
 }

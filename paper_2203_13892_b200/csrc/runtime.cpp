@@ -31,7 +31,6 @@ struct tqsim_handle {
   std::vector<std::vector<tq::JitPass>> jit;   // specialized pass kernels [level][pass]
   double compile_s = 0.0;
   uint8_t* d_two = nullptr;
-  double* d_cm = nullptr;
   tqsim_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -286,20 +285,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
       ckc(cudaMemcpy(h->d_two, two.data(), two.size(), cudaMemcpyHostToDevice), "upload two");
       // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
       h->jit = jit_build(h->pp, h->gates, &h->compile_s);
-      std::vector<double> cm;
-      std::vector<size_t> off;
-      for (auto& lv : h->jit)
-        for (auto& jp : lv) {
-          off.push_back(cm.size());
-          cm.insert(cm.end(), jp.coefs.begin(), jp.coefs.end());
-        }
-      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_cm), std::max<size_t>(1, cm.size()) * 8),
-          "cudaMalloc coefficients");
-      if (!cm.empty())
-        ckc(cudaMemcpy(h->d_cm, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice), "upload coefficients");
-      size_t i = 0;
-      for (auto& lv : h->jit)
-        for (auto& jp : lv) jp.d_cm = h->d_cm + off[i++];
+
     }
   } catch (...) {
     tqsim_destroy(h);
@@ -521,7 +507,6 @@ tqsim_status tqsim_get_stats(const tqsim_handle* h, tqsim_stats* out) {
 void tqsim_destroy(tqsim_handle* h) {
   if (!h) return;
   if (h->d_two) cudaFree(h->d_two);
-  if (h->d_cm) cudaFree(h->d_cm);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   delete h;
 }

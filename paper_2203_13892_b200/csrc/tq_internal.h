@@ -121,8 +121,7 @@ struct JitPass {
   void* kernel = nullptr;   // cudaKernel_t
   int threads = 0;
   size_t smem = 0;
-  std::vector<double> coefs;      // gate-matrix coefficients the kernel reads (run-time data)
-  const double* d_cm = nullptr;   // their copy in HBM (owned by the handle)
+  std::vector<double> coefs;      // by-value coefficient parameter (TQSIM_JIT_COEF=0 mode)
 };
 std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vector<LGate>& gates,
                                             double* compile_seconds);
