@@ -18,6 +18,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -231,12 +232,65 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       for (int k = 0; k < 16; ++k) o << "    r" << k << " = tile[sb ^ " << soff[k] << "u];\n";
       o << "    __syncthreads();\n";
     }
+    // Error-free path: monomial gates (CX, CZ, X, diagonal) are composed at code
+    // generation time into a register renaming + a pending phase per logical
+    // amplitude, folded into the next general gate's coefficients or applied once
+    // at the end of the phase.  Exact up to fp rounding (R30).
+    typedef std::complex<double> cplx;
+    cplx dph[16];
+    for (int k = 0; k < 16; ++k) dph[k] = cplx(1.0, 0.0);
+    auto permute = [&](auto perm) {   // new logical k <- old logical perm(k)
+      int nrm[16];
+      cplx nd[16];
+      for (int k = 0; k < 16; ++k) {
+        nrm[k] = g.rm[perm(k)];
+        nd[k] = dph[perm(k)];
+      }
+      for (int k = 0; k < 16; ++k) {
+        g.rm[k] = nrm[k];
+        dph[k] = nd[k];
+      }
+    };
     for (uint32_t oi = P.op_begin; oi < P.op_end; ++oi) {
       const OpDesc& od = pp.ops[oi];
       const LGate& lg = gates[od.gate];
       const int ci = (int)(oi - pd.op_begin);
       const int ba = od.ra, bb = od.rb;
       o << "    // g" << od.gate << "\n";
+      if (!with_errors) {
+        const double* m = lg.m;
+        const bool is_x = od.type != OP_CX && od.type != OP_CZ && m[0] == 0 && m[1] == 0 &&
+                          m[2] == 1 && m[3] == 0 && m[4] == 1 && m[5] == 0 && m[6] == 0 && m[7] == 0;
+        if (od.type == OP_CX) {
+          permute([&](int k) { return k ^ (((k >> ba) & 1) << bb); });
+        } else if (od.type == OP_CZ) {
+          for (int k = 0; k < 16; ++k)
+            if ((k >> ba & 1) && (k >> bb & 1)) dph[k] = -dph[k];
+        } else if (is_x) {
+          permute([&](int k) { return k ^ (1 << ba); });
+        } else if (od.type == OP_DIAG) {
+          const cplx d0(m[0], m[1]), d1(m[6], m[7]);
+          for (int k = 0; k < 16; ++k) dph[k] *= ((k >> ba) & 1) ? d1 : d0;
+        } else {
+          std::ostringstream oo;
+          pool.begin_op();
+          const cplx m00(m[0], m[1]), m01(m[2], m[3]), m10(m[4], m[5]), m11(m[6], m[7]);
+          for (int k = 0; k < 16; ++k) {
+            if (k >> ba & 1) continue;
+            const int k1 = k | 1 << ba;
+            const cplx a00 = m00 * dph[k], a01 = m01 * dph[k1], a10 = m10 * dph[k], a11 = m11 * dph[k1];
+            dph[k] = dph[k1] = cplx(1.0, 0.0);
+            const std::string va = g.r(k), vb = g.r(k1);
+            oo << "      { const tq_d2 x = " << va << ", y = " << vb << ";\n";
+            oo << "        " << va << ".x = " << lin(a00.real(), a00.imag(), "x", a01.real(), a01.imag(), "y", false) << ";\n";
+            oo << "        " << va << ".y = " << lin(a00.real(), a00.imag(), "x", a01.real(), a01.imag(), "y", true) << ";\n";
+            oo << "        " << vb << ".x = " << lin(a10.real(), a10.imag(), "x", a11.real(), a11.imag(), "y", false) << ";\n";
+            oo << "        " << vb << ".y = " << lin(a10.real(), a10.imag(), "x", a11.real(), a11.imag(), "y", true) << "; }\n";
+          }
+          o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+        }
+        continue;
+      }
       if (od.type == OP_CX) {
         for (int k = 0; k < 16; ++k)
           if ((k >> ba & 1) && !(k >> bb & 1)) std::swap(g.rm[k], g.rm[k | 1 << bb]);
@@ -292,6 +346,18 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           if (!(k >> ba & 1)) o << "        tq_pauli_rt(" << g.r(k) << ", " << g.r(k | 1 << ba) << ", c);\n";
       }
       o << "      } }\n";
+    }
+    if (!with_errors) {   // flush the pending phases
+      std::ostringstream oo;
+      pool.begin_op();
+      for (int k = 0; k < 16; ++k) {
+        if (dph[k] == cplx(1.0, 0.0)) continue;
+        const std::string v = g.r(k);
+        oo << "      { const tq_d2 x = " << v << "; " << v << ".x = "
+           << lin(dph[k].real(), dph[k].imag(), "x", 0, 0, "x", false) << "; " << v << ".y = "
+           << lin(dph[k].real(), dph[k].imag(), "x", 0, 0, "x", true) << "; }\n";
+      }
+      o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
     }
     if (last) {
       o << "    const tq_u32 gbs = " << gb.str() << ";\n";
