@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--batch-log2", type=int, default=0)
+    ap.add_argument("--shard", default="", help="r/w: time only shard r of w (single-GPU experiments)")
     return ap.parse_args()
 
 
@@ -171,6 +172,10 @@ def main():
     import torch.distributed as dist
     import paper_2203_13892_b200.tqsim as T
 
+    if args.shard and world == 1:
+        rank, world_override = (int(v) for v in args.shard.split("/"))
+    else:
+        world_override = None
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -180,13 +185,14 @@ def main():
     h = T.tqsim_create(n, gates, noise, shots, ar, opts)
     plan = h.plan
     N = int(plan.n_outcomes)
-    ws = torch.empty(h.workspace_bytes(rank, world), dtype=torch.uint8, device=dev)
+    xw = world_override or world          # shards the tree is cut into
+    ws = torch.empty(h.workspace_bytes(rank, xw), dtype=torch.uint8, device=dev)
     out = torch.zeros(N, dtype=torch.int32, device=dev)
     st = torch.cuda.current_stream(dev)
 
     def step(seed):
         out.zero_()
-        h.execute(seed, rank, world, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
+        h.execute(seed, rank, xw, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
         if world > 1:
             dist.all_reduce(out, op=dist.ReduceOp.SUM)
 
@@ -222,7 +228,7 @@ def main():
     pass_launches = 0
     for i in range(max(1, min(args.steps, 3))):
         out.zero_()
-        hp.execute(i, rank, world, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
+        hp.execute(i, rank, xw, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
         s = hp.stats()
         pass_ms += s.pass_ms
         meas_ms += s.measure_ms

@@ -70,7 +70,11 @@ PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, cons
   PassPlan pp;
   const int n = std::max<int>((int)n_qubits, RBITS);
   pp.n_sim = n;
-  int K = o.tile_qubits ? (int)o.tile_qubits : 12;
+  // Auto tile width (measured on B200): 2^12-amplitude tiles (2 CTAs
+  // x 8 warps per SM) for n < 22, where passes are FP64/latency bound; 2^11 tiles (4
+  // CTAs x 4 warps) for wide states, whose passes are HBM bound and gain more from
+  // independent CTAs than they lose to the extra passes.
+  int K = o.tile_qubits ? (int)o.tile_qubits : (n >= 22 ? 11 : 12);
   K = std::max(K, std::min(n, LOW_Q + 2));   // >= 2 free high slots so any 2q gate fits
   K = std::min(K, n);
   const int low = std::min(LOW_Q, K);
