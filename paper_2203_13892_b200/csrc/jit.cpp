@@ -44,6 +44,7 @@ struct __align__(16) tq_d2 { double x, y; };
 struct TqJitArgs {
   const tq_d2* src; tq_d2* dst; tq_u64 seed; double p1, p2;
   tq_u64 child_first, parent_first; tq_u32 arity, batch;
+  double* runsum;   // leaf level: |a|^2 sums of 8-amplitude runs, 2^(n-3) per state
 };
 __device__ __forceinline__ void tq_pauli_rt(tq_d2& x, tq_d2& y, tq_u32 p) {
   if (p == 1u) { const tq_d2 t = x; x = y; y = t; }
@@ -59,6 +60,7 @@ struct HostJitArgs {   // mirrors TqJitArgs
   double p1, p2;
   uint64_t child_first, parent_first;
   uint32_t arity, batch;
+  double* runsum;
 };
 
 std::string hexd(double v) {
@@ -380,6 +382,40 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     if (last) {
       o << "    const tq_u32 gbs = " << gb.str() << ";\n";
       for (int k = 0; k < 16; ++k) o << "    dst[gbs + " << goff[k] << "u] = " << g.r(k) << ";\n";
+      if (pd.leaf_sums) {
+        // |a|^2 sums of the 8-amplitude runs (qubits 0..2): reduce over the register bits
+        // holding positions 0..2, then butterfly-shuffle over the lane bits holding the
+        // rest (the last phase puts the lowest non-register positions on lanes 0..4).
+        int rbits_low = 0;      // register bits whose position is < RUN_Q
+        for (int b = 0; b < RBITS; ++b)
+          if (P.rpos[b] < RUN_Q) rbits_low |= 1 << b;
+        std::vector<int> lane_bits;
+        for (int m = 0; m < K - RBITS; ++m)
+          if (P.tpos[m] < RUN_Q) lane_bits.push_back(m);
+        if ((int)lane_bits.size() + __builtin_popcount(rbits_low) != RUN_Q || (!lane_bits.empty() && lane_bits.back() >= 5))
+          throw Error{TQSIM_EINTERNAL, "run-sum layout: low qubits not on registers/lanes"};
+        std::vector<int> reps;   // one k per run held by this thread
+        for (int k = 0; k < 16; ++k)
+          if (!(k & rbits_low)) reps.push_back(k);
+        for (size_t i = 0; i < reps.size(); ++i) {
+          o << "    double rs" << i << " = 0.0;\n";
+          for (int k = 0; k < 16; ++k)
+            if ((k & ~rbits_low) == reps[i])
+              o << "    rs" << i << " = fma(" << g.r(k) << ".x, " << g.r(k) << ".x, fma(" << g.r(k) << ".y, "
+                << g.r(k) << ".y, rs" << i << "));\n";
+        }
+        for (int m : lane_bits)
+          for (size_t i = 0; i < reps.size(); ++i)
+            o << "    rs" << i << " += __shfl_xor_sync(" << (T >= 32 ? 0xffffffffu : (1u << T) - 1u) << "u, rs" << i
+              << ", " << (1 << m) << ");\n";
+        int lane_mask = 0;
+        for (int m : lane_bits) lane_mask |= 1 << m;
+        o << "    if ((tid & " << lane_mask << "u) == 0u) {\n";
+        for (size_t i = 0; i < reps.size(); ++i)
+          o << "      a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + ((gbs + " << goff[reps[i]] << "u) >> "
+            << RUN_Q << ")] = rs" << i << ";\n";
+        o << "    }\n";
+      }
     } else {
       o << "    const tq_u32 sbs = tq_swz(" << lb.str() << ");\n";
       for (int k = 0; k < 16; ++k) o << "    tile[sbs ^ " << soff[k] << "u] = " << g.r(k) << ";\n";
@@ -580,7 +616,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
-                L.arity ? L.arity : 1u, L.batch};
+                L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum)};
   const uint64_t grid = (uint64_t)L.batch << pd.n_out;
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;

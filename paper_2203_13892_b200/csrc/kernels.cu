@@ -2,11 +2,12 @@
 // debug hooks.  The gate-pass kernels (row a5) are specialized per pass at run
 // time (jit.cpp); both include the same device functions (tq_device_common.cuh).
 //
-//  chunk_sums       |a|^2 sums of 2^C-amplitude contiguous chunks of leaf states
-//  sample_kernel    one CTA per leaf: warp-shuffle block scan over the chunk
-//                   sums -> chunk, re-read the chunk, block scan -> the smallest
-//                   x with C(x) > u*total (§2.3 "the final outcome is
-//                   sampled", reading R9), readout flips (R11).
+//  chunk_sums       sums of 2^C-amplitude chunks from the 8-amplitude |a|^2 run
+//                   sums the leaf's last gate pass writes (fused, jit.cpp)
+//  sample_kernel    one CTA per leaf: warp-shuffle block scans -> chunk -> run ->
+//                   amplitude: the smallest x with C(x) > u*total (§2.3
+//                   "the final outcome is sampled", reading R9), then readout
+//                   flips (R11).
 #include <cuda_runtime.h>
 
 #include "tq_device_common.cuh"
@@ -63,24 +64,82 @@ __device__ __forceinline__ int block_first(bool pred, int* sh) {
   return *sh;
 }
 
-__global__ void __launch_bounds__(MT) chunk_sums_kernel(const cd* __restrict__ states, uint32_t n,
+// Chunk sums over the leaf's run sums (written by the fused last gate pass):
+// chunk = 2^chunk_log2 amplitudes = 2^(chunk_log2 - RUN_Q) runs.
+__global__ void __launch_bounds__(MT) chunk_sums_kernel(const double* __restrict__ runs, uint32_t n,
                                                         uint32_t chunk_log2,
                                                         double* __restrict__ sums) {
   __shared__ double red[MT / 32];
-  const uint64_t n_chunks = 1ull << (n - chunk_log2);
-  const uint64_t bid = blockIdx.x;
-  const uint64_t s = bid >> (n - chunk_log2), c = bid & (n_chunks - 1);
-  const cd* p = states + (s << n) + (c << chunk_log2);
+  const uint32_t rpc = 1u << (chunk_log2 - RUN_Q);   // runs per chunk
+  const uint64_t bid = blockIdx.x;                   // = state * n_chunks + chunk
+  const double* p = runs + bid * rpc;
   double acc = 0.0;
-  for (uint32_t i = threadIdx.x; i < (1u << chunk_log2); i += MT) {
-    const cd v = p[i];
-    acc = fma(v.x, v.x, fma(v.y, v.y, acc));
-  }
+  for (uint32_t i = threadIdx.x; i < rpc; i += MT) acc += p[i];
   const double tot = block_sum(acc, red);
   if (threadIdx.x == 0) sums[bid] = tot;
 }
 
+// First index i of v[0..len) whose running sum from `base` exceeds target, found by
+// the whole block over per-thread contiguous ranges (block scan + ballot).  Returns
+// len if none; *before = running sum before v[i].
+__device__ __forceinline__ uint64_t block_search(const double* __restrict__ v, uint64_t len,
+                                                 double target, double* before, double* wsum,
+                                                 int* first_sh, uint64_t* pick_sh,
+                                                 double* before_sh) {
+  const uint64_t per = (len + MT - 1) / MT;
+  const uint64_t c0 = per * threadIdx.x < len ? per * threadIdx.x : len;
+  const uint64_t c1 = c0 + per < len ? c0 + per : len;
+  double loc = 0.0;
+  for (uint64_t c = c0; c < c1; ++c) loc += v[c];
+  const double incl = block_incl_scan(loc, wsum);
+  const int tsel = block_first(incl > target, first_sh);
+  if (threadIdx.x == 0) {
+    *pick_sh = len;
+    *before_sh = 0.0;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x == tsel) {
+    double acc = incl - loc;
+    uint64_t pick = len;
+    for (uint64_t c = c0; c < c1; ++c) {
+      if (acc + v[c] > target) {
+        pick = c;
+        break;
+      }
+      acc += v[c];
+    }
+    if (pick == len) {   // rounding between the scan and the sequential walk: last non-empty
+      acc = incl - loc;
+      for (uint64_t c = c0; c < c1; ++c)
+        if (v[c] > 0.0) pick = c;
+      for (uint64_t c = c0; c < pick && pick < len; ++c) acc += v[c];
+    }
+    *pick_sh = pick;
+    *before_sh = acc;
+  }
+  __syncthreads();
+  if (*pick_sh == len) {   // target beyond the total (rounding): last non-empty entry
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t c = len;
+      double acc = 0.0;
+      for (uint64_t i = 0; i < len; ++i)
+        if (v[i] > 0.0) c = i;
+      if (c == len) c = len - 1;
+      for (uint64_t i = 0; i < c; ++i) acc += v[i];
+      *pick_sh = c;
+      *before_sh = acc;
+    }
+    __syncthreads();
+  }
+  *before = *before_sh;
+  const uint64_t r = *pick_sh;
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ states,
+                                                    const double* __restrict__ runs,
                                                     const double* __restrict__ sums, uint32_t n,
                                                     uint32_t n_user, uint32_t chunk_log2,
                                                     uint64_t leaf_first, uint64_t seed, double p01,
@@ -89,110 +148,41 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
   __shared__ int first_sh;
   __shared__ uint64_t pick_sh;
   __shared__ double before_sh, total_sh;
-  __shared__ int64_t x_sh;
   const uint32_t s = blockIdx.x;
   const uint64_t leaf = leaf_first + s;
   const uint64_t nc = 1ull << (n - chunk_log2);
+  const uint32_t rpc = 1u << (chunk_log2 - RUN_Q);
   const double* cs = sums + (uint64_t)s * nc;
-  const cd* st = states + ((uint64_t)s << n);
   const double u = tq_measure_uniform(leaf, seed);
 
-  // (a) chunk selection over contiguous per-thread ranges of chunk sums
-  const uint64_t per = (nc + MT - 1) / MT;
-  const uint64_t c0 = per * threadIdx.x < nc ? per * threadIdx.x : nc;
-  const uint64_t c1 = c0 + per < nc ? c0 + per : nc;
+  // total = sum of chunk sums (block reduction in a fixed order)
   double loc = 0.0;
-  for (uint64_t c = c0; c < c1; ++c) loc += cs[c];
-  const double incl = block_incl_scan(loc, wsum);
-  if (threadIdx.x == MT - 1) total_sh = incl;
+  for (uint64_t c = threadIdx.x; c < nc; c += MT) loc += cs[c];
+  const double tot = block_sum(loc, wsum);
+  if (threadIdx.x == 0) total_sh = tot;
   __syncthreads();
   const double target = u * total_sh;
-  const int tsel = block_first(incl > target, &first_sh);
+  // level 1: chunk;  level 2: 8-amplitude run inside the chunk;  level 3: amplitude
+  double before1 = 0.0, before2 = 0.0;
+  const uint64_t chunk = block_search(cs, nc, target, &before1, wsum, &first_sh, &pick_sh, &before_sh);
+  const double* rs = runs + ((uint64_t)s << (n - RUN_Q)) + chunk * rpc;
+  const uint64_t run = block_search(rs, rpc, target - before1, &before2, wsum, &first_sh, &pick_sh,
+                                    &before_sh);
   if (threadIdx.x == 0) {
-    pick_sh = ~0ull;
-    before_sh = 0.0;
-  }
-  __syncthreads();
-  if ((int)threadIdx.x == tsel) {
-    double acc = incl - loc;
-    uint64_t pick = ~0ull;
-    for (uint64_t c = c0; c < c1; ++c) {
-      if (acc + cs[c] > target) {
-        pick = c;
-        break;
-      }
-      acc += cs[c];
+    const double t3 = target - before1 - before2;
+    const uint64_t base = ((chunk * rpc + run) << RUN_Q);
+    const cd* ap = states + ((uint64_t)s << n) + base;
+    double acc = 0.0;
+    int x = -1, lastnz = -1;
+    for (int e = 0; e < (1 << RUN_Q); ++e) {
+      const cd v = ap[e];
+      const double pr = v.x * v.x + v.y * v.y;
+      if (pr > 0.0) lastnz = e;
+      acc += pr;
+      if (x < 0 && acc > t3) x = e;
     }
-    if (pick == ~0ull) {   // rounding: the last non-empty chunk of the range
-      acc = incl - loc;
-      for (uint64_t c = c0; c < c1; ++c)
-        if (cs[c] > 0.0) pick = c;
-      for (uint64_t c = c0; c < pick; ++c) acc += cs[c];
-    }
-    pick_sh = pick;
-    before_sh = acc;
-  }
-  __syncthreads();
-  if (pick_sh == ~0ull) {   // target beyond the total (rounding): last non-empty chunk
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t c = nc;
-      double acc = 0.0;
-      for (uint64_t i = 0; i < nc; ++i)
-        if (cs[i] > 0.0) c = i;
-      if (c == nc) c = nc - 1;
-      for (uint64_t i = 0; i < c; ++i) acc += cs[i];
-      pick_sh = c;
-      before_sh = acc;
-    }
-    __syncthreads();
-  }
-  const uint64_t chunk = pick_sh;
-  const double target2 = target - before_sh;
-
-  // (b) within the chunk: per-thread contiguous runs of |a|^2
-  const uint32_t clen = 1u << chunk_log2;
-  const uint32_t per2 = (clen + MT - 1) / MT;
-  const uint32_t e0 = min(clen, per2 * threadIdx.x), e1 = min(clen, e0 + per2);
-  const cd* cp = st + (chunk << chunk_log2);
-  double loc2 = 0.0;
-  for (uint32_t e = e0; e < e1; ++e) {
-    const cd v = cp[e];
-    loc2 += v.x * v.x + v.y * v.y;
-  }
-  const double incl2 = block_incl_scan(loc2, wsum);
-  const int tsel2 = block_first(incl2 > target2, &first_sh);
-  if (threadIdx.x == 0) x_sh = -1;
-  __syncthreads();
-  if (tsel2 < MT && (int)threadIdx.x == tsel2) {
-    double acc = incl2 - loc2;
-    int64_t x = -1;
-    for (uint32_t e = e0; e < e1; ++e) {
-      const cd v = cp[e];
-      acc += v.x * v.x + v.y * v.y;
-      if (acc > target2) {
-        x = e;
-        break;
-      }
-    }
-    if (x < 0)
-      for (uint32_t e = e0; e < e1; ++e) {
-        const cd v = cp[e];
-        if (v.x * v.x + v.y * v.y > 0.0) x = e;
-      }
-    x_sh = x;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t x = x_sh;
-    if (x < 0) {   // fall back to the last non-zero amplitude of the chunk
-      for (uint32_t e = 0; e < clen; ++e) {
-        const cd v = cp[e];
-        if (v.x * v.x + v.y * v.y > 0.0) x = e;
-      }
-      if (x < 0) x = 0;
-    }
-    const uint32_t xi = (uint32_t)((chunk << chunk_log2) + (uint64_t)x);
+    if (x < 0) x = lastnz >= 0 ? lastnz : 0;   // rounding: the last non-zero amplitude of the run
+    const uint32_t xi = (uint32_t)(base + (uint64_t)x);
     // readout (R11): bit b flips iff word (b&3) of Philox(ctr=(b>>2, leaf, 2, 0)) * 2^-32 < p
     uint32_t mask = 0;
     if (p01 > 0.0 || p10 > 0.0) {
@@ -234,21 +224,21 @@ __global__ void noise_table_kernel(const uint8_t* two, uint32_t slice_begin, uin
 }  // namespace dev
 
 // ------------------------------------------------------------------ launchers
-int launch_chunk_sums(const void* states, uint32_t batch, int n_sim, int chunk_log2, double* sums,
-                      void* stream) {
+int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
+                      double* sums, void* stream) {
   const uint64_t grid = (uint64_t)batch << (n_sim - chunk_log2);
   if (grid == 0) return 0;
   dev::chunk_sums_kernel<<<(unsigned)grid, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const dev::cd*>(states), (uint32_t)n_sim, (uint32_t)chunk_log2, sums);
+      runsums, (uint32_t)n_sim, (uint32_t)chunk_log2, sums);
   return (int)cudaGetLastError();
 }
 
-int launch_sample(const void* states, const double* sums, uint32_t batch, int n_sim, int n_user,
-                  int chunk_log2, uint64_t leaf_first, uint64_t seed, double p01, double p10,
-                  uint32_t* d_out, void* stream) {
+int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
+                  int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, uint64_t seed,
+                  double p01, double p10, uint32_t* d_out, void* stream) {
   if (batch == 0) return 0;
   dev::sample_kernel<<<batch, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const dev::cd*>(states), sums, (uint32_t)n_sim, (uint32_t)n_user,
+      static_cast<const dev::cd*>(states), runsums, sums, (uint32_t)n_sim, (uint32_t)n_user,
       (uint32_t)chunk_log2, leaf_first, seed, p01, p10, d_out);
   return (int)cudaGetLastError();
 }

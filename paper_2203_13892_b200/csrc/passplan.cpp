@@ -1,9 +1,9 @@
 // Pass planner: slice -> HBM passes -> register phases.
 //
 // Not in the paper (its underlying simulator is Qulacs); this is the
-// B200 design of DESIGN.md §"Kernels".  Every HBM pass stages tiles of 2^K
-// amplitudes spanning the K tile qubits {0..4} ∪ H (qubits 0..4 give 512-byte
-// contiguous segments) in shared memory; inside a tile each thread holds 16
+// B200 design of DESIGN.md §6.1.  Every HBM pass stages tiles of 2^K
+// amplitudes spanning the K tile qubits {0,1,2} ∪ H (qubits 0..2 give 128-byte
+// contiguous runs) in shared memory; inside a tile each thread holds 16
 // amplitudes spanning RBITS = 4 tile positions in registers ("phase"), applies
 // every consecutive gate on those positions, then the tile is re-shuffled
 // through shared memory for the next phase.
@@ -153,6 +153,9 @@ PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, cons
         pdsc.op_end = (uint32_t)pp.ops.size();
         pp.phases.push_back(pdsc);
       }
+      // The leaf level's last pass also writes |a|^2 sums of 2^RUN_Q-amplitude runs
+      // (qubits 0..RUN_Q-1) for the sampler (jit.cpp).
+      if (d + 2 == plan.bounds.size() && pi + 1 == passes.size()) pd.leaf_sums = true;
       pd.phase_end = (uint32_t)pp.phases.size();
       pd.op_end = (uint32_t)pp.ops.size();
       lvl.push_back(pd);

@@ -98,7 +98,7 @@ void require_device() {
 struct Layout {
   std::vector<uint64_t> cap;       // states per level batch
   std::vector<uint64_t> off;       // byte offset of level buffer
-  uint64_t sums_off = 0, total = 0;
+  uint64_t runs_off = 0, sums_off = 0, total = 0;
   int chunk_log2 = 0;
 };
 
@@ -132,6 +132,8 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
       l.off.push_back(off);
       off = align_up(off + l.cap[d] * S);
     }
+    l.runs_off = off;
+    off = align_up(off + l.cap.back() * (8ull << (n - RUN_Q)));
     l.sums_off = off;
     off = align_up(off + l.cap.back() * (8ull << (n - l.chunk_log2)));
     l.total = off;
@@ -224,6 +226,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       pl.seed = x.seed;
       pl.p1 = h->noise.p1;
       pl.p2 = h->noise.p2;
+      pl.runsum = x.ws + x.L.runs_off;
       mark(x, 0);
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
       mark(x, 0);
@@ -244,15 +247,19 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     dump_if_requested(x, d, b, cnt, buf);
     if (d + 1 == levels) {
       double* sums = reinterpret_cast<double*>(x.ws + x.L.sums_off);
+      const double* runs = reinterpret_cast<const double*>(x.ws + x.L.runs_off);
       mark(x, 1);
-      ck(launch_chunk_sums(buf, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
-      ck(launch_sample(buf, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, x.seed,
+      ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
+      ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, x.seed,
                        h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
          "sample launch");
       mark(x, 1);
       h->stats.kernel_launches += 2;
       h->stats.measure_launches += 2;
-      h->stats.measure_bytes += (cnt << n) * 16 + (cnt << x.L.chunk_log2) * 16;
+      // run sums read once; per leaf the chunk sums, one chunk of run sums, 8 amplitudes
+      h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8 +
+                                cnt * ((8ull << (n - x.L.chunk_log2)) +
+                                       (8ull << (x.L.chunk_log2 - RUN_Q)) + (16ull << RUN_Q));
       h->stats.leaves += cnt;
     } else {
       const uint64_t A = h->plan.arities[d + 1];

@@ -55,6 +55,7 @@ constexpr int RBITS = 4;        // amplitudes per thread = 2^RBITS (register-res
 constexpr int MAX_K = 13;       // max tile qubits per HBM pass (2^13 * 16 B = 128 KiB smem)
 constexpr int LOW_Q = 3;        // qubits 0..4 are in every tile (512 B contiguous segments)
 constexpr int MAX_PASS_OPS = 192; // gates per pass kernel (code size / shared codes bound)
+constexpr int RUN_Q = 3;          // leaf |a|^2 run sums cover 2^RUN_Q consecutive amplitudes
 
 struct OpDesc {                 // 8 bytes, device-readable
   uint8_t type;                 // OpType
@@ -79,6 +80,7 @@ struct PassDesc {
   uint32_t phase_begin = 0, phase_end = 0;
   uint32_t op_begin = 0, op_end = 0;
   uint64_t tile_mask = 0;
+  bool leaf_sums = false;       // last pass of the leaf level: also writes |a|^2 run sums
 };
 
 struct PassPlan {
@@ -103,13 +105,14 @@ struct PassLaunch {
   uint32_t batch;
   uint64_t seed;
   double p1, p2;
+  void* runsum;                 // leaf |a|^2 run sums (leaf_sums passes only)
 };
 
-int launch_chunk_sums(const void* states, uint32_t batch, int n_sim, int chunk_log2, double* sums,
-                      void* stream);
-int launch_sample(const void* states, const double* sums, uint32_t batch, int n_sim, int n_user,
-                  int chunk_log2, uint64_t leaf_first, uint64_t seed, double p01, double p10,
-                  uint32_t* d_out, void* stream);
+int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
+                      double* sums, void* stream);
+int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
+                  int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, uint64_t seed,
+                  double p01, double p10, uint32_t* d_out, void* stream);
 int launch_philox_debug(const uint32_t* d_in, uint64_t n, uint32_t* d_out);
 int launch_noise_table(const uint8_t* d_two, uint32_t slice_begin, uint32_t slice_len,
                        uint64_t inst_begin, uint64_t count, uint64_t seed, double p1, double p2,
