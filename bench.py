@@ -240,19 +240,51 @@ def main():
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9 if pass_ms > 0 else 0.0
     pt = torch.tensor([pass_ms, meas_ms], dtype=torch.float64, device=dev)
 
-    # end to end through the public C-ABI call (host buffers)
+    # end to end through the public API with HOST buffers: N=1 the north_star call
+    # tqsim_run (host circuit in -> lowering, planning, kernel-cache lookup, tree, D2H of
+    # the outcomes, host histogram); N>1 each rank: tqsim_create + tqsim_execute of its
+    # shard + all_reduce + D2H + histogram on rank 0.
     e2e = None
-    if not args.no_e2e and world == 1:
-        T.tqsim_run(n, gates, noise, shots, ar, 0)     # warm (arena, module load)
-        t0 = time.perf_counter()
-        for i in range(args.steps):
-            r = T.tqsim_run(n, gates, noise, shots, ar, i)
-        dt = time.perf_counter() - t0
-        h2d = (len(T.tqsim_lower_circuit(n, gates)) * (8 * 8 + 1)
-               + int(plan.hbm_passes and 0))   # gate matrices + 2q flags; op/phase tables below
+    if not args.no_e2e and not args.shard:
+        from paper_2203_13892_b200.distributed import histogram
+        if world == 1:
+            T.tqsim_run(n, gates, noise, shots, ar, 0)     # warm (arena, kernel cache)
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                T.tqsim_run(n, gates, noise, shots, ar, i)
+            dt = time.perf_counter() - t0
+        else:
+            host = torch.empty(N, dtype=torch.int32, pin_memory=True)
+
+            def e2e_step(seed):
+                hh = T.tqsim_create(n, gates, noise, shots, ar, opts)
+                out.zero_()
+                hh.execute(seed, rank, world, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
+                dist.all_reduce(out, op=dist.ReduceOp.SUM)
+                host.copy_(out)
+                if rank == 0:
+                    histogram(host.numpy())
+                hh.close()
+
+            e2e_step(0)
+            dist.barrier()
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                e2e_step(i)
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            dt = float(dt.item())
+        n_low = len(T.tqsim_lower_circuit(n, gates))
         e2e = {"value": N * args.steps / dt, "unit": "shots/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": N * 4,
-               "note": "tqsim_run: lowering+planning+H2D gate tables+tree+D2H outcomes+histogram"}
+               "h2d_bytes_per_step": len(gates) * 40 + n_low + 80 * launches_per_step,
+               "d2h_bytes_per_step": N * 4,
+               "note": "h2d = tqsim_gate array + noise-flag table + kernel parameters; "
+                       "d2h = leaf outcomes (uint32)"}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_%s.json" % w.name)
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -268,18 +300,22 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "n_qubits": n, "shots": shots, "outcomes": N,
                        "arities": plan.arity_list, "lowered_gates": int(plan.n_lowered_gates),
-                       "tile_qubits": args.tile or 12,
+                       "tile_qubits": args.tile or (11 if n >= 22 else 12),
                        "l2": "inputs larger than L2 (state batches >= 1 GiB per launch group)",
                        "parallelism": "top-level branch sharding x%d" % world},
             "gate_amp_updates_per_s": gau,
             "tree_vs_flat_gate_ratio": plan.flat_gate_amp_updates / plan.gate_amp_updates,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
-                         "peak_source": peak_src, "kernel": "pass_kernel<K>",
+                         "frac": achieved / hbm_peak if hbm_peak else None,
+                         "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None,
+                         "alg_bytes_same_launch": traffic["alg_bytes_per_launch"] if traffic else None,
+                         "peak_source": peak_src,
+                         "kernel": "tq_pass_l*_p* (run-time specialized gate pass, all launches)",
                          "pass_share_of_step": float(pt[0].item()) / (float(pt[0].item()) + float(pt[1].item()))
                          if (pt[0].item() + pt[1].item()) > 0 else None,
                          "pass_launches_profiled": pass_launches},
-            "gpu_launches": launches_per_step * args.steps + (args.steps if world > 1 else 0) * 0,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
