@@ -145,13 +145,300 @@ struct Gen {
   std::string r(int logical) { return "r" + std::to_string(rm[logical]); }
 };
 
+
+// ---------------------------------------------------------------- error-free fast path
+// In the fast path (no Pauli drawn for any gate of the pass) runs of consecutive gates
+// on at most two qubits whose product is DIAGONAL (e.g. the 5-gate lowered CP, or
+// CX.RZ.CX) are fused into one diagonal op.  A diagonal op needs no register slot:
+// its phase is a function of index bits the thread knows -- register bits at code
+// generation time, thread/tile bits at run time -- so the fast path is planned into
+// phases around the non-diagonal gates only (fewer shared-memory tile exchanges).
+typedef std::complex<double> cplx;
+
+struct FOp {
+  enum Kind { GEN, XPERM, CX, DIAG } kind = GEN;
+  int qa = -1, qb = -1;   // global qubits (qb = -1: one-qubit op)
+  cplx m[4];              // GEN: row-major 2x2
+  cplx d[4];              // DIAG: entry for index bit_qa | bit_qb << 1
+};
+
+struct PhaseSpec {
+  PhaseDesc P;
+  std::vector<int> items;   // careful path: indices into pp.ops; fast path: into fops
+};
+
+// 4x4 over (s0, s1), local index = bit_s0 | bit_s1 << 1
+struct M4 {
+  cplx a[4][4];
+  static M4 id() {
+    M4 r;
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) r.a[i][j] = i == j ? cplx(1, 0) : cplx(0, 0);
+    return r;
+  }
+  M4 mul(const M4& b) const {   // this * b
+    M4 r;
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) {
+        cplx acc(0, 0);
+        for (int k = 0; k < 4; ++k)
+          if (a[i][k] != cplx(0, 0) && b.a[k][j] != cplx(0, 0)) acc += a[i][k] * b.a[k][j];
+        r.a[i][j] = acc;
+      }
+    return r;
+  }
+  bool diagonal() const {
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j)
+        if (i != j && a[i][j] != cplx(0, 0)) return false;
+    return true;
+  }
+};
+
+M4 op_matrix(const LGate& g, int s0, int s1) {
+  M4 r;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) r.a[i][j] = cplx(0, 0);
+  auto bit = [&](int idx, int q) { return q == s0 ? (idx & 1) : ((idx >> 1) & 1); };
+  if (!g.two) {
+    const cplx m[4] = {cplx(g.m[0], g.m[1]), cplx(g.m[2], g.m[3]), cplx(g.m[4], g.m[5]),
+                       cplx(g.m[6], g.m[7])};
+    const int q = (int)g.q0, o = q == s0 ? 1 : 0;   // bit position of the other slot
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) {
+        const int oi = o ? ((i >> 1) & 1) : (i & 1), oj = o ? ((j >> 1) & 1) : (j & 1);
+        if (oi != oj) continue;
+        r.a[i][j] = m[bit(i, q) * 2 + bit(j, q)];
+      }
+    return r;
+  }
+  const int c = (int)g.q0, t = (int)g.q1;
+  for (int j = 0; j < 4; ++j) {
+    if (g.op == OP_CX) {
+      int i = j;
+      if (bit(j, c)) i ^= (t == s0 ? 1 : 2);
+      r.a[i][j] = cplx(1, 0);
+    } else {   // CZ
+      r.a[j][j] = (bit(j, c) && bit(j, t)) ? cplx(-1, 0) : cplx(1, 0);
+    }
+  }
+  return r;
+}
+
+bool is_x_gate(const LGate& lg) {
+  const double* m = lg.m;
+  return !lg.two && m[0] == 0 && m[1] == 0 && m[2] == 1 && m[3] == 0 && m[4] == 1 && m[5] == 0 &&
+         m[6] == 0 && m[7] == 0;
+}
+
+bool is_swap(const M4& P) {   // exchanges |01> and |10>, fixes |00>, |11>
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      const int si = (i == 1) ? 2 : (i == 2) ? 1 : i;
+      if (P.a[i][j] != (j == si ? cplx(1, 0) : cplx(0, 0))) return false;
+    }
+  return true;
+}
+
+// Fast-path op list.  SWAPs (a fused run whose product is the swap permutation) are
+// not executed: both qubits are tile qubits, so the swap is a relabeling of tile
+// positions -- later ops are rewritten to PHYSICAL qubit labels and the final store
+// writes position p to logical qubit log_of_phys[tile_q[p]].
+std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
+                               const std::vector<LGate>& gates, bool allow_swap,
+                               std::vector<int>& log_of_phys) {
+  std::vector<FOp> out;
+  std::vector<int> phys_of(64);
+  for (int q = 0; q < 64; ++q) phys_of[q] = q;
+  const int n = (int)(pd.op_end - pd.op_begin);
+  auto lg_of = [&](int i) -> const LGate& { return gates[pp.ops[pd.op_begin + i].gate]; };
+  int i = 0;
+  while (i < n) {
+    const LGate& g0 = lg_of(i);
+    int s0 = (int)g0.q0, s1 = g0.two ? (int)g0.q1 : -1;
+    M4 P = op_matrix(g0, s0, s1 < 0 ? (s0 == 0 ? 1 : 0) : s1);
+    int best = P.diagonal() ? i : -1, best_swap = -1;
+    M4 bestP = P;
+    int bs1 = s1, sw1 = -1;
+    for (int j = i + 1; j < n && j < i + 12; ++j) {
+      const LGate& gj = lg_of(j);
+      int ns1 = s1;
+      const int qs[2] = {(int)gj.q0, gj.two ? (int)gj.q1 : -1};
+      bool ok = true;
+      for (int q : qs) {
+        if (q < 0 || q == s0 || q == ns1) continue;
+        if (ns1 < 0) ns1 = q;
+        else ok = false;
+      }
+      if (!ok) break;
+      if (s1 < 0 && ns1 >= 0) {
+        // lift: the product so far acted on s0 with a placeholder second slot; the
+        // placeholder was identity, so the 4x4 is unchanged when s1 becomes real.
+      }
+      s1 = ns1;
+      P = op_matrix(gj, s0, s1 < 0 ? (s0 == 0 ? 1 : 0) : s1).mul(P);
+      if (P.diagonal()) {
+        best = j;
+        bestP = P;
+        bs1 = s1;
+      } else if (allow_swap && s1 >= 0 && is_swap(P)) {
+        best_swap = j;
+        sw1 = s1;
+      }
+    }
+    if (best_swap > best) {   // relabel instead of moving amplitudes
+      std::swap(phys_of[s0], phys_of[sw1]);
+      i = best_swap + 1;
+      continue;
+    }
+    if (best >= 0) {
+      FOp f;
+      f.kind = FOp::DIAG;
+      f.qa = phys_of[s0];
+      f.qb = bs1 >= 0 ? phys_of[bs1] : -1;
+      for (int k = 0; k < 4; ++k) f.d[k] = bestP.a[k][k];
+      bool trivial = true;
+      for (int k = 0; k < 4; ++k)
+        if (f.d[k] != cplx(1, 0)) trivial = false;
+      if (!trivial) out.push_back(f);
+      i = best + 1;
+      continue;
+    }
+    FOp f;
+    f.qa = phys_of[g0.q0];
+    if (g0.two) {   // CX (CZ is diagonal and handled above)
+      f.kind = FOp::CX;
+      f.qb = phys_of[g0.q1];
+    } else if (is_x_gate(g0)) {
+      f.kind = FOp::XPERM;
+    } else {
+      f.kind = FOp::GEN;
+      for (int k = 0; k < 4; ++k) f.m[k] = cplx(g0.m[2 * k], g0.m[2 * k + 1]);
+    }
+    out.push_back(f);
+    ++i;
+  }
+  log_of_phys.assign(64, 0);
+  for (int q = 0; q < 64; ++q) log_of_phys[phys_of[q]] = q;
+  return out;
+}
+
+PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool global_phase) {
+  for (int p = K - 1; p >= 0 && __builtin_popcountll(R) < RBITS; --p)
+    if (!(R >> p & 1) && p >= low) R |= 1ull << p;
+  for (int p = 0; p < K && __builtin_popcountll(R) < RBITS; ++p)
+    if (!(R >> p & 1)) R |= 1ull << p;
+  PhaseDesc P{};
+  int rb = 0;
+  for (int p = 0; p < K; ++p)
+    if (R >> p & 1) P.rpos[rb++] = (uint8_t)p;
+  std::vector<int> nonr;
+  for (int p = 0; p < K; ++p)
+    if (!(R >> p & 1)) nonr.push_back(p);
+  std::vector<int> tmap;
+  if (!global_phase && nonr.size() >= 3) {
+    std::vector<int> rest = nonr;
+    for (int r = 0; r < 3; ++r)
+      for (size_t i = 0; i < rest.size(); ++i)
+        if (rest[i] % 3 == r) {
+          tmap.push_back(rest[i]);
+          rest.erase(rest.begin() + i);
+          break;
+        }
+    tmap.insert(tmap.end(), rest.begin(), rest.end());
+  } else {
+    tmap = nonr;
+  }
+  for (size_t m = 0; m < tmap.size(); ++m) P.tpos[m] = (uint8_t)tmap[m];
+  return P;
+}
+
+std::vector<PhaseSpec> plan_fast_phases(const std::vector<FOp>& fops, const PassDesc& pd,
+                                        const PhaseDesc& first) {
+  int qpos[64];
+  for (int q = 0; q < 64; ++q) qpos[q] = -1;
+  for (int p = 0; p < pd.K; ++p) qpos[pd.tile_q[p]] = p;
+  auto qmask = [&](const FOp& f) { return (1ull << f.qa) | (f.qb >= 0 ? 1ull << f.qb : 0ull); };
+  auto pmask = [&](const FOp& f) {
+    return (1ull << qpos[f.qa]) | (f.qb >= 0 ? 1ull << qpos[f.qb] : 0ull);
+  };
+  uint64_t R0 = 0;
+  for (int b = 0; b < RBITS; ++b) R0 |= 1ull << first.rpos[b];
+  std::vector<std::pair<std::vector<int>, uint64_t>> groups;
+  std::vector<int> remaining(fops.size());
+  for (size_t i = 0; i < fops.size(); ++i) remaining[i] = (int)i;
+  bool firstg = true;
+  while (!remaining.empty() || firstg) {
+    uint64_t used = firstg ? R0 : 0, blocked = 0;
+    std::vector<int> in, deferred;
+    for (int fi : remaining) {
+      const FOp& f = fops[fi];
+      const uint64_t qm = qmask(f);
+      if (qm & blocked) {
+        deferred.push_back(fi);
+        blocked |= qm;
+        continue;
+      }
+      if (f.kind == FOp::DIAG) {
+        in.push_back(fi);
+        continue;
+      }
+      const uint64_t need = pmask(f);
+      const bool ok = firstg ? ((need & ~R0) == 0) : (__builtin_popcountll(used | need) <= RBITS);
+      if (ok) {
+        used |= need;
+        in.push_back(fi);
+      } else {
+        deferred.push_back(fi);
+        blocked |= qm;
+      }
+    }
+    if (!firstg && in.empty()) throw Error{TQSIM_EINTERNAL, "fast-path planner made no progress"};
+    groups.emplace_back(std::move(in), used);
+    remaining.swap(deferred);
+    firstg = false;
+  }
+  std::vector<PhaseSpec> out;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    PhaseSpec ps;
+    if (gi == 0) ps.P = first;
+    else ps.P = make_phase_layout(groups[gi].second, pd.K, std::min(LOW_Q, pd.K), gi + 1 == groups.size());
+    ps.items = groups[gi].first;
+    out.push_back(ps);
+  }
+  return out;
+}
+
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs) {
   const int K = pd.K, T = 1 << (K - RBITS);
-  const int nph = (int)(pd.phase_end - pd.phase_begin);
   const int nops = (int)(pd.op_end - pd.op_begin);
-  const bool use_smem = nph > 1;
+  std::vector<PhaseSpec> careful;
+  for (uint32_t ph = pd.phase_begin; ph < pd.phase_end; ++ph) {
+    PhaseSpec ps;
+    ps.P = pp.phases[ph];
+    for (uint32_t oi = ps.P.op_begin; oi < ps.P.op_end; ++oi) ps.items.push_back((int)oi);
+    careful.push_back(ps);
+  }
+  std::vector<int> log_of_phys;
+  const std::vector<FOp> fops = fuse_fast_ops(pd, pp, gates, !pd.leaf_sums, log_of_phys);
+  const std::vector<PhaseSpec> fast = plan_fast_phases(fops, pd, pp.phases[pd.phase_begin]);
+  if (const char* e = std::getenv("TQSIM_JIT_DEBUG")) {
+    if (e[0] == '1') {
+      std::fprintf(stderr, "[tqsim jit] %s: %d ops -> %zu fast ops; phases careful %zu fast %zu\n",
+                   name.c_str(), nops, fops.size(), careful.size(), fast.size());
+      for (size_t ph = 0; ph < fast.size(); ++ph) {
+        std::fprintf(stderr, "   fast phase %zu R=", ph);
+        for (int b = 0; b < RBITS; ++b) std::fprintf(stderr, "%d,", pd.tile_q[fast[ph].P.rpos[b]]);
+        std::fprintf(stderr, " ops:");
+        for (int it : fast[ph].items)
+          std::fprintf(stderr, " %s(%d,%d)", fops[it].kind == FOp::DIAG ? "D" : fops[it].kind == FOp::GEN ? "G" : fops[it].kind == FOp::CX ? "CX" : "X", fops[it].qa, fops[it].qb);
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
+  const bool use_smem = careful.size() > 1 || fast.size() > 1;
   threads = T;
   smem = use_smem ? (size_t)16 << K : 0;
   Gen g;
@@ -213,9 +500,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   o << "  int any_err = 0;\n";
   o << "  for (tq_u32 i = tid; i < " << nops << "u; i += " << T << "u) any_err |= codes[i] != 0;\n";
   o << "  if (!__syncthreads_or(any_err)) {\n";
-  auto emit_phases = [&](bool with_errors) {
+  auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors) {
+  const int nph = (int)specs.size();
   for (int ph = 0; ph < nph; ++ph) {
-    const PhaseDesc& P = pp.phases[pd.phase_begin + ph];
+    const PhaseDesc& P = specs[ph].P;
     const bool first = ph == 0, last = ph == nph - 1;
     g.reset_map();
     // thread-dependent part of the tile-local index and of the global index
@@ -271,34 +559,43 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         dph[k] = nd[k];
       }
     };
-    for (uint32_t oi = P.op_begin; oi < P.op_end; ++oi) {
-      const OpDesc& od = pp.ops[oi];
-      const LGate& lg = gates[od.gate];
-      const int ci = (int)(oi - pd.op_begin);
-      const int ba = od.ra, bb = od.rb;
-      o << "    // g" << od.gate << "\n";
-      if (!with_errors) {
-        const double* m = lg.m;
-        const bool is_x = od.type != OP_CX && od.type != OP_CZ && m[0] == 0 && m[1] == 0 &&
-                          m[2] == 1 && m[3] == 0 && m[4] == 1 && m[5] == 0 && m[6] == 0 && m[7] == 0;
-        if (od.type == OP_CX) {
+    // register bit of a global qubit in this phase (-1: not in registers)
+    auto rbit = [&](int q) {
+      for (int b = 0; b < RBITS; ++b)
+        if (pd.tile_q[P.rpos[b]] == q) return b;
+      return -1;
+    };
+    bool gph_on = false;
+    if (!with_errors) {
+      // run-time index bits of the qubits diagonal ops need outside the registers
+      uint64_t rtq = 0;
+      for (int it : specs[ph].items) {
+        const FOp& f = fops[it];
+        if (f.kind != FOp::DIAG) continue;
+        if (rbit(f.qa) < 0) rtq |= 1ull << f.qa;
+        if (f.qb >= 0 && rbit(f.qb) < 0) rtq |= 1ull << f.qb;
+      }
+      if (rtq) {
+        o << "    const tq_u32 gbp = " << gb.str() << ";\n";
+        for (int q = 0; q < 64; ++q)
+          if (rtq >> q & 1) o << "    const bool rt" << q << " = (gbp >> " << q << ") & 1u;\n";
+      }
+      for (int it : specs[ph].items) {
+        const FOp& f = fops[it];
+        if (f.kind == FOp::CX) {
+          const int ba = rbit(f.qa), bb = rbit(f.qb);
           permute([&](int k) { return k ^ (((k >> ba) & 1) << bb); });
-        } else if (od.type == OP_CZ) {
-          for (int k = 0; k < 16; ++k)
-            if ((k >> ba & 1) && (k >> bb & 1)) dph[k] = -dph[k];
-        } else if (is_x) {
+        } else if (f.kind == FOp::XPERM) {
+          const int ba = rbit(f.qa);
           permute([&](int k) { return k ^ (1 << ba); });
-        } else if (od.type == OP_DIAG) {
-          const cplx d0(m[0], m[1]), d1(m[6], m[7]);
-          for (int k = 0; k < 16; ++k) dph[k] *= ((k >> ba) & 1) ? d1 : d0;
-        } else {
+        } else if (f.kind == FOp::GEN) {
+          const int ba = rbit(f.qa);
           std::ostringstream oo;
           pool.begin_op();
-          const cplx m00(m[0], m[1]), m01(m[2], m[3]), m10(m[4], m[5]), m11(m[6], m[7]);
           for (int k = 0; k < 16; ++k) {
             if (k >> ba & 1) continue;
             const int k1 = k | 1 << ba;
-            const cplx a00 = m00 * dph[k], a01 = m01 * dph[k1], a10 = m10 * dph[k], a11 = m11 * dph[k1];
+            const cplx a00 = f.m[0] * dph[k], a01 = f.m[1] * dph[k1], a10 = f.m[2] * dph[k], a11 = f.m[3] * dph[k1];
             dph[k] = dph[k1] = cplx(1.0, 0.0);
             const std::string va = g.r(k), vb = g.r(k1);
             oo << "      { const tq_d2 x = " << va << ", y = " << vb << ";\n";
@@ -308,9 +605,67 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             oo << "        " << vb << ".y = " << lin(a10.real(), a10.imag(), "x", a11.real(), a11.imag(), "y", true) << "; }\n";
           }
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+        } else {   // DIAG
+          const int ra = rbit(f.qa), rb = f.qb >= 0 ? rbit(f.qb) : -2;
+          const bool rta = ra < 0, rtb = rb == -1;
+          auto entry = [&](int bita, int bitb) { return f.d[bita | (bitb << 1)]; };
+          if (!rta && !rtb) {
+            for (int k = 0; k < 16; ++k) dph[k] *= entry(k >> ra & 1, rb >= 0 ? (k >> rb & 1) : 0);
+          } else if (rta && (rtb || rb == -2)) {   // factor common to the 16 amplitudes
+            std::ostringstream oo;
+            pool.begin_op();
+            std::string sel_r, sel_i;
+            auto val = [&](const cplx& v, bool im) { return g_pool->ref(im ? v.imag() : v.real()); };
+            if (rb == -2) {
+              sel_r = "(rt" + std::to_string(f.qa) + " ? " + val(entry(1, 0), false) + " : " + val(entry(0, 0), false) + ")";
+              sel_i = "(rt" + std::to_string(f.qa) + " ? " + val(entry(1, 0), true) + " : " + val(entry(0, 0), true) + ")";
+            } else {
+              const std::string A = "rt" + std::to_string(f.qa), B = "rt" + std::to_string(f.qb);
+              auto sel = [&](bool im) {
+                return "(" + B + " ? (" + A + " ? " + val(entry(1, 1), im) + " : " + val(entry(0, 1), im) + ") : (" +
+                       A + " ? " + val(entry(1, 0), im) + " : " + val(entry(0, 0), im) + "))";
+              };
+              sel_r = sel(false);
+              sel_i = sel(true);
+            }
+            if (!gph_on) {
+              o << "    double gphx = 1.0, gphy = 0.0;\n";
+              gph_on = true;
+            }
+            oo << "      { const double fr = " << sel_r << ", fi = " << sel_i << ";\n"
+               << "        const double tx = fma(gphx, fr, -gphy * fi); gphy = fma(gphx, fi, gphy * fr); gphx = tx; }\n";
+            o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+          } else {   // one register bit, one run-time bit
+            const bool a_reg = !rta;
+            const int rbit_reg = a_reg ? ra : rb;
+            const std::string RT = "rt" + std::to_string(a_reg ? f.qb : f.qa);
+            std::ostringstream oo;
+            pool.begin_op();
+            for (int k = 0; k < 16; ++k) {
+              const int bk = k >> rbit_reg & 1;
+              const cplx e0 = a_reg ? entry(bk, 0) : entry(0, bk), e1 = a_reg ? entry(bk, 1) : entry(1, bk);
+              if (e0 == e1) {
+                dph[k] *= e0;
+                continue;
+              }
+              const std::string v = g.r(k);
+              oo << "      { const double fr = " << RT << " ? " << g_pool->ref(e1.real()) << " : " << g_pool->ref(e0.real())
+                 << ", fi = " << RT << " ? " << g_pool->ref(e1.imag()) << " : " << g_pool->ref(e0.imag()) << ";\n"
+                 << "        const tq_d2 x = " << v << "; " << v << ".x = fma(fr, x.x, -fi * x.y); " << v
+                 << ".y = fma(fr, x.y, fi * x.x); }\n";
+            }
+            o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+          }
         }
-        continue;
       }
+    }
+    for (int it : (with_errors ? specs[ph].items : std::vector<int>())) {
+      const uint32_t oi = (uint32_t)it;
+      const OpDesc& od = pp.ops[oi];
+      const LGate& lg = gates[od.gate];
+      const int ci = (int)(oi - pd.op_begin);
+      const int ba = od.ra, bb = od.rb;
+      o << "    // g" << od.gate << "\n";
       if (od.type == OP_CX) {
         for (int k = 0; k < 16; ++k)
           if ((k >> ba & 1) && !(k >> bb & 1)) std::swap(g.rm[k], g.rm[k | 1 << bb]);
@@ -367,7 +722,13 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       }
       o << "      } }\n";
     }
-    if (!with_errors) {   // flush the pending phases
+    if (!with_errors) {   // flush the pending phases (run-time common factor, then compile-time)
+      if (gph_on)
+        for (int k = 0; k < 16; ++k) {
+          const std::string v = g.r(k);
+          o << "    { const tq_d2 x = " << v << "; " << v << ".x = fma(gphx, x.x, -gphy * x.y); " << v
+            << ".y = fma(gphx, x.y, gphy * x.x); }\n";
+        }
       std::ostringstream oo;
       pool.begin_op();
       for (int k = 0; k < 16; ++k) {
@@ -380,7 +741,19 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
     }
     if (last) {
-      o << "    const tq_u32 gbs = " << gb.str() << ";\n";
+      // fast path: physical tile qubit tile_q[p] holds logical qubit log_of_phys[tile_q[p]]
+      auto lq = [&](int p) { return with_errors ? (int)pd.tile_q[p] : log_of_phys[pd.tile_q[p]]; };
+      std::ostringstream gbl;
+      gbl << "gtile";
+      for (int m = 0; m < K - RBITS; ++m)
+        gbl << " | (((tid >> " << m << ") & 1u) << " << lq(P.tpos[m]) << ")";
+      for (int k = 0; k < 16; ++k) {
+        uint32_t go = 0;
+        for (int b = 0; b < RBITS; ++b)
+          if (k >> b & 1) go |= 1u << lq(P.rpos[b]);
+        goff[k] = go;
+      }
+      o << "    const tq_u32 gbs = " << gbl.str() << ";\n";
       for (int k = 0; k < 16; ++k) o << "    dst[gbs + " << goff[k] << "u] = " << g.r(k) << ";\n";
       if (pd.leaf_sums) {
         // |a|^2 sums of the 8-amplitude runs (qubits 0..2): reduce over the register bits
@@ -423,9 +796,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  }\n";
   }
   };
-  emit_phases(false);
+  emit_phases(fast, false);
   o << "  } else {\n";
-  emit_phases(true);
+  emit_phases(careful, true);
   o << "  }\n";
   o << "}\n";
   g_pool = nullptr;
