@@ -127,6 +127,8 @@ typedef struct {
   double pass_ms;                   /* sum of gate-pass launch durations (profile=1 only) */
   double measure_ms;                /* sum of measurement launch durations (profile=1 only) */
   uint64_t leaves;                  /* leaves sampled by this shard */
+  uint64_t noise_launches;          /* noise-row kernels (one per level batch) */
+  double noise_ms;                  /* sum of noise-row launch durations (profile=1 only) */
 } tqsim_stats;
 
 typedef struct {

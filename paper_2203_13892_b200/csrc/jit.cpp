@@ -45,6 +45,7 @@ struct TqJitArgs {
   const tq_d2* src; tq_d2* dst; tq_u64 seed; double p1, p2;
   tq_u64 child_first, parent_first; tq_u32 arity, batch;
   double* runsum;   // leaf level: |a|^2 sums of 8-amplitude runs, 2^(n-3) per state
+  const unsigned char* rows; tq_u32 row_bytes;   // noise rows of the batch (launch_noise_rows)
 };
 __device__ __forceinline__ void tq_pauli_rt(tq_d2& x, tq_d2& y, tq_u32 p) {
   if (p == 1u) { const tq_d2 t = x; x = y; y = t; }
@@ -61,6 +62,8 @@ struct HostJitArgs {   // mirrors TqJitArgs
   uint64_t child_first, parent_first;
   uint32_t arity, batch;
   double* runsum;
+  const void* rows;
+  uint32_t row_bytes;
 };
 
 std::string hexd(double v) {
@@ -323,7 +326,15 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
   return out;
 }
 
-PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool global_phase) {
+// Register layout of one phase: the 4 tile positions R held in registers, the
+// other K-4 on thread-index bits.  `coalesced` (the phases that touch HBM: the
+// first loads, the last stores) puts lanes on the remaining positions in
+// ascending order, so with R free of positions 0..2 lanes 0..2 walk qubits 0..2
+// and every warp access covers whole 128-byte lines (measured: scattered lanes
+// cost ~30% of HBM throughput, scripts/microbench/stream_bench.cu).  Exchange
+// phases put lanes 0..2 on positions of distinct residue mod 3, which makes the
+// 16-byte shared-memory accesses conflict-free under tq_swz.
+PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool coalesced) {
   for (int p = K - 1; p >= 0 && __builtin_popcountll(R) < RBITS; --p)
     if (!(R >> p & 1) && p >= low) R |= 1ull << p;
   for (int p = 0; p < K && __builtin_popcountll(R) < RBITS; ++p)
@@ -336,7 +347,7 @@ PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool global_phase) {
   for (int p = 0; p < K; ++p)
     if (!(R >> p & 1)) nonr.push_back(p);
   std::vector<int> tmap;
-  if (!global_phase && nonr.size() >= 3) {
+  if (!coalesced && nonr.size() >= 3) {
     std::vector<int> rest = nonr;
     for (int r = 0; r < 3; ++r)
       for (size_t i = 0; i < rest.size(); ++i)
@@ -353,77 +364,112 @@ PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool global_phase) {
   return P;
 }
 
-std::vector<PhaseSpec> plan_fast_phases(const std::vector<FOp>& fops, const PassDesc& pd,
-                                        const PhaseDesc& first) {
-  int qpos[64];
-  for (int q = 0; q < 64; ++q) qpos[q] = -1;
-  for (int p = 0; p < pd.K; ++p) qpos[pd.tile_q[p]] = p;
-  auto qmask = [&](const FOp& f) { return (1ull << f.qa) | (f.qb >= 0 ? 1ull << f.qb : 0ull); };
-  auto pmask = [&](const FOp& f) {
-    return (1ull << qpos[f.qa]) | (f.qb >= 0 ? 1ull << qpos[f.qb] : 0ull);
-  };
-  uint64_t R0 = 0;
-  for (int b = 0; b < RBITS; ++b) R0 |= 1ull << first.rpos[b];
+// One schedulable item of a phase plan: tile positions it needs in registers and
+// the global qubits it touches (for the order constraints).
+struct PItem {
+  uint64_t need, qm;
+  int idx;
+};
+
+// Greedy in-order grouping of items into register phases with commuting
+// look-ahead (an item moves ahead of deferred items only if it shares no qubit
+// with them).  Phase 0 is fixed to the register set R0 the kernel loads; the last
+// phase is the store layout: when `coal` it must hold no position < low in
+// registers, so a trailing re-layout phase is added if the last group needs one.
+std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint64_t R0, bool coal) {
+  const int low = std::min(LOW_Q, K);
+  const uint64_t lowm = (1ull << low) - 1;
   std::vector<std::pair<std::vector<int>, uint64_t>> groups;
-  std::vector<int> remaining(fops.size());
-  for (size_t i = 0; i < fops.size(); ++i) remaining[i] = (int)i;
-  bool firstg = true;
-  while (!remaining.empty() || firstg) {
-    uint64_t used = firstg ? R0 : 0, blocked = 0;
+  std::vector<int> remaining(items.size());
+  for (size_t i = 0; i < items.size(); ++i) remaining[i] = (int)i;
+  bool first = true;
+  while (first || !remaining.empty()) {
+    uint64_t used = first ? R0 : 0, blocked = 0;
     std::vector<int> in, deferred;
-    for (int fi : remaining) {
-      const FOp& f = fops[fi];
-      const uint64_t qm = qmask(f);
-      if (qm & blocked) {
-        deferred.push_back(fi);
-        blocked |= qm;
+    for (int ii : remaining) {
+      const PItem& it = items[ii];
+      if (it.qm & blocked) {
+        deferred.push_back(ii);
+        blocked |= it.qm;
         continue;
       }
-      if (f.kind == FOp::DIAG) {
-        in.push_back(fi);
-        continue;
-      }
-      const uint64_t need = pmask(f);
-      const bool ok = firstg ? ((need & ~R0) == 0) : (__builtin_popcountll(used | need) <= RBITS);
+      const bool ok = first ? (it.need & ~R0) == 0 : __builtin_popcountll(used | it.need) <= RBITS;
       if (ok) {
-        used |= need;
-        in.push_back(fi);
+        used |= it.need;
+        in.push_back(ii);
       } else {
-        deferred.push_back(fi);
-        blocked |= qm;
+        deferred.push_back(ii);
+        blocked |= it.qm;
       }
     }
-    if (!firstg && in.empty()) throw Error{TQSIM_EINTERNAL, "fast-path planner made no progress"};
+    if (!first && in.empty()) throw Error{TQSIM_EINTERNAL, "phase planner made no progress"};
     groups.emplace_back(std::move(in), used);
     remaining.swap(deferred);
-    firstg = false;
+    first = false;
   }
+  if (coal && groups.size() > 1 && (groups.back().second & lowm)) groups.emplace_back(std::vector<int>(), 0);
   std::vector<PhaseSpec> out;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     PhaseSpec ps;
-    if (gi == 0) ps.P = first;
-    else ps.P = make_phase_layout(groups[gi].second, pd.K, std::min(LOW_Q, pd.K), gi + 1 == groups.size());
-    ps.items = groups[gi].first;
+    const bool io = gi == 0 || gi + 1 == groups.size();
+    ps.P = make_phase_layout(gi == 0 ? R0 : groups[gi].second, K, low, io);
+    for (int ii : groups[gi].first) ps.items.push_back(items[ii].idx);
     out.push_back(ps);
   }
   return out;
+}
+
+// Register set of the load phase: as many leading items as fit in 4 positions
+// >= low (positions 0..low-1 stay on lanes: coalesced), padded with high positions.
+uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal) {
+  const int low = std::min(LOW_Q, K);
+  const uint64_t lowm = (1ull << low) - 1;
+  uint64_t used = 0, blocked = 0;
+  for (const PItem& it : items) {
+    if (it.qm & blocked) continue;
+    const bool ok = (!coal || !(it.need & lowm)) && __builtin_popcountll(used | it.need) <= RBITS;
+    if (ok) used |= it.need;
+    else blocked |= it.qm;
+  }
+  PhaseDesc P = make_phase_layout(used, K, low, true);
+  uint64_t R = 0;
+  for (int b = 0; b < RBITS; ++b) R |= 1ull << P.rpos[b];
+  return R;
 }
 
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs) {
   const int K = pd.K, T = 1 << (K - RBITS);
+  const int low = std::min(LOW_Q, K);
+  const bool coal = K - RBITS >= low;   // enough lane bits to keep qubits 0..2 on lanes 0..2
+  const uint32_t CROW = noise_row_bytes(pd.slice_len);
   const int nops = (int)(pd.op_end - pd.op_begin);
-  std::vector<PhaseSpec> careful;
-  for (uint32_t ph = pd.phase_begin; ph < pd.phase_end; ++ph) {
-    PhaseSpec ps;
-    ps.P = pp.phases[ph];
-    for (uint32_t oi = ps.P.op_begin; oi < ps.P.op_end; ++oi) ps.items.push_back((int)oi);
-    careful.push_back(ps);
-  }
+  int qpos[64];
+  for (int q = 0; q < 64; ++q) qpos[q] = -1;
+  for (int p = 0; p < K; ++p) qpos[pd.tile_q[p]] = p;
+  auto posm = [&](int qa, int qb) { return (1ull << qpos[qa]) | (qb >= 0 ? 1ull << qpos[qb] : 0ull); };
+  auto qmk = [&](int qa, int qb) { return (1ull << qa) | (qb >= 0 ? 1ull << qb : 0ull); };
+
   std::vector<int> log_of_phys;
   const std::vector<FOp> fops = fuse_fast_ops(pd, pp, gates, !pd.leaf_sums, log_of_phys);
-  const std::vector<PhaseSpec> fast = plan_fast_phases(fops, pd, pp.phases[pd.phase_begin]);
+  // fast path: diagonal ops need no register slot (index bits are known, jit below)
+  std::vector<PItem> fitems, citems;
+  for (size_t i = 0; i < fops.size(); ++i) {
+    const FOp& f = fops[i];
+    fitems.push_back({f.kind == FOp::DIAG ? 0ull : posm(f.qa, f.qb), qmk(f.qa, f.qb), (int)i});
+  }
+  // careful path: every gate in registers, its Pauli right after it
+  for (int i = 0; i < nops; ++i) {
+    const LGate& lg = gates[pp.ops[pd.op_begin + i].gate];
+    const int qb = lg.two ? (int)lg.q1 : -1;
+    citems.push_back({posm((int)lg.q0, qb), qmk((int)lg.q0, qb), (int)(pd.op_begin + i)});
+  }
+  // the load layout is shared by both paths (loaded before the error branch); the
+  // fast path (most instances) picks it.  SWAP relabelings change only the store.
+  const uint64_t R0 = choose_load_regs(fitems, K, coal);
+  const std::vector<PhaseSpec> fast = plan_phases(fitems, K, R0, coal);
+  const std::vector<PhaseSpec> careful = plan_phases(citems, K, R0, coal);
   if (const char* e = std::getenv("TQSIM_JIT_DEBUG")) {
     if (e[0] == '1') {
       std::fprintf(stderr, "[tqsim jit] %s: %d ops -> %zu fast ops; phases careful %zu fast %zu\n",
@@ -449,94 +495,82 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     pool.mode = (e && e[0] == '0') ? 0 : 2;
   }
   g_pool = &pool;
-  o << "static __constant__ tq_u32 GIDX[" << std::max(nops, 1) << "] = {";
-  for (int i = 0; i < nops; ++i) o << (i ? "," : "") << pp.ops[pd.op_begin + i].gate << "u";
-  if (!nops) o << "0u";
-  o << "};\nstatic __constant__ unsigned char TWO[" << std::max(nops, 1) << "] = {";
-  for (int i = 0; i < nops; ++i) o << (i ? "," : "") << (int)pp.ops[pd.op_begin + i].two;
-  if (!nops) o << "0";
-  o << "};\n";
   // 16 resident warps per SM (128 registers / thread), as many independent CTAs as fit
   const int minb = K >= 13 ? 1
                            : std::max(1, std::min(512 / T, (int)((227 * 1024) / ((16 << K) + 1024))));
   o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << std::min(minb, 32) << ") "
     << name << "(const TqJitArgs a, const TqCoef cf) {\n";
   if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
-  o << "  __shared__ unsigned char codes[" << std::max(nops, 1) << "];\n";
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
   o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
-  o << "  const tq_u64 inst = a.child_first + s;\n  tq_u32 gtile = 0u;\n";
+  o << "  tq_u32 gtile = 0u;\n";
   for (int i = 0; i < pd.n_out; ++i)
     o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << ";\n";
   o << "  tq_d2* __restrict__ dst = a.dst + ((tq_u64)s << " << n << ");\n";
   if (mode == 1)
-    o << "  const tq_d2* __restrict__ src = a.src + ((inst / a.arity - a.parent_first) << " << n << ");\n";
+    o << "  const tq_d2* __restrict__ src = a.src + ((((tq_u64)a.child_first + s) / a.arity - a.parent_first) << "
+      << n << ");\n";
   else if (mode == 2)
     o << "  const tq_d2* src = dst;\n";
   o << "  tq_d2 r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, r10, r11, r12, r13, r14, r15;\n";
-  // Wide states (n >= 20): the phase-0 loads are issued first so their HBM latency
-  // overlaps the noise draws (measured: C3 -3%; at n = 15 it costs C2 +4%).
-  const bool hoist = mode != 0 && n >= 20;
-  if (hoist) {
-    const PhaseDesc& P0 = pp.phases[pd.phase_begin];
-    o << "  {\n    const tq_u32 gb = gtile";
-    for (int m = 0; m < K - RBITS; ++m)
-      o << " | (((tid >> " << m << ") & 1u) << " << (int)pd.tile_q[P0.tpos[m]] << ")";
-    o << ";\n";
-    for (int k = 0; k < 16; ++k) {
-      uint32_t go = 0;
-      for (int b = 0; b < RBITS; ++b)
-        if (k >> b & 1) go |= 1u << pd.tile_q[P0.rpos[b]];
-      o << "    r" << k << " = src[gb + " << go << "u];\n";
-    }
-    o << "  }\n";
-  }
-  o << "  for (tq_u32 i = tid; i < " << nops << "u; i += " << T << "u)\n"
-    << "    codes[i] = (unsigned char)tq_noise_code(GIDX[i], inst, a.seed, TWO[i] ? a.p2 : a.p1, TWO[i] != 0);\n";
-  o << "  __syncthreads();\n";
-  // Error-free instances (the common case: no Pauli drawn for any gate of the
-  // pass) run a path without any per-gate error check; the others run the same
-  // pass with the keyed Pauli applied after its gate.  Uniform per CTA.
-  o << "  int any_err = 0;\n";
-  o << "  for (tq_u32 i = tid; i < " << nops << "u; i += " << T << "u) any_err |= codes[i] != 0;\n";
-  o << "  if (!__syncthreads_or(any_err)) {\n";
-  auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors) {
-  const int nph = (int)specs.size();
-  for (int ph = 0; ph < nph; ++ph) {
-    const PhaseDesc& P = specs[ph].P;
-    const bool first = ph == 0, last = ph == nph - 1;
-    g.reset_map();
-    // thread-dependent part of the tile-local index and of the global index
-    std::ostringstream lb, gb;
-    lb << "0u";
-    gb << "gtile";
+
+  // phase-0 registers, shared by both paths: the parent state in the first pass of a
+  // node (fused fan-out), |0..0> at the root, else the node's own state
+  auto offsets = [&](const PhaseDesc& P, const std::vector<int>* lq, uint32_t* goff, uint32_t* soff,
+                     std::string& lb, std::string& gb) {
+    auto qof = [&](int p) { return lq ? (*lq)[pd.tile_q[p]] : (int)pd.tile_q[p]; };
+    std::ostringstream l, gg;
+    l << "0u";
+    gg << "gtile";
     for (int m = 0; m < K - RBITS; ++m) {
-      lb << " | (((tid >> " << m << ") & 1u) << " << (int)P.tpos[m] << ")";
-      gb << " | (((tid >> " << m << ") & 1u) << " << (int)pd.tile_q[P.tpos[m]] << ")";
+      l << " | (((tid >> " << m << ") & 1u) << " << (int)P.tpos[m] << ")";
+      gg << " | (((tid >> " << m << ") & 1u) << " << qof(P.tpos[m]) << ")";
     }
-    uint32_t goff[16], soff[16];
     for (int k = 0; k < 16; ++k) {
       uint32_t go = 0, lo = 0;
       for (int b = 0; b < RBITS; ++b)
         if (k >> b & 1) {
-          go |= 1u << pd.tile_q[P.rpos[b]];
+          go |= 1u << qof(P.rpos[b]);
           lo |= 1u << P.rpos[b];
         }
       goff[k] = go;
       soff[k] = host_swz(lo);
     }
+    lb = l.str();
+    gb = gg.str();
+  };
+  auto emit_load = [&]() {
+    uint32_t goff[16], soff[16];
+    std::string lb, gb;
+    offsets(fast[0].P, nullptr, goff, soff, lb, gb);
+    o << "  {\n    const tq_u32 gb = " << gb << ";\n";
+    for (int k = 0; k < 16; ++k) {
+      if (mode == 0)
+        o << "    r" << k << ".x = (gb + " << goff[k] << "u == 0u) ? 1.0 : 0.0; r" << k << ".y = 0.0;\n";
+      else
+        o << "    r" << k << " = src[gb + " << goff[k] << "u];\n";
+    }
+    o << "  }\n";
+  };
+  emit_load();
+  // noise row of the instance (launch_noise_rows): error-free instances (the common
+  // case) run the fused fast path, the others apply each keyed Pauli after its gate
+  o << "  const unsigned char* __restrict__ codes = a.rows + (tq_u64)s * " << CROW << "u;\n";
+  o << "  const tq_u32 emask = __ldg(reinterpret_cast<const unsigned int*>(codes));\n";
+  o << "  if (!((emask >> " << std::min<uint32_t>(pd.pass_index, 31) << ") & 1u)) {\n";
+
+  auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors) {
+  const int nph = (int)specs.size();
+  for (int ph = 0; ph < nph; ++ph) {
+    const PhaseDesc& P = specs[ph].P;
+    const bool last = ph == nph - 1;
+    g.reset_map();
+    uint32_t goff[16], soff[16];
+    std::string lbs, gbs;
+    offsets(P, nullptr, goff, soff, lbs, gbs);
     o << "  { // phase " << ph << "\n";
-    if (first) {
-      if (mode == 0) {   // root: synthesize |0..0>
-        o << "    const tq_u32 gb = " << gb.str() << ";\n";
-        for (int k = 0; k < 16; ++k)
-          o << "    r" << k << ".x = (gb + " << goff[k] << "u == 0u) ? 1.0 : 0.0; r" << k << ".y = 0.0;\n";
-      } else if (!hoist) {
-        o << "    const tq_u32 gb = " << gb.str() << ";\n";
-        for (int k = 0; k < 16; ++k) o << "    r" << k << " = src[gb + " << goff[k] << "u];\n";
-      }
-    } else {
-      o << "    __syncthreads();\n    const tq_u32 sb = tq_swz(" << lb.str() << ");\n";
+    if (ph > 0) {
+      o << "    __syncthreads();\n    const tq_u32 sb = tq_swz(" << lbs << ");\n";
       for (int k = 0; k < 16; ++k) o << "    r" << k << " = tile[sb ^ " << soff[k] << "u];\n";
       o << "    __syncthreads();\n";
     }
@@ -544,7 +578,6 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     // generation time into a register renaming + a pending phase per logical
     // amplitude, folded into the next general gate's coefficients or applied once
     // at the end of the phase.  Exact up to fp rounding (R30).
-    typedef std::complex<double> cplx;
     cplx dph[16];
     for (int k = 0; k < 16; ++k) dph[k] = cplx(1.0, 0.0);
     auto permute = [&](auto perm) {   // new logical k <- old logical perm(k)
@@ -576,7 +609,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         if (f.qb >= 0 && rbit(f.qb) < 0) rtq |= 1ull << f.qb;
       }
       if (rtq) {
-        o << "    const tq_u32 gbp = " << gb.str() << ";\n";
+        o << "    const tq_u32 gbp = " << gbs << ";\n";
         for (int q = 0; q < 64; ++q)
           if (rtq >> q & 1) o << "    const bool rt" << q << " = (gbp >> " << q << ") & 1u;\n";
       }
@@ -663,8 +696,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       const uint32_t oi = (uint32_t)it;
       const OpDesc& od = pp.ops[oi];
       const LGate& lg = gates[od.gate];
-      const int ci = (int)(oi - pd.op_begin);
-      const int ba = od.ra, bb = od.rb;
+      const int ba = rbit((int)lg.q0), bb = lg.two ? rbit((int)lg.q1) : ba;
       o << "    // g" << od.gate << "\n";
       if (od.type == OP_CX) {
         for (int k = 0; k < 16; ++k)
@@ -675,9 +707,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             o << "    " << g.r(k) << ".x = -" << g.r(k) << ".x; " << g.r(k) << ".y = -" << g.r(k) << ".y;\n";
       } else {
         const double* m = lg.m;
-        const bool is_x = m[0] == 0 && m[1] == 0 && m[2] == 1 && m[3] == 0 && m[4] == 1 && m[5] == 0 &&
-                          m[6] == 0 && m[7] == 0;
-        if (is_x) {
+        if (is_x_gate(lg)) {
           for (int k = 0; k < 16; ++k)
             if (!(k >> ba & 1)) std::swap(g.rm[k], g.rm[k | 1 << ba]);
         } else if (od.type == OP_DIAG) {
@@ -707,9 +737,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
         }
       }
-      if (!with_errors) continue;
-      // keyed Pauli error after the gate (rare branch)
-      o << "    { const tq_u32 c = codes[" << ci << "];\n      if (c != 0u) {\n";
+      // keyed Pauli error after the gate (rare branch; P:277)
+      o << "    { const tq_u32 c = __ldg(codes + " << 4 + (od.gate - pd.slice_begin) << ");\n      if (c != 0u) {\n";
       if (od.two) {
         o << "        const tq_u32 pa = c >> 2, pb = c & 3u;\n";
         for (int k = 0; k < 16; ++k)
@@ -742,23 +771,15 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     }
     if (last) {
       // fast path: physical tile qubit tile_q[p] holds logical qubit log_of_phys[tile_q[p]]
-      auto lq = [&](int p) { return with_errors ? (int)pd.tile_q[p] : log_of_phys[pd.tile_q[p]]; };
-      std::ostringstream gbl;
-      gbl << "gtile";
-      for (int m = 0; m < K - RBITS; ++m)
-        gbl << " | (((tid >> " << m << ") & 1u) << " << lq(P.tpos[m]) << ")";
-      for (int k = 0; k < 16; ++k) {
-        uint32_t go = 0;
-        for (int b = 0; b < RBITS; ++b)
-          if (k >> b & 1) go |= 1u << lq(P.rpos[b]);
-        goff[k] = go;
-      }
-      o << "    const tq_u32 gbs = " << gbl.str() << ";\n";
-      for (int k = 0; k < 16; ++k) o << "    dst[gbs + " << goff[k] << "u] = " << g.r(k) << ";\n";
+      uint32_t gofs[16], sofs[16];
+      std::string lbx, gbl;
+      offsets(P, with_errors ? nullptr : &log_of_phys, gofs, sofs, lbx, gbl);
+      o << "    const tq_u32 gbs = " << gbl << ";\n";
+      for (int k = 0; k < 16; ++k) o << "    dst[gbs + " << gofs[k] << "u] = " << g.r(k) << ";\n";
       if (pd.leaf_sums) {
         // |a|^2 sums of the 8-amplitude runs (qubits 0..2): reduce over the register bits
         // holding positions 0..2, then butterfly-shuffle over the lane bits holding the
-        // rest (the last phase puts the lowest non-register positions on lanes 0..4).
+        // rest (the store layout puts the lowest non-register positions on lanes 0..4).
         int rbits_low = 0;      // register bits whose position is < RUN_Q
         for (int b = 0; b < RBITS; ++b)
           if (P.rpos[b] < RUN_Q) rbits_low |= 1 << b;
@@ -785,12 +806,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         for (int m : lane_bits) lane_mask |= 1 << m;
         o << "    if ((tid & " << lane_mask << "u) == 0u) {\n";
         for (size_t i = 0; i < reps.size(); ++i)
-          o << "      a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + ((gbs + " << goff[reps[i]] << "u) >> "
+          o << "      a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + ((gbs + " << gofs[reps[i]] << "u) >> "
             << RUN_Q << ")] = rs" << i << ";\n";
         o << "    }\n";
       }
     } else {
-      o << "    const tq_u32 sbs = tq_swz(" << lb.str() << ");\n";
+      o << "    const tq_u32 sbs = tq_swz(" << lbs << ");\n";
       for (int k = 0; k < 16; ++k) o << "    tile[sbs ^ " << soff[k] << "u] = " << g.r(k) << ";\n";
     }
     o << "  }\n";
@@ -798,6 +819,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   };
   emit_phases(fast, false);
   o << "  } else {\n";
+  // the careful path reloads its tile (L1/L2 hits): the fast path's registers are
+  // then dead across the branch, so the careful path's register pressure cannot
+  // make ptxas spill them in the common code
+  emit_load();
   emit_phases(careful, true);
   o << "  }\n";
   o << "}\n";
@@ -989,7 +1014,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
-                L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum)};
+                L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes};
   const uint64_t grid = (uint64_t)L.batch << pd.n_out;
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;

@@ -221,9 +221,45 @@ __global__ void noise_table_kernel(const uint8_t* two, uint32_t slice_begin, uin
   out[i] = (uint8_t)tq_noise_code(slice_begin + t, inst, seed, tw ? p2 : p1, tw);
 }
 
+// Noise rows (row a3, §2.5, "after each of the gates", R1/R7/R8): one
+// warp per instance of a level batch draws the keyed Pauli code of every gate of
+// the slice and ORs the pass bitmask the gate-pass kernels branch on (error-free
+// instances take the fused fast path).  Drawn once per instance, not per tile.
+__global__ void __launch_bounds__(256) noise_rows_kernel(
+    const uint8_t* __restrict__ two, const uint8_t* __restrict__ pass_of, uint32_t slice_begin,
+    uint32_t slice_len, uint64_t inst_first, uint32_t count, uint64_t seed, double p1, double p2,
+    uint32_t row_bytes, uint8_t* __restrict__ rows) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (w >= count) return;
+  const uint64_t inst = inst_first + w;
+  uint8_t* row = rows + w * row_bytes;
+  uint32_t mask = 0;
+  for (uint32_t t = lane; t < slice_len; t += 32u) {
+    const uint32_t g = slice_begin + t;
+    const bool tw = two[g] != 0;
+    const uint32_t c = tq_noise_code(g, inst, seed, tw ? p2 : p1, tw);
+    row[4 + t] = (uint8_t)c;
+    if (c) mask |= 1u << pass_of[g];
+  }
+  mask = __reduce_or_sync(0xffffffffu, mask);
+  if (lane == 0) *reinterpret_cast<uint32_t*>(row) = mask;
+}
+
 }  // namespace dev
 
 // ------------------------------------------------------------------ launchers
+int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t slice_begin,
+                      uint32_t slice_len, uint64_t inst_first, uint32_t count, uint64_t seed,
+                      double p1, double p2, uint32_t row_bytes, uint8_t* d_rows, void* stream) {
+  if (count == 0) return 0;
+  const uint64_t threads = (uint64_t)count * 32;
+  dev::noise_rows_kernel<<<(unsigned)((threads + 255) / 256), 256, 0,
+                           static_cast<cudaStream_t>(stream)>>>(
+      d_two, d_pass_of, slice_begin, slice_len, inst_first, count, seed, p1, p2, row_bytes, d_rows);
+  return (int)cudaGetLastError();
+}
+
 int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
                       double* sums, void* stream) {
   const uint64_t grid = (uint64_t)batch << (n_sim - chunk_log2);

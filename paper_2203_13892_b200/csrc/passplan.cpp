@@ -94,6 +94,9 @@ PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, cons
         if (!(H >> q & 1)) H |= 1ull << q;
       PassDesc pd;
       pd.K = K;
+      pd.slice_begin = (uint32_t)plan.bounds[d];
+      pd.pass_index = (uint32_t)pi;
+      pd.slice_len = (uint32_t)(plan.bounds[d + 1] - plan.bounds[d]);
       int pos = 0;
       int qpos[64];
       for (int q = 0; q < 64; ++q) qpos[q] = -1;

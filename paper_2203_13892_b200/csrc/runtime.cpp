@@ -31,10 +31,11 @@ struct tqsim_handle {
   std::vector<std::vector<tq::JitPass>> jit;   // specialized pass kernels [level][pass]
   double compile_s = 0.0;
   uint8_t* d_two = nullptr;
+  uint8_t* d_pass_of = nullptr;   // per lowered gate: index of its pass in its level (<= 31)
   tqsim_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<std::pair<int, size_t>> ev_marks;   // (kind 0 pass / 1 measure, event index)
+  std::vector<std::pair<int, size_t>> ev_marks;   // (kind 0 pass / 1 measure / 2 noise, event index)
   const tqsim_debug* debug = nullptr;
   cudaStream_t debug_stream = nullptr;
 };
@@ -98,7 +99,7 @@ void require_device() {
 struct Layout {
   std::vector<uint64_t> cap;       // states per level batch
   std::vector<uint64_t> off;       // byte offset of level buffer
-  uint64_t runs_off = 0, sums_off = 0, total = 0;
+  uint64_t runs_off = 0, sums_off = 0, rows_off = 0, total = 0;
   int chunk_log2 = 0;
 };
 
@@ -136,6 +137,12 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
     off = align_up(off + l.cap.back() * (8ull << (n - RUN_Q)));
     l.sums_off = off;
     off = align_up(off + l.cap.back() * (8ull << (n - l.chunk_log2)));
+    l.rows_off = off;   // noise rows of the level batch being executed (one level at a time)
+    uint64_t rows = 0;
+    for (size_t d = 0; d < levels; ++d)
+      rows = std::max<uint64_t>(rows, l.cap[d] * noise_row_bytes((uint32_t)(h->plan.bounds[d + 1] -
+                                                                            h->plan.bounds[d])));
+    off = align_up(off + rows);
     l.total = off;
     return off;
   };
@@ -212,8 +219,20 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   char* buf = x.ws + x.L.off[d];
   const char* pbuf = d > 0 ? x.ws + x.L.off[d - 1] : nullptr;
   const auto& passes = h->pp.levels[d];
+  const uint32_t slice_begin = (uint32_t)h->plan.bounds[d];
+  const uint32_t slice_len = (uint32_t)(h->plan.bounds[d + 1] - slice_begin);
+  const uint32_t row_bytes = noise_row_bytes(slice_len);
+  uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off);
   for (uint64_t b = i0; b < i1; b += cap) {
     const uint64_t cnt = std::min(cap, i1 - b);
+    // noise rows of the batch (row a3): keyed Pauli codes + per-pass error bitmask
+    mark(x, 2);
+    ck(launch_noise_rows(h->d_two, h->d_pass_of, slice_begin, slice_len, b, (uint32_t)cnt, x.seed,
+                         h->noise.p1, h->noise.p2, row_bytes, rows, x.st),
+       "noise rows launch");
+    mark(x, 2);
+    h->stats.kernel_launches++;
+    h->stats.noise_launches++;
     for (size_t p = 0; p < passes.size(); ++p) {
       PassLaunch pl{};
       pl.src_mode = p > 0 ? 2u : (d == 0 ? 0u : 1u);
@@ -227,6 +246,8 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       pl.p1 = h->noise.p1;
       pl.p2 = h->noise.p2;
       pl.runsum = x.ws + x.L.runs_off;
+      pl.rows = rows;
+      pl.row_bytes = row_bytes;
       mark(x, 0);
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
       mark(x, 0);
@@ -290,6 +311,14 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
       for (size_t g = 0; g < h->gates.size(); ++g) two[g] = h->gates[g].two ? 1 : 0;
       ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_two), two.size()), "cudaMalloc two");
       ckc(cudaMemcpy(h->d_two, two.data(), two.size(), cudaMemcpyHostToDevice), "upload two");
+      std::vector<uint8_t> pass_of(h->gates.size(), 0);
+      for (const auto& lvl : h->pp.levels)
+        for (const PassDesc& pd : lvl)
+          for (uint32_t oi = pd.op_begin; oi < pd.op_end; ++oi)
+            pass_of[h->pp.ops[oi].gate] = (uint8_t)std::min<uint32_t>(pd.pass_index, 31);
+      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_pass_of), pass_of.size()), "cudaMalloc pass_of");
+      ckc(cudaMemcpy(h->d_pass_of, pass_of.data(), pass_of.size(), cudaMemcpyHostToDevice),
+          "upload pass_of");
       // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
       h->jit = jit_build(h->pp, h->gates, &h->compile_s);
 
@@ -322,7 +351,8 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
                                h->ev_pool[h->ev_marks[i + 1].second]),
           "cudaEventElapsedTime");
       if (h->ev_marks[i].first == 0) h->stats.pass_ms += ms;
-      else h->stats.measure_ms += ms;
+      else if (h->ev_marks[i].first == 1) h->stats.measure_ms += ms;
+      else h->stats.noise_ms += ms;
     }
   }
 }
@@ -514,6 +544,7 @@ tqsim_status tqsim_get_stats(const tqsim_handle* h, tqsim_stats* out) {
 void tqsim_destroy(tqsim_handle* h) {
   if (!h) return;
   if (h->d_two) cudaFree(h->d_two);
+  if (h->d_pass_of) cudaFree(h->d_pass_of);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   delete h;
 }

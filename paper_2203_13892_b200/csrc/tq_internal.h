@@ -81,6 +81,9 @@ struct PassDesc {
   uint32_t op_begin = 0, op_end = 0;
   uint64_t tile_mask = 0;
   bool leaf_sums = false;       // last pass of the leaf level: also writes |a|^2 run sums
+  uint32_t slice_begin = 0;     // first lowered gate of the level's slice
+  uint32_t pass_index = 0;      // index of this pass within its level
+  uint32_t slice_len = 0;       // gates of the level's slice
 };
 
 struct PassPlan {
@@ -106,7 +109,17 @@ struct PassLaunch {
   uint64_t seed;
   double p1, p2;
   void* runsum;                 // leaf |a|^2 run sums (leaf_sums passes only)
+  const void* rows;             // noise rows of the batch (launch_noise_rows), row_bytes each
+  uint32_t row_bytes;
 };
+
+// Noise rows of one level batch (row a3): per instance a row of row_bytes bytes,
+// [0..4) = u32 bitmask of the level's passes with >= 1 drawn error (bit min(p, 31)),
+// [4 + t] = Pauli code of slice gate t (0 = none).  One warp per instance.
+inline uint32_t noise_row_bytes(uint32_t slice_len) { return (4u + slice_len + 15u) / 16u * 16u; }
+int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t slice_begin,
+                      uint32_t slice_len, uint64_t inst_first, uint32_t count, uint64_t seed,
+                      double p1, double p2, uint32_t row_bytes, uint8_t* d_rows, void* stream);
 
 int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
                       double* sums, void* stream);

@@ -78,7 +78,7 @@ class tqsim_stats(C.Structure):
                 ("measure_launches", C.c_uint64), ("node_executions", C.c_uint64),
                 ("gate_amp_updates", C.c_uint64), ("pass_bytes", C.c_uint64),
                 ("measure_bytes", C.c_uint64), ("pass_ms", C.c_double), ("measure_ms", C.c_double),
-                ("leaves", C.c_uint64)]
+                ("leaves", C.c_uint64), ("noise_launches", C.c_uint64), ("noise_ms", C.c_double)]
 
 
 class tqsim_result(C.Structure):
