@@ -47,10 +47,11 @@ struct TqJitArgs {
   double* runsum;   // leaf level: |a|^2 sums of 8-amplitude runs, 2^(n-3) per state
   const unsigned char* rows; tq_u32 row_bytes;   // noise rows of the batch (launch_noise_rows)
 };
-__device__ __forceinline__ void tq_pauli_rt(tq_d2& x, tq_d2& y, tq_u32 p) {
-  if (p == 1u) { const tq_d2 t = x; x = y; y = t; }
-  else if (p == 2u) { const tq_d2 t = x; x.x = y.y; x.y = -y.x; y.x = -t.y; y.y = t.x; }
-  else if (p == 3u) { y.x = -y.x; y.y = -y.y; }
+// r *= i^q
+__device__ __forceinline__ void tq_rot(tq_d2& r, tq_u32 q) {
+  const double a = (q & 1u) ? r.y : r.x, b = (q & 1u) ? r.x : r.y;
+  r.x = (((q + 1u) >> 1) & 1u) ? -a : a;
+  r.y = ((q >> 1) & 1u) ? -b : b;
 }
 )TQ";
 
@@ -158,11 +159,31 @@ struct Gen {
 // phases around the non-diagonal gates only (fewer shared-memory tile exchanges).
 typedef std::complex<double> cplx;
 
+// Effect of the keyed Pauli of one gate (code c) propagated to the END of the fused
+// run containing the gate: E' = R E R^dagger with R the run's later gates (monomial,
+// so E' = (diagonal) x (bit flips)).  Either Pauli-type E' = i^k X^x Z^z, or generic
+// E' = D X^x with D a diagonal on the run's two qubits.  Masks over PHYSICAL tile
+// positions (after the run's SWAP relabeling, if any).
+struct ErrEff {
+  uint32_t x = 0, z = 0, k = 0;
+  bool generic = false;
+  cplx D[4];                // generic: entry for local index bit_s0 | bit_s1 << 1
+};
+struct ErrSite {
+  uint32_t gate = 0;        // lowered gate index g
+  uint32_t local = 0;       // index of the gate in the pass's op list
+  std::vector<ErrEff> eff;  // per code c = 1..(3 or 15)
+};
+
 struct FOp {
-  enum Kind { GEN, XPERM, CX, DIAG } kind = GEN;
-  int qa = -1, qb = -1;   // global qubits (qb = -1: one-qubit op)
+  enum Kind { GEN, XPERM, CX, DIAG, NOP } kind = GEN;
+  int qa = -1, qb = -1;   // global (physical) qubits (qb = -1: one-qubit op)
   cplx m[4];              // GEN: row-major 2x2
   cplx d[4];              // DIAG: entry for index bit_qa | bit_qb << 1
+  // careful path: the run's gates in order, and its two PHYSICAL qubits after the run
+  // (the local frame of generic error diagonals; -1 = dummy slot)
+  std::vector<ErrSite> sites;
+  int ea = -1, eb = -1;
 };
 
 struct PhaseSpec {
@@ -247,12 +268,96 @@ bool is_swap(const M4& P) {   // exchanges |01> and |10>, fixes |00>, |11>
 // not executed: both qubits are tile qubits, so the swap is a relabeling of tile
 // positions -- later ops are rewritten to PHYSICAL qubit labels and the final store
 // writes position p to logical qubit log_of_phys[tile_q[p]].
+// Pauli p (0 I, 1 X, 2 Y, 3 Z) as a 2x2
+void pauli2(int p, cplx m[2][2]) {
+  const cplx I(0, 1);
+  m[0][0] = m[1][1] = m[0][1] = m[1][0] = 0;
+  if (p == 0) m[0][0] = m[1][1] = 1;
+  else if (p == 1) m[0][1] = m[1][0] = 1;
+  else if (p == 2) { m[0][1] = -I; m[1][0] = I; }
+  else { m[0][0] = 1; m[1][1] = -1; }
+}
+
+// 4x4 of Pauli pa on slot a and pb on slot b (local index bit_s0 | bit_s1 << 1)
+M4 pauli4(int pa, int slot_a, int pb, int slot_b) {
+  cplx A[2][2], B[2][2];
+  pauli2(pa, A);
+  pauli2(pb, B);
+  M4 r;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      const int ia = (i >> slot_a) & 1, ja = (j >> slot_a) & 1;
+      const int ib = (i >> slot_b) & 1, jb = (j >> slot_b) & 1;
+      r.a[i][j] = A[ia][ja] * B[ib][jb];
+    }
+  return r;
+}
+
+M4 dagger(const M4& m) {
+  M4 r;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) r.a[i][j] = std::conj(m.a[j][i]);
+  return r;
+}
+
+bool near(const cplx& a, const cplx& b) { return std::abs(a - b) < 1e-13; }
+
+// E' = R E R^dagger (monomial) -> Pauli-type i^k X^x Z^z or generic D X^x, local masks
+ErrEff decompose(const M4& M) {
+  ErrEff e;
+  int xe = -1;
+  for (int r = 0; r < 4; ++r)
+    if (std::abs(M.a[r][0]) > 1e-12) xe = r;
+  if (xe < 0) throw Error{TQSIM_EINTERNAL, "error propagation: not monomial"};
+  cplx v[4];
+  for (int j = 0; j < 4; ++j) {
+    for (int r = 0; r < 4; ++r)
+      if (r != (j ^ xe) && std::abs(M.a[r][j]) > 1e-12)
+        throw Error{TQSIM_EINTERNAL, "error propagation: not an X-type permutation"};
+    v[j] = M.a[j ^ xe][j];
+  }
+  e.x = (uint32_t)xe;
+  const cplx I(0, 1), ph[4] = {cplx(1, 0), I, cplx(-1, 0), -I};
+  int k = -1;
+  for (int t = 0; t < 4; ++t)
+    if (near(v[0], ph[t])) k = t;
+  bool pauli = k >= 0;
+  uint32_t z = 0;
+  if (pauli) {
+    for (int b = 0; b < 2; ++b) {
+      const cplx rr = v[1 << b] / v[0];
+      if (near(rr, cplx(-1, 0))) z |= 1u << b;
+      else if (!near(rr, cplx(1, 0))) pauli = false;
+    }
+    if (pauli)
+      for (int j = 0; j < 4; ++j)
+        if (!near(v[j], v[0] * ((__builtin_popcount(z & (uint32_t)j) & 1) ? -1.0 : 1.0))) pauli = false;
+  }
+  if (pauli) {
+    e.k = (uint32_t)k;
+    e.z = z;
+  } else {
+    // M = D X^x: D(i) = M[i][i ^ x]
+    e.generic = true;
+    for (int i = 0; i < 4; ++i) e.D[i] = M.a[i][i ^ xe];
+  }
+  return e;
+}
+
+// Fast-path op list.  SWAPs (a fused run whose product is the swap permutation) are
+// not executed: both qubits are tile qubits, so the swap is a relabeling of tile
+// positions -- later ops are rewritten to PHYSICAL qubit labels and the final store
+// writes position p to logical qubit log_of_phys[tile_q[p]].  Runs that cancel to
+// the identity become NOPs (they still carry their gates' error sites).
 std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
                                const std::vector<LGate>& gates, bool allow_swap,
                                std::vector<int>& log_of_phys) {
   std::vector<FOp> out;
   std::vector<int> phys_of(64);
   for (int q = 0; q < 64; ++q) phys_of[q] = q;
+  int qpos[64];
+  for (int q = 0; q < 64; ++q) qpos[q] = -1;
+  for (int p = 0; p < pd.K; ++p) qpos[pd.tile_q[p]] = p;
   const int n = (int)(pd.op_end - pd.op_begin);
   auto lg_of = [&](int i) -> const LGate& { return gates[pp.ops[pd.op_begin + i].gate]; };
   int i = 0;
@@ -274,10 +379,8 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
         else ok = false;
       }
       if (!ok) break;
-      if (s1 < 0 && ns1 >= 0) {
-        // lift: the product so far acted on s0 with a placeholder second slot; the
-        // placeholder was identity, so the 4x4 is unchanged when s1 becomes real.
-      }
+      // (a product over s0 alone used a placeholder second slot on which it acts
+      // as the identity, so the 4x4 is unchanged when s1 becomes a real qubit)
       s1 = ns1;
       P = op_matrix(gj, s0, s1 < 0 ? (s0 == 0 ? 1 : 0) : s1).mul(P);
       if (P.diagonal()) {
@@ -289,13 +392,18 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
         sw1 = s1;
       }
     }
+    FOp f;
+    int e_end, S1;
     if (best_swap > best) {   // relabel instead of moving amplitudes
+      e_end = best_swap;
+      S1 = sw1;
       std::swap(phys_of[s0], phys_of[sw1]);
-      i = best_swap + 1;
-      continue;
-    }
-    if (best >= 0) {
-      FOp f;
+      f.kind = FOp::NOP;
+      f.qa = phys_of[s0];   // the pair of physical qubits the relabeling exchanges
+      f.qb = phys_of[sw1];
+    } else if (best >= 0) {
+      e_end = best;
+      S1 = bs1;
       f.kind = FOp::DIAG;
       f.qa = phys_of[s0];
       f.qb = bs1 >= 0 ? phys_of[bs1] : -1;
@@ -303,23 +411,60 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
       bool trivial = true;
       for (int k = 0; k < 4; ++k)
         if (f.d[k] != cplx(1, 0)) trivial = false;
-      if (!trivial) out.push_back(f);
-      i = best + 1;
-      continue;
-    }
-    FOp f;
-    f.qa = phys_of[g0.q0];
-    if (g0.two) {   // CX (CZ is diagonal and handled above)
-      f.kind = FOp::CX;
-      f.qb = phys_of[g0.q1];
-    } else if (is_x_gate(g0)) {
-      f.kind = FOp::XPERM;
+      if (trivial) f.kind = FOp::NOP;
     } else {
-      f.kind = FOp::GEN;
-      for (int k = 0; k < 4; ++k) f.m[k] = cplx(g0.m[2 * k], g0.m[2 * k + 1]);
+      e_end = i;
+      S1 = g0.two ? (int)g0.q1 : -1;
+      f.qa = phys_of[g0.q0];
+      if (g0.two) {   // CX (CZ is diagonal and handled above)
+        f.kind = FOp::CX;
+        f.qb = phys_of[g0.q1];
+      } else if (is_x_gate(g0)) {
+        f.kind = FOp::XPERM;
+      } else {
+        f.kind = FOp::GEN;
+        for (int k = 0; k < 4; ++k) f.m[k] = cplx(g0.m[2 * k], g0.m[2 * k + 1]);
+      }
     }
+    // error sites of the run (careful path): each gate's Pauli pushed to the run end
+    const int slot1 = S1 >= 0 ? S1 : (s0 == 0 ? 1 : 0);
+    std::vector<M4> mats;
+    for (int t = i; t <= e_end; ++t) mats.push_back(op_matrix(lg_of(t), s0, slot1));
+    f.ea = qpos[phys_of[s0]];
+    f.eb = S1 >= 0 ? qpos[phys_of[S1]] : -1;
+    M4 R = M4::id();   // product of the gates after t
+    std::vector<ErrSite> sites(e_end - i + 1);
+    for (int t = e_end; t >= i; --t) {
+      const LGate& lg = lg_of(t);
+      ErrSite& es = sites[t - i];
+      es.gate = pp.ops[pd.op_begin + t].gate;
+      es.local = (uint32_t)t;
+      const M4 Rd = dagger(R);
+      auto slot = [&](int q) { return q == s0 ? 0 : 1; };
+      const int ncode = lg.two ? 15 : 3;
+      for (int c = 1; c <= ncode; ++c) {
+        M4 E = lg.two ? pauli4(c >> 2, slot((int)lg.q0), c & 3, slot((int)lg.q1))
+                      : pauli4(c, slot((int)lg.q0), 0, 1 - slot((int)lg.q0));
+        ErrEff ef = decompose(R.mul(E).mul(Rd));
+        // local slot masks -> physical tile positions after the run
+        auto to_pos = [&](uint32_t m) {
+          uint32_t r = 0;
+          if (m & 1u) r |= 1u << f.ea;
+          if (m & 2u) {
+            if (f.eb < 0) throw Error{TQSIM_EINTERNAL, "error propagation touched the placeholder slot"};
+            r |= 1u << f.eb;
+          }
+          return r;
+        };
+        ef.x = to_pos(ef.x);
+        ef.z = to_pos(ef.z);
+        es.eff.push_back(ef);
+      }
+      R = R.mul(mats[t - i]);
+    }
+    f.sites = std::move(sites);
     out.push_back(f);
-    ++i;
+    i = e_end + 1;
   }
   log_of_phys.assign(64, 0);
   for (int q = 0; q < 64; ++q) log_of_phys[phys_of[q]] = q;
@@ -453,38 +598,33 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
 
   std::vector<int> log_of_phys;
   const std::vector<FOp> fops = fuse_fast_ops(pd, pp, gates, !pd.leaf_sums, log_of_phys);
-  // fast path: diagonal ops need no register slot (index bits are known, jit below)
-  std::vector<PItem> fitems, citems;
+  // diagonal ops need no register slot (index bits are known, jit below)
+  std::vector<PItem> fitems;
   for (size_t i = 0; i < fops.size(); ++i) {
     const FOp& f = fops[i];
-    fitems.push_back({f.kind == FOp::DIAG ? 0ull : posm(f.qa, f.qb), qmk(f.qa, f.qb), (int)i});
+    const bool noreg = f.kind == FOp::DIAG || f.kind == FOp::NOP;
+    fitems.push_back({noreg ? 0ull : posm(f.qa, f.qb), qmk(f.qa, f.qb), (int)i});
   }
-  // careful path: every gate in registers, its Pauli right after it
-  for (int i = 0; i < nops; ++i) {
-    const LGate& lg = gates[pp.ops[pd.op_begin + i].gate];
-    const int qb = lg.two ? (int)lg.q1 : -1;
-    citems.push_back({posm((int)lg.q0, qb), qmk((int)lg.q0, qb), (int)(pd.op_begin + i)});
-  }
-  // the load layout is shared by both paths (loaded before the error branch); the
-  // fast path (most instances) picks it.  SWAP relabelings change only the store.
+  // One phase plan for both paths: the error-free fast path and the careful path,
+  // which runs the same fused ops under a run-time Pauli frame (below).
   const uint64_t R0 = choose_load_regs(fitems, K, coal);
   const std::vector<PhaseSpec> fast = plan_phases(fitems, K, R0, coal);
-  const std::vector<PhaseSpec> careful = plan_phases(citems, K, R0, coal);
   if (const char* e = std::getenv("TQSIM_JIT_DEBUG")) {
     if (e[0] == '1') {
-      std::fprintf(stderr, "[tqsim jit] %s: %d ops -> %zu fast ops; phases careful %zu fast %zu\n",
-                   name.c_str(), nops, fops.size(), careful.size(), fast.size());
+      std::fprintf(stderr, "[tqsim jit] %s: %d ops -> %zu fused ops; %zu phases\n", name.c_str(), nops,
+                   fops.size(), fast.size());
       for (size_t ph = 0; ph < fast.size(); ++ph) {
-        std::fprintf(stderr, "   fast phase %zu R=", ph);
+        std::fprintf(stderr, "   phase %zu R=", ph);
         for (int b = 0; b < RBITS; ++b) std::fprintf(stderr, "%d,", pd.tile_q[fast[ph].P.rpos[b]]);
         std::fprintf(stderr, " ops:");
+        static const char* kn[] = {"G", "X", "CX", "D", "NOP"};
         for (int it : fast[ph].items)
-          std::fprintf(stderr, " %s(%d,%d)", fops[it].kind == FOp::DIAG ? "D" : fops[it].kind == FOp::GEN ? "G" : fops[it].kind == FOp::CX ? "CX" : "X", fops[it].qa, fops[it].qb);
+          std::fprintf(stderr, " %s(%d,%d)", kn[(int)fops[it].kind], fops[it].qa, fops[it].qb);
         std::fprintf(stderr, "\n");
       }
     }
   }
-  const bool use_smem = careful.size() > 1 || fast.size() > 1;
+  const bool use_smem = fast.size() > 1;
   threads = T;
   smem = use_smem ? (size_t)16 << K : 0;
   Gen g;
@@ -495,12 +635,57 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     pool.mode = (e && e[0] == '0') ? 0 : 2;
   }
   g_pool = &pool;
+  // Careful-path tables.  GOFF: slice-relative gate index of pass op li (its noise
+  // code is codes[4 + GOFF[li]]).  ERRW[li * 16 + c]: the propagated error of code c
+  // of op li -- bits 0..12 X mask (tile positions), 13..14 phase power k, 15 generic,
+  // 16..31 Z mask (Pauli-type) or index into GD (generic: 4 complex diagonal entries).
+  std::vector<uint32_t> errw((size_t)std::max(nops, 1) * 16, 0u);
+  std::vector<double> gd;
+  std::map<std::vector<double>, uint32_t> gd_index;
+  for (const FOp& f : fops)
+    for (const ErrSite& es : f.sites)
+      for (size_t c = 0; c < es.eff.size(); ++c) {
+        const ErrEff& ef = es.eff[c];
+        uint32_t w = (ef.x & 0x1fffu) | ((ef.k & 3u) << 13);
+        if (ef.generic) {
+          std::vector<double> key;
+          for (int i = 0; i < 4; ++i) {
+            key.push_back(ef.D[i].real());
+            key.push_back(ef.D[i].imag());
+          }
+          auto it = gd_index.find(key);
+          uint32_t di;
+          if (it == gd_index.end()) {
+            di = (uint32_t)(gd.size() / 8);
+            gd_index[key] = di;
+            gd.insert(gd.end(), key.begin(), key.end());
+          } else {
+            di = it->second;
+          }
+          if (di > 0xffffu) throw Error{TQSIM_EINTERNAL, "too many generic error diagonals"};
+          w |= 0x8000u | (di << 16);
+        } else {
+          w |= (ef.z & 0xffffu) << 16;
+        }
+        errw[(size_t)es.local * 16 + c + 1] = w;
+      }
+  o << "static __constant__ unsigned short GOFF[" << std::max(nops, 1) << "] = {";
+  for (int i = 0; i < nops; ++i) o << (i ? "," : "") << (pp.ops[pd.op_begin + i].gate - pd.slice_begin);
+  if (!nops) o << "0";
+  o << "};\nstatic __device__ const tq_u32 ERRW[" << errw.size() << "] = {";
+  for (size_t i = 0; i < errw.size(); ++i) o << (i ? "," : "") << errw[i] << "u";
+  o << "};\nstatic __device__ const double GD[" << std::max<size_t>(gd.size(), 8) << "] = {";
+  for (size_t i = 0; i < gd.size(); ++i) o << (i ? "," : "") << hexd(gd[i]);
+  if (gd.empty()) o << "0.0";
+  o << "};\n";
+  const int NW = std::max(1, (nops + 31) / 32);
   // 16 resident warps per SM (128 registers / thread), as many independent CTAs as fit
   const int minb = K >= 13 ? 1
-                           : std::max(1, std::min(512 / T, (int)((227 * 1024) / ((16 << K) + 1024))));
+                           : std::max(1, std::min(512 / std::max(T, 32), (int)((227 * 1024) / ((16 << K) + 1024))));
   o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << std::min(minb, 32) << ") "
     << name << "(const TqJitArgs a, const TqCoef cf) {\n";
   if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
+  o << "  __shared__ tq_u32 tq_errb[" << NW << "];\n";
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
   o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
   o << "  tq_u32 gtile = 0u;\n";
@@ -516,6 +701,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
 
   // phase-0 registers, shared by both paths: the parent state in the first pass of a
   // node (fused fan-out), |0..0> at the root, else the node's own state
+  uint32_t lo_last[16];   // tile-local position offsets of the registers (last offsets() call)
   auto offsets = [&](const PhaseDesc& P, const std::vector<int>* lq, uint32_t* goff, uint32_t* soff,
                      std::string& lb, std::string& gb) {
     auto qof = [&](int p) { return lq ? (*lq)[pd.tile_q[p]] : (int)pd.tile_q[p]; };
@@ -535,6 +721,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         }
       goff[k] = go;
       soff[k] = host_swz(lo);
+      lo_last[k] = lo;
     }
     lb = l.str();
     gb = gg.str();
@@ -638,7 +825,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             oo << "        " << vb << ".y = " << lin(a10.real(), a10.imag(), "x", a11.real(), a11.imag(), "y", true) << "; }\n";
           }
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
-        } else {   // DIAG
+        } else if (f.kind == FOp::DIAG) {
           const int ra = rbit(f.qa), rb = f.qb >= 0 ? rbit(f.qb) : -2;
           const bool rta = ra < 0, rtb = rb == -1;
           auto entry = [&](int bita, int bitb) { return f.d[bita | (bitb << 1)]; };
@@ -692,64 +879,189 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         }
       }
     }
-    for (int it : (with_errors ? specs[ph].items : std::vector<int>())) {
-      const uint32_t oi = (uint32_t)it;
-      const OpDesc& od = pp.ops[oi];
-      const LGate& lg = gates[od.gate];
-      const int ba = rbit((int)lg.q0), bb = lg.two ? rbit((int)lg.q1) : ba;
-      o << "    // g" << od.gate << "\n";
-      if (od.type == OP_CX) {
-        for (int k = 0; k < 16; ++k)
-          if ((k >> ba & 1) && !(k >> bb & 1)) std::swap(g.rm[k], g.rm[k | 1 << bb]);
-      } else if (od.type == OP_CZ) {
-        for (int k = 0; k < 16; ++k)
-          if ((k >> ba & 1) && (k >> bb & 1))
-            o << "    " << g.r(k) << ".x = -" << g.r(k) << ".x; " << g.r(k) << ".y = -" << g.r(k) << ".y;\n";
-      } else {
-        const double* m = lg.m;
-        if (is_x_gate(lg)) {
-          for (int k = 0; k < 16; ++k)
-            if (!(k >> ba & 1)) std::swap(g.rm[k], g.rm[k | 1 << ba]);
-        } else if (od.type == OP_DIAG) {
-          std::ostringstream oo;
-          pool.begin_op();
-          for (int k = 0; k < 16; ++k) {
-            const bool one = (k >> ba) & 1;
-            const double dr = one ? m[6] : m[0], di = one ? m[7] : m[1];
-            if (dr == 1.0 && di == 0.0) continue;
+    if (with_errors) {
+      // Careful path: the same fused ops on the stored state psi_s, with the true state
+      // = F psi_s for the run-time Pauli frame F = i^fk X^fx Z^fz (tile positions,
+      // uniform per CTA).  Cliffords (CX, X) run unchanged and conjugate the frame;
+      // GEN / DIAG ops run conjugated by the frame (F^+ U F); each drawn error, pushed
+      // to the end of its fused run at code generation time (ERRW), multiplies into the
+      // frame (and, for errors inside diagonal runs, applies a diagonal).  The frame is
+      // applied at the store (address XOR + phase).  Exact up to fp rounding (R30).
+      o << "    const tq_u32 lth = " << lbs << ";\n";
+      auto pos_bit = [&](int pos, const std::string& frame_bit_var, int k, std::string& expr) {
+        // index bit of tile position pos for register k (compile-time or thread bit) ^ frame bit
+        int rb = -1;
+        for (int b = 0; b < RBITS; ++b)
+          if (P.rpos[b] == pos) rb = b;
+        const std::string fb = frame_bit_var;
+        if (rb >= 0) expr = "(" + fb + " ^ " + std::to_string((k >> rb) & 1) + "u)";
+        else expr = "(" + fb + " ^ ((lth >> " + std::to_string(pos) + ") & 1u))";
+        return rb;
+      };
+      // apply a diagonal with entries E(i) (i = bit_pa | bit_pb << 1) under the frame:
+      // register k gets E((bits of k's index) ^ (frame X bits))
+      auto emit_frame_diag = [&](int pa, int pb, const std::string* ent /*8 exprs re,im x4*/,
+                                 bool rt_entries) {
+        o << "      { const tq_u32 xa = (fx >> " << pa << ") & 1u";
+        if (pb >= 0) o << ", xb = (fx >> " << pb << ") & 1u";
+        o << ";\n";
+        // classes of registers by (bit at pa, bit at pb)
+        std::map<std::string, std::vector<int>> cls;
+        for (int k = 0; k < 16; ++k) {
+          std::string ea, eb = "0u";
+          pos_bit(pa, "xa", k, ea);
+          if (pb >= 0) pos_bit(pb, "xb", k, eb);
+          cls["(" + ea + " | (" + eb + " << 1))"].push_back(k);
+        }
+        int ci = 0;
+        for (auto& kv : cls) {
+          bool all_one = !rt_entries;
+          if (!rt_entries)
+            for (int i = 0; i < (pb >= 0 ? 4 : 2); ++i)
+              if (ent[2 * i] != "1.0" || ent[2 * i + 1] != "0.0") all_one = false;
+          if (all_one) continue;
+          o << "        { const tq_u32 ic = " << kv.first << ";\n";
+          auto sel = [&](int part) {
+            if (pb < 0) return "(ic & 1u) ? " + ent[2 + part] + " : " + ent[part];
+            return "(ic & 2u) ? ((ic & 1u) ? " + ent[6 + part] + " : " + ent[4 + part] + ") : ((ic & 1u) ? " +
+                   ent[2 + part] + " : " + ent[part] + ")";
+          };
+          o << "          const double fr = " << sel(0) << ", fi = " << sel(1) << ";\n";
+          for (int k : kv.second) {
             const std::string v = g.r(k);
-            oo << "      { const tq_d2 x = " << v << "; " << v << ".x = " << lin(dr, di, "x", 0, 0, "x", false)
-               << "; " << v << ".y = " << lin(dr, di, "x", 0, 0, "x", true) << "; }\n";
+            o << "          { const tq_d2 x = " << v << "; " << v << ".x = fma(fr, x.x, -fi * x.y); " << v
+              << ".y = fma(fr, x.y, fi * x.x); }\n";
           }
-          o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
-        } else {
-          std::ostringstream oo;
+          o << "        }\n";
+          ++ci;
+        }
+        o << "      }\n";
+      };
+      for (int it : specs[ph].items) {
+        const FOp& f = fops[it];
+        const int pa = f.qa >= 0 ? qpos[f.qa] : -1, pb = f.qb >= 0 ? qpos[f.qb] : -1;
+        if (f.kind == FOp::CX) {
+          const int ba = rbit(f.qa), bb = rbit(f.qb);
+          permute([&](int k) { return k ^ (((k >> ba) & 1) << bb); });
+          o << "    fx ^= ((fx >> " << pa << ") & 1u) << " << pb << "; fz ^= ((fz >> " << pb << ") & 1u) << " << pa
+            << ";\n";
+        } else if (f.kind == FOp::XPERM) {
+          const int ba = rbit(f.qa);
+          permute([&](int k) { return k ^ (1 << ba); });
+          o << "    fk += ((fz >> " << pa << ") & 1u) << 1;\n";
+        } else if (f.kind == FOp::GEN) {
+          // F^+ U F on this qubit: variant v = x | z << 1 of Z^z X^x U X^x Z^z
+          const int ba = rbit(f.qa);
+          cplx V[4][4];   // [v][entry]
+          for (int v = 0; v < 4; ++v) {
+            cplx u[4] = {f.m[0], f.m[1], f.m[2], f.m[3]};
+            if (v & 1) { cplx t[4] = {u[3], u[2], u[1], u[0]}; for (int i = 0; i < 4; ++i) u[i] = t[i]; }
+            if (v & 2) { u[1] = -u[1]; u[2] = -u[2]; }
+            for (int i = 0; i < 4; ++i) V[v][i] = u[i];
+          }
           pool.begin_op();
+          std::ostringstream oo;
+          oo << "      const tq_u32 v = ((fx >> " << pa << ") & 1u) | (((fz >> " << pa << ") & 1u) << 1);\n";
+          std::string cr[4], ci[4];   // coefficient expressions
+          bool zr[4], zi[4];
+          for (int e = 0; e < 4; ++e) {
+            for (int part = 0; part < 2; ++part) {
+              double val[4];
+              bool same = true, zero = true;
+              for (int v = 0; v < 4; ++v) {
+                val[v] = part ? V[v][e].imag() : V[v][e].real();
+                if (val[v] != val[0]) same = false;
+                if (val[v] != 0.0) zero = false;
+              }
+              std::string ex;
+              if (same) ex = g_pool->ref(val[0]);
+              else {
+                const std::string nm = "c" + std::to_string(e) + (part ? "i" : "r");
+                oo << "      const double " << nm << " = (v & 2u) ? ((v & 1u) ? " << g_pool->ref(val[3]) << " : "
+                   << g_pool->ref(val[2]) << ") : ((v & 1u) ? " << g_pool->ref(val[1]) << " : " << g_pool->ref(val[0])
+                   << ");\n";
+                ex = nm;
+              }
+              (part ? ci[e] : cr[e]) = ex;
+              (part ? zi[e] : zr[e]) = zero;
+            }
+          }
+          // re/im of a*x + b*y with coefficient expressions (zero terms skipped)
+          auto linx = [&](int ea_, const std::string& x, int eb_, const std::string& y, bool imag) {
+            std::vector<std::string> t;
+            if (!imag) {
+              if (!zr[ea_]) t.push_back(cr[ea_] + " * " + x + ".x");
+              if (!zi[ea_]) t.push_back("-" + ci[ea_] + " * " + x + ".y");
+              if (!zr[eb_]) t.push_back(cr[eb_] + " * " + y + ".x");
+              if (!zi[eb_]) t.push_back("-" + ci[eb_] + " * " + y + ".y");
+            } else {
+              if (!zr[ea_]) t.push_back(cr[ea_] + " * " + x + ".y");
+              if (!zi[ea_]) t.push_back(ci[ea_] + " * " + x + ".x");
+              if (!zr[eb_]) t.push_back(cr[eb_] + " * " + y + ".y");
+              if (!zi[eb_]) t.push_back(ci[eb_] + " * " + y + ".x");
+            }
+            if (t.empty()) return std::string("0.0");
+            std::string e = t[0];
+            for (size_t i = 1; i < t.size(); ++i) e += " + " + t[i];
+            return "(" + e + ")";
+          };
           for (int k = 0; k < 16; ++k) {
             if (k >> ba & 1) continue;
             const std::string va = g.r(k), vb = g.r(k | 1 << ba);
             oo << "      { const tq_d2 x = " << va << ", y = " << vb << ";\n";
-            oo << "        " << va << ".x = " << lin(m[0], m[1], "x", m[2], m[3], "y", false) << ";\n";
-            oo << "        " << va << ".y = " << lin(m[0], m[1], "x", m[2], m[3], "y", true) << ";\n";
-            oo << "        " << vb << ".x = " << lin(m[4], m[5], "x", m[6], m[7], "y", false) << ";\n";
-            oo << "        " << vb << ".y = " << lin(m[4], m[5], "x", m[6], m[7], "y", true) << "; }\n";
+            oo << "        " << va << ".x = " << linx(0, "x", 1, "y", false) << ";\n";
+            oo << "        " << va << ".y = " << linx(0, "x", 1, "y", true) << ";\n";
+            oo << "        " << vb << ".x = " << linx(2, "x", 3, "y", false) << ";\n";
+            oo << "        " << vb << ".y = " << linx(2, "x", 3, "y", true) << "; }\n";
           }
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+        } else if (f.kind == FOp::DIAG) {
+          pool.begin_op();
+          std::string ent[8];
+          for (int i = 0; i < 4; ++i) {
+            const cplx d = f.d[i];
+            ent[2 * i] = d.real() == 1.0 ? "1.0" : d.real() == 0.0 ? "0.0" : g_pool->ref(d.real());
+            ent[2 * i + 1] = d.imag() == 0.0 ? "0.0" : g_pool->ref(d.imag());
+          }
+          o << "    {\n" << pool.decl.str();
+          emit_frame_diag(pa, pb, ent, false);
+          o << "    }\n";
+        }
+        // the run's drawn errors, in gate order (uniform branch; rare)
+        if (!f.sites.empty()) {
+          const uint32_t l0 = f.sites.front().local, l1 = f.sites.back().local;
+          bool any_gen = false;
+          for (const ErrSite& es : f.sites)
+            for (const ErrEff& ef : es.eff) any_gen |= ef.generic;
+          std::ostringstream cond;
+          cond << "0u";
+          for (uint32_t w = l0 >> 5; w <= (l1 >> 5); ++w) {
+            uint32_t m = 0;
+            for (uint32_t li = std::max(l0, w * 32); li <= std::min(l1, w * 32 + 31); ++li) m |= 1u << (li & 31);
+            cond << " | (eb" << w << " & " << m << "u)";
+          }
+          o << "    if (" << cond.str() << ") {\n";
+          o << "      for (tq_u32 li = " << l0 << "u; li <= " << l1 << "u; ++li) {\n";
+          o << "        if (!((tq_errb[li >> 5] >> (li & 31u)) & 1u)) continue;\n";
+          o << "        const tq_u32 c = codes[4u + GOFF[li]];\n";
+          o << "        const tq_u32 w = __ldg(ERRW + li * 16u + c);\n";
+          o << "        if (!(w & 0x8000u)) {\n"
+            << "          const tq_u32 ze = w >> 16;\n"
+            << "          fk += ((w >> 13) & 3u) + ((__popc(ze & fx) & 1u) << 1);\n"
+            << "          fx ^= w & 0x1fffu; fz ^= ze;\n";
+          if (any_gen) {
+            o << "        } else {\n          fx ^= w & 0x1fffu;\n"
+              << "          const double* __restrict__ D = GD + 8u * (w >> 16);\n";
+            std::string ent[8];
+            for (int i = 0; i < 8; ++i) {
+              ent[i] = "e" + std::to_string(i);
+              o << "          const double e" << i << " = __ldg(D + " << i << ");\n";
+            }
+            emit_frame_diag(f.ea, f.eb, ent, true);
+          }
+          o << "        }\n      }\n    }\n";
         }
       }
-      // keyed Pauli error after the gate (rare branch)
-      o << "    { const tq_u32 c = __ldg(codes + " << 4 + (od.gate - pd.slice_begin) << ");\n      if (c != 0u) {\n";
-      if (od.two) {
-        o << "        const tq_u32 pa = c >> 2, pb = c & 3u;\n";
-        for (int k = 0; k < 16; ++k)
-          if (!(k >> ba & 1)) o << "        tq_pauli_rt(" << g.r(k) << ", " << g.r(k | 1 << ba) << ", pa);\n";
-        for (int k = 0; k < 16; ++k)
-          if (!(k >> bb & 1)) o << "        tq_pauli_rt(" << g.r(k) << ", " << g.r(k | 1 << bb) << ", pb);\n";
-      } else {
-        for (int k = 0; k < 16; ++k)
-          if (!(k >> ba & 1)) o << "        tq_pauli_rt(" << g.r(k) << ", " << g.r(k | 1 << ba) << ", c);\n";
-      }
-      o << "      } }\n";
     }
     if (!with_errors) {   // flush the pending phases (run-time common factor, then compile-time)
       if (gph_on)
@@ -773,9 +1085,22 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       // fast path: physical tile qubit tile_q[p] holds logical qubit log_of_phys[tile_q[p]]
       uint32_t gofs[16], sofs[16];
       std::string lbx, gbl;
-      offsets(P, with_errors ? nullptr : &log_of_phys, gofs, sofs, lbx, gbl);
+      offsets(P, &log_of_phys, gofs, sofs, lbx, gbl);
       o << "    const tq_u32 gbs = " << gbl << ";\n";
-      for (int k = 0; k < 16; ++k) o << "    dst[gbs + " << gofs[k] << "u] = " << g.r(k) << ";\n";
+      std::string xl = "";
+      if (with_errors) {
+        // true state = i^fk X^fx Z^fz psi_s: amplitude at tile index i goes to i ^ fx,
+        // times i^fk (-1)^popc(fz & i); fx mapped to global (logical) address bits
+        o << "    tq_u32 xl = 0u;\n";
+        for (int p = 0; p < K; ++p)
+          o << "    xl |= ((fx >> " << p << ") & 1u) << " << log_of_phys[pd.tile_q[p]] << ";\n";
+        o << "    const tq_u32 zt = __popc(fz & lth);\n";
+        for (int k = 0; k < 16; ++k)
+          o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << lo_last[k] << "u)) << 1));\n";
+        xl = " ^ xl";
+      }
+      for (int k = 0; k < 16; ++k)
+        o << "    dst[(gbs + " << gofs[k] << "u)" << xl << "] = " << g.r(k) << ";\n";
       if (pd.leaf_sums) {
         // |a|^2 sums of the 8-amplitude runs (qubits 0..2): reduce over the register bits
         // holding positions 0..2, then butterfly-shuffle over the lane bits holding the
@@ -806,8 +1131,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         for (int m : lane_bits) lane_mask |= 1 << m;
         o << "    if ((tid & " << lane_mask << "u) == 0u) {\n";
         for (size_t i = 0; i < reps.size(); ++i)
-          o << "      a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + ((gbs + " << gofs[reps[i]] << "u) >> "
-            << RUN_Q << ")] = rs" << i << ";\n";
+          o << "      a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + (((gbs + " << gofs[reps[i]] << "u)" << xl
+            << ") >> " << RUN_Q << ")] = rs" << i << ";\n";
         o << "    }\n";
       }
     } else {
@@ -823,7 +1148,14 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // then dead across the branch, so the careful path's register pressure cannot
   // make ptxas spill them in the common code
   emit_load();
-  emit_phases(careful, true);
+  // bitmap of the pass ops whose gate drew an error
+  o << "  if (tid < " << NW << "u) tq_errb[tid] = 0u;\n  __syncthreads();\n";
+  o << "  for (tq_u32 li = tid; li < " << nops << "u; li += " << T << "u)\n"
+    << "    if (codes[4u + GOFF[li]] != 0) atomicOr(&tq_errb[li >> 5], 1u << (li & 31u));\n";
+  o << "  __syncthreads();\n";
+  for (int w = 0; w < NW; ++w) o << "  const tq_u32 eb" << w << " = tq_errb[" << w << "];\n";
+  o << "  tq_u32 fx = 0u, fz = 0u, fk = 0u;\n";
+  emit_phases(fast, true);
   o << "  }\n";
   o << "}\n";
   g_pool = nullptr;

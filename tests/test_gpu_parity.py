@@ -200,3 +200,33 @@ def test_device_philox_matches_curand():
     assert ref.curand_philox_ref(words.ctypes.data_as(C.c_void_p), C.c_uint64(4096),
                                  want.ctypes.data_as(C.c_void_p)) == 0
     assert np.array_equal(T.tqsim_debug_philox(words), want)
+
+
+def _structured_circuit(n, rng):
+    """QFT (lowered CP runs) + RZZ (CX.RZ.CX runs) + SWAPs + a general layer: every
+    fused-run kind of the fast path, so errors land inside diagonal runs (generic
+    propagated diagonals), inside SWAP relabelings and on single gates."""
+    from workloads.generators import g1, g2, random_3_regular_edges
+    gates = basis_prep_gates(int(rng.integers(0, 2 ** n)), n) + qft_gates(n)
+    edges = random_3_regular_edges(n, rng) if n % 2 == 0 else [(q, (q + 3) % n) for q in range(n)]
+    for (u, v) in edges:
+        gates += [g2("cx", u, v), g1("rz", v, float(rng.uniform(0, 6.28))), g2("cx", u, v)]
+    for q in range(n):
+        gates.append(g1("u", q, *[float(a) for a in rng.uniform(0, 6.28, 3)]))
+    for q in range(0, n - 1, 2):
+        gates.append(g2("swap", q, n - 1 - q))
+    gates.append(g2("cp", 0, n - 1, 0.7))
+    return gates
+
+
+@pytest.mark.parametrize("tile,p", [(0, 0.05), (7, 0.3), (9, 0.1), (12, 0.3), (10, 1.0)])
+def test_error_frame_structured(tile, p):
+    """The careful path (fused ops under a run-time Pauli frame) vs the oracle with many
+    errors per pass, including p = 1 (every gate draws a Pauli)."""
+    rng = np.random.default_rng(int(p * 1000) + tile)
+    n = 12
+    gates = _structured_circuit(n, rng)
+    nm = NoiseModel(p, min(1.0, 2 * p), 0.02, 0.03)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    run_and_compare(n, gates, nm, 24, [3, 2, 4], 77 + tile, opts,
+                    dumps=[(0, 0), (0, 2), (1, 5), (2, 23)])
