@@ -24,6 +24,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <set>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -786,6 +787,28 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       return -1;
     };
     bool gph_on = false;
+    struct FBv {
+      bool on = false;
+      bool one[2] = {true, true};   // F_b[v] still exactly 1 (never assigned)
+      std::string var[2];
+    };
+    FBv fb[RBITS];
+    std::set<std::string> declared;
+    // apply pending F_b to the registers (before an op mixing bit b), then reset it
+    auto fb_flush = [&](int b, int& gen) {
+      if (b < 0 || !fb[b].on) return;
+      for (int k = 0; k < 16; ++k) {
+        const int v = (k >> b) & 1;
+        if (fb[b].one[v]) continue;
+        const std::string X = fb[b].var[v], r = g.r(k);
+        o << "    { const tq_d2 x = " << r << "; " << r << ".x = fma(" << X << "r, x.x, -" << X << "i * x.y); " << r
+          << ".y = fma(" << X << "r, x.y, " << X << "i * x.x); }\n";
+      }
+      ++gen;
+      fb[b] = FBv();
+      for (int v = 0; v < 2; ++v)
+        fb[b].var[v] = "fb" + std::to_string(b) + "_" + std::to_string(v) + "g" + std::to_string(gen);
+    };
     if (!with_errors) {
       // run-time index bits of the qubits diagonal ops need outside the registers
       uint64_t rtq = 0;
@@ -800,16 +823,28 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         for (int q = 0; q < 64; ++q)
           if (rtq >> q & 1) o << "    const bool rt" << q << " = (gbp >> " << q << ") & 1u;\n";
       }
+      // Diagonals on (thread bit, register bit b) accumulate into per-thread factors
+      // F_b[0], F_b[1] (one per value of logical register bit b), applied once -- at
+      // the phase end through a product tree, or before an op that mixes bit b.
+      for (int b = 0; b < RBITS; ++b) {
+        fb[b] = FBv();
+        for (int v = 0; v < 2; ++v) fb[b].var[v] = "fb" + std::to_string(b) + "_" + std::to_string(v);
+      }
+      int fb_gen = 0;
       for (int it : specs[ph].items) {
         const FOp& f = fops[it];
         if (f.kind == FOp::CX) {
           const int ba = rbit(f.qa), bb = rbit(f.qb);
+          fb_flush(bb, fb_gen);
           permute([&](int k) { return k ^ (((k >> ba) & 1) << bb); });
         } else if (f.kind == FOp::XPERM) {
           const int ba = rbit(f.qa);
+          std::swap(fb[ba].var[0], fb[ba].var[1]);
+          std::swap(fb[ba].one[0], fb[ba].one[1]);
           permute([&](int k) { return k ^ (1 << ba); });
         } else if (f.kind == FOp::GEN) {
           const int ba = rbit(f.qa);
+          fb_flush(ba, fb_gen);
           std::ostringstream oo;
           pool.begin_op();
           for (int k = 0; k < 16; ++k) {
@@ -861,18 +896,31 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             const std::string RT = "rt" + std::to_string(a_reg ? f.qb : f.qa);
             std::ostringstream oo;
             pool.begin_op();
-            for (int k = 0; k < 16; ++k) {
-              const int bk = k >> rbit_reg & 1;
+            for (int bk = 0; bk < 2; ++bk) {
+              // e0 / e1: the entry for thread bit 0 / 1 at register-bit value bk
               const cplx e0 = a_reg ? entry(bk, 0) : entry(0, bk), e1 = a_reg ? entry(bk, 1) : entry(1, bk);
-              if (e0 == e1) {
-                dph[k] *= e0;
+              if (e0 == e1) {   // independent of the thread bit: a compile-time phase
+                for (int k = 0; k < 16; ++k)
+                  if ((k >> rbit_reg & 1) == bk) dph[k] *= e0;
                 continue;
               }
-              const std::string v = g.r(k);
-              oo << "      { const double fr = " << RT << " ? " << g_pool->ref(e1.real()) << " : " << g_pool->ref(e0.real())
-                 << ", fi = " << RT << " ? " << g_pool->ref(e1.imag()) << " : " << g_pool->ref(e0.imag()) << ";\n"
-                 << "        const tq_d2 x = " << v << "; " << v << ".x = fma(fr, x.x, -fi * x.y); " << v
-                 << ".y = fma(fr, x.y, fi * x.x); }\n";
+              FBv& F = fb[rbit_reg];
+              const std::string fr = RT + " ? " + g_pool->ref(e1.real()) + " : " + g_pool->ref(e0.real());
+              const std::string fi = RT + " ? " + g_pool->ref(e1.imag()) + " : " + g_pool->ref(e0.imag());
+              const std::string& X = F.var[bk];
+              if (F.one[bk]) {
+                if (!declared.count(X)) {
+                  o << "    double " << X << "r, " << X << "i;\n";
+                  declared.insert(X);
+                }
+                oo << "      " << X << "r = " << fr << "; " << X << "i = " << fi << ";\n";
+                F.one[bk] = false;
+              } else {
+                oo << "      { const double er = " << fr << ", ei = " << fi << ";\n"
+                   << "        const double t = fma(" << X << "r, er, -" << X << "i * ei); " << X << "i = fma(" << X
+                   << "r, ei, " << X << "i * er); " << X << "r = t; }\n";
+              }
+              F.on = true;
             }
             o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
           }
@@ -1063,13 +1111,39 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         }
       }
     }
-    if (!with_errors) {   // flush the pending phases (run-time common factor, then compile-time)
-      if (gph_on)
-        for (int k = 0; k < 16; ++k) {
-          const std::string v = g.r(k);
-          o << "    { const tq_d2 x = " << v << "; " << v << ".x = fma(gphx, x.x, -gphy * x.y); " << v
-            << ".y = fma(gphx, x.y, gphy * x.x); }\n";
-        }
+    if (!with_errors) {   // flush the pending phases (run-time factors, then compile-time)
+      // product tree T[idx] = gph * prod_{b in L} F_b[bit of idx], idx over the pending bits L
+      std::vector<int> L;
+      for (int b = 0; b < RBITS; ++b)
+        if (fb[b].on) L.push_back(b);
+      std::vector<std::string> Tn(1, gph_on ? std::string("gph") : std::string());
+      int tcount = 0;
+      for (size_t li = 0; li < L.size(); ++li) {
+        std::vector<std::string> nt(Tn.size() * 2);
+        for (size_t i = 0; i < Tn.size(); ++i)
+          for (int v = 0; v < 2; ++v) {
+            const FBv& F = fb[L[li]];
+            if (F.one[v]) { nt[i | (v << li)] = Tn[i]; continue; }
+            if (Tn[i].empty()) { nt[i | (v << li)] = F.var[v]; continue; }
+            const std::string nm = "tf" + std::to_string(tcount++), A = Tn[i], B = F.var[v];
+            auto re = [&](const std::string& x) { return x == "gph" ? std::string("gphx") : x + "r"; };
+            auto im = [&](const std::string& x) { return x == "gph" ? std::string("gphy") : x + "i"; };
+            o << "    const double " << nm << "r = fma(" << re(A) << ", " << re(B) << ", -" << im(A) << " * " << im(B)
+              << "), " << nm << "i = fma(" << re(A) << ", " << im(B) << ", " << im(A) << " * " << re(B) << ");\n";
+            nt[i | (v << li)] = nm;
+          }
+        Tn.swap(nt);
+      }
+      for (int k = 0; k < 16; ++k) {
+        size_t idx = 0;
+        for (size_t li = 0; li < L.size(); ++li) idx |= (size_t)((k >> L[li]) & 1) << li;
+        const std::string& X = Tn[idx];
+        if (X.empty()) continue;
+        const std::string xr = X == "gph" ? "gphx" : X + "r", xi = X == "gph" ? "gphy" : X + "i";
+        const std::string v = g.r(k);
+        o << "    { const tq_d2 x = " << v << "; " << v << ".x = fma(" << xr << ", x.x, -" << xi << " * x.y); " << v
+          << ".y = fma(" << xr << ", x.y, " << xi << " * x.x); }\n";
+      }
       std::ostringstream oo;
       pool.begin_op();
       for (int k = 0; k < 16; ++k) {
