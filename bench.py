@@ -300,7 +300,7 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "n_qubits": n, "shots": shots, "outcomes": N,
                        "arities": plan.arity_list, "lowered_gates": int(plan.n_lowered_gates),
-                       "tile_qubits": args.tile or (11 if n >= 22 else 12),
+                       "tile_qubits": int(plan.tile_qubits),
                        "l2": "inputs larger than L2 (state batches >= 1 GiB per launch group)",
                        "parallelism": "top-level branch sharding x%d" % world},
             "gate_amp_updates_per_s": gau,
@@ -314,7 +314,9 @@ def main():
                          "kernel": "tq_pass_l*_p* (run-time specialized gate pass, all launches)",
                          "pass_share_of_step": float(pt[0].item()) / (float(pt[0].item()) + float(pt[1].item()))
                          if (pt[0].item() + pt[1].item()) > 0 else None,
-                         "pass_launches_profiled": pass_launches},
+                         "pass_launches_profiled": pass_launches,
+                         "alg_bytes_per_launch": pass_bytes / pass_launches if pass_launches else None,
+                         "pass_launches_per_step": pass_launches / max(1, min(args.steps, 3))},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "e2e": e2e,

@@ -65,16 +65,36 @@ uint64_t PassPlan::passes_total(const std::vector<uint64_t>& inst) const {
   return t;
 }
 
+namespace {
+PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan, int K);
+}
+
 PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan,
                         const Options& o) {
+  if (o.tile_qubits) return make_pass_plan_k(gates, n_qubits, plan, (int)o.tile_qubits);
+  // Auto tile width (measured on B200): 2^11-amplitude tiles (4 CTAs x
+  // 4 warps per SM) hide HBM latency ~10% better than 2^12 tiles (2 CTAs x 8 warps) but
+  // may need more HBM passes; pick the smaller  sum_d instances_d * passes_d / eta_K.
+  const std::vector<uint64_t> inst = instances(plan);
+  PassPlan best;
+  double best_cost = 0.0;
+  for (int K : {12, 11}) {
+    PassPlan pp = make_pass_plan_k(gates, n_qubits, plan, K);
+    const double eta = K == 11 ? 1.10 : 1.0;
+    const double cost = (double)pp.passes_total(inst) / eta;
+    if (best.levels.empty() || cost < best_cost) {
+      best = std::move(pp);
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+namespace {
+PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan, int K) {
   PassPlan pp;
   const int n = std::max<int>((int)n_qubits, RBITS);
   pp.n_sim = n;
-  // Auto tile width (measured on B200): 2^12-amplitude tiles (2 CTAs
-  // x 8 warps per SM) for n < 22, where passes are FP64/latency bound; 2^11 tiles (4
-  // CTAs x 4 warps) for wide states, whose passes are HBM bound and gain more from
-  // independent CTAs than they lose to the extra passes.
-  int K = o.tile_qubits ? (int)o.tile_qubits : (n >= 22 ? 11 : 12);
   K = std::max(K, std::min(n, LOW_Q + 2));   // >= 2 free high slots so any 2q gate fits
   K = std::min(K, n);
   const int low = std::min(LOW_Q, K);
@@ -167,5 +187,6 @@ PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, cons
   }
   return pp;
 }
+}  // namespace
 
 }  // namespace tq

@@ -305,6 +305,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     h->n_sim = h->pp.n_sim;
     h->inst = instances(h->plan);
     fill_plan(h->plan, c->n_qubits, h->gates.size(), h->pp.passes_total(h->inst), &h->cplan);
+    h->cplan.tile_qubits = h->pp.levels.empty() || h->pp.levels[0].empty() ? 0u : (uint32_t)h->pp.levels[0][0].K;
     if (need_gpu) {
       require_device();
       std::vector<uint8_t> two(h->gates.size());

@@ -211,7 +211,7 @@ float time_it(Fn fn, int reps = 10) {
   return ms / reps;
 }
 
-int main() {
+int main(int argc, char** argv) {
   const size_t bytes = 1ull << 30, ntiles = bytes / (16 * TILE);
   d2* st; CK(cudaMalloc(&st, bytes)); CK(cudaMemset(st, 0, bytes));
   int nsm = 0; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
@@ -225,6 +225,12 @@ int main() {
     report("ldgsts X=" #X " F=" #F, time_it([&] { k<<<nsm, T, sm>>>(st, ntiles, c, s); })); }
 #define BULK(R, X, F) { auto k = bulk_kernel<R, X, F>; size_t sm = NS * TILE * 16; CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     report("bulk run=2^" #R " X=" #X " F=" #F, time_it([&] { k<<<nsm, T, sm>>>(st, ntiles, c, s); })); }
+  if (argc > 1) {   // compute-heavy sweep: does prefetching the next tile pay?
+    DIRECT(true, 1, 8) DIRECT(true, 1, 16) DIRECT(true, 1, 32) DIRECT(true, 2, 16)
+    LDGSTS(1, 8) LDGSTS(1, 16) LDGSTS(1, 32) LDGSTS(2, 16)
+    BULK(6, 1, 8) BULK(6, 1, 16) BULK(6, 1, 32) BULK(6, 2, 16)
+    return 0;
+  }
   DIRECT(true, 0, 0) DIRECT(false, 0, 0) DIRECT(true, 1, 0) DIRECT(false, 1, 0) DIRECT(true, 1, 4) DIRECT(true, 3, 2)
   LDGSTS(0, 0) LDGSTS(1, 0) LDGSTS(1, 4) LDGSTS(3, 2)
   BULK(3, 0, 0) BULK(6, 0, 0) BULK(12, 0, 0) BULK(6, 1, 0) BULK(6, 1, 4) BULK(6, 3, 2) BULK(3, 1, 0)
