@@ -32,6 +32,7 @@ struct tqsim_handle {
   double compile_s = 0.0;
   uint8_t* d_two = nullptr;
   uint8_t* d_pass_of = nullptr;   // per lowered gate: index of its pass in its level (<= 31)
+  std::vector<uint8_t> h_tables;  // host copy: [two flags | pass index] per lowered gate
   tqsim_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -158,6 +159,20 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
 std::mutex g_arena_mu;
 void* g_arena = nullptr;
 size_t g_arena_size = 0;
+cudaStream_t g_stream = nullptr;   // tqsim_run's stream (created once)
+
+// Prepared-handle cache of tqsim_run (the plan cache of FFT-style libraries): lowering,
+// DCP, pass plan and the run-time specialized kernels of a (circuit, noise, shots,
+// arities, options) input are reused by later calls with byte-identical inputs; the
+// per-gate device tables are still uploaded every call.  Guarded by g_arena_mu.
+struct CachedHandle {
+  std::string key;
+  tqsim_handle* h;
+  uint64_t last_use;
+};
+std::vector<CachedHandle> g_hcache;
+uint64_t g_hcache_clock = 0;
+constexpr size_t HCACHE_MAX = 8;
 
 void* arena_get(size_t bytes) {
   if (g_arena_size >= bytes) return g_arena;
@@ -289,6 +304,13 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   }
 }
 
+// per-gate device tables: 2q flag (noise class) and pass index (error bitmask bit)
+void upload_gate_tables(tqsim_handle* h, cudaStream_t st) {
+  const size_t G = h->h_tables.size() / 2;
+  ckc(cudaMemcpyAsync(h->d_two, h->h_tables.data(), G, cudaMemcpyHostToDevice, st), "upload two");
+  ckc(cudaMemcpyAsync(h->d_pass_of, h->h_tables.data() + G, G, cudaMemcpyHostToDevice, st), "upload pass_of");
+}
+
 tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,
                             const uint32_t* arities, uint32_t n_levels, const tqsim_options* o,
                             bool need_gpu) {
@@ -308,18 +330,17 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     h->cplan.tile_qubits = h->pp.levels.empty() || h->pp.levels[0].empty() ? 0u : (uint32_t)h->pp.levels[0][0].K;
     if (need_gpu) {
       require_device();
-      std::vector<uint8_t> two(h->gates.size());
-      for (size_t g = 0; g < h->gates.size(); ++g) two[g] = h->gates[g].two ? 1 : 0;
-      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_two), two.size()), "cudaMalloc two");
-      ckc(cudaMemcpy(h->d_two, two.data(), two.size(), cudaMemcpyHostToDevice), "upload two");
-      std::vector<uint8_t> pass_of(h->gates.size(), 0);
+      const size_t G = std::max<size_t>(h->gates.size(), 1);
+      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_two), G), "cudaMalloc two");
+      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_pass_of), G), "cudaMalloc pass_of");
+      h->h_tables.assign(2 * G, 0);
+      for (size_t g = 0; g < h->gates.size(); ++g) h->h_tables[g] = h->gates[g].two ? 1 : 0;
       for (const auto& lvl : h->pp.levels)
         for (const PassDesc& pd : lvl)
           for (uint32_t oi = pd.op_begin; oi < pd.op_end; ++oi)
-            pass_of[h->pp.ops[oi].gate] = (uint8_t)std::min<uint32_t>(pd.pass_index, 31);
-      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_pass_of), pass_of.size()), "cudaMalloc pass_of");
-      ckc(cudaMemcpy(h->d_pass_of, pass_of.data(), pass_of.size(), cudaMemcpyHostToDevice),
-          "upload pass_of");
+            h->h_tables[G + h->pp.ops[oi].gate] = (uint8_t)std::min<uint32_t>(pd.pass_index, 31);
+      upload_gate_tables(h, nullptr);
+      ckc(cudaStreamSynchronize(nullptr), "upload gate tables");
       // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
       h->jit = jit_build(h->pp, h->gates, &h->compile_s);
 
@@ -575,10 +596,40 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, u
   return guarded([&] {
     if (!out) throw Error{TQSIM_EINVAL, "out is NULL"};
     const auto t_start = std::chrono::steady_clock::now();
-    tqsim_handle* h = create_handle(c, nm, n_shots, arities, n_levels, o, true);
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    // cache key: the exact bytes of every input that shapes the prepared handle
+    std::string key;
+    auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+    if (!c || (!c->gates && c->n_gates)) throw Error{TQSIM_EINVAL, "circuit is NULL"};
+    validate_noise(nm);
+    put(&c->n_qubits, sizeof(c->n_qubits));
+    put(&c->n_gates, sizeof(c->n_gates));
+    put(c->gates, sizeof(tqsim_gate) * c->n_gates);
+    put(nm, sizeof(*nm));
+    put(&n_shots, sizeof(n_shots));
+    put(&n_levels, sizeof(n_levels));
+    if (arities) put(arities, sizeof(uint32_t) * n_levels);
+    else key.push_back('A');
+    if (o) put(o, sizeof(*o));
+    else key.push_back('D');
+    tqsim_handle* h = nullptr;
+    for (auto& e : g_hcache)
+      if (e.key == key) {
+        h = e.h;
+        e.last_use = ++g_hcache_clock;
+      }
+    if (!h) {
+      h = create_handle(c, nm, n_shots, arities, n_levels, o, true);
+      if (g_hcache.size() >= HCACHE_MAX) {
+        auto lru = std::min_element(g_hcache.begin(), g_hcache.end(),
+                                    [](const CachedHandle& a, const CachedHandle& b) { return a.last_use < b.last_use; });
+        tqsim_destroy(lru->h);
+        g_hcache.erase(lru);
+      }
+      g_hcache.push_back(CachedHandle{key, h, ++g_hcache_clock});
+    }
     cudaStream_t st = nullptr;
     try {
-      std::lock_guard<std::mutex> lock(g_arena_mu);
       h->debug = debug;
       uint64_t t0, t1;
       shard(h->cplan, 0, 1, t0, t1);
@@ -586,24 +637,27 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, u
       const uint64_t nout = h->cplan.n_outcomes;
       const uint64_t out_off = align_up(ws);
       char* base = static_cast<char*>(arena_get(out_off + nout * 4));
-      ckc(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+      if (!g_stream) ckc(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      st = g_stream;
+      // this call's per-gate tables (2q flags, pass index) from the host circuit
+      upload_gate_tables(h, st);
       uint32_t* d_out = reinterpret_cast<uint32_t*>(base + out_off);
       ckc(cudaMemsetAsync(d_out, 0, nout * 4, st), "memset outcomes");
       execute(h, seed, 0, 1, st, base, ws, d_out);
       std::vector<uint32_t> outs(nout);
       ckc(cudaMemcpyAsync(outs.data(), d_out, nout * 4, cudaMemcpyDeviceToHost, st), "D2H outcomes");
       ckc(cudaStreamSynchronize(st), "stream sync");
-      cudaStreamDestroy(st);
-      st = nullptr;
+      h->debug = nullptr;
       const double wall =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       build_result(h, outs, wall, out);
     } catch (...) {
-      if (st) cudaStreamDestroy(st);
+      h->debug = nullptr;
+      for (size_t i = 0; i < g_hcache.size(); ++i)   // a failed handle is not reused
+        if (g_hcache[i].h == h) g_hcache.erase(g_hcache.begin() + i);
       tqsim_destroy(h);
       throw;
     }
-    tqsim_destroy(h);
   });
 }
 

@@ -369,8 +369,9 @@ def tqsim_run_ex(n_qubits, gates, noise, n_shots, arities=None, seed=0, options=
 
 
 def tqsim_run(n_qubits, gates, noise, n_shots, arities=None, seed=0) -> Result:
-    """The north_star call: returns outcome counts (and the leaf-ordered outcomes)."""
-    ca = CircuitArg(n_qubits, gates)
+    """The north_star call: returns outcome counts (and the leaf-ordered outcomes).
+    `gates` is a gate list or a prebuilt CircuitArg (marshalled once, reused)."""
+    ca = gates if isinstance(gates, CircuitArg) else CircuitArg(n_qubits, gates)
     a, L = _arities(arities)
     r = C.POINTER(tqsim_result)()
     _check(lib().tqsim_run(C.byref(ca.c), C.byref(noise), int(n_shots), a, L, int(seed),
@@ -383,7 +384,7 @@ def tqsim_run(n_qubits, gates, noise, n_shots, arities=None, seed=0) -> Result:
         bits = np.ctypeslib.as_array(res.bitstrings, shape=(max(nd, 1),))[:nd]
         cnts = np.ctypeslib.as_array(res.counts, shape=(max(nd, 1),))[:nd]
         out = Result(tqsim_plan.from_buffer_copy(res.plan),
-                     {int(b): int(c) for b, c in zip(bits, cnts)}, leaf, float(res.wall_s),
+                     dict(zip(bits.tolist(), cnts.tolist())), leaf, float(res.wall_s),
                      tqsim_stats.from_buffer_copy(res.stats))
     finally:
         lib().tqsim_result_free(r)

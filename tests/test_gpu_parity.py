@@ -230,3 +230,21 @@ def test_error_frame_structured(tile, p):
     opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
     run_and_compare(n, gates, nm, 24, [3, 2, 4], 77 + tile, opts,
                     dumps=[(0, 0), (0, 2), (1, 5), (2, 23)])
+
+
+def test_run_plan_cache_reuse():
+    """tqsim_run reuses its prepared plan for byte-identical inputs: results are the
+    same as a fresh preparation (run_ex with explicit default options = another key)."""
+    w = load_config("c1_qft5")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    ca = T.CircuitArg(n, gates)
+    a = T.tqsim_run(n, ca, noise, shots, ar, 5)
+    b = T.tqsim_run(n, ca, noise, shots, ar, 5)
+    c = T.tqsim_run(n, ca, noise, shots, ar, 6)
+    fresh = T.tqsim_run_ex(n, gates, noise, shots, ar, 6, T.default_options())
+    assert np.array_equal(a.leaf_outcomes, b.leaf_outcomes)
+    assert np.array_equal(c.leaf_outcomes, fresh.leaf_outcomes)
+    assert not np.array_equal(a.leaf_outcomes, c.leaf_outcomes)
+    other = T.tqsim_run(n, ca, T.noise_arg(0, 0), shots, ar, 5)   # noise model is part of the key
+    ref = T.tqsim_run_ex(n, gates, T.noise_arg(0, 0), shots, ar, 5, T.default_options())
+    assert np.array_equal(other.leaf_outcomes, ref.leaf_outcomes)
