@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <complex>
@@ -48,6 +49,13 @@ struct TqJitArgs {
   double* runsum;   // leaf level: |a|^2 sums of 8-amplitude runs, 2^(n-3) per state
   const unsigned char* rows; tq_u32 row_bytes;   // noise rows of the batch (launch_noise_rows)
 };
+// 16-byte global load the compiler may not sink below the error-branch: the tile loads
+// are issued before the (dependent) noise-row mask load is waited on
+__device__ __forceinline__ tq_d2 tq_ld(const tq_d2* p) {
+  tq_d2 r;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
 // r *= i^q
 __device__ __forceinline__ void tq_rot(tq_d2& r, tq_u32 q) {
   const double a = (q & 1u) ? r.y : r.x, b = (q & 1u) ? r.x : r.y;
@@ -510,6 +518,29 @@ PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool coalesced) {
   return P;
 }
 
+// Layout of a phase that touches HBM, coalesced in the address order `key` (key[p] =
+// address bit of tile position p: the physical qubit for loads, the LOGICAL qubit for
+// stores after SWAP relabelings): registers padded with the highest-key positions,
+// lanes on the rest in ascending key order, so lanes 0..2 walk address bits 0..2 when
+// R holds none of them.
+PhaseDesc make_io_layout(uint64_t R, int K, const int* key) {
+  std::vector<int> order(K);
+  for (int p = 0; p < K; ++p) order[p] = p;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return key[a] < key[b]; });
+  for (int i = K - 1; i >= 0 && __builtin_popcountll(R) < RBITS; --i)
+    if (!(R >> order[i] & 1) && key[order[i]] >= LOW_Q) R |= 1ull << order[i];
+  for (int i = 0; i < K && __builtin_popcountll(R) < RBITS; ++i)
+    if (!(R >> order[i] & 1)) R |= 1ull << order[i];
+  PhaseDesc P{};
+  int rb = 0;
+  for (int p = 0; p < K; ++p)
+    if (R >> p & 1) P.rpos[rb++] = (uint8_t)p;
+  int m = 0;
+  for (int i = 0; i < K; ++i)
+    if (!(R >> order[i] & 1)) P.tpos[m++] = (uint8_t)order[i];
+  return P;
+}
+
 // One schedulable item of a phase plan: tile positions it needs in registers and
 // the global qubits it touches (for the order constraints).
 struct PItem {
@@ -522,9 +553,17 @@ struct PItem {
 // with them).  Phase 0 is fixed to the register set R0 the kernel loads; the last
 // phase is the store layout: when `coal` it must hold no position < low in
 // registers, so a trailing re-layout phase is added if the last group needs one.
-std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint64_t R0, bool coal) {
+std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint64_t R0, bool coal,
+                                   const int* store_key) {
   const int low = std::min(LOW_Q, K);
   const uint64_t lowm = (1ull << low) - 1;
+  uint64_t store_low = 0;   // positions of the store's address bits 0..low-1
+  bool same_low = true;     // the load's and the store's low lanes coincide
+  for (int p = 0; p < K; ++p)
+    if (store_key[p] < low) {
+      store_low |= 1ull << p;
+      if (store_key[p] != p) same_low = false;
+    }
   std::vector<std::pair<std::vector<int>, uint64_t>> groups;
   std::vector<int> remaining(items.size());
   for (size_t i = 0; i < items.size(); ++i) remaining[i] = (int)i;
@@ -553,12 +592,21 @@ std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint6
     remaining.swap(deferred);
     first = false;
   }
-  if (coal && groups.size() > 1 && (groups.back().second & lowm)) groups.emplace_back(std::vector<int>(), 0);
+  if (coal) {
+    const uint64_t last_regs = groups.size() == 1 ? R0 : groups.back().second;
+    if ((last_regs & store_low) || (groups.size() == 1 && !same_low)) groups.emplace_back(std::vector<int>(), 0);
+  }
+  (void)lowm;
   std::vector<PhaseSpec> out;
+  int load_key[64];
+  for (int p = 0; p < K; ++p) load_key[p] = p;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     PhaseSpec ps;
-    const bool io = gi == 0 || gi + 1 == groups.size();
-    ps.P = make_phase_layout(gi == 0 ? R0 : groups[gi].second, K, low, io);
+    const bool ld = gi == 0, st = gi + 1 == groups.size();
+    const uint64_t R = gi == 0 ? R0 : groups[gi].second;
+    if (st && coal) ps.P = make_io_layout(R, K, store_key);
+    else if (ld) ps.P = make_io_layout(R, K, load_key);
+    else ps.P = make_phase_layout(R, K, low, st);
     for (int ii : groups[gi].first) ps.items.push_back(items[ii].idx);
     out.push_back(ps);
   }
@@ -609,7 +657,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // One phase plan for both paths: the error-free fast path and the careful path,
   // which runs the same fused ops under a run-time Pauli frame (below).
   const uint64_t R0 = choose_load_regs(fitems, K, coal);
-  const std::vector<PhaseSpec> fast = plan_phases(fitems, K, R0, coal);
+  int store_key[64];   // the store writes tile position p to logical qubit log_of_phys[tile_q[p]]
+  for (int p = 0; p < K; ++p) store_key[p] = log_of_phys[pd.tile_q[p]];
+  const std::vector<PhaseSpec> fast = plan_phases(fitems, K, R0, coal, store_key);
   if (const char* e = std::getenv("TQSIM_JIT_DEBUG")) {
     if (e[0] == '1') {
       std::fprintf(stderr, "[tqsim jit] %s: %d ops -> %zu fused ops; %zu phases\n", name.c_str(), nops,
@@ -736,7 +786,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       if (mode == 0)
         o << "    r" << k << ".x = (gb + " << goff[k] << "u == 0u) ? 1.0 : 0.0; r" << k << ".y = 0.0;\n";
       else
-        o << "    r" << k << " = src[gb + " << goff[k] << "u];\n";
+        o << "    r" << k << " = tq_ld(src + (gb + " << goff[k] << "u));\n";
     }
     o << "  }\n";
   };
@@ -1218,10 +1268,6 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   };
   emit_phases(fast, false);
   o << "  } else {\n";
-  // the careful path reloads its tile (L1/L2 hits): the fast path's registers are
-  // then dead across the branch, so the careful path's register pressure cannot
-  // make ptxas spill them in the common code
-  emit_load();
   // bitmap of the pass ops whose gate drew an error
   o << "  if (tid < " << NW << "u) tq_errb[tid] = 0u;\n  __syncthreads();\n";
   o << "  for (tq_u32 li = tid; li < " << nops << "u; li += " << T << "u)\n"
