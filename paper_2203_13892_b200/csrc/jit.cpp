@@ -171,8 +171,8 @@ typedef std::complex<double> cplx;
 // Effect of the keyed Pauli of one gate (code c) propagated to the END of the fused
 // run containing the gate: E' = R E R^dagger with R the run's later gates (monomial,
 // so E' = (diagonal) x (bit flips)).  Either Pauli-type E' = i^k X^x Z^z, or generic
-// E' = D X^x with D a diagonal on the run's two qubits.  Masks over PHYSICAL tile
-// positions (after the run's SWAP relabeling, if any).
+// E' = D X^x with D a diagonal on the run's two qubits.  Masks over PHYSICAL qubits
+// (after the run's SWAP relabeling, if any).
 struct ErrEff {
   uint32_t x = 0, z = 0, k = 0;
   bool generic = false;
@@ -439,8 +439,8 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     const int slot1 = S1 >= 0 ? S1 : (s0 == 0 ? 1 : 0);
     std::vector<M4> mats;
     for (int t = i; t <= e_end; ++t) mats.push_back(op_matrix(lg_of(t), s0, slot1));
-    f.ea = qpos[phys_of[s0]];
-    f.eb = S1 >= 0 ? qpos[phys_of[S1]] : -1;
+    f.ea = phys_of[s0];
+    f.eb = S1 >= 0 ? phys_of[S1] : -1;
     M4 R = M4::id();   // product of the gates after t
     std::vector<ErrSite> sites(e_end - i + 1);
     for (int t = e_end; t >= i; --t) {
@@ -646,7 +646,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   auto qmk = [&](int qa, int qb) { return (1ull << qa) | (qb >= 0 ? 1ull << qb : 0ull); };
 
   std::vector<int> log_of_phys;
-  const std::vector<FOp> fops = fuse_fast_ops(pd, pp, gates, !pd.leaf_sums, log_of_phys);
+  const std::vector<FOp> fops = fuse_fast_ops(pd, pp, gates, true, log_of_phys);
   // diagonal ops need no register slot (index bits are known, jit below)
   std::vector<PItem> fitems;
   for (size_t i = 0; i < fops.size(); ++i) {
@@ -687,17 +687,19 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   }
   g_pool = &pool;
   // Careful-path tables.  GOFF: slice-relative gate index of pass op li (its noise
-  // code is codes[4 + GOFF[li]]).  ERRW[li * 16 + c]: the propagated error of code c
-  // of op li -- bits 0..12 X mask (tile positions), 13..14 phase power k, 15 generic,
-  // 16..31 Z mask (Pauli-type) or index into GD (generic: 4 complex diagonal entries).
-  std::vector<uint32_t> errw((size_t)std::max(nops, 1) * 16, 0u);
+  // code is codes[4 + GOFF[li]]).  ERRX/ERRZ[li * 16 + c]: the propagated error of
+  // code c of op li -- ERRX: bits 0..29 X mask (physical qubits), 30..31 phase power
+  // k; ERRZ: Z mask (Pauli-type) or 0x80000000 | index into GD (generic: 4 complex
+  // diagonal entries).
+  std::vector<uint32_t> errx((size_t)std::max(nops, 1) * 16, 0u), errz(errx.size(), 0u);
   std::vector<double> gd;
   std::map<std::vector<double>, uint32_t> gd_index;
   for (const FOp& f : fops)
     for (const ErrSite& es : f.sites)
       for (size_t c = 0; c < es.eff.size(); ++c) {
         const ErrEff& ef = es.eff[c];
-        uint32_t w = (ef.x & 0x1fffu) | ((ef.k & 3u) << 13);
+        if (ef.x >> 30 || ef.z >> 30) throw Error{TQSIM_EINTERNAL, "error frame needs qubits < 30"};
+        uint32_t wx = ef.x | ((ef.k & 3u) << 30), wz = ef.z;
         if (ef.generic) {
           std::vector<double> key;
           for (int i = 0; i < 4; ++i) {
@@ -713,18 +715,18 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           } else {
             di = it->second;
           }
-          if (di > 0xffffu) throw Error{TQSIM_EINTERNAL, "too many generic error diagonals"};
-          w |= 0x8000u | (di << 16);
-        } else {
-          w |= (ef.z & 0xffffu) << 16;
+          wz = 0x80000000u | di;
         }
-        errw[(size_t)es.local * 16 + c + 1] = w;
+        errx[(size_t)es.local * 16 + c + 1] = wx;
+        errz[(size_t)es.local * 16 + c + 1] = wz;
       }
   o << "static __constant__ unsigned short GOFF[" << std::max(nops, 1) << "] = {";
   for (int i = 0; i < nops; ++i) o << (i ? "," : "") << (pp.ops[pd.op_begin + i].gate - pd.slice_begin);
   if (!nops) o << "0";
-  o << "};\nstatic __device__ const tq_u32 ERRW[" << errw.size() << "] = {";
-  for (size_t i = 0; i < errw.size(); ++i) o << (i ? "," : "") << errw[i] << "u";
+  o << "};\nstatic __device__ const tq_u32 ERRX[" << errx.size() << "] = {";
+  for (size_t i = 0; i < errx.size(); ++i) o << (i ? "," : "") << errx[i] << "u";
+  o << "};\nstatic __device__ const tq_u32 ERRZ[" << errz.size() << "] = {";
+  for (size_t i = 0; i < errz.size(); ++i) o << (i ? "," : "") << errz[i] << "u";
   o << "};\nstatic __device__ const double GD[" << std::max<size_t>(gd.size(), 8) << "] = {";
   for (size_t i = 0; i < gd.size(); ++i) o << (i ? "," : "") << hexd(gd[i]);
   if (gd.empty()) o << "0.0";
@@ -739,9 +741,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   o << "  __shared__ tq_u32 tq_errb[" << NW << "];\n";
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
   o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
-  o << "  tq_u32 gtile = 0u;\n";
+  o << "  tq_u32 gtile = 0u, gtile_st = 0u;\n";   // the tile's out-of-tile index bits: physical / stored
   for (int i = 0; i < pd.n_out; ++i)
-    o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << ";\n";
+    o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << "; gtile_st |= (tq_u32)((t >> "
+      << i << ") & 1ull) << " << log_of_phys[pd.out_q[i]] << ";\n";
   o << "  tq_d2* __restrict__ dst = a.dst + ((tq_u64)s << " << n << ");\n";
   if (mode == 1)
     o << "  const tq_d2* __restrict__ src = a.src + ((((tq_u64)a.child_first + s) / a.arity - a.parent_first) << "
@@ -758,7 +761,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     auto qof = [&](int p) { return lq ? (*lq)[pd.tile_q[p]] : (int)pd.tile_q[p]; };
     std::ostringstream l, gg;
     l << "0u";
-    gg << "gtile";
+    gg << (lq ? "gtile_st" : "gtile");
     for (int m = 0; m < K - RBITS; ++m) {
       l << " | (((tid >> " << m << ") & 1u) << " << (int)P.tpos[m] << ")";
       gg << " | (((tid >> " << m << ") & 1u) << " << qof(P.tpos[m]) << ")";
@@ -982,33 +985,37 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       // = F psi_s for the run-time Pauli frame F = i^fk X^fx Z^fz (tile positions,
       // uniform per CTA).  Cliffords (CX, X) run unchanged and conjugate the frame;
       // GEN / DIAG ops run conjugated by the frame (F^+ U F); each drawn error, pushed
-      // to the end of its fused run at code generation time (ERRW), multiplies into the
+      // to the end of its fused run at code generation time (ERRX/ERRZ), multiplies into the
       // frame (and, for errors inside diagonal runs, applies a diagonal).  The frame is
       // applied at the store (address XOR + phase).  Exact up to fp rounding (R30).
       o << "    const tq_u32 lth = " << lbs << ";\n";
-      auto pos_bit = [&](int pos, const std::string& frame_bit_var, int k, std::string& expr) {
-        // index bit of tile position pos for register k (compile-time or thread bit) ^ frame bit
+      auto pos_bit = [&](int q, const std::string& frame_bit_var, int k, std::string& expr) {
+        // index bit of physical qubit q for register k (compile-time, thread bit, or --
+        // outside the tile -- the CTA's tile-index bit) ^ frame bit
+        const int pos = qpos[q];
         int rb = -1;
         for (int b = 0; b < RBITS; ++b)
-          if (P.rpos[b] == pos) rb = b;
+          if (pos >= 0 && P.rpos[b] == pos) rb = b;
         const std::string fb = frame_bit_var;
         if (rb >= 0) expr = "(" + fb + " ^ " + std::to_string((k >> rb) & 1) + "u)";
-        else expr = "(" + fb + " ^ ((lth >> " + std::to_string(pos) + ") & 1u))";
+        else if (pos >= 0) expr = "(" + fb + " ^ ((lth >> " + std::to_string(pos) + ") & 1u))";
+        else expr = "(" + fb + " ^ ((gtile >> " + std::to_string(q) + ") & 1u))";
         return rb;
       };
-      // apply a diagonal with entries E(i) (i = bit_pa | bit_pb << 1) under the frame:
-      // register k gets E((bits of k's index) ^ (frame X bits))
-      auto emit_frame_diag = [&](int pa, int pb, const std::string* ent /*8 exprs re,im x4*/,
+      // apply a diagonal with entries E(i) (i = bit_qa | bit_qb << 1, physical qubits)
+      // under the frame: register k gets E((bits of k's index) ^ (frame X bits))
+      auto emit_frame_diag = [&](int qa, int qb, const std::string* ent /*8 exprs re,im x4*/,
                                  bool rt_entries) {
-        o << "      { const tq_u32 xa = (fx >> " << pa << ") & 1u";
-        if (pb >= 0) o << ", xb = (fx >> " << pb << ") & 1u";
+        const int pb = qb;
+        o << "      { const tq_u32 xa = (fx >> " << qa << ") & 1u";
+        if (qb >= 0) o << ", xb = (fx >> " << qb << ") & 1u";
         o << ";\n";
-        // classes of registers by (bit at pa, bit at pb)
+        // classes of registers by (bit at qa, bit at qb)
         std::map<std::string, std::vector<int>> cls;
         for (int k = 0; k < 16; ++k) {
           std::string ea, eb = "0u";
-          pos_bit(pa, "xa", k, ea);
-          if (pb >= 0) pos_bit(pb, "xb", k, eb);
+          pos_bit(qa, "xa", k, ea);
+          if (qb >= 0) pos_bit(qb, "xb", k, eb);
           cls["(" + ea + " | (" + eb + " << 1))"].push_back(k);
         }
         int ci = 0;
@@ -1037,16 +1044,16 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       };
       for (int it : specs[ph].items) {
         const FOp& f = fops[it];
-        const int pa = f.qa >= 0 ? qpos[f.qa] : -1, pb = f.qb >= 0 ? qpos[f.qb] : -1;
+
         if (f.kind == FOp::CX) {
           const int ba = rbit(f.qa), bb = rbit(f.qb);
           permute([&](int k) { return k ^ (((k >> ba) & 1) << bb); });
-          o << "    fx ^= ((fx >> " << pa << ") & 1u) << " << pb << "; fz ^= ((fz >> " << pb << ") & 1u) << " << pa
-            << ";\n";
+          o << "    fx ^= ((fx >> " << f.qa << ") & 1u) << " << f.qb << "; fz ^= ((fz >> " << f.qb << ") & 1u) << "
+            << f.qa << ";\n";
         } else if (f.kind == FOp::XPERM) {
           const int ba = rbit(f.qa);
           permute([&](int k) { return k ^ (1 << ba); });
-          o << "    fk += ((fz >> " << pa << ") & 1u) << 1;\n";
+          o << "    fk += ((fz >> " << f.qa << ") & 1u) << 1;\n";
         } else if (f.kind == FOp::GEN) {
           // F^+ U F on this qubit: variant v = x | z << 1 of Z^z X^x U X^x Z^z
           const int ba = rbit(f.qa);
@@ -1059,7 +1066,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           }
           pool.begin_op();
           std::ostringstream oo;
-          oo << "      const tq_u32 v = ((fx >> " << pa << ") & 1u) | (((fz >> " << pa << ") & 1u) << 1);\n";
+          oo << "      const tq_u32 v = ((fx >> " << f.qa << ") & 1u) | (((fz >> " << f.qa << ") & 1u) << 1);\n";
           std::string cr[4], ci[4];   // coefficient expressions
           bool zr[4], zi[4];
           for (int e = 0; e < 4; ++e) {
@@ -1122,7 +1129,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             ent[2 * i + 1] = d.imag() == 0.0 ? "0.0" : g_pool->ref(d.imag());
           }
           o << "    {\n" << pool.decl.str();
-          emit_frame_diag(pa, pb, ent, false);
+          emit_frame_diag(f.qa, f.qb, ent, false);
           o << "    }\n";
         }
         // the run's drawn errors, in gate order (uniform branch; rare)
@@ -1142,14 +1149,13 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           o << "      for (tq_u32 li = " << l0 << "u; li <= " << l1 << "u; ++li) {\n";
           o << "        if (!((tq_errb[li >> 5] >> (li & 31u)) & 1u)) continue;\n";
           o << "        const tq_u32 c = codes[4u + GOFF[li]];\n";
-          o << "        const tq_u32 w = __ldg(ERRW + li * 16u + c);\n";
-          o << "        if (!(w & 0x8000u)) {\n"
-            << "          const tq_u32 ze = w >> 16;\n"
-            << "          fk += ((w >> 13) & 3u) + ((__popc(ze & fx) & 1u) << 1);\n"
-            << "          fx ^= w & 0x1fffu; fz ^= ze;\n";
+          o << "        const tq_u32 wx = __ldg(ERRX + li * 16u + c), wz = __ldg(ERRZ + li * 16u + c);\n";
+          o << "        if (!(wz & 0x80000000u)) {\n"
+            << "          fk += (wx >> 30) + ((__popc(wz & fx) & 1u) << 1);\n"
+            << "          fx ^= wx & 0x3fffffffu; fz ^= wz;\n";
           if (any_gen) {
-            o << "        } else {\n          fx ^= w & 0x1fffu;\n"
-              << "          const double* __restrict__ D = GD + 8u * (w >> 16);\n";
+            o << "        } else {\n          fx ^= wx & 0x3fffffffu;\n"
+              << "          const double* __restrict__ D = GD + 8u * (wz & 0x7fffffffu);\n";
             std::string ent[8];
             for (int i = 0; i < 8; ++i) {
               ent[i] = "e" + std::to_string(i);
@@ -1213,14 +1219,17 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       o << "    const tq_u32 gbs = " << gbl << ";\n";
       std::string xl = "";
       if (with_errors) {
-        // true state = i^fk X^fx Z^fz psi_s: amplitude at tile index i goes to i ^ fx,
-        // times i^fk (-1)^popc(fz & i); fx mapped to global (logical) address bits
+        // true state = i^fk X^fx Z^fz psi_s: the amplitude at physical index i goes to
+        // i ^ fx, times i^fk (-1)^popc(fz & i); fx mapped to stored (logical) address bits
+        uint32_t gph[16], sph[16];
+        std::string lbp, gbp;
+        offsets(P, nullptr, gph, sph, lbp, gbp);
         o << "    tq_u32 xl = 0u;\n";
-        for (int p = 0; p < K; ++p)
-          o << "    xl |= ((fx >> " << p << ") & 1u) << " << log_of_phys[pd.tile_q[p]] << ";\n";
-        o << "    const tq_u32 zt = __popc(fz & lth);\n";
+        for (int q = 0; q < n; ++q)
+          o << "    xl |= ((fx >> " << q << ") & 1u) << " << log_of_phys[q] << ";\n";
+        o << "    const tq_u32 zt = __popc(fz & (" << gbp << "));\n";
         for (int k = 0; k < 16; ++k)
-          o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << lo_last[k] << "u)) << 1));\n";
+          o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << gph[k] << "u)) << 1));\n";
         xl = " ^ xl";
       }
       for (int k = 0; k < 16; ++k)
@@ -1229,12 +1238,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         // |a|^2 sums of the 8-amplitude runs (qubits 0..2): reduce over the register bits
         // holding positions 0..2, then butterfly-shuffle over the lane bits holding the
         // rest (the store layout puts the lowest non-register positions on lanes 0..4).
-        int rbits_low = 0;      // register bits whose position is < RUN_Q
+        int rbits_low = 0;      // register bits holding stored (logical) qubits < RUN_Q
         for (int b = 0; b < RBITS; ++b)
-          if (P.rpos[b] < RUN_Q) rbits_low |= 1 << b;
+          if (store_key[P.rpos[b]] < RUN_Q) rbits_low |= 1 << b;
         std::vector<int> lane_bits;
         for (int m = 0; m < K - RBITS; ++m)
-          if (P.tpos[m] < RUN_Q) lane_bits.push_back(m);
+          if (store_key[P.tpos[m]] < RUN_Q) lane_bits.push_back(m);
         if ((int)lane_bits.size() + __builtin_popcount(rbits_low) != RUN_Q || (!lane_bits.empty() && lane_bits.back() >= 5))
           throw Error{TQSIM_EINTERNAL, "run-sum layout: low qubits not on registers/lanes"};
         std::vector<int> reps;   // one k per run held by this thread

@@ -25,16 +25,41 @@ inline int popc(uint64_t v) { return __builtin_popcountll(v); }
 // Greedy in-order grouping with commuting look-ahead.  `cost_mask(g)` is the
 // set of resources gate g needs beyond the always-present ones; `cap` bounds
 // the resources of one group.  Returns groups of gate indices.
+// A lowered SWAP: CX(a,b) CX(b,a) CX(a,b) at order positions i, i+1, i+2.
+bool swap_triple_at(const std::vector<uint32_t>& v, size_t i, const std::vector<LGate>& gates) {
+  if (i + 2 >= v.size()) return false;
+  const LGate &x = gates[v[i]], &y = gates[v[i + 1]], &z = gates[v[i + 2]];
+  return x.op == OP_CX && y.op == OP_CX && z.op == OP_CX && x.q0 == z.q0 && x.q1 == z.q1 &&
+         y.q0 == x.q1 && y.q1 == x.q0;
+}
+
+// absorb_swaps (first pass of a level: out of place, so its store may permute the
+// address bits freely): a SWAP on qubits >= low that does not fit the tile joins the
+// group as a pure relabeling needing no tile slot; later gates on its qubits are
+// deferred to the next pass.
 template <class MaskFn>
 std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
     const std::vector<uint32_t>& order, const std::vector<LGate>& gates, MaskFn need_mask,
-    int cap, size_t max_items = ~size_t(0)) {
+    int cap, size_t max_items = ~size_t(0), bool absorb_swaps = false, int low = 0) {
   std::vector<std::pair<std::vector<uint32_t>, uint64_t>> groups;
   std::vector<uint32_t> remaining = order;
+  bool first_group = true;
   while (!remaining.empty()) {
     uint64_t used = 0, blocked = 0;
     std::vector<uint32_t> in, deferred;
-    for (uint32_t g : remaining) {
+    for (size_t ri = 0; ri < remaining.size(); ++ri) {
+      const uint32_t g = remaining[ri];
+      if (absorb_swaps && first_group && swap_triple_at(remaining, ri, gates) && in.size() + 3 <= max_items) {
+        const LGate& x = gates[g];
+        const uint64_t qm = qmask(x);
+        const uint64_t need = need_mask(g);
+        if (!(qm & blocked) && popc(used | need) > cap && (int)x.q0 >= low && (int)x.q1 >= low) {
+          for (int t = 0; t < 3; ++t) in.push_back(remaining[ri + t]);
+          blocked |= qm;   // nothing later in this pass touches the relabeled pair
+          ri += 2;
+          continue;
+        }
+      }
       const uint64_t qm = qmask(gates[g]);
       if ((qm & blocked) || in.size() >= max_items) {
         deferred.push_back(g);
@@ -53,6 +78,7 @@ std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
     if (in.empty()) throw Error{TQSIM_EINTERNAL, "pass planner made no progress"};
     groups.emplace_back(std::move(in), used);
     remaining.swap(deferred);
+    first_group = false;
   }
   return groups;
 }
@@ -106,7 +132,7 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
     for (uint64_t g = plan.bounds[d]; g < plan.bounds[d + 1]; ++g) order.push_back((uint32_t)g);
     auto passes = group_gates(order, gates,
                               [&](uint32_t g) { return qmask(gates[g]) & ~low_mask; }, hcap,
-                              MAX_PASS_OPS);
+                              MAX_PASS_OPS, /*absorb_swaps=*/true, low);
     std::vector<PassDesc> lvl;
     for (size_t pi = 0; pi < passes.size(); ++pi) {
       uint64_t H = passes[pi].second;
@@ -128,8 +154,10 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
       for (int q = 0; q < n; ++q)
         if (!(pd.tile_mask >> q & 1)) pd.out_q[pd.n_out++] = (uint8_t)q;
       // phases over tile positions
-      auto pos_mask = [&](uint32_t g) {
-        return (1ull << qpos[gates[g].q0]) | (1ull << qpos[gates[g].q1]);
+      auto pos_mask = [&](uint32_t g) {   // absorbed SWAP relabelings (non-tile qubits): none
+        const int a = qpos[gates[g].q0], b = qpos[gates[g].q1];
+        if (a < 0 || b < 0) return 0ull;
+        return (1ull << a) | (1ull << b);
       };
       auto phases = group_gates(passes[pi].first, gates, pos_mask, RBITS);
       pd.phase_begin = (uint32_t)pp.phases.size();
@@ -169,8 +197,9 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
           od.type = lg.op;
           od.two = lg.two ? 1 : 0;
           od.gate = g;
-          od.ra = (uint8_t)rbit_of_pos[qpos[lg.q0]];
-          od.rb = lg.two ? (uint8_t)rbit_of_pos[qpos[lg.q1]] : od.ra;
+          const bool intile = qpos[lg.q0] >= 0 && qpos[lg.q1] >= 0;
+          od.ra = intile ? (uint8_t)rbit_of_pos[qpos[lg.q0]] : 0;
+          od.rb = intile && lg.two ? (uint8_t)rbit_of_pos[qpos[lg.q1]] : od.ra;
           pp.ops.push_back(od);
         }
         pdsc.op_end = (uint32_t)pp.ops.size();
