@@ -115,6 +115,10 @@ def main():
     if os.environ.get("HARNESS_COMPILE_ONLY"):
         print("compiled", exe)
         return
+    if os.environ.get("HARNESS_NCU"):   # --set full capture of one launch of the kernel
+        subprocess.run(["ncu", "--set", "full", "--clock-control", "none", "-s", "3", "-c", "1", "-o",
+                        os.environ["HARNESS_NCU"], "-f", exe], check=True)
+        return
     subprocess.run([exe], check=True)
 
 

@@ -95,3 +95,20 @@ def test_c3_general_sampled_leaves_dense_oracle():
         assert np.max(np.abs(res.dumps[i] - psi)) <= 1e-10
         if not r.flagged:
             assert int(res.leaf_outcomes[l]) == r.outcome
+
+
+def test_c4_general_sampled_leaves_dense_oracle():
+    """C4 (24 qubits, general angles) at its full plan: two leaves in different
+    top-level subtrees recomputed flat by the dense oracle (amplitudes + outcomes)."""
+    w = load_config("c4_qaoa24")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    L = T.tqsim_plan_circuit(n, gates, noise, shots, ar).n_levels
+    leaves = [3, 8190]
+    res = T.tqsim_run_ex(n, gates, noise, shots, ar, w.seed, None, [(L - 1, l) for l in leaves])
+    plan = Plan(res.plan.arity_list, res.plan.boundary_list)
+    low = OG.lower(gates)
+    for i, l in enumerate(leaves):
+        r, psi, _ = simulate_leaf_flat(n, low, plan, nm_of(w), w.seed, l, want_states=True)
+        assert np.max(np.abs(res.dumps[i] - psi)) <= 1e-10
+        if not r.flagged:
+            assert int(res.leaf_outcomes[l]) == r.outcome
