@@ -520,14 +520,18 @@ PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool coalesced) {
 
 // Layout of a phase that touches HBM, coalesced in the address order `key` (key[p] =
 // address bit of tile position p: the physical qubit for loads, the LOGICAL qubit for
-// stores after SWAP relabelings): registers padded with the highest-key positions,
-// lanes on the rest in ascending key order, so lanes 0..2 walk address bits 0..2 when
-// R holds none of them.
+// stores after SWAP relabelings): registers padded with the lowest keys >= 5, lanes on
+// the rest in ascending key order, so lanes 0..2 walk address bits 0..2 when R holds
+// none of them.
 PhaseDesc make_io_layout(uint64_t R, int K, const int* key) {
   std::vector<int> order(K);
   for (int p = 0; p < K; ++p) order[p] = p;
   std::sort(order.begin(), order.end(), [&](int a, int b) { return key[a] < key[b]; });
-  for (int i = K - 1; i >= 0 && __builtin_popcountll(R) < RBITS; --i)
+  // pad the registers with address bits 5, 6, ... (lanes keep bits 0..4: every warp
+  // access is 512 contiguous bytes, and the leaf run sums a warp holds are consecutive)
+  for (int i = 0; i < K && __builtin_popcountll(R) < RBITS; ++i)
+    if (!(R >> order[i] & 1) && key[order[i]] >= LOW_Q + 2) R |= 1ull << order[i];
+  for (int i = 0; i < K && __builtin_popcountll(R) < RBITS; ++i)
     if (!(R >> order[i] & 1) && key[order[i]] >= LOW_Q) R |= 1ull << order[i];
   for (int i = 0; i < K && __builtin_popcountll(R) < RBITS; ++i)
     if (!(R >> order[i] & 1)) R |= 1ull << order[i];
@@ -625,7 +629,9 @@ uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal) {
     if (ok) used |= it.need;
     else blocked |= it.qm;
   }
-  PhaseDesc P = make_phase_layout(used, K, low, true);
+  int load_key[64];
+  for (int p = 0; p < K; ++p) load_key[p] = p;
+  PhaseDesc P = make_io_layout(used, K, load_key);
   uint64_t R = 0;
   for (int b = 0; b < RBITS; ++b) R |= 1ull << P.rpos[b];
   return R;
@@ -1256,17 +1262,40 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
               o << "    rs" << i << " = fma(" << g.r(k) << ".x, " << g.r(k) << ".x, fma(" << g.r(k) << ".y, "
                 << g.r(k) << ".y, rs" << i << "));\n";
         }
-        for (int m : lane_bits)
-          for (size_t i = 0; i < reps.size(); ++i)
-            o << "    rs" << i << " += __shfl_xor_sync(" << (T >= 32 ? 0xffffffffu : (1u << T) - 1u) << "u, rs" << i
-              << ", " << (1 << m) << ");\n";
-        int lane_mask = 0;
-        for (int m : lane_bits) lane_mask |= 1 << m;
-        o << "    if ((tid & " << lane_mask << "u) == 0u) {\n";
-        for (size_t i = 0; i < reps.size(); ++i)
-          o << "      a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + (((gbs + " << gofs[reps[i]] << "u)" << xl
-            << ") >> " << RUN_Q << ")] = rs" << i << ";\n";
-        o << "    }\n";
+        // Reduce-scatter over the lane bits holding the run's qubits: at each lane bit the
+        // lane keeps half of its partial sums (the half selected by its bit) and adds the
+        // partner's copy of that half -- R/2 + R/4 + ... shuffles instead of R per bit, and
+        // every lane ends with R >> |lane_bits| finished run sums to store.
+        const unsigned fm = T >= 32 ? 0xffffffffu : (1u << T) - 1u;
+        std::vector<std::string> v;
+        for (size_t i = 0; i < reps.size(); ++i) v.push_back("rs" + std::to_string(i));
+        std::vector<std::string> base_terms;   // runtime index of the first kept sum
+        int stage = 0;
+        for (int m : lane_bits) {
+          const size_t L = v.size(), half = L / 2;
+          if (half == 0) throw Error{TQSIM_EINTERNAL, "run-sum reduce-scatter ran out of sums"};
+          o << "    const bool hb" << stage << " = (tid >> " << m << ") & 1u;\n";
+          std::vector<std::string> nv;
+          for (size_t j = 0; j < half; ++j) {
+            const std::string nm = "ru" + std::to_string(stage) + "_" + std::to_string(j);
+            o << "    const double " << nm << " = (hb" << stage << " ? " << v[j + half] << " : " << v[j]
+              << ") + __shfl_xor_sync(" << fm << "u, hb" << stage << " ? " << v[j] << " : " << v[j + half] << ", "
+              << (1 << m) << ");\n";
+            nv.push_back(nm);
+          }
+          base_terms.push_back("(hb" + std::to_string(stage) + " ? " + std::to_string(half) + "u : 0u)");
+          v.swap(nv);
+          ++stage;
+        }
+        o << "    const tq_u32 rbase = 0u";
+        for (auto& t : base_terms) o << " + " << t;
+        o << ";\n";
+        o << "    static __constant__ tq_u32 ROFF[" << reps.size() << "] = {";
+        for (size_t i = 0; i < reps.size(); ++i) o << (i ? "," : "") << gofs[reps[i]] << "u";
+        o << "};\n";
+        for (size_t j = 0; j < v.size(); ++j)
+          o << "    a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + (((gbs + ROFF[rbase + " << j << "u])" << xl
+            << ") >> " << RUN_Q << ")] = " << v[j] << ";\n";
       }
     } else {
       o << "    const tq_u32 sbs = tq_swz(" << lbs << ");\n";

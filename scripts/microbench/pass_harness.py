@@ -63,6 +63,16 @@ VARIANTS = {
     "base": lambda s: s,
     # no phase-exchange barriers' work: drop every fast-path op block (keeps loads/stores/exchanges)
     "nocompute": lambda s: re.sub(r"\n    \{\n(?:      [^\n]*\n)+    \}\n", "\n", s),
+    # the store ignores relabelings of out-of-tile qubits (wrong results; timing only)
+    "norelabel": lambda s: re.sub(r"gtile_st \|= \(tq_u32\)\(\(t >> (\d+)\) & 1ull\) << \d+;", "", s).replace(
+        "  tq_d2* __restrict__ dst =", "  gtile_st = gtile;\n  tq_d2* __restrict__ dst =", 1),
+    # no leaf run sums (timing only)
+    "nosums": lambda s: re.sub(r"\n    a\.runsum\[[^\n]*", "", s),
+    # run sums computed, stores predicated off (never taken)
+    "sumsnostore": lambda s: re.sub(r"\n    a\.runsum\[[^\n]*\] = ([^;]*);", r"\n    if (\1 < -1.0) a.runsum[0] = \1;", s),
+    # run sums stored to a contiguous per-thread slot (address pattern only)
+    "sumsflat": lambda s: re.sub(r"\n    a\.runsum\[[^\n]*\+ (\d+)u\][^\n]*\] = ([^;]*);",
+                                 r"\n    a.runsum[((tq_u64)bid * blockDim.x + tid) * 2 + \1] = \2;", s),
 }
 
 
