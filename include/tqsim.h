@@ -169,6 +169,18 @@ const char* tqsim_last_error(void);
 const char* tqsim_version(void);
 
 /* [host] Lower a circuit (R4).  Writes up to `cap` gates; *n_out = lowered count. */
+/* [host] Parse an OpenQASM 2.0 program (SPEC S:52-60, S:95 subset:
+ * qreg/creg (several qregs concatenated in declaration order), x y z h s sdg t tdg id,
+ * rx ry rz p u1 (1 angle), u2, u u3 U (3 angles), cx CX cz swap cp cu1, barrier,
+ * terminal measure; angles are pi-expressions with + - * / and parentheses; a
+ * register argument broadcasts the gate).  `id` becomes U(0,0,0) (a noise location).
+ * out: capacity `cap` gates (NULL / 0 to query); *n_gates, *n_qubits: sizes;
+ * *measured (may be NULL): 1 if a measure statement was seen.
+ * Errors: TQSIM_EINVAL "line L col C: ..." (syntax, unsupported gate, index range,
+ * more than TQSIM_MAX_QUBITS qubits). */
+tqsim_status tqsim_parse_qasm(const char* text, tqsim_gate* out, uint64_t cap, uint64_t* n_gates,
+                              uint32_t* n_qubits, uint32_t* measured);
+
 tqsim_status tqsim_lower_circuit(const tqsim_circuit* circuit, tqsim_gate* out, uint64_t cap,
                                  uint64_t* n_out);
 

@@ -410,6 +410,9 @@ void build_result(tqsim_handle* h, const std::vector<uint32_t>& outs, double wal
 }
 
 }  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
 }  // namespace tq
 
 using namespace tq;

@@ -106,6 +106,8 @@ _SIGS = {
     "tqsim_last_error": (C.c_char_p, []),
     "tqsim_version": (C.c_char_p, []),
     "tqsim_lower_circuit": (C.c_int, [_P(tqsim_circuit), _P(tqsim_gate), C.c_uint64, _P(C.c_uint64)]),
+    "tqsim_parse_qasm": (C.c_int, [C.c_char_p, _P(tqsim_gate), C.c_uint64, _P(C.c_uint64),
+                                   _P(C.c_uint32), _P(C.c_uint32)]),
     "tqsim_plan_circuit": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
                                      _P(C.c_uint32), C.c_uint32, _P(tqsim_options), _P(tqsim_plan)]),
     "tqsim_describe_passes": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
@@ -199,6 +201,23 @@ def _arities(arities):
 # ------------------------------------------------------------------ C-ABI mirrors
 def tqsim_version() -> str:
     return lib().tqsim_version().decode()
+
+
+def tqsim_parse_qasm(text: str):
+    """OpenQASM 2.0 subset -> (n_qubits, gates, measured); gates as the tuples CircuitArg
+    takes: (kind, q0, q1 or -1, theta, phi, lambda)."""
+    b = text.encode()
+    n, w, m = C.c_uint64(), C.c_uint32(), C.c_uint32()
+    _check(lib().tqsim_parse_qasm(b, None, 0, C.byref(n), C.byref(w), C.byref(m)))
+    out = (tqsim_gate * max(1, n.value))()
+    _check(lib().tqsim_parse_qasm(b, out, n.value, C.byref(n), C.byref(w), C.byref(m)))
+    gates = []
+    for i in range(n.value):
+        g = out[i]
+        kind = GATE_KINDS[g.kind]
+        two = kind in ("cx", "cz", "swap", "cp")
+        gates.append((kind, int(g.q0), int(g.q1) if two else -1, float(g.theta), float(g.phi), float(g.lam)))
+    return int(w.value), gates, bool(m.value)
 
 
 def tqsim_lower_circuit(n_qubits: int, gates) -> List[Tuple[str, int, int]]:

@@ -248,3 +248,17 @@ def test_run_plan_cache_reuse():
     other = T.tqsim_run(n, ca, T.noise_arg(0, 0), shots, ar, 5)   # noise model is part of the key
     ref = T.tqsim_run_ex(n, gates, T.noise_arg(0, 0), shots, ar, 5, T.default_options())
     assert np.array_equal(other.leaf_outcomes, ref.leaf_outcomes)
+
+
+def test_qasm_program_runs_like_generator():
+    """A QASM program through tqsim_parse_qasm runs to the same leaf
+    outcomes as the same circuit from the generator, and matches the oracle."""
+    from test_qasm import to_qasm
+    w = load_config("c1_qft5")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    n2, g2, measured = T.tqsim_parse_qasm(to_qasm(n, [tuple(g) for g in w.circuit.gates]))
+    assert n2 == n and measured
+    a = T.tqsim_run_ex(n, gates, noise, shots, ar, 3)
+    b = T.tqsim_run_ex(n2, g2, noise, shots, ar, 3)
+    assert np.array_equal(a.leaf_outcomes, b.leaf_outcomes)
+    run_and_compare(n2, g2, NoiseModel(w.p1, w.p2, w.readout_p01, w.readout_p10), shots, ar, 3)
