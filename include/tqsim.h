@@ -257,6 +257,16 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* circuit, const tqsim_noise_model*
                           tqsim_result** out);
 void tqsim_result_free(tqsim_result* r);
 
+/* [gpu] B200 state-copy cost in gate units (§3.3, fig:copy-overhead; SURVEY
+ * §8(f) #2): *copy_ms = device-to-device copy of a 1 GiB batch of n-qubit states,
+ * *gate_ms = the engine's time per gate application on the same batch (seeded probe
+ * slice of n_probe_gates random U / CX gates, noise-free), *copy_cost_gates = their
+ * ratio -- the value to pass as tqsim_options.copy_cost_gates for a device-measured
+ * DCP first-slice length (the default 10 is the paper's desktop-GPU figure, R14).
+ * n_qubits in [4, 28]; copy_ms / gate_ms may be NULL. */
+tqsim_status tqsim_profile_copy_cost(uint32_t n_qubits, uint32_t n_probe_gates, uint64_t seed,
+                                     double* copy_cost_gates, double* copy_ms, double* gate_ms);
+
 /* [gpu] Debug / parity hooks running the SAME device functions as the hot path.
  * Philox4x32-10 on n counters: in = n x {c0,c1,c2,c3,k0,k1}, out = n x 4 words. */
 tqsim_status tqsim_debug_philox(const uint32_t* in, uint64_t n, uint32_t* out);

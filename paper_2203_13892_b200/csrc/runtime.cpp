@@ -678,6 +678,103 @@ void tqsim_result_free(tqsim_result* r) {
   std::free(r);
 }
 
+// B200 analogue of the paper's state-copy cost measurement (§3.3,
+// fig:copy-overhead): the time of copying a batch of states
+// device-to-device, in units of the engine's time per gate application on the same
+// batch (a seeded probe slice of random U and CX gates, noise-free, run as level 1 of
+// a [1, B] tree so its passes are the engine's ordinary fused passes).
+tqsim_status tqsim_profile_copy_cost(uint32_t n_qubits, uint32_t n_probe_gates, uint64_t seed,
+                                     double* copy_cost_gates, double* copy_ms, double* gate_ms) {
+  void* a = nullptr;
+  void* b = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  tqsim_handle* h = nullptr;
+  auto cleanup = [&] {
+    if (h) tqsim_destroy(h);
+    if (a) cudaFree(a);
+    if (b) cudaFree(b);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (st) cudaStreamDestroy(st);
+  };
+  const tqsim_status r = guarded([&] {
+    if (!copy_cost_gates) throw Error{TQSIM_EINVAL, "copy_cost_gates is NULL"};
+    if (n_qubits < 4 || n_qubits > 28 || n_probe_gates < 1 || n_probe_gates > 4096)
+      throw Error{TQSIM_EINVAL, "profile needs 4 <= n_qubits <= 28 and 1..4096 probe gates"};
+    require_device();
+    const uint64_t S = 16ull << n_qubits;
+    const uint64_t B = std::max<uint64_t>(1, (1ull << 26) >> n_qubits);
+    ckc(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    ckc(cudaEventCreate(&e0), "event");
+    ckc(cudaEventCreate(&e1), "event");
+    ckc(cudaMalloc(&a, B * S), "cudaMalloc copy source");
+    ckc(cudaMalloc(&b, B * S), "cudaMalloc copy target");
+    ckc(cudaMemsetAsync(a, 0, B * S, st), "memset");
+    for (int i = 0; i < 2; ++i) ckc(cudaMemcpyAsync(b, a, B * S, cudaMemcpyDeviceToDevice, st), "copy");
+    ckc(cudaEventRecord(e0, st), "record");
+    const int reps = 5;
+    for (int i = 0; i < reps; ++i) ckc(cudaMemcpyAsync(b, a, B * S, cudaMemcpyDeviceToDevice, st), "copy");
+    ckc(cudaEventRecord(e1, st), "record");
+    ckc(cudaEventSynchronize(e1), "sync");
+    float cms = 0.f;
+    ckc(cudaEventElapsedTime(&cms, e0, e1), "elapsed");
+    const double t_copy = cms / reps;
+    cudaFree(b);
+    b = nullptr;
+    // probe slice: seeded random U(theta, phi, lambda) and CX gates; level 0 repeats it
+    // on the single root instance, level 1 runs it on the B-state batch
+    uint64_t x = seed * 0x9E3779B97F4A7C15ull + 1;
+    auto rnd = [&] {
+      x ^= x << 13;
+      x ^= x >> 7;
+      x ^= x << 17;
+      return x;
+    };
+    std::vector<tqsim_gate> probe;
+    for (uint32_t i = 0; i < 2 * n_probe_gates; ++i) {
+      tqsim_gate g{};
+      if (rnd() % 3 == 0) {
+        g.kind = TQ_CX;
+        g.q0 = (uint32_t)(rnd() % n_qubits);
+        g.q1 = (g.q0 + 1 + (uint32_t)(rnd() % (n_qubits - 1))) % n_qubits;
+      } else {
+        g.kind = TQ_U;
+        g.q0 = (uint32_t)(rnd() % n_qubits);
+        g.theta = (double)(rnd() % 1000000) * 6.283185307179586e-6;
+        g.phi = (double)(rnd() % 1000000) * 6.283185307179586e-6;
+        g.lambda = (double)(rnd() % 1000000) * 6.283185307179586e-6;
+      }
+      probe.push_back(g);
+    }
+    const tqsim_circuit c{n_qubits, 0, probe.size(), probe.data()};
+    const tqsim_noise_model nm{0.0, 0.0, 0.0, 0.0};
+    tqsim_options o;
+    tqsim_default_options(&o);
+    o.profile = 1;
+    const uint32_t ar[2] = {1, (uint32_t)B};
+    h = create_handle(&c, &nm, B, ar, 2, &o, true);
+    uint64_t t0, t1;
+    shard(h->cplan, 0, 1, t0, t1);
+    const Layout L = layout(h, t1 - t0);
+    cudaFree(a);
+    a = nullptr;
+    ckc(cudaMalloc(&a, L.total + h->cplan.n_outcomes * 4 + ALIGN), "cudaMalloc workspace");
+    uint32_t* d_out = reinterpret_cast<uint32_t*>(static_cast<char*>(a) + align_up(L.total));
+    double best = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      execute(h, 1 + i, 0, 1, st, a, L.total, d_out);
+      if (i == 0 || h->stats.pass_ms < best) best = h->stats.pass_ms;
+    }
+    const double t_gate = best / n_probe_gates;   // level 0 (one state) is ~1/B of it
+    *copy_cost_gates = t_copy / t_gate;
+    if (copy_ms) *copy_ms = t_copy;
+    if (gate_ms) *gate_ms = t_gate;
+  });
+  cleanup();
+  return r;
+}
+
 tqsim_status tqsim_debug_philox(const uint32_t* in, uint64_t n, uint32_t* out) {
   return guarded([&] {
     if (!in || !out) throw Error{TQSIM_EINVAL, "NULL argument"};

@@ -108,6 +108,8 @@ _SIGS = {
     "tqsim_lower_circuit": (C.c_int, [_P(tqsim_circuit), _P(tqsim_gate), C.c_uint64, _P(C.c_uint64)]),
     "tqsim_parse_qasm": (C.c_int, [C.c_char_p, _P(tqsim_gate), C.c_uint64, _P(C.c_uint64),
                                    _P(C.c_uint32), _P(C.c_uint32)]),
+    "tqsim_profile_copy_cost": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, _P(C.c_double),
+                                          _P(C.c_double), _P(C.c_double)]),
     "tqsim_plan_circuit": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
                                      _P(C.c_uint32), C.c_uint32, _P(tqsim_options), _P(tqsim_plan)]),
     "tqsim_describe_passes": (C.c_int, [_P(tqsim_circuit), _P(tqsim_noise_model), C.c_uint64,
@@ -218,6 +220,14 @@ def tqsim_parse_qasm(text: str):
         two = kind in ("cx", "cz", "swap", "cp")
         gates.append((kind, int(g.q0), int(g.q1) if two else -1, float(g.theta), float(g.phi), float(g.lam)))
     return int(w.value), gates, bool(m.value)
+
+
+def tqsim_profile_copy_cost(n_qubits: int, n_probe_gates: int = 64, seed: int = 0):
+    """(copy_cost_gates, copy_ms, gate_ms) measured on this GPU (SURVEY §8(f) #2)."""
+    c, cm, gm = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().tqsim_profile_copy_cost(int(n_qubits), int(n_probe_gates), int(seed), C.byref(c),
+                                         C.byref(cm), C.byref(gm)))
+    return c.value, cm.value, gm.value
 
 
 def tqsim_lower_circuit(n_qubits: int, gates) -> List[Tuple[str, int, int]]:

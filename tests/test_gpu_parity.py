@@ -262,3 +262,17 @@ def test_qasm_program_runs_like_generator():
     b = T.tqsim_run_ex(n2, g2, noise, shots, ar, 3)
     assert np.array_equal(a.leaf_outcomes, b.leaf_outcomes)
     run_and_compare(n2, g2, NoiseModel(w.p1, w.p2, w.readout_p01, w.readout_p10), shots, ar, 3)
+
+
+def test_copy_cost_profiler_feeds_dcp():
+    """the measured B200 copy cost (gate units) is finite and positive,
+    and as tqsim_options.copy_cost_gates it sets DCP's first-slice length."""
+    c, cm, gm = T.tqsim_profile_copy_cost(15, 64, 0)
+    assert np.isfinite(c) and c > 0 and cm > 0 and gm > 0
+    assert abs(c - cm / gm) <= 1e-9 * c
+    w = load_config("c2_qft15")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    p = T.tqsim_plan_circuit(n, gates, noise, shots, None, T.default_options(copy_cost_gates=c))
+    m = max(1, int(np.floor(c + 0.5)))
+    if p.n_levels > 1:
+        assert p.boundary_list[1] == m

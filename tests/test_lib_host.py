@@ -118,13 +118,27 @@ def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
     plan = T.tqsim_plan_circuit(n, gates, noise, shots, arities, options)
     low = OG.lower(gates)
     assert sorted(r.gate for r in recs) == list(range(len(low)))     # every gate exactly once
+    def in_swap_triple(g):   # CX(a,b) CX(b,a) CX(a,b): one lowered SWAP
+        for s0 in (g - 2, g - 1, g):
+            if s0 < 0 or s0 + 2 >= len(low):
+                continue
+            x, y, z = low[s0], low[s0 + 1], low[s0 + 2]
+            if x[0] == y[0] == z[0] == "cx" and x[1:3] == z[1:3] and y[1:3] == (x[2], x[1]):
+                return True
+        return False
+
     pos = {}
     for i, r in enumerate(recs):
         b = plan.boundary_list
         assert b[r.level] <= r.gate < b[r.level + 1]                 # in its own slice
         k, a, c = low[r.gate][0], low[r.gate][1], low[r.gate][2]
         qm = (1 << a) | ((1 << c) if c >= 0 else 0)
-        assert qm & ~r.reg_qubit_mask == 0                           # gate qubits in registers
+        if qm & ~r.tile_qubit_mask:
+            # absorbed SWAP: a store-address relabeling in the first (out-of-place) pass
+            # of its level, on qubits >= 3 (never the leaf run qubits)
+            assert in_swap_triple(r.gate) and r.pass_ == 0 and min(a, c) >= 3, (r.gate, r.pass_)
+        else:
+            assert qm & ~r.reg_qubit_mask == 0                       # gate qubits in registers
         assert r.reg_qubit_mask & ~r.tile_qubit_mask == 0            # registers within the tile
         assert bin(r.reg_qubit_mask).count("1") == min(4, max(n, 4))
         pos[r.gate] = (r.level, r.pass_, r.phase, i)
