@@ -1,4 +1,5 @@
-"""Fidelity metrics -- oracle copy (test infrastructure only).
+"""Fidelity metrics -- oracle copy (test infrastructure only; pinned by closed forms and
+invariants in tests/test_metrics.py).
 
 Eq.6:  F_s(P, Q) = (sum_x sqrt(P(x) Q(x)))^2
 Eq.7:  F(P_ideal, P_out) = (F_s(P_ideal, P_out) - F_s(P_ideal, P_uni))

@@ -276,3 +276,17 @@ def test_copy_cost_profiler_feeds_dcp():
     m = max(1, int(np.floor(c + 0.5)))
     if p.n_levels > 1:
         assert p.boundary_list[1] == m
+
+
+def test_accuracy_tree_vs_flat_normalized_fidelity():
+    """tree and flat outputs have matching
+    normalized fidelity (a loose statistical bound at 4,000 shots)."""
+    import importlib.util
+    import os
+    from tq_testutil import ROOT
+    spec = importlib.util.spec_from_file_location("tq_accuracy", os.path.join(ROOT, "scripts", "accuracy.py"))
+    acc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(acc)
+    r = acc.study("qft10h", 4000, 2, T.noise_arg(1e-3, 1e-2, 1e-2, 1e-2))
+    assert 0.0 < r["F_tree_mean"] <= 1.0 and 0.0 < r["F_flat_mean"] <= 1.0
+    assert r["absdiff_max"] < 0.05, r
