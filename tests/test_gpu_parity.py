@@ -287,6 +287,7 @@ def test_accuracy_tree_vs_flat_normalized_fidelity():
     spec = importlib.util.spec_from_file_location("tq_accuracy", os.path.join(ROOT, "scripts", "accuracy.py"))
     acc = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(acc)
-    r = acc.study("qft10h", 4000, 2, T.noise_arg(1e-3, 1e-2, 1e-2, 1e-2))
+    r = acc.study("qft10h", 16000, 4, T.noise_arg(1e-3, 1e-2, 1e-2, 1e-2))
     assert 0.0 < r["F_tree_mean"] <= 1.0 and 0.0 < r["F_flat_mean"] <= 1.0
-    assert r["absdiff_max"] < 0.05, r
+    assert len(r["tree_arities"]) > 1                      # a real tree (DCP), not the flat plan
+    assert r["diff_of_means"] < 0.06, r                   # statistical: ~0.02 expected
