@@ -846,12 +846,15 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       return -1;
     };
     bool gph_on = false;
+    int fb_gen = 0;
     struct FBv {
       bool on = false;
       bool one[2] = {true, true};   // F_b[v] still exactly 1 (never assigned)
       std::string var[2];
     };
     FBv fb[RBITS];
+    for (int b = 0; b < RBITS; ++b)
+      for (int v = 0; v < 2; ++v) fb[b].var[v] = "fb" + std::to_string(b) + "_" + std::to_string(v);
     std::set<std::string> declared;
     // apply pending F_b to the registers (before an op mixing bit b), then reset it
     auto fb_flush = [&](int b, int& gen) {
@@ -885,11 +888,6 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       // Diagonals on (thread bit, register bit b) accumulate into per-thread factors
       // F_b[0], F_b[1] (one per value of logical register bit b), applied once -- at
       // the phase end through a product tree, or before an op that mixes bit b.
-      for (int b = 0; b < RBITS; ++b) {
-        fb[b] = FBv();
-        for (int v = 0; v < 2; ++v) fb[b].var[v] = "fb" + std::to_string(b) + "_" + std::to_string(v);
-      }
-      int fb_gen = 0;
       for (int it : specs[ph].items) {
         const FOp& f = fops[it];
         if (f.kind == FOp::CX) {
@@ -1053,16 +1051,20 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
 
         if (f.kind == FOp::CX) {
           const int ba = rbit(f.qa), bb = rbit(f.qb);
+          fb_flush(bb, fb_gen);
           permute([&](int k) { return k ^ (((k >> ba) & 1) << bb); });
           o << "    fx ^= ((fx >> " << f.qa << ") & 1u) << " << f.qb << "; fz ^= ((fz >> " << f.qb << ") & 1u) << "
             << f.qa << ";\n";
         } else if (f.kind == FOp::XPERM) {
           const int ba = rbit(f.qa);
+          std::swap(fb[ba].var[0], fb[ba].var[1]);
+          std::swap(fb[ba].one[0], fb[ba].one[1]);
           permute([&](int k) { return k ^ (1 << ba); });
           o << "    fk += ((fz >> " << f.qa << ") & 1u) << 1;\n";
         } else if (f.kind == FOp::GEN) {
           // F^+ U F on this qubit: variant v = x | z << 1 of Z^z X^x U X^x Z^z
           const int ba = rbit(f.qa);
+          fb_flush(ba, fb_gen);
           cplx V[4][4];   // [v][entry]
           for (int v = 0; v < 4; ++v) {
             cplx u[4] = {f.m[0], f.m[1], f.m[2], f.m[3]};
@@ -1128,15 +1130,74 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
         } else if (f.kind == FOp::DIAG) {
           pool.begin_op();
-          std::string ent[8];
-          for (int i = 0; i < 4; ++i) {
-            const cplx d = f.d[i];
-            ent[2 * i] = d.real() == 1.0 ? "1.0" : d.real() == 0.0 ? "0.0" : g_pool->ref(d.real());
-            ent[2 * i + 1] = d.imag() == 0.0 ? "0.0" : g_pool->ref(d.imag());
+          const int ra = rbit(f.qa), rb = f.qb >= 0 ? rbit(f.qb) : -2;
+          const bool rta = ra < 0, rtb = rb == -1;
+          auto entry = [&](int bita, int bitb) { return f.d[bita | (bitb << 1)]; };
+          auto val = [&](const cplx& v, bool im) { return g_pool->ref(im ? v.imag() : v.real()); };
+          // thread bit of qubit q XOR its frame bit (frame-conjugated diagonal: D(i ^ x))
+          auto tbit = [&](int q) {
+            return "(((lth >> " + std::to_string(qpos[q]) + ") ^ (fx >> " + std::to_string(q) + ")) & 1u)";
+          };
+          if (!rta && !rtb) {   // both register bits: applied now (frame-dependent, no folding)
+            std::string ent[8];
+            for (int i = 0; i < 4; ++i) {
+              const cplx d = f.d[i];
+              ent[2 * i] = d.real() == 1.0 ? "1.0" : d.real() == 0.0 ? "0.0" : g_pool->ref(d.real());
+              ent[2 * i + 1] = d.imag() == 0.0 ? "0.0" : g_pool->ref(d.imag());
+            }
+            o << "    {\n" << pool.decl.str();
+            emit_frame_diag(f.qa, f.qb, ent, false);
+            o << "    }\n";
+          } else if (rta && (rtb || rb == -2)) {   // thread bits only: into the common factor
+            std::ostringstream oo;
+            const std::string A = tbit(f.qa), B = rb == -2 ? std::string("0u") : tbit(f.qb);
+            auto sel = [&](bool im) {
+              return "(" + B + " ? (" + A + " ? " + val(entry(1, 1), im) + " : " + val(entry(0, 1), im) + ") : (" +
+                     A + " ? " + val(entry(1, 0), im) + " : " + val(entry(0, 0), im) + "))";
+            };
+            if (!gph_on) {
+              o << "    double gphx = 1.0, gphy = 0.0;\n";
+              gph_on = true;
+            }
+            oo << "      { const double fr = " << sel(false) << ", fi = " << sel(true) << ";\n"
+               << "        const double tx = fma(gphx, fr, -gphy * fi); gphy = fma(gphx, fi, gphy * fr); gphx = tx; }\n";
+            o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+          } else {   // one register bit, one thread bit: per-bit factors F_b[v]
+            const bool a_reg = !rta;
+            const int rbit_reg = a_reg ? ra : rb, q_reg = a_reg ? f.qa : f.qb, q_rt = a_reg ? f.qb : f.qa;
+            const std::string TB = tbit(q_rt), XR = "((fx >> " + std::to_string(q_reg) + ") & 1u)";
+            std::ostringstream oo;
+            for (int bk = 0; bk < 2; ++bk) {
+              // entry at (thread bit t, register value w) in the op's (a, b) orientation
+              auto E = [&](int t, int w) { return a_reg ? entry(w, t) : entry(t, w); };
+              bool all_one = true;
+              for (int t = 0; t < 2; ++t)
+                for (int w = 0; w < 2; ++w)
+                  if (E(t, w) != cplx(1, 0)) all_one = false;
+              if (all_one) continue;
+              FBv& F = fb[rbit_reg];
+              // register value seen by the diagonal: bk ^ frame bit
+              auto sel = [&](bool im) {
+                return "(" + XR + " ? (" + TB + " ? " + val(E(1, bk ^ 1), im) + " : " + val(E(0, bk ^ 1), im) +
+                       ") : (" + TB + " ? " + val(E(1, bk), im) + " : " + val(E(0, bk), im) + "))";
+              };
+              const std::string& X = F.var[bk];
+              if (F.one[bk]) {
+                if (!declared.count(X)) {
+                  o << "    double " << X << "r, " << X << "i;\n";
+                  declared.insert(X);
+                }
+                oo << "      " << X << "r = " << sel(false) << "; " << X << "i = " << sel(true) << ";\n";
+                F.one[bk] = false;
+              } else {
+                oo << "      { const double er = " << sel(false) << ", ei = " << sel(true) << ";\n"
+                   << "        const double t = fma(" << X << "r, er, -" << X << "i * ei); " << X << "i = fma(" << X
+                   << "r, ei, " << X << "i * er); " << X << "r = t; }\n";
+              }
+              F.on = true;
+            }
+            o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
           }
-          o << "    {\n" << pool.decl.str();
-          emit_frame_diag(f.qa, f.qb, ent, false);
-          o << "    }\n";
         }
         // the run's drawn errors, in gate order (uniform branch; rare)
         if (!f.sites.empty()) {
@@ -1173,7 +1234,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         }
       }
     }
-    if (!with_errors) {   // flush the pending phases (run-time factors, then compile-time)
+    {   // flush the pending phases (run-time factors, then compile-time)
       // product tree T[idx] = gph * prod_{b in L} F_b[bit of idx], idx over the pending bits L
       std::vector<int> L;
       for (int b = 0; b < RBITS; ++b)
