@@ -198,6 +198,94 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
   }
 }
 
+// Small states (<= 2^17 amplitudes): one CTA per leaf reads all of the leaf's run sums
+// (16-64 per thread, contiguous), block-scans the per-thread totals, and the thread
+// whose range crosses u*total walks its runs; then the run's 8 amplitudes -> x and
+// readout -- the chunk level (and its kernel) is not needed (§2.3, R9, R11).
+__device__ __forceinline__ uint32_t readout_flips(uint32_t xi, uint32_t n_user, uint64_t leaf,
+                                                  uint64_t seed, double p01, double p10) {
+  uint32_t mask = 0;
+  if (p01 > 0.0 || p10 > 0.0) {
+    tq_w4 rw = {0, 0, 0, 0};
+    for (uint32_t b = 0; b < n_user; ++b) {
+      if ((b & 3u) == 0) rw = tq_philox_keyed(b >> 2, leaf, 2u, seed);
+      const uint32_t wv = (b & 3u) == 0 ? rw.x : (b & 3u) == 1 ? rw.y : (b & 3u) == 2 ? rw.z : rw.w;
+      const double p = ((xi >> b) & 1u) ? p10 : p01;
+      if ((double)wv * 0x1p-32 < p) mask |= 1u << b;
+    }
+  }
+  return mask;
+}
+
+__global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__ states,
+                                                          const double* __restrict__ runs,
+                                                          uint32_t n, uint32_t n_user,
+                                                          uint64_t leaf_first, uint64_t seed,
+                                                          double p01, double p10,
+                                                          uint32_t* __restrict__ out) {
+  __shared__ double wsum[MT / 32];
+  __shared__ int first_sh;
+  const uint32_t s = blockIdx.x;
+  const uint64_t leaf = leaf_first + s;
+  const uint32_t R = 1u << (n - RUN_Q);              // runs per state
+  const uint32_t per = R > MT ? R / MT : 1u;         // runs per thread (power of two)
+  const double* rs = runs + ((uint64_t)s << (n - RUN_Q));
+  const uint32_t r0 = threadIdx.x * per;
+  double loc = 0.0;
+  if (r0 < R)
+    for (uint32_t j = 0; j < per; ++j) loc += rs[r0 + j];
+  const double incl = block_incl_scan(loc, wsum);
+  __shared__ double total_sh;
+  if (threadIdx.x == MT - 1) total_sh = incl;
+  __syncthreads();
+  const double total = total_sh;
+  const double target = tq_measure_uniform(leaf, seed) * total;
+  int t = block_first(incl > target, &first_sh);
+  if (t >= MT) {   // rounding: u*total at the very top -> the last thread with mass
+    __syncthreads();
+    if (threadIdx.x == 0) first_sh = -1;
+    __syncthreads();
+    if (loc > 0.0) atomicMax(&first_sh, (int)threadIdx.x);
+    __syncthreads();
+    t = first_sh < 0 ? 0 : first_sh;
+  }
+  if ((int)threadIdx.x == t) {
+    double acc = incl - loc;
+    uint32_t run = r0, lastnz = r0;
+    bool found = false;
+    for (uint32_t j = 0; j < per && r0 + j < R; ++j) {
+      const double v = rs[r0 + j];
+      if (v > 0.0) lastnz = r0 + j;
+      if (acc + v > target) {
+        run = r0 + j;
+        found = true;
+        break;
+      }
+      acc += v;
+    }
+    if (!found) {   // rounding between the scan and the walk: the last run with mass
+      run = lastnz;
+      acc = incl - loc;
+      for (uint32_t j = r0; j < run; ++j) acc += rs[j];
+    }
+    const double t3 = target - acc;
+    const uint64_t base = (uint64_t)run << RUN_Q;
+    const cd* ap = states + ((uint64_t)s << n) + base;
+    double c = 0.0;
+    int x = -1, lastamp = -1;
+    for (int e = 0; e < (1 << RUN_Q); ++e) {
+      const cd v = ap[e];
+      const double pr = v.x * v.x + v.y * v.y;
+      if (pr > 0.0) lastamp = e;
+      c += pr;
+      if (x < 0 && c > t3) x = e;
+    }
+    if (x < 0) x = lastamp >= 0 ? lastamp : 0;
+    const uint32_t xi = (uint32_t)(base + (uint64_t)x);
+    out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
+  }
+}
+
 // ------------------------------------------------------------------ debug hooks
 __global__ void philox_debug_kernel(const uint32_t* in, uint64_t n, uint32_t* out) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -276,6 +364,16 @@ int launch_sample(const void* states, const double* runsums, const double* sums,
   dev::sample_kernel<<<batch, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const dev::cd*>(states), runsums, sums, (uint32_t)n_sim, (uint32_t)n_user,
       (uint32_t)chunk_log2, leaf_first, seed, p01, p10, d_out);
+  return (int)cudaGetLastError();
+}
+
+int launch_sample_small(const void* states, const double* runsums, uint32_t batch, int n_sim,
+                        int n_user, uint64_t leaf_first, uint64_t seed, double p01, double p10,
+                        uint32_t* d_out, void* stream) {
+  if (batch == 0) return 0;
+  dev::sample_small_kernel<<<batch, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const dev::cd*>(states), runsums, (uint32_t)n_sim, (uint32_t)n_user, leaf_first,
+      seed, p01, p10, d_out);
   return (int)cudaGetLastError();
 }
 

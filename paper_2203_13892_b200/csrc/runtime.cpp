@@ -285,17 +285,25 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       double* sums = reinterpret_cast<double*>(x.ws + x.L.sums_off);
       const double* runs = reinterpret_cast<const double*>(x.ws + x.L.runs_off);
       mark(x, 1);
-      ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
-      ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, x.seed,
-                       h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
-         "sample launch");
-      mark(x, 1);
-      h->stats.kernel_launches += 2;
-      h->stats.measure_launches += 2;
-      // run sums read once; per leaf the chunk sums, one chunk of run sums, 8 amplitudes
-      h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8 +
-                                cnt * ((8ull << (n - x.L.chunk_log2)) +
-                                       (8ull << (x.L.chunk_log2 - RUN_Q)) + (16ull << RUN_Q));
+      if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {   // one kernel: all run sums of each leaf
+        ck(launch_sample_small(buf, runs, (uint32_t)cnt, n, (int)h->n_user, b, x.seed,
+                               h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
+           "sample launch");
+        h->stats.kernel_launches += 1;
+        h->stats.measure_launches += 1;
+        h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8 + cnt * (16ull << RUN_Q);
+      } else {
+        ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
+        ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, x.seed,
+                         h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
+           "sample launch");
+        h->stats.kernel_launches += 2;
+        h->stats.measure_launches += 2;
+        // run sums read once; per leaf the chunk sums, one chunk of run sums, 8 amplitudes
+        h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8 +
+                                  cnt * ((8ull << (n - x.L.chunk_log2)) +
+                                         (8ull << (x.L.chunk_log2 - RUN_Q)) + (16ull << RUN_Q));
+      }
       h->stats.leaves += cnt;
     } else {
       const uint64_t A = h->plan.arities[d + 1];

@@ -126,6 +126,11 @@ int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chun
 int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
                   int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, uint64_t seed,
                   double p01, double p10, uint32_t* d_out, void* stream);
+// n_sim - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2: one kernel reads all run sums of a leaf
+constexpr int SMALL_SAMPLE_RUNS_LOG2 = 14;
+int launch_sample_small(const void* states, const double* runsums, uint32_t batch, int n_sim,
+                        int n_user, uint64_t leaf_first, uint64_t seed, double p01, double p10,
+                        uint32_t* d_out, void* stream);
 int launch_philox_debug(const uint32_t* d_in, uint64_t n, uint32_t* d_out);
 int launch_noise_table(const uint8_t* d_two, uint32_t slice_begin, uint32_t slice_len,
                        uint64_t inst_begin, uint64_t count, uint64_t seed, double p1, double p2,
