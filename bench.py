@@ -15,8 +15,9 @@ value     noisy shots/s = outcomes per tree * K / (max over ranks of the CUDA-ev
 e2e       the same metric through the C-ABI call a user makes (tqsim_run for N=1:
           host circuit in, host histogram out; planning, H2D of the gate tables,
           D2H of the outcomes and the histogram inside the timed region).
-roofline  gate-pass kernel: algorithmic bytes / summed CUDA-event launch time of
-          the pass kernels in profiled steps, vs MEASURED_PEAKS.json hbm_gbs.
+roofline  gate-pass kernels: algorithmic bytes / CUDA-event time of every distinct pass
+          kernel (5 back-to-back launches on its in-tree operands, tqsim_profile_passes),
+          weighted by its launches per tree, vs MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline  the oracle (oracle/, numpy, 1 thread) on a bounded sample of the
           same workload (one top-level subtree), rank 0 only.
 """
@@ -220,25 +221,19 @@ def main():
     ms = float(t.item())
     clocks = clk.summary()
 
-    # roofline of the gate-pass kernel: profiled steps (CUDA events around every launch)
-    popts = T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, profile=1)
-    hp = T.tqsim_create(n, gates, noise, shots, ar, popts)
-    pass_ms = meas_ms = 0.0
-    pass_bytes = meas_bytes = 0
-    pass_launches = 0
-    for i in range(max(1, min(args.steps, 3))):
-        out.zero_()
-        hp.execute(i, rank, xw, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
-        s = hp.stats()
-        pass_ms += s.pass_ms
-        meas_ms += s.measure_ms
-        pass_bytes += s.pass_bytes
-        meas_bytes += s.measure_bytes
-        pass_launches += s.pass_launches
-    hp.close()
+    # roofline of the gate-pass kernel family: every distinct pass kernel timed live with
+    # CUDA events on this stream over back-to-back launches on its in-tree operands
+    # (tqsim_profile_passes), weighted by its launches per tree.  (Per-launch events
+    # around every kernel of the tree under-measured the kernels by ~25% on B200 --
+    # their sum disagreed with the step time and the ncu launch list -- so they are not used.)
+    timings = h.profile_passes(0, rank, xw, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr(), reps=5)
+    pass_ms = sum(t.ms_per_launch * t.launches_per_tree for t in timings)
+    pass_bytes = sum(t.alg_bytes_per_launch * t.launches_per_tree for t in timings)
+    pass_launches = sum(t.launches_per_tree for t in timings)
+    top = max(timings, key=lambda t: t.ms_per_launch * t.launches_per_tree)
     hbm_peak, peak_src = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9 if pass_ms > 0 else 0.0
-    pt = torch.tensor([pass_ms, meas_ms], dtype=torch.float64, device=dev)
+    top_achieved = top.alg_bytes_per_launch / (top.ms_per_launch * 1e-3) / 1e9
 
     # end to end through the public API with HOST buffers: N=1 the north_star call
     # tqsim_run (host circuit in -> lowering, planning, kernel-cache lookup, tree, D2H of
@@ -319,12 +314,17 @@ def main():
                          "traffic_source": traffic["source"] if traffic else None,
                          "alg_bytes_same_launch": traffic["alg_bytes_per_launch"] if traffic else None,
                          "peak_source": peak_src,
-                         "kernel": "tq_pass_l*_p* (run-time specialized gate pass, all launches)",
-                         "pass_share_of_step": float(pt[0].item()) / (float(pt[0].item()) + float(pt[1].item()))
-                         if (pt[0].item() + pt[1].item()) > 0 else None,
-                         "pass_launches_profiled": pass_launches,
+                         "kernel": "tq_pass_l*_p* (run-time specialized gate pass, all launches, "
+                                   "weighted by launches per tree)",
+                         "method": "per-kernel CUDA events over 5 back-to-back launches on in-tree operands",
+                         "pass_ms_per_step": pass_ms,
+                         "pass_share_of_step": pass_ms / (ms / args.steps),
                          "alg_bytes_per_launch": pass_bytes / pass_launches if pass_launches else None,
-                         "pass_launches_per_step": pass_launches / max(1, min(args.steps, 3))},
+                         "pass_launches_per_step": pass_launches,
+                         "top_kernel": {"name": "tq_pass_l%d_p%d" % (top.level, top.pass_),
+                                        "ms_per_launch": top.ms_per_launch,
+                                        "launches_per_step": top.launches_per_tree,
+                                        "achieved_gbs": top_achieved, "frac": top_achieved / hbm_peak}},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "e2e": e2e,

@@ -161,6 +161,16 @@ typedef struct {
   uint64_t reg_qubit_mask;             /* global qubits held in registers in the phase */
 } tqsim_op_record;
 
+/* Timing of one gate-pass kernel (tqsim_profile_passes). */
+typedef struct {
+  uint32_t level, pass;
+  uint32_t states_per_launch;        /* batch the kernel was timed on (a full level batch) */
+  uint32_t reserved;
+  double launches_per_tree;          /* this shard's launches of the kernel, in full-batch units */
+  double ms_per_launch;              /* CUDA-event average over `reps` back-to-back launches */
+  double alg_bytes_per_launch;       /* algorithmic HBM bytes of one launch */
+} tqsim_pass_timing;
+
 typedef struct tqsim_handle tqsim_handle;
 
 /* [host] */
@@ -243,6 +253,16 @@ tqsim_status tqsim_workspace_bytes(const tqsim_handle* h, uint32_t rank, uint32_
 tqsim_status tqsim_execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world,
                            void* stream, void* d_workspace, uint64_t workspace_bytes,
                            uint32_t* d_leaf_outcomes);
+
+/* [gpu] Live timing of every gate-pass kernel of the handle (the roofline input of
+ * bench.py): runs the shard once (seed) to fill the workspace with real states, then
+ * for each (level, pass) re-runs that level's first batch's noise rows and times `reps`
+ * back-to-back launches of the pass on its in-tree operands with CUDA events on
+ * `stream`.  Synchronous; out: capacity `cap` records (NULL / 0 to query *n_out). */
+tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world,
+                                  void* stream, void* d_workspace, uint64_t workspace_bytes,
+                                  uint32_t* d_leaf_outcomes, uint32_t reps, tqsim_pass_timing* out,
+                                  uint64_t cap, uint64_t* n_out);
 
 /* [gpu] The north_star call: host circuit in, host histogram out (allocates
  * its own workspace, synchronous).  tree_arities NULL = auto (DCP). */

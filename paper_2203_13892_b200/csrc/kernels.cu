@@ -142,8 +142,9 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
                                                     const double* __restrict__ runs,
                                                     const double* __restrict__ sums, uint32_t n,
                                                     uint32_t n_user, uint32_t chunk_log2,
-                                                    uint64_t leaf_first, uint64_t seed, double p01,
-                                                    double p10, uint32_t* __restrict__ out) {
+                                                    uint64_t leaf_first, const uint64_t* __restrict__ seedp,
+                                                    double p01, double p10, uint32_t* __restrict__ out) {
+  const uint64_t seed = *seedp;
   __shared__ double wsum[MT / 32];
   __shared__ int first_sh;
   __shared__ uint64_t pick_sh;
@@ -220,9 +221,11 @@ __device__ __forceinline__ uint32_t readout_flips(uint32_t xi, uint32_t n_user, 
 __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__ states,
                                                           const double* __restrict__ runs,
                                                           uint32_t n, uint32_t n_user,
-                                                          uint64_t leaf_first, uint64_t seed,
+                                                          uint64_t leaf_first,
+                                                          const uint64_t* __restrict__ seedp,
                                                           double p01, double p10,
                                                           uint32_t* __restrict__ out) {
+  const uint64_t seed = *seedp;
   __shared__ double wsum[MT / 32];
   __shared__ int first_sh;
   const uint32_t s = blockIdx.x;
@@ -315,8 +318,9 @@ __global__ void noise_table_kernel(const uint8_t* two, uint32_t slice_begin, uin
 // instances take the fused fast path).  Drawn once per instance, not per tile.
 __global__ void __launch_bounds__(256) noise_rows_kernel(
     const uint8_t* __restrict__ two, const uint8_t* __restrict__ pass_of, uint32_t slice_begin,
-    uint32_t slice_len, uint64_t inst_first, uint32_t count, uint64_t seed, double p1, double p2,
-    uint32_t row_bytes, uint8_t* __restrict__ rows) {
+    uint32_t slice_len, uint64_t inst_first, uint32_t count, const uint64_t* __restrict__ seedp,
+    double p1, double p2, uint32_t row_bytes, uint8_t* __restrict__ rows) {
+  const uint64_t seed = *seedp;
   const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
   if (w >= count) return;
@@ -334,17 +338,25 @@ __global__ void __launch_bounds__(256) noise_rows_kernel(
   if (lane == 0) *reinterpret_cast<uint32_t*>(row) = mask;
 }
 
+// The run's seed in device memory: the tree's launches (a replayed CUDA graph) read it
+__global__ void set_seed_kernel(uint64_t* d_seed, uint64_t seed) { *d_seed = seed; }
+
 }  // namespace dev
 
 // ------------------------------------------------------------------ launchers
+int launch_set_seed(uint64_t* d_seed, uint64_t seed, void* stream) {
+  dev::set_seed_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_seed, seed);
+  return (int)cudaGetLastError();
+}
+
 int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t slice_begin,
-                      uint32_t slice_len, uint64_t inst_first, uint32_t count, uint64_t seed,
+                      uint32_t slice_len, uint64_t inst_first, uint32_t count, const uint64_t* d_seed,
                       double p1, double p2, uint32_t row_bytes, uint8_t* d_rows, void* stream) {
   if (count == 0) return 0;
   const uint64_t threads = (uint64_t)count * 32;
   dev::noise_rows_kernel<<<(unsigned)((threads + 255) / 256), 256, 0,
                            static_cast<cudaStream_t>(stream)>>>(
-      d_two, d_pass_of, slice_begin, slice_len, inst_first, count, seed, p1, p2, row_bytes, d_rows);
+      d_two, d_pass_of, slice_begin, slice_len, inst_first, count, d_seed, p1, p2, row_bytes, d_rows);
   return (int)cudaGetLastError();
 }
 
@@ -358,22 +370,22 @@ int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chun
 }
 
 int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
-                  int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, uint64_t seed,
+                  int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, const uint64_t* d_seed,
                   double p01, double p10, uint32_t* d_out, void* stream) {
   if (batch == 0) return 0;
   dev::sample_kernel<<<batch, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const dev::cd*>(states), runsums, sums, (uint32_t)n_sim, (uint32_t)n_user,
-      (uint32_t)chunk_log2, leaf_first, seed, p01, p10, d_out);
+      (uint32_t)chunk_log2, leaf_first, d_seed, p01, p10, d_out);
   return (int)cudaGetLastError();
 }
 
 int launch_sample_small(const void* states, const double* runsums, uint32_t batch, int n_sim,
-                        int n_user, uint64_t leaf_first, uint64_t seed, double p01, double p10,
+                        int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
                         uint32_t* d_out, void* stream) {
   if (batch == 0) return 0;
   dev::sample_small_kernel<<<batch, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const dev::cd*>(states), runsums, (uint32_t)n_sim, (uint32_t)n_user, leaf_first,
-      seed, p01, p10, d_out);
+      d_seed, p01, p10, d_out);
   return (int)cudaGetLastError();
 }
 

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -32,6 +34,13 @@ struct tqsim_handle {
   double compile_s = 0.0;
   uint8_t* d_two = nullptr;
   uint8_t* d_pass_of = nullptr;   // per lowered gate: index of its pass in its level (<= 31)
+  uint64_t* d_seed = nullptr;     // the run's seed (set by a 1-thread kernel before the tree)
+  // CUDA graph of the whole tree (every launch of run_level), replayed by later executes
+  // with the same workspace / outcome buffers / shard; seed-independent (read from d_seed)
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t capture_stream = nullptr;
+  std::vector<uint64_t> graph_key;
+  tqsim_stats graph_stats{};
   std::vector<uint8_t> h_tables;  // host copy: [two flags | pass index] per lowered gate
   tqsim_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
@@ -205,6 +214,11 @@ cudaEvent_t next_event(tqsim_handle* h) {
 
 void mark(Exec& x, int kind) {
   if (!x.h->opts.profile) return;
+  static const bool sync = [] {
+    const char* e = std::getenv("TQSIM_PROFILE_SYNC");
+    return e && e[0] == '1';
+  }();
+  if (sync) ckc(cudaStreamSynchronize(x.st), "profile sync");
   cudaEvent_t e = next_event(x.h);
   ckc(cudaEventRecord(e, x.st), "cudaEventRecord");
   x.h->ev_marks.push_back({kind, x.h->ev_used - 1});
@@ -242,7 +256,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     const uint64_t cnt = std::min(cap, i1 - b);
     // noise rows of the batch (row a3): keyed Pauli codes + per-pass error bitmask
     mark(x, 2);
-    ck(launch_noise_rows(h->d_two, h->d_pass_of, slice_begin, slice_len, b, (uint32_t)cnt, x.seed,
+    ck(launch_noise_rows(h->d_two, h->d_pass_of, slice_begin, slice_len, b, (uint32_t)cnt, h->d_seed,
                          h->noise.p1, h->noise.p2, row_bytes, rows, x.st),
        "noise rows launch");
     mark(x, 2);
@@ -286,7 +300,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       const double* runs = reinterpret_cast<const double*>(x.ws + x.L.runs_off);
       mark(x, 1);
       if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {   // one kernel: all run sums of each leaf
-        ck(launch_sample_small(buf, runs, (uint32_t)cnt, n, (int)h->n_user, b, x.seed,
+        ck(launch_sample_small(buf, runs, (uint32_t)cnt, n, (int)h->n_user, b, h->d_seed,
                                h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
            "sample launch");
         h->stats.kernel_launches += 1;
@@ -294,7 +308,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
         h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8 + cnt * (16ull << RUN_Q);
       } else {
         ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
-        ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, x.seed,
+        ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, h->d_seed,
                          h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
            "sample launch");
         h->stats.kernel_launches += 2;
@@ -341,6 +355,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
       const size_t G = std::max<size_t>(h->gates.size(), 1);
       ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_two), G), "cudaMalloc two");
       ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_pass_of), G), "cudaMalloc pass_of");
+      ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_seed), 8), "cudaMalloc seed");
       h->h_tables.assign(2 * G, 0);
       for (size_t g = 0; g < h->gates.size(); ++g) h->h_tables[g] = h->gates[g].two ? 1 : 0;
       for (const auto& lvl : h->pp.levels)
@@ -372,7 +387,46 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
   h->stats = tqsim_stats{};
   h->ev_used = 0;
   h->ev_marks.clear();
+  ck(launch_set_seed(h->d_seed, seed, st), "seed launch");
+  static const bool graphs = [] {
+    const char* e = std::getenv("TQSIM_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  const bool dumps = h->debug && h->debug->n_dumps;
+  if (t1 > t0 && graphs && !h->opts.profile && !dumps) {
+    // replay the captured tree: one graph launch instead of one host launch per kernel
+    const std::vector<uint64_t> key = {reinterpret_cast<uint64_t>(ws), ws_bytes, reinterpret_cast<uint64_t>(d_out),
+                                       rank, world};
+    if (!h->graph_exec || h->graph_key != key) {
+      if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+      h->graph_exec = nullptr;
+      if (!h->capture_stream)
+        ckc(cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking), "capture stream");
+      Exec xc = x;
+      xc.st = h->capture_stream;
+      ckc(cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+      cudaGraph_t g = nullptr;
+      try {
+        run_level(xc, 0, t0, t1, 0);
+      } catch (...) {
+        cudaStreamEndCapture(h->capture_stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      ckc(cudaStreamEndCapture(h->capture_stream, &g), "end capture");
+      const cudaError_t e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      ckc(e, "graph instantiate");
+      h->graph_key = key;
+      h->graph_stats = h->stats;
+    }
+    h->stats = h->graph_stats;
+    h->stats.kernel_launches += 1;   // the seed kernel
+    ckc(cudaGraphLaunch(h->graph_exec, st), "graph launch");
+    return;
+  }
   if (t1 > t0) run_level(x, 0, t0, t1, 0);
+  h->stats.kernel_launches += 1;     // the seed kernel
   if (h->opts.profile) {
     ckc(cudaStreamSynchronize(st), "profile sync");
     for (size_t i = 0; i + 1 < h->ev_marks.size(); i += 2) {
@@ -383,6 +437,16 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
       if (h->ev_marks[i].first == 0) h->stats.pass_ms += ms;
       else if (h->ev_marks[i].first == 1) h->stats.measure_ms += ms;
       else h->stats.noise_ms += ms;
+    }
+    if (const char* path = std::getenv("TQSIM_PROFILE_DUMP")) {   // every interval: kind, ms
+      if (FILE* f = std::fopen(path, "a")) {
+        for (size_t i = 0; i + 1 < h->ev_marks.size(); ++i) {
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, h->ev_pool[h->ev_marks[i].second], h->ev_pool[h->ev_marks[i + 1].second]);
+          std::fprintf(f, "%d %d %.6f\n", h->ev_marks[i].first, (int)(i & 1), ms);
+        }
+        std::fclose(f);
+      }
     }
   }
 }
@@ -578,6 +642,9 @@ void tqsim_destroy(tqsim_handle* h) {
   if (!h) return;
   if (h->d_two) cudaFree(h->d_two);
   if (h->d_pass_of) cudaFree(h->d_pass_of);
+  if (h->d_seed) cudaFree(h->d_seed);
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   delete h;
 }
@@ -599,6 +666,85 @@ tqsim_status tqsim_execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32
     execute(h, seed, rank, world, static_cast<cudaStream_t>(stream), d_workspace, workspace_bytes,
             d_leaf_outcomes);
   });
+}
+
+tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world,
+                                  void* stream, void* d_workspace, uint64_t workspace_bytes,
+                                  uint32_t* d_leaf_outcomes, uint32_t reps, tqsim_pass_timing* out,
+                                  uint64_t cap, uint64_t* n_out) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const tqsim_status r = guarded([&] {
+    if (!h || !n_out || reps < 1) throw Error{TQSIM_EINVAL, "NULL argument or reps < 1"};
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // one real run: every level buffer holds states of the tree (batch 0 of each level)
+    execute(h, seed, rank, world, st, d_workspace, workspace_bytes, d_leaf_outcomes);
+    ckc(cudaStreamSynchronize(st), "sync");
+    uint64_t t0, t1;
+    shard(h->cplan, rank, world, t0, t1);
+    Exec x{h, seed, st, static_cast<char*>(d_workspace), layout(h, t1 - t0), d_leaf_outcomes};
+    ckc(cudaEventCreate(&e0), "event");
+    ckc(cudaEventCreate(&e1), "event");
+    const int n = h->n_sim;
+    uint64_t k = 0, inst = t1 - t0;
+    for (size_t d = 0; d < h->pp.levels.size(); ++d) {
+      if (d > 0) inst *= h->plan.arities[d];
+      const uint64_t cnt = std::min<uint64_t>(x.L.cap[d], inst);
+      const uint64_t first = d == 0 ? t0 : (t0 * (inst / (t1 - t0)));   // first instance of the shard
+      const uint32_t slice_begin = (uint32_t)h->plan.bounds[d];
+      const uint32_t slice_len = (uint32_t)(h->plan.bounds[d + 1] - slice_begin);
+      const uint32_t row_bytes = noise_row_bytes(slice_len);
+      uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off);
+      ck(launch_noise_rows(h->d_two, h->d_pass_of, slice_begin, slice_len, first, (uint32_t)cnt, h->d_seed,
+                           h->noise.p1, h->noise.p2, row_bytes, rows, st),
+         "noise rows launch");
+      for (size_t p = 0; p < h->pp.levels[d].size(); ++p) {
+        PassLaunch pl{};
+        pl.src_mode = p > 0 ? 2u : (d == 0 ? 0u : 1u);
+        pl.src = d > 0 ? x.ws + x.L.off[d - 1] : nullptr;
+        pl.dst = x.ws + x.L.off[d];
+        pl.child_first = first;
+        pl.parent_first = d > 0 ? first / h->plan.arities[d] : 0;
+        pl.arity = h->plan.arities[d];
+        pl.batch = (uint32_t)cnt;
+        pl.seed = seed;
+        pl.p1 = h->noise.p1;
+        pl.p2 = h->noise.p2;
+        pl.runsum = x.ws + x.L.runs_off;
+        pl.rows = rows;
+        pl.row_bytes = row_bytes;
+        const PassDesc& pd = h->pp.levels[d][p];
+        ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");   // warm
+        ckc(cudaEventRecord(e0, st), "record");
+        for (uint32_t i = 0; i < reps; ++i) ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");
+        ckc(cudaEventRecord(e1, st), "record");
+        ckc(cudaEventSynchronize(e1), "sync");
+        float ms = 0.f;
+        ckc(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+        const uint64_t amps = cnt << n;
+        double bytes = (double)amps * 16;
+        if (pl.src_mode == 2) bytes += (double)amps * 16;
+        else if (pl.src_mode == 1) {
+          const uint64_t A = pl.arity, parents = (first + cnt - 1) / A - first / A + 1;
+          bytes += (double)(parents << n) * 16;
+        }
+        if (out && k < cap) {
+          tqsim_pass_timing& o = out[k];
+          o.level = (uint32_t)d;
+          o.pass = (uint32_t)p;
+          o.states_per_launch = (uint32_t)cnt;
+          o.reserved = 0;
+          o.launches_per_tree = (double)inst / (double)cnt;
+          o.ms_per_launch = ms / reps;
+          o.alg_bytes_per_launch = bytes;
+        }
+        ++k;
+      }
+    }
+    *n_out = k;
+  });
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  return r;
 }
 
 tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,

@@ -118,18 +118,19 @@ struct PassLaunch {
 // [4 + t] = Pauli code of slice gate t (0 = none).  One warp per instance.
 inline uint32_t noise_row_bytes(uint32_t slice_len) { return (4u + slice_len + 15u) / 16u * 16u; }
 int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t slice_begin,
-                      uint32_t slice_len, uint64_t inst_first, uint32_t count, uint64_t seed,
+                      uint32_t slice_len, uint64_t inst_first, uint32_t count, const uint64_t* d_seed,
                       double p1, double p2, uint32_t row_bytes, uint8_t* d_rows, void* stream);
+int launch_set_seed(uint64_t* d_seed, uint64_t seed, void* stream);
 
 int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
                       double* sums, void* stream);
 int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
-                  int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, uint64_t seed,
+                  int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, const uint64_t* d_seed,
                   double p01, double p10, uint32_t* d_out, void* stream);
 // n_sim - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2: one kernel reads all run sums of a leaf
 constexpr int SMALL_SAMPLE_RUNS_LOG2 = 14;
 int launch_sample_small(const void* states, const double* runsums, uint32_t batch, int n_sim,
-                        int n_user, uint64_t leaf_first, uint64_t seed, double p01, double p10,
+                        int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
                         uint32_t* d_out, void* stream);
 int launch_philox_debug(const uint32_t* d_in, uint64_t n, uint32_t* d_out);
 int launch_noise_table(const uint8_t* d_two, uint32_t slice_begin, uint32_t slice_len,

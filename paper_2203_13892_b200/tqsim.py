@@ -81,6 +81,12 @@ class tqsim_stats(C.Structure):
                 ("leaves", C.c_uint64), ("noise_launches", C.c_uint64), ("noise_ms", C.c_double)]
 
 
+class tqsim_pass_timing(C.Structure):
+    _fields_ = [("level", C.c_uint32), ("pass_", C.c_uint32), ("states_per_launch", C.c_uint32),
+                ("reserved", C.c_uint32), ("launches_per_tree", C.c_double),
+                ("ms_per_launch", C.c_double), ("alg_bytes_per_launch", C.c_double)]
+
+
 class tqsim_result(C.Structure):
     _fields_ = [("plan", tqsim_plan), ("n_distinct", C.c_uint64),
                 ("bitstrings", C.POINTER(C.c_uint64)), ("counts", C.POINTER(C.c_uint64)),
@@ -106,6 +112,9 @@ _SIGS = {
     "tqsim_last_error": (C.c_char_p, []),
     "tqsim_version": (C.c_char_p, []),
     "tqsim_lower_circuit": (C.c_int, [_P(tqsim_circuit), _P(tqsim_gate), C.c_uint64, _P(C.c_uint64)]),
+    "tqsim_profile_passes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
+                                       C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,
+                                       _P(tqsim_pass_timing), C.c_uint64, _P(C.c_uint64)]),
     "tqsim_parse_qasm": (C.c_int, [C.c_char_p, _P(tqsim_gate), C.c_uint64, _P(C.c_uint64),
                                    _P(C.c_uint32), _P(C.c_uint32)]),
     "tqsim_profile_copy_cost": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, _P(C.c_double),
@@ -325,6 +334,17 @@ class Handle:
         _check(lib().tqsim_execute(self.h, int(seed), rank, world, C.c_void_p(stream),
                                    C.c_void_p(d_workspace), int(workspace_bytes),
                                    C.c_void_p(d_leaf_outcomes)))
+
+    def profile_passes(self, seed: int, rank: int, world: int, stream: int, d_workspace: int,
+                       workspace_bytes: int, d_leaf_outcomes: int, reps: int = 5):
+        """Live CUDA-event timing of every gate-pass kernel (tqsim_profile_passes)."""
+        n = C.c_uint64()
+        args = (self.h, int(seed), rank, world, C.c_void_p(stream), C.c_void_p(d_workspace),
+                int(workspace_bytes), C.c_void_p(d_leaf_outcomes), int(reps))
+        _check(lib().tqsim_profile_passes(*args, None, 0, C.byref(n)))
+        out = (tqsim_pass_timing * max(1, n.value))()
+        _check(lib().tqsim_profile_passes(*args, out, n.value, C.byref(n)))
+        return [out[i] for i in range(n.value)]
 
     def noise_table(self, seed: int, level: int, inst_begin: int, count: int) -> np.ndarray:
         p = self.plan
