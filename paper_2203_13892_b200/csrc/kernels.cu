@@ -225,68 +225,84 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
                                                           const uint64_t* __restrict__ seedp,
                                                           double p01, double p10,
                                                           uint32_t* __restrict__ out) {
+  // warp w owns the contiguous run segment [w*seg, (w+1)*seg); lanes read it coalesced
+  constexpr uint32_t W = MT / 32;
+  __shared__ double wtot[W];
   const uint64_t seed = *seedp;
-  __shared__ double wsum[MT / 32];
-  __shared__ int first_sh;
-  const uint32_t s = blockIdx.x;
+  const uint32_t s = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint64_t leaf = leaf_first + s;
-  const uint32_t R = 1u << (n - RUN_Q);              // runs per state
-  const uint32_t per = R > MT ? R / MT : 1u;         // runs per thread (power of two)
+  const uint32_t R = 1u << (n - RUN_Q);
+  const uint32_t seg = (R + W - 1) / W;
   const double* rs = runs + ((uint64_t)s << (n - RUN_Q));
-  const uint32_t r0 = threadIdx.x * per;
-  double loc = 0.0;
-  if (r0 < R)
-    for (uint32_t j = 0; j < per; ++j) loc += rs[r0 + j];
-  const double incl = block_incl_scan(loc, wsum);
-  __shared__ double total_sh;
-  if (threadIdx.x == MT - 1) total_sh = incl;
+  const uint32_t s0 = w * seg, s1 = min(R, s0 + seg);
+  double part = 0.0;
+  for (uint32_t i = s0 + lane; i < s1; i += 32u) part += rs[i];
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) wtot[w] = part;
   __syncthreads();
-  const double total = total_sh;
+  // every warp walks the W segment totals (identical order -> identical decision)
+  double total = 0.0;
+  for (uint32_t i = 0; i < W; ++i) total += wtot[i];
   const double target = tq_measure_uniform(leaf, seed) * total;
-  int t = block_first(incl > target, &first_sh);
-  if (t >= MT) {   // rounding: u*total at the very top -> the last thread with mass
-    __syncthreads();
-    if (threadIdx.x == 0) first_sh = -1;
-    __syncthreads();
-    if (loc > 0.0) atomicMax(&first_sh, (int)threadIdx.x);
-    __syncthreads();
-    t = first_sh < 0 ? 0 : first_sh;
+  double before = 0.0;
+  int ws = -1, wlast = 0;
+  for (uint32_t i = 0; i < W; ++i) {
+    if (wtot[i] > 0.0) wlast = (int)i;
+    if (ws < 0 && before + wtot[i] > target) ws = (int)i;
+    if (ws < 0) before += wtot[i];
   }
-  if ((int)threadIdx.x == t) {
-    double acc = incl - loc;
-    uint32_t run = r0, lastnz = r0;
-    bool found = false;
-    for (uint32_t j = 0; j < per && r0 + j < R; ++j) {
-      const double v = rs[r0 + j];
-      if (v > 0.0) lastnz = r0 + j;
-      if (acc + v > target) {
-        run = r0 + j;
-        found = true;
-        break;
-      }
-      acc += v;
-    }
-    if (!found) {   // rounding between the scan and the walk: the last run with mass
-      run = lastnz;
-      acc = incl - loc;
-      for (uint32_t j = r0; j < run; ++j) acc += rs[j];
-    }
-    const double t3 = target - acc;
-    const uint64_t base = (uint64_t)run << RUN_Q;
-    const cd* ap = states + ((uint64_t)s << n) + base;
-    double c = 0.0;
-    int x = -1, lastamp = -1;
-    for (int e = 0; e < (1 << RUN_Q); ++e) {
-      const cd v = ap[e];
-      const double pr = v.x * v.x + v.y * v.y;
-      if (pr > 0.0) lastamp = e;
-      c += pr;
-      if (x < 0 && c > t3) x = e;
-    }
-    if (x < 0) x = lastamp >= 0 ? lastamp : 0;
-    const uint32_t xi = (uint32_t)(base + (uint64_t)x);
-    out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
+  if (ws < 0) {   // rounding: target at the very top -> the last segment with mass
+    ws = wlast;
+    before = 0.0;
+    for (int i = 0; i < ws; ++i) before += wtot[i];
   }
+  if ((int)w != ws) return;
+  // this warp: 32-run rounds, warp inclusive scan + ballot finds the first crossing
+  const uint32_t a0 = ws * seg, a1 = min(R, a0 + seg);
+  uint32_t run = a1 - 1, lastnz = a0;
+  double acc = before;
+  bool found = false;
+  for (uint32_t base = a0; base < a1 && !found; base += 32u) {
+    const uint32_t i = base + lane;
+    const double v = i < a1 ? rs[i] : 0.0;
+    double incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += t;
+    }
+    const unsigned nz = __ballot_sync(0xffffffffu, v > 0.0);
+    if (nz) lastnz = base + 31u - __clz(nz);
+    const unsigned hit = __ballot_sync(0xffffffffu, acc + incl > target);
+    if (hit) {
+      const int f = __ffs(hit) - 1;
+      run = base + (uint32_t)f;
+      acc += __shfl_sync(0xffffffffu, incl - v, f);
+      found = true;
+    } else {
+      acc += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  if (!found) {   // rounding between the segment total and the walk: last run with mass
+    run = lastnz;
+    acc = before;
+    for (uint32_t i = a0; i < run; ++i) acc += rs[i];
+  }
+  if (lane != 0) return;
+  const double t3 = target - acc;
+  const uint64_t abase = (uint64_t)run << RUN_Q;
+  const cd* ap = states + ((uint64_t)s << n) + abase;
+  double c = 0.0;
+  int x = -1, lastamp = -1;
+  for (int e = 0; e < (1 << RUN_Q); ++e) {
+    const cd v = ap[e];
+    const double pr = v.x * v.x + v.y * v.y;
+    if (pr > 0.0) lastamp = e;
+    c += pr;
+    if (x < 0 && c > t3) x = e;
+  }
+  if (x < 0) x = lastamp >= 0 ? lastamp : 0;
+  const uint32_t xi = (uint32_t)(abase + (uint64_t)x);
+  out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
 }
 
 // ------------------------------------------------------------------ debug hooks
@@ -338,12 +354,49 @@ __global__ void __launch_bounds__(256) noise_rows_kernel(
   if (lane == 0) *reinterpret_cast<uint32_t*>(row) = mask;
 }
 
+// Every noise row of a shard (all levels) in one launch: warp w -> (level, instance) by
+// the levels' cumulative counts; the row as in noise_rows_kernel.
+__global__ void __launch_bounds__(256) noise_rows_all_kernel(
+    const uint8_t* __restrict__ two, const uint8_t* __restrict__ pass_of, const __grid_constant__ NoiseLevels L,
+    uint64_t total, const uint64_t* __restrict__ seedp, double p1, double p2, uint8_t* __restrict__ rows) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (w >= total) return;
+  uint64_t rem = w;
+  uint32_t d = 0;
+  while (d + 1 < L.n_levels && rem >= L.lv[d].count) rem -= L.lv[d].count, ++d;
+  const NoiseLevel& lv = L.lv[d];
+  const uint64_t seed = *seedp;
+  const uint64_t inst = lv.inst_first + rem;
+  uint8_t* row = rows + lv.rows_off + rem * lv.row_bytes;
+  uint32_t mask = 0;
+  for (uint32_t t = lane; t < lv.slice_len; t += 32u) {
+    const uint32_t g = lv.slice_begin + t;
+    const bool tw = two[g] != 0;
+    const uint32_t c = tq_noise_code(g, inst, seed, tw ? p2 : p1, tw);
+    row[4 + t] = (uint8_t)c;
+    if (c) mask |= 1u << pass_of[g];
+  }
+  mask = __reduce_or_sync(0xffffffffu, mask);
+  if (lane == 0) *reinterpret_cast<uint32_t*>(row) = mask;
+}
+
 // The run's seed in device memory: the tree's launches (a replayed CUDA graph) read it
 __global__ void set_seed_kernel(uint64_t* d_seed, uint64_t seed) { *d_seed = seed; }
 
 }  // namespace dev
 
 // ------------------------------------------------------------------ launchers
+int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const NoiseLevels& L,
+                          uint64_t total_instances, const uint64_t* d_seed, double p1, double p2,
+                          uint8_t* d_rows, void* stream) {
+  if (total_instances == 0) return 0;
+  const uint64_t threads = total_instances * 32;
+  dev::noise_rows_all_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_two, d_pass_of, L, total_instances, d_seed, p1, p2, d_rows);
+  return (int)cudaGetLastError();
+}
+
 int launch_set_seed(uint64_t* d_seed, uint64_t seed, void* stream) {
   dev::set_seed_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_seed, seed);
   return (int)cudaGetLastError();

@@ -110,6 +110,8 @@ struct Layout {
   std::vector<uint64_t> cap;       // states per level batch
   std::vector<uint64_t> off;       // byte offset of level buffer
   uint64_t runs_off = 0, sums_off = 0, rows_off = 0, total = 0;
+  std::vector<uint64_t> lvl_count;      // the shard's instances per level
+  std::vector<uint64_t> rows_lvl_off;   // byte offset of each level's noise rows (in the rows region)
   int chunk_log2 = 0;
 };
 
@@ -134,6 +136,7 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
   for (size_t d = 0; d < levels; ++d) {
     if (d > 0) per *= h->plan.arities[d];
     L.cap.push_back(std::max<uint64_t>(1, std::min(per, target)));
+    L.lvl_count.push_back(top_count ? per : 0);
   }
   L.chunk_log2 = std::min(n, 12);
   auto total_of = [&](Layout& l) {
@@ -147,11 +150,14 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
     off = align_up(off + l.cap.back() * (8ull << (n - RUN_Q)));
     l.sums_off = off;
     off = align_up(off + l.cap.back() * (8ull << (n - l.chunk_log2)));
-    l.rows_off = off;   // noise rows of the level batch being executed (one level at a time)
+    l.rows_off = off;   // noise rows of every instance of the shard (drawn in one launch)
     uint64_t rows = 0;
-    for (size_t d = 0; d < levels; ++d)
-      rows = std::max<uint64_t>(rows, l.cap[d] * noise_row_bytes((uint32_t)(h->plan.bounds[d + 1] -
-                                                                            h->plan.bounds[d])));
+    l.rows_lvl_off.clear();
+    for (size_t d = 0; d < levels; ++d) {
+      l.rows_lvl_off.push_back(rows);
+      rows = align_up(rows + l.lvl_count[d] * noise_row_bytes((uint32_t)(h->plan.bounds[d + 1] -
+                                                                         h->plan.bounds[d])));
+    }
     off = align_up(off + rows);
     l.total = off;
     return off;
@@ -201,7 +207,18 @@ struct Exec {
   char* ws;
   Layout L;
   uint32_t* d_out;
+  std::vector<uint64_t> lvl_first;   // global id of the shard's first instance per level
 };
+
+std::vector<uint64_t> level_firsts(const tqsim_handle* h, uint64_t t0) {
+  std::vector<uint64_t> f;
+  uint64_t v = t0;
+  for (size_t d = 0; d < h->plan.arities.size(); ++d) {
+    if (d > 0) v *= h->plan.arities[d];
+    f.push_back(v);
+  }
+  return f;
+}
 
 cudaEvent_t next_event(tqsim_handle* h) {
   if (h->ev_used == h->ev_pool.size()) {
@@ -251,17 +268,12 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   const uint32_t slice_begin = (uint32_t)h->plan.bounds[d];
   const uint32_t slice_len = (uint32_t)(h->plan.bounds[d + 1] - slice_begin);
   const uint32_t row_bytes = noise_row_bytes(slice_len);
-  uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off);
+  (void)slice_begin;
   for (uint64_t b = i0; b < i1; b += cap) {
     const uint64_t cnt = std::min(cap, i1 - b);
-    // noise rows of the batch (row a3): keyed Pauli codes + per-pass error bitmask
-    mark(x, 2);
-    ck(launch_noise_rows(h->d_two, h->d_pass_of, slice_begin, slice_len, b, (uint32_t)cnt, h->d_seed,
-                         h->noise.p1, h->noise.p2, row_bytes, rows, x.st),
-       "noise rows launch");
-    mark(x, 2);
-    h->stats.kernel_launches++;
-    h->stats.noise_launches++;
+    // the batch's noise rows (row a3), drawn for the whole shard at the start of the tree
+    uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d]) +
+                    (b - x.lvl_first[d]) * row_bytes;
     for (size_t p = 0; p < passes.size(); ++p) {
       PassLaunch pl{};
       pl.src_mode = p > 0 ? 2u : (d == 0 ? 0u : 1u);
@@ -326,6 +338,34 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   }
 }
 
+// Every noise row of the shard (all levels) in one launch, then the tree.
+void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
+  tqsim_handle* h = x.h;
+  NoiseLevels NL{};
+  const size_t levels = h->plan.arities.size();
+  if (levels > (size_t)NOISE_MAX_LEVELS) throw Error{TQSIM_EINTERNAL, "too many levels for the noise rows"};
+  uint64_t total = 0;
+  for (size_t d = 0; d < levels; ++d) {
+    NoiseLevel& lv = NL.lv[d];
+    lv.inst_first = x.lvl_first[d];
+    lv.count = x.L.lvl_count[d];
+    lv.rows_off = x.L.rows_lvl_off[d];
+    lv.slice_begin = (uint32_t)h->plan.bounds[d];
+    lv.slice_len = (uint32_t)(h->plan.bounds[d + 1] - h->plan.bounds[d]);
+    lv.row_bytes = noise_row_bytes(lv.slice_len);
+    total += lv.count;
+  }
+  NL.n_levels = (uint32_t)levels;
+  mark(x, 2);
+  ck(launch_noise_rows_all(h->d_two, h->d_pass_of, NL, total, h->d_seed, h->noise.p1, h->noise.p2,
+                           reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off), x.st),
+     "noise rows launch");
+  mark(x, 2);
+  h->stats.kernel_launches++;
+  h->stats.noise_launches++;
+  run_level(x, 0, t0, t1, 0);
+}
+
 // per-gate device tables: 2q flag (noise class) and pass index (error bitmask bit)
 void upload_gate_tables(tqsim_handle* h, cudaStream_t st) {
   const size_t G = h->h_tables.size() / 2;
@@ -381,7 +421,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
   if (!d_out) throw Error{TQSIM_EINVAL, "d_leaf_outcomes is NULL"};
   uint64_t t0, t1;
   shard(h->cplan, rank, world, t0, t1);
-  Exec x{h, seed, st, static_cast<char*>(ws), layout(h, t1 - t0), d_out};
+  Exec x{h, seed, st, static_cast<char*>(ws), layout(h, t1 - t0), d_out, level_firsts(h, t0)};
   if (!ws || ws_bytes < x.L.total) throw Error{TQSIM_ECAPACITY, "workspace too small"};
   if (reinterpret_cast<uintptr_t>(ws) % ALIGN) throw Error{TQSIM_EINVAL, "workspace not 256-byte aligned"};
   h->stats = tqsim_stats{};
@@ -407,7 +447,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
       ckc(cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
       cudaGraph_t g = nullptr;
       try {
-        run_level(xc, 0, t0, t1, 0);
+        run_tree(xc, t0, t1);
       } catch (...) {
         cudaStreamEndCapture(h->capture_stream, &g);
         if (g) cudaGraphDestroy(g);
@@ -425,7 +465,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
     ckc(cudaGraphLaunch(h->graph_exec, st), "graph launch");
     return;
   }
-  if (t1 > t0) run_level(x, 0, t0, t1, 0);
+  if (t1 > t0) run_tree(x, t0, t1);
   h->stats.kernel_launches += 1;     // the seed kernel
   if (h->opts.profile) {
     ckc(cudaStreamSynchronize(st), "profile sync");
@@ -681,7 +721,7 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
     ckc(cudaStreamSynchronize(st), "sync");
     uint64_t t0, t1;
     shard(h->cplan, rank, world, t0, t1);
-    Exec x{h, seed, st, static_cast<char*>(d_workspace), layout(h, t1 - t0), d_leaf_outcomes};
+    Exec x{h, seed, st, static_cast<char*>(d_workspace), layout(h, t1 - t0), d_leaf_outcomes, level_firsts(h, t0)};
     ckc(cudaEventCreate(&e0), "event");
     ckc(cudaEventCreate(&e1), "event");
     const int n = h->n_sim;
@@ -693,10 +733,9 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
       const uint32_t slice_begin = (uint32_t)h->plan.bounds[d];
       const uint32_t slice_len = (uint32_t)(h->plan.bounds[d + 1] - slice_begin);
       const uint32_t row_bytes = noise_row_bytes(slice_len);
-      uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off);
-      ck(launch_noise_rows(h->d_two, h->d_pass_of, slice_begin, slice_len, first, (uint32_t)cnt, h->d_seed,
-                           h->noise.p1, h->noise.p2, row_bytes, rows, st),
-         "noise rows launch");
+      // the level's first batch's noise rows (drawn by the run above)
+      uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d]);
+      (void)slice_begin;
       for (size_t p = 0; p < h->pp.levels[d].size(); ++p) {
         PassLaunch pl{};
         pl.src_mode = p > 0 ? 2u : (d == 0 ? 0u : 1u);

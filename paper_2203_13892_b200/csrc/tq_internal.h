@@ -121,6 +121,21 @@ int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t s
                       uint32_t slice_len, uint64_t inst_first, uint32_t count, const uint64_t* d_seed,
                       double p1, double p2, uint32_t row_bytes, uint8_t* d_rows, void* stream);
 int launch_set_seed(uint64_t* d_seed, uint64_t seed, void* stream);
+// All noise rows of a shard in one launch (one warp per instance of every level).
+struct NoiseLevel {
+  uint64_t inst_first;   // global instance id of the shard's first instance at this level
+  uint64_t count;        // the shard's instances at this level
+  uint64_t rows_off;     // byte offset of the level's rows in the rows region
+  uint32_t slice_begin, slice_len, row_bytes, pad;
+};
+constexpr int NOISE_MAX_LEVELS = 64;
+struct NoiseLevels {
+  NoiseLevel lv[NOISE_MAX_LEVELS];
+  uint32_t n_levels;
+};
+int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const NoiseLevels& L,
+                          uint64_t total_instances, const uint64_t* d_seed, double p1, double p2,
+                          uint8_t* d_rows, void* stream);
 
 int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
                       double* sums, void* stream);
