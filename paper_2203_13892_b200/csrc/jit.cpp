@@ -48,6 +48,8 @@ struct TqJitArgs {
   tq_u64 child_first, parent_first; tq_u32 arity, batch;
   double* runsum;   // leaf level: |a|^2 sums of 8-amplitude runs, 2^(n-3) per state
   const unsigned char* rows; tq_u32 row_bytes;   // noise rows of the batch (launch_noise_rows)
+  // leaf measurement without the state store (variants 1/2, see gen_pass)
+  const tq_u32* tiles; const tq_u32* runsel; tq_d2* scratch; tq_u32* xlout;
 };
 // 16-byte global load the compiler may not sink below the error-branch: the tile loads
 // are issued before the (dependent) noise-row mask load is waited on
@@ -74,6 +76,10 @@ struct HostJitArgs {   // mirrors TqJitArgs
   double* runsum;
   const void* rows;
   uint32_t row_bytes;
+  const uint32_t* tiles;
+  const uint32_t* runsel;
+  void* scratch;
+  uint32_t* xlout;
 };
 
 std::string hexd(double v) {
@@ -637,9 +643,13 @@ uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal) {
   return R;
 }
 
+// variant (leaf-sum passes only): 0 = store the state (and run sums); 1 = run sums only,
+// no state store, the instance's store-address frame XOR to xlout; 2 = recompute one
+// tile per leaf (tiles[s]) and store only the 8 amplitudes of run runsel[s] to scratch.
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
-                     std::vector<double>& coefs) {
+                     std::vector<double>& coefs, int variant = 0,
+                     std::vector<uint8_t>* out_logical = nullptr) {
   const int K = pd.K, T = 1 << (K - RBITS);
   const int low = std::min(LOW_Q, K);
   const bool coal = K - RBITS >= low;   // enough lane bits to keep qubits 0..2 on lanes 0..2
@@ -663,6 +673,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // One phase plan for both paths: the error-free fast path and the careful path,
   // which runs the same fused ops under a run-time Pauli frame (below).
   const uint64_t R0 = choose_load_regs(fitems, K, coal);
+  if (out_logical) {   // stored (logical) address bit of every out-of-tile qubit
+    out_logical->clear();
+    for (int i = 0; i < pd.n_out; ++i) out_logical->push_back((uint8_t)log_of_phys[pd.out_q[i]]);
+  }
   int store_key[64];   // the store writes tile position p to logical qubit log_of_phys[tile_q[p]]
   for (int p = 0; p < K; ++p) store_key[p] = log_of_phys[pd.tile_q[p]];
   const std::vector<PhaseSpec> fast = plan_phases(fitems, K, R0, coal, store_key);
@@ -746,7 +760,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
   o << "  __shared__ tq_u32 tq_errb[" << NW << "];\n";
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
-  o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
+  if (variant == 2)   // one CTA per leaf, on the tile holding its selected run
+    o << "  const tq_u32 s = (tq_u32)bid;\n  const tq_u64 t = a.tiles[s];\n  const tq_u32 rsel = a.runsel[s];\n";
+  else
+    o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
   o << "  tq_u32 gtile = 0u, gtile_st = 0u;\n";   // the tile's out-of-tile index bits: physical / stored
   for (int i = 0; i < pd.n_out; ++i)
     o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << "; gtile_st |= (tq_u32)((t >> "
@@ -1299,9 +1316,18 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << gph[k] << "u)) << 1));\n";
         xl = " ^ xl";
       }
-      for (int k = 0; k < 16; ++k)
-        o << "    dst[(gbs + " << gofs[k] << "u)" << xl << "] = " << g.r(k) << ";\n";
-      if (pd.leaf_sums) {
+      if (variant == 0) {
+        for (int k = 0; k < 16; ++k)
+          o << "    dst[(gbs + " << gofs[k] << "u)" << xl << "] = " << g.r(k) << ";\n";
+      } else if (variant == 1) {   // the instance's store-address XOR (uniform per instance)
+        o << "    if (t == 0 && tid == 0u) a.xlout[s] = " << (with_errors ? "xl" : "0u") << ";\n";
+      } else {                     // the selected run's 8 amplitudes only
+        for (int k = 0; k < 16; ++k)
+          o << "    { const tq_u32 ad = (gbs + " << gofs[k] << "u)" << xl << "; if ((ad >> " << RUN_Q
+            << ") == rsel) a.scratch[((tq_u64)s << " << RUN_Q << ") | (ad & " << ((1 << RUN_Q) - 1) << "u)] = "
+            << g.r(k) << "; }\n";
+      }
+      if (pd.leaf_sums && variant != 2) {
         // |a|^2 sums of the 8-amplitude runs (qubits 0..2): reduce over the register bits
         // holding positions 0..2, then butterfly-shuffle over the lane bits holding the
         // rest (the store layout puts the lowest non-register positions on lanes 0..4).
@@ -1476,27 +1502,33 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
                                             double* compile_seconds) {
   struct Job {
     size_t d, p;
+    int variant;
     std::string name, src;
     int threads;
     size_t smem;
     std::string cubin;
     std::string err;
     std::vector<double> coefs;
+    std::vector<uint8_t> out_logical;
   };
   std::vector<Job> jobs;
   std::vector<std::vector<JitPass>> out(pp.levels.size());
   for (size_t d = 0; d < pp.levels.size(); ++d) {
     out[d].resize(pp.levels[d].size());
     for (size_t p = 0; p < pp.levels[d].size(); ++p) {
-      Job j;
-      j.d = d;
-      j.p = p;
-      j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p);
-      const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
-      std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
-                                  j.smem, j.coefs);
-      j.src = std::string(kPrelude) + kJitTypes + body;
-      jobs.push_back(std::move(j));
+      const int nvar = pp.levels[d][p].leaf_sums ? 3 : 1;
+      for (int v = 0; v < nvar; ++v) {
+        Job j;
+        j.d = d;
+        j.p = p;
+        j.variant = v;
+        j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : "");
+        const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
+        std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
+                                    j.smem, j.coefs, v, &j.out_logical);
+        j.src = std::string(kPrelude) + kJitTypes + body;
+        jobs.push_back(std::move(j));
+      }
     }
   }
   const auto t0 = std::chrono::steady_clock::now();
@@ -1551,12 +1583,16 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (Job& j : jobs) {
     const CompiledKernel& ck = g_cache.at(j.src);
-    JitPass jp;
-    jp.kernel = reinterpret_cast<void*>(ck.fn);
-    jp.threads = j.threads;
-    jp.smem = j.smem;
-    jp.coefs = j.coefs;
-    out[j.d][j.p] = jp;
+    JitPass& jp = out[j.d][j.p];
+    if (j.variant == 0) {
+      jp.kernel = reinterpret_cast<void*>(ck.fn);
+      jp.threads = j.threads;
+      jp.smem = j.smem;
+      jp.coefs = j.coefs;
+      jp.out_logical = j.out_logical;
+    } else {
+      (j.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute) = reinterpret_cast<void*>(ck.fn);
+    }
   }
   return out;
 }
@@ -1565,13 +1601,16 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
-                L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes};
-  const uint64_t grid = (uint64_t)L.batch << pd.n_out;
+                L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes,
+                L.tiles, L.runsel, L.scratch, L.xlout};
+  const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute;
+  if (!kern) return (int)cudaErrorInvalidDeviceFunction;
+  const uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;
   static const double zero = 0.0;
   void* args[] = {&a, const_cast<double*>(jp.coefs.empty() ? &zero : jp.coefs.data())};
-  return (int)cudaLaunchKernel(jp.kernel, dim3((unsigned)grid), dim3(jp.threads), args, jp.smem,
+  return (int)cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(jp.threads), args, jp.smem,
                                static_cast<cudaStream_t>(stream));
 }
 

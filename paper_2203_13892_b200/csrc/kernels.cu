@@ -18,6 +18,26 @@ namespace dev {
 
 constexpr int MT = 256;   // threads of the measurement kernels
 
+// Leaf sampling without a stored leaf state: the select phase writes, per leaf, the run
+// holding u*total (runsel), the residual target inside the run (t3) and the tile the
+// leaf pass must recompute to produce that run (tile); the finish phase walks the 8
+// recomputed amplitudes (scratch).
+struct SelectOut {
+  uint32_t* runsel;
+  double* t3;
+  uint32_t* tile;
+  const uint32_t* xl;         // the leaf pass's store-address XOR per leaf
+  uint32_t n_out;
+  uint8_t out_logical[32];    // stored address bit of out-of-tile qubit i
+};
+
+__device__ __forceinline__ uint32_t tile_of_run(uint64_t run, uint32_t xl, const SelectOut& so) {
+  const uint64_t a = (run << RUN_Q) ^ (uint64_t)xl;   // source (physical) index, logical bits
+  uint32_t t = 0;
+  for (uint32_t i = 0; i < so.n_out; ++i) t |= (uint32_t)((a >> so.out_logical[i]) & 1u) << i;
+  return t;
+}
+
 struct __align__(16) cd {
   double x, y;
 };
@@ -143,7 +163,8 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
                                                     const double* __restrict__ sums, uint32_t n,
                                                     uint32_t n_user, uint32_t chunk_log2,
                                                     uint64_t leaf_first, const uint64_t* __restrict__ seedp,
-                                                    double p01, double p10, uint32_t* __restrict__ out) {
+                                                    double p01, double p10, uint32_t* __restrict__ out,
+                                                    const __grid_constant__ SelectOut so) {
   const uint64_t seed = *seedp;
   __shared__ double wsum[MT / 32];
   __shared__ int first_sh;
@@ -169,6 +190,13 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
   const double* rs = runs + ((uint64_t)s << (n - RUN_Q)) + chunk * rpc;
   const uint64_t run = block_search(rs, rpc, target - before1, &before2, wsum, &first_sh, &pick_sh,
                                     &before_sh);
+  if (threadIdx.x == 0 && so.runsel) {   // select phase only (the leaf state was not stored)
+    const uint64_t r = chunk * rpc + run;
+    so.runsel[s] = (uint32_t)r;
+    so.t3[s] = target - before1 - before2;
+    so.tile[s] = tile_of_run(r, so.xl[s], so);
+    return;
+  }
   if (threadIdx.x == 0) {
     const double t3 = target - before1 - before2;
     const uint64_t base = ((chunk * rpc + run) << RUN_Q);
@@ -224,7 +252,8 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
                                                           uint64_t leaf_first,
                                                           const uint64_t* __restrict__ seedp,
                                                           double p01, double p10,
-                                                          uint32_t* __restrict__ out) {
+                                                          uint32_t* __restrict__ out,
+                                                          const __grid_constant__ SelectOut so) {
   // warp w owns the contiguous run segment [w*seg, (w+1)*seg); lanes read it coalesced
   constexpr uint32_t W = MT / 32;
   __shared__ double wtot[W];
@@ -289,6 +318,12 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
   }
   if (lane != 0) return;
   const double t3 = target - acc;
+  if (so.runsel) {   // select phase only (the leaf state was not stored)
+    so.runsel[s] = run;
+    so.t3[s] = t3;
+    so.tile[s] = tile_of_run(run, so.xl[s], so);
+    return;
+  }
   const uint64_t abase = (uint64_t)run << RUN_Q;
   const cd* ap = states + ((uint64_t)s << n) + abase;
   double c = 0.0;
@@ -302,6 +337,34 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
   }
   if (x < 0) x = lastamp >= 0 ? lastamp : 0;
   const uint32_t xi = (uint32_t)(abase + (uint64_t)x);
+  out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
+}
+
+// Finish phase: one thread per leaf walks the recomputed run (8 amplitudes) for the
+// smallest x with C(x) > u*total (R9), then the readout flips (R11).
+__global__ void __launch_bounds__(MT) sample_finish_kernel(const cd* __restrict__ scratch,
+                                                           const uint32_t* __restrict__ runsel,
+                                                           const double* __restrict__ t3s, uint32_t batch,
+                                                           uint32_t n_user, uint64_t leaf_first,
+                                                           const uint64_t* __restrict__ seedp, double p01,
+                                                           double p10, uint32_t* __restrict__ out) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= batch) return;
+  const uint64_t seed = *seedp;
+  const uint64_t leaf = leaf_first + s;
+  const double t3 = t3s[s];
+  const cd* ap = scratch + ((uint64_t)s << RUN_Q);
+  double c = 0.0;
+  int x = -1, lastamp = -1;
+  for (int e = 0; e < (1 << RUN_Q); ++e) {
+    const cd v = ap[e];
+    const double pr = v.x * v.x + v.y * v.y;
+    if (pr > 0.0) lastamp = e;
+    c += pr;
+    if (x < 0 && c > t3) x = e;
+  }
+  if (x < 0) x = lastamp >= 0 ? lastamp : 0;
+  const uint32_t xi = (uint32_t)(((uint64_t)runsel[s] << RUN_Q) + (uint64_t)x);
   out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
 }
 
@@ -422,23 +485,45 @@ int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chun
   return (int)cudaGetLastError();
 }
 
+static dev::SelectOut select_out(const LeafSelect* sel) {
+  dev::SelectOut so{};
+  if (!sel) return so;
+  so.runsel = sel->runsel;
+  so.t3 = sel->t3;
+  so.tile = sel->tile;
+  so.xl = sel->xl;
+  so.n_out = sel->n_out;
+  for (uint32_t i = 0; i < sel->n_out && i < 32; ++i) so.out_logical[i] = sel->out_logical[i];
+  return so;
+}
+
 int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
                   int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, const uint64_t* d_seed,
-                  double p01, double p10, uint32_t* d_out, void* stream) {
+                  double p01, double p10, uint32_t* d_out, void* stream, const LeafSelect* sel) {
   if (batch == 0) return 0;
   dev::sample_kernel<<<batch, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const dev::cd*>(states), runsums, sums, (uint32_t)n_sim, (uint32_t)n_user,
-      (uint32_t)chunk_log2, leaf_first, d_seed, p01, p10, d_out);
+      (uint32_t)chunk_log2, leaf_first, d_seed, p01, p10, d_out, select_out(sel));
+  return (int)cudaGetLastError();
+}
+
+int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
+                         int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
+                         uint32_t* d_out, void* stream) {
+  if (batch == 0) return 0;
+  dev::sample_finish_kernel<<<(batch + dev::MT - 1) / dev::MT, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const dev::cd*>(scratch), runsel, t3, batch, (uint32_t)n_user, leaf_first, d_seed, p01, p10,
+      d_out);
   return (int)cudaGetLastError();
 }
 
 int launch_sample_small(const void* states, const double* runsums, uint32_t batch, int n_sim,
                         int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
-                        uint32_t* d_out, void* stream) {
+                        uint32_t* d_out, void* stream, const LeafSelect* sel) {
   if (batch == 0) return 0;
   dev::sample_small_kernel<<<batch, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const dev::cd*>(states), runsums, (uint32_t)n_sim, (uint32_t)n_user, leaf_first,
-      d_seed, p01, p10, d_out);
+      d_seed, p01, p10, d_out, select_out(sel));
   return (int)cudaGetLastError();
 }
 

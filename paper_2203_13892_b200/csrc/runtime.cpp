@@ -112,6 +112,8 @@ struct Layout {
   uint64_t runs_off = 0, sums_off = 0, rows_off = 0, total = 0;
   std::vector<uint64_t> lvl_count;      // the shard's instances per level
   std::vector<uint64_t> rows_lvl_off;   // byte offset of each level's noise rows (in the rows region)
+  uint64_t sel_off = 0;                 // leaf select / recompute buffers (per leaf of a batch):
+                                        // runsel u32, tile u32, xl u32, t3 f64, 8 amplitudes
   int chunk_log2 = 0;
 };
 
@@ -159,6 +161,8 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
                                                                          h->plan.bounds[d])));
     }
     off = align_up(off + rows);
+    l.sel_off = off;
+    off = align_up(off + l.cap.back() * (4 + 4 + 4 + 8 + (16ull << RUN_Q)) + 4 * ALIGN);
     l.total = off;
     return off;
   };
@@ -274,6 +278,17 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     // the batch's noise rows (row a3), drawn for the whole shard at the start of the tree
     uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d]) +
                     (b - x.lvl_first[d]) * row_bytes;
+    // leaf: the last pass writes run sums only (no state store) unless state dumps are asked for
+    const bool leaf = d + 1 == levels;
+    const bool nostore = leaf && !(h->debug && h->debug->n_dumps);
+    char* sel = x.ws + x.L.sel_off;
+    const uint64_t capl = x.L.cap.back();
+    uint32_t* runsel = reinterpret_cast<uint32_t*>(sel);
+    uint32_t* tiles = reinterpret_cast<uint32_t*>(sel + align_up(4 * capl));
+    uint32_t* xlv = reinterpret_cast<uint32_t*>(sel + 2 * align_up(4 * capl));
+    double* t3 = reinterpret_cast<double*>(sel + 3 * align_up(4 * capl));
+    void* scratch = sel + 3 * align_up(4 * capl) + align_up(8 * capl);
+    PassLaunch last{};
     for (size_t p = 0; p < passes.size(); ++p) {
       PassLaunch pl{};
       pl.src_mode = p > 0 ? 2u : (d == 0 ? 0u : 1u);
@@ -289,13 +304,18 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       pl.runsum = x.ws + x.L.runs_off;
       pl.rows = rows;
       pl.row_bytes = row_bytes;
+      const bool runsums_only = nostore && passes[p].leaf_sums;
+      pl.variant = runsums_only ? 1u : 0u;
+      pl.xlout = xlv;
       mark(x, 0);
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
       mark(x, 0);
       h->stats.kernel_launches++;
       h->stats.pass_launches++;
+      if (passes[p].leaf_sums) last = pl;
       const uint64_t amps = cnt << n;
-      uint64_t bytes = amps * 16;   // write
+      // write (or, without the leaf state store, the run sums: 8 B per 8 amplitudes)
+      uint64_t bytes = runsums_only ? amps : amps * 16;
       if (pl.src_mode == 2) bytes += amps * 16;
       else if (pl.src_mode == 1) {
         const uint64_t A = pl.arity;
@@ -307,7 +327,54 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     h->stats.node_executions += cnt;
     h->stats.gate_amp_updates += (cnt * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
     dump_if_requested(x, d, b, cnt, buf);
-    if (d + 1 == levels) {
+    if (leaf && nostore) {
+      // select each leaf's run from the run sums -> recompute the one tile holding it
+      // (variant 2 of the last pass, same operands) -> walk its 8 amplitudes
+      double* sums = reinterpret_cast<double*>(x.ws + x.L.sums_off);
+      const double* runs = reinterpret_cast<const double*>(x.ws + x.L.runs_off);
+      const size_t lp = passes.size() - 1;
+      const JitPass& jp = h->jit[d][lp];
+      LeafSelect ls{};
+      ls.runsel = runsel;
+      ls.t3 = t3;
+      ls.tile = tiles;
+      ls.xl = xlv;
+      ls.n_out = (uint32_t)jp.out_logical.size();
+      for (size_t i = 0; i < jp.out_logical.size() && i < 32; ++i) ls.out_logical[i] = jp.out_logical[i];
+      mark(x, 1);
+      if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {
+        ck(launch_sample_small(buf, runs, (uint32_t)cnt, n, (int)h->n_user, b, h->d_seed, h->noise.readout_p01,
+                               h->noise.readout_p10, x.d_out, x.st, &ls),
+           "sample select launch");
+        h->stats.kernel_launches += 1;
+        h->stats.measure_launches += 1;
+        h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8;
+      } else {
+        ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
+        ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, h->d_seed,
+                         h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st, &ls),
+           "sample select launch");
+        h->stats.kernel_launches += 2;
+        h->stats.measure_launches += 2;
+        h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8 +
+                                  cnt * ((8ull << (n - x.L.chunk_log2)) + (8ull << (x.L.chunk_log2 - RUN_Q)));
+      }
+      PassLaunch rc = last;
+      rc.variant = 2;
+      rc.tiles = tiles;
+      rc.runsel = runsel;
+      rc.scratch = scratch;
+      ck(launch_jit_pass(jp, passes[lp], rc, x.st), "leaf recompute launch");
+      ck(launch_sample_finish(scratch, runsel, t3, (uint32_t)cnt, (int)h->n_user, b, h->d_seed,
+                              h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
+         "sample finish launch");
+      mark(x, 1);
+      h->stats.kernel_launches += 2;
+      h->stats.measure_launches += 2;
+      // the recomputed tile per leaf (read its share of the source + 8 amplitudes written)
+      h->stats.measure_bytes += cnt * ((16ull << passes[lp].K) + (16ull << RUN_Q) * 2);
+      h->stats.leaves += cnt;
+    } else if (leaf) {
       double* sums = reinterpret_cast<double*>(x.ws + x.L.sums_off);
       const double* runs = reinterpret_cast<const double*>(x.ws + x.L.runs_off);
       mark(x, 1);
@@ -752,6 +819,9 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
         pl.rows = rows;
         pl.row_bytes = row_bytes;
         const PassDesc& pd = h->pp.levels[d][p];
+        // as in the tree: the leaf's last pass stores run sums only
+        pl.variant = pd.leaf_sums ? 1u : 0u;
+        pl.xlout = reinterpret_cast<uint32_t*>(x.ws + x.L.sel_off + 2 * align_up(4 * x.L.cap.back()));
         ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");   // warm
         ckc(cudaEventRecord(e0, st), "record");
         for (uint32_t i = 0; i < reps; ++i) ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");
@@ -760,7 +830,7 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
         float ms = 0.f;
         ckc(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
         const uint64_t amps = cnt << n;
-        double bytes = (double)amps * 16;
+        double bytes = pl.variant == 1 ? (double)amps : (double)amps * 16;
         if (pl.src_mode == 2) bytes += (double)amps * 16;
         else if (pl.src_mode == 1) {
           const uint64_t A = pl.arity, parents = (first + cnt - 1) / A - first / A + 1;

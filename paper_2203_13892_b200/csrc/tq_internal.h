@@ -111,6 +111,11 @@ struct PassLaunch {
   void* runsum;                 // leaf |a|^2 run sums (leaf_sums passes only)
   const void* rows;             // noise rows of the batch (launch_noise_rows), row_bytes each
   uint32_t row_bytes;
+  uint32_t variant;             // leaf-sum passes: 0 store, 1 run sums only, 2 recompute
+  const uint32_t* tiles;        // variant 2: tile index per leaf
+  const uint32_t* runsel;       // variant 2: selected run per leaf
+  void* scratch;                // variant 2: 8 amplitudes per leaf (double2)
+  uint32_t* xlout;              // variant 1: store-address XOR per leaf
 };
 
 // Noise rows of one level batch (row a3): per instance a row of row_bytes bytes,
@@ -139,14 +144,26 @@ int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const 
 
 int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
                       double* sums, void* stream);
+// leaf sampling without a stored leaf state (select -> recompute one tile -> finish)
+struct LeafSelect {
+  uint32_t* runsel;
+  double* t3;
+  uint32_t* tile;
+  const uint32_t* xl;
+  uint32_t n_out;
+  uint8_t out_logical[32];
+};
+int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
+                         int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
+                         uint32_t* d_out, void* stream);
 int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
                   int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, const uint64_t* d_seed,
-                  double p01, double p10, uint32_t* d_out, void* stream);
+                  double p01, double p10, uint32_t* d_out, void* stream, const LeafSelect* sel = nullptr);
 // n_sim - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2: one kernel reads all run sums of a leaf
 constexpr int SMALL_SAMPLE_RUNS_LOG2 = 14;
 int launch_sample_small(const void* states, const double* runsums, uint32_t batch, int n_sim,
                         int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
-                        uint32_t* d_out, void* stream);
+                        uint32_t* d_out, void* stream, const LeafSelect* sel = nullptr);
 int launch_philox_debug(const uint32_t* d_in, uint64_t n, uint32_t* d_out);
 int launch_noise_table(const uint8_t* d_two, uint32_t slice_begin, uint32_t slice_len,
                        uint64_t inst_begin, uint64_t count, uint64_t seed, double p1, double p2,
@@ -156,6 +173,9 @@ const char* cuda_error_string(int code);
 // ---------------------------------------------------------------- JIT pass kernels (jit.cpp)
 struct JitPass {
   void* kernel = nullptr;   // cudaKernel_t
+  void* kernel_nostore = nullptr;     // leaf-sum passes: run sums only (variant 1)
+  void* kernel_recompute = nullptr;   // leaf-sum passes: one tile per leaf, 8 amps (variant 2)
+  std::vector<uint8_t> out_logical;   // stored address bit of every out-of-tile qubit
   int threads = 0;
   size_t smem = 0;
   std::vector<double> coefs;      // by-value coefficient parameter (TQSIM_JIT_COEF=0 mode)

@@ -291,3 +291,22 @@ def test_accuracy_tree_vs_flat_normalized_fidelity():
     assert 0.0 < r["F_tree_mean"] <= 1.0 and 0.0 < r["F_flat_mean"] <= 1.0
     assert len(r["tree_arities"]) > 1                      # a real tree (DCP), not the flat plan
     assert r["diff_of_means"] < 0.06, r                   # statistical: ~0.02 expected
+
+
+@pytest.mark.parametrize("cfg,p", [("c1_qft5", 0.05), ("c2_qft15", None)])
+def test_leaf_without_state_store_equals_stored_path(cfg, p):
+    """The leaf measurement without a stored leaf state (run sums -> select -> recompute
+    the run's tile -> finish) gives the same outcomes as the stored-state path (state
+    dumps force it), including careful (error-frame) leaves; and matches the oracle."""
+    w = load_config(cfg)
+    n, gates, noise, shots, ar = T.workload_args(w)
+    if p is not None:
+        noise = T.noise_arg(p, 2 * p, 0.02, 0.03)
+    L = T.tqsim_plan_circuit(n, gates, noise, shots, ar).n_levels
+    a = T.tqsim_run_ex(n, gates, noise, shots, ar, 11)                       # no store
+    b = T.tqsim_run_ex(n, gates, noise, shots, ar, 11, None, [(L - 1, 0)])   # stored
+    assert np.array_equal(a.leaf_outcomes, b.leaf_outcomes)
+    if cfg == "c1_qft5":
+        nm = NoiseModel(noise.p1, noise.p2, noise.readout_p01, noise.readout_p10)
+        ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 11)
+        assert_leaves_match(a.leaf_outcomes, ref.leaves)
