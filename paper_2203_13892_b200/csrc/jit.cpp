@@ -1047,6 +1047,28 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
               if (ent[2 * i] != "1.0" || ent[2 * i + 1] != "0.0") all_one = false;
           if (all_one) continue;
           o << "        { const tq_u32 ic = " << kv.first << ";\n";
+          // compile-time entries with few non-unit values (CP, CZ: one): a uniform branch per
+          // non-unit entry, so only the registers whose (frame-shifted) index selects it pay
+          // a complex multiply
+          int nonunit = 0;
+          for (int i = 0; i < (pb >= 0 ? 4 : 2); ++i)
+            if (ent[2 * i] != "1.0" || ent[2 * i + 1] != "0.0") ++nonunit;
+          if (!rt_entries && nonunit <= 2) {
+            for (int i = 0; i < (pb >= 0 ? 4 : 2); ++i) {
+              if (ent[2 * i] == "1.0" && ent[2 * i + 1] == "0.0") continue;
+              o << "          if (ic == " << i << "u) {\n";
+              for (int k : kv.second) {
+                const std::string v = g.r(k);
+                o << "            { const tq_d2 x = " << v << "; " << v << ".x = fma(" << ent[2 * i] << ", x.x, -("
+                  << ent[2 * i + 1] << ") * x.y); " << v << ".y = fma(" << ent[2 * i] << ", x.y, (" << ent[2 * i + 1]
+                  << ") * x.x); }\n";
+              }
+              o << "          }\n";
+            }
+            o << "        }\n";
+            ++ci;
+            continue;
+          }
           auto sel = [&](int part) {
             if (pb < 0) return "(ic & 1u) ? " + ent[2 + part] + " : " + ent[part];
             return "(ic & 2u) ? ((ic & 1u) ? " + ent[6 + part] + " : " + ent[4 + part] + ") : ((ic & 1u) ? " +
@@ -1311,9 +1333,11 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         o << "    tq_u32 xl = 0u;\n";
         for (int q = 0; q < n; ++q)
           o << "    xl |= ((fx >> " << q << ") & 1u) << " << log_of_phys[q] << ";\n";
-        o << "    const tq_u32 zt = __popc(fz & (" << gbp << "));\n";
-        for (int k = 0; k < 16; ++k)
-          o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << gph[k] << "u)) << 1));\n";
+        if (variant == 0) {   // variants 1/2 feed only |a|^2: the frame's phase does not matter
+          o << "    const tq_u32 zt = __popc(fz & (" << gbp << "));\n";
+          for (int k = 0; k < 16; ++k)
+            o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << gph[k] << "u)) << 1));\n";
+        }
         xl = " ^ xl";
       }
       if (variant == 0) {
@@ -1457,8 +1481,11 @@ std::string jit_source(const PassPlan& pp, const std::vector<LGate>& gates, size
   size_t sm;
   std::vector<double> cf;
   const int mode = pass > 0 ? 2 : (level == 0 ? 0 : 1);
+  int variant = 0;   // TQSIM_JIT_VARIANT=1/2 (leaf-sum passes): the no-store / recompute kernels
+  if (const char* e = std::getenv("TQSIM_JIT_VARIANT"))
+    if (pp.levels[level][pass].leaf_sums) variant = std::atoi(e);
   return std::string(kPrelude) + kJitTypes +
-         gen_pass(pp.levels[level][pass], pp, gates, pp.n_sim, mode, name, th, sm, cf);
+         gen_pass(pp.levels[level][pass], pp, gates, pp.n_sim, mode, name, th, sm, cf, variant);
 }
 
 uint64_t jit_compile_count() { return g_compiles.load(); }
@@ -1468,8 +1495,16 @@ void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint6
   std::vector<std::string> srcs, names;
   for (size_t d = 0; d < pp.levels.size(); ++d)
     for (size_t p = 0; p < pp.levels[d].size(); ++p) {
-      names.push_back("tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p));
-      srcs.push_back(jit_source(pp, gates, d, p, names.back()));
+      const int nvar = pp.levels[d][p].leaf_sums ? 3 : 1;
+      for (int v = 0; v < nvar; ++v) {
+        names.push_back("tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : ""));
+        const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
+        int th;
+        size_t sm;
+        std::vector<double> cf;
+        srcs.push_back(std::string(kPrelude) + kJitTypes +
+                       gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, names.back(), th, sm, cf, v));
+      }
     }
   std::vector<std::string> errs(srcs.size());
   std::vector<size_t> sizes(srcs.size(), 0);

@@ -41,6 +41,7 @@ int main() {
   a.src = mode == 1 ? src : dst; a.dst = dst; a.seed = 1; a.p1 = 0; a.p2 = 0;
   a.child_first = 0; a.parent_first = 0; a.arity = mode == 1 ? arity : 1; a.batch = batch;
   a.runsum = runsum; a.rows = rows; a.row_bytes = crow;
+  unsigned* xlout; CK(cudaMalloc(&xlout, batch * 4)); a.xlout = xlout; a.tiles = nullptr; a.runsel = nullptr; a.scratch = nullptr;
   TqCoef cf = {};
   const size_t smem = SMEM;
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(tq_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -53,7 +54,7 @@ int main() {
   for (int i = 0; i < reps; ++i) tq_pass<<<grid, T, smem>>>(a, cf);
   CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); CK(cudaGetLastError());
   float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); ms /= reps;
-  const double bytes = (double)batch * S * 16 + (double)(mode == 0 ? 0 : (mode == 1 ? nparent : batch)) * S * 16;
+  const double bytes = (getenv("TQSIM_JIT_VARIANT") ? (double)batch * S : (double)batch * S * 16) + (double)(mode == 0 ? 0 : (mode == 1 ? nparent : batch)) * S * 16;
   printf("%-28s %8.4f ms  %7.0f GB/s(alg)  grid %u x %d  smem %zu\n", "VARIANT", ms, bytes / (ms * 1e-3) / 1e9, grid, T, smem);
   return 0;
 }

@@ -198,3 +198,19 @@ def test_gpu_entry_points_fail_loudly_without_device():
     with pytest.raises(T.TqsimError) as e:
         T.tqsim_run(*T.workload_args(w))
     assert e.value.status == 4
+
+
+def test_jit_compiles_every_variant_on_host():
+    """NVRTC compiles every generated pass kernel (incl. the leaf no-store / recompute
+    variants) without a GPU: a host-side check of the code generator."""
+    for name in ("c1_qft5", "c2_qft15"):
+        w = load_config(name)
+        k, nbytes, sec = T.tqsim_compile_passes(*T.workload_args(w))
+        assert k > 0 and nbytes > 0
+    rng = np.random.default_rng(7)
+    for tq in (0, 7, 12):
+        n = int(rng.integers(5, 14))
+        gates = random_circuit(n, 50, rng)
+        k, _, _ = T.tqsim_compile_passes(n, gates, T.noise_arg(0.1, 0.2), 40, [4, 10],
+                                         T.default_options(tile_qubits=tq))
+        assert k > 0
