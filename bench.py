@@ -252,17 +252,15 @@ def main():
                 T.tqsim_run(n, ca, noise, shots, ar, i)
             dt = time.perf_counter() - t0
         else:
+            from paper_2203_13892_b200.distributed import ShardRunner
             host = torch.empty(N, dtype=torch.int32, pin_memory=True)
+            runner = ShardRunner(h, rank, world, dev)      # the multi-GPU public API
 
             def e2e_step(seed):
-                hh = T.tqsim_create(n, gates, noise, shots, ar, opts)
-                out.zero_()
-                hh.execute(seed, rank, world, st.cuda_stream, ws.data_ptr(), ws.numel(), out.data_ptr())
-                dist.all_reduce(out, op=dist.ReduceOp.SUM)
-                host.copy_(out)
+                res = runner.run(seed, stream=st)              # shard + NCCL all_reduce(SUM)
+                host.copy_(res)                                # D2H of the combined outcomes
                 if rank == 0:
                     histogram(host.numpy())
-                hh.close()
 
             e2e_step(0)
             dist.barrier()
@@ -275,13 +273,19 @@ def main():
         n_low = len(T.tqsim_lower_circuit(n, gates))
         if world > 1:
             first_call_s = None
+        if world == 1:
+            note = ("tqsim_run per step: host circuit in (validated, hashed; the prepared plan and its "
+                    "specialized kernels are reused from the library's plan cache after the first call), "
+                    "h2d = per-gate noise-class and pass tables (2 B / lowered gate) + kernel parameters, "
+                    "d2h = leaf outcomes (uint32), host histogram")
+            h2d = 2 * n_low + 96 * launches_per_step
+        else:
+            note = ("distributed.ShardRunner per step on every rank: the shard (replayed CUDA graph), "
+                    "NCCL all_reduce(SUM) of the leaf outcomes, D2H, histogram on rank 0; h2d = kernel "
+                    "parameters (seed); max over ranks")
+            h2d = 96
         e2e = {"value": N * args.steps / dt, "unit": "shots/s",
-               "h2d_bytes_per_step": 2 * n_low + 96 * launches_per_step,
-               "d2h_bytes_per_step": N * 4,
-               "note": "tqsim_run per step: host circuit in (validated, hashed; the prepared plan "
-                       "and its specialized kernels are reused from the library's plan cache after "
-                       "the first call), h2d = per-gate noise-class and pass tables (2 B / lowered "
-                       "gate) + kernel parameters, d2h = leaf outcomes (uint32), host histogram",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": N * 4, "note": note,
                "first_call_s": first_call_s}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_%s.json" % w.name)
