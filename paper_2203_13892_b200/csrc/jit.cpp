@@ -174,6 +174,26 @@ struct Gen {
 // phases around the non-diagonal gates only (fewer shared-memory tile exchanges).
 typedef std::complex<double> cplx;
 
+// re/im of sum_j c_j * v_j (complex coefficients, compile-time; zero terms skipped)
+std::string linN(const cplx* c, const std::string* v, int nterms, bool imag) {
+  std::vector<std::pair<double, std::string>> t;
+  for (int j = 0; j < nterms; ++j) {
+    if (!imag) {
+      if (c[j].real() != 0) t.push_back({c[j].real(), v[j] + ".x"});
+      if (c[j].imag() != 0) t.push_back({-c[j].imag(), v[j] + ".y"});
+    } else {
+      if (c[j].real() != 0) t.push_back({c[j].real(), v[j] + ".y"});
+      if (c[j].imag() != 0) t.push_back({c[j].imag(), v[j] + ".x"});
+    }
+  }
+  if (t.empty()) return "0.0";
+  std::string e = "(" + g_pool->ref(t.back().first) + " * " + t.back().second + ")";
+  for (int i = (int)t.size() - 2; i >= 0; --i)
+    e = "fma(" + g_pool->ref(t[i].first) + ", " + t[i].second + ", " + e + ")";
+  return e;
+}
+
+
 // Effect of the keyed Pauli of one gate (code c) propagated to the END of the fused
 // run containing the gate: E' = R E R^dagger with R the run's later gates (monomial,
 // so E' = (diagonal) x (bit flips)).  Either Pauli-type E' = i^k X^x Z^z, or generic
@@ -191,7 +211,9 @@ struct ErrSite {
 };
 
 struct FOp {
-  enum Kind { GEN, XPERM, CX, DIAG, NOP } kind = GEN;
+  enum Kind { GEN, XPERM, CX, DIAG, NOP, GEN2 } kind = GEN;
+  cplx m4[16];            // GEN2: row-major 4x4, local index bit_qa | bit_qb << 1
+  std::vector<FOp> comps; // GEN2: its gates (careful path), each with its own site
   int qa = -1, qb = -1;   // global (physical) qubits (qb = -1: one-qubit op)
   cplx m[4];              // GEN: row-major 2x2
   cplx d[4];              // DIAG: entry for index bit_qa | bit_qb << 1
@@ -364,17 +386,165 @@ ErrEff decompose(const M4& M) {
 // positions -- later ops are rewritten to PHYSICAL qubit labels and the final store
 // writes position p to logical qubit log_of_phys[tile_q[p]].  Runs that cancel to
 // the identity become NOPs (they still carry their gates' error sites).
+// FP64 cost (per amplitude) of one gate applied alone in the fast path: a general
+// complex 2x2 8, a real one 4, diagonals / permutations ~free.
+int gate_cost(const LGate& g) {
+  if (g.two || g.op == OP_DIAG) return g.two ? 0 : 1;
+  if (is_x_gate(g)) return 0;
+  bool real = true;
+  for (int k = 1; k < 8; k += 2)
+    if (g.m[k] != 0.0) real = false;
+  return real ? 4 : 8;
+}
+
+// Commutation-aware 2-qubit blocks: gates on disjoint qubits commute, so a gate joins
+// the open block(s) holding its qubits while their union has <= 2 qubits; otherwise
+// those blocks close (are emitted, in order) and the gate opens a new block.  Emitting
+// a block when it closes is a valid topological order (blocks open at the same time
+// are on disjoint qubits).  Returns the pass's local op indices, block by block.
+std::vector<int> block_order(int n, const std::function<const LGate&(int)>& lg_of) {
+  struct Blk {
+    std::vector<int> ops;
+    uint64_t qm = 0;
+    bool open = true;
+  };
+  std::vector<Blk> blks;
+  std::map<int, int> owner;   // qubit -> open block
+  std::vector<int> ord;
+  auto close = [&](int bi) {
+    if (!blks[bi].open) return;
+    blks[bi].open = false;
+    for (int q = 0; q < 64; ++q)
+      if (blks[bi].qm >> q & 1) owner.erase(q);
+    ord.insert(ord.end(), blks[bi].ops.begin(), blks[bi].ops.end());
+  };
+  for (int i = 0; i < n; ++i) {
+    const LGate& g = lg_of(i);
+    const uint64_t Q = (1ull << g.q0) | (g.two ? 1ull << g.q1 : 0ull);
+    std::vector<int> own;
+    for (int q = 0; q < 64; ++q)
+      if (Q >> q & 1) {
+        auto it = owner.find(q);
+        if (it != owner.end() && std::find(own.begin(), own.end(), it->second) == own.end()) own.push_back(it->second);
+      }
+    std::sort(own.begin(), own.end());
+    uint64_t U = Q;
+    for (int bi : own) U |= blks[bi].qm;
+    if (__builtin_popcountll(U) <= 2) {
+      Blk nb;
+      for (int bi : own) {
+        nb.ops.insert(nb.ops.end(), blks[bi].ops.begin(), blks[bi].ops.end());
+        blks[bi].open = false;
+        blks[bi].ops.clear();
+      }
+      nb.ops.push_back(i);
+      nb.qm = U;
+      blks.push_back(nb);
+      for (int q = 0; q < 64; ++q)
+        if (U >> q & 1) owner[q] = (int)blks.size() - 1;
+      continue;
+    }
+    for (int bi : own) close(bi);
+    Blk nb;
+    nb.ops.push_back(i);
+    nb.qm = Q;
+    blks.push_back(nb);
+    for (int q = 0; q < 64; ++q)
+      if (Q >> q & 1) owner[q] = (int)blks.size() - 1;
+  }
+  for (size_t bi = 0; bi < blks.size(); ++bi) close((int)bi);
+  return ord;
+}
+
+// Fast-path op list.  SWAPs (a fused run whose product is the swap permutation) are
+// not executed: both qubits are tile qubits, so the swap is a relabeling of tile
+// positions -- later ops are rewritten to PHYSICAL qubit labels and the final store
+// writes position p to logical qubit log_of_phys[tile_q[p]].  Runs that cancel to
+// the identity become NOPs (they still carry their gates' error sites).  A run on two
+// qubits whose gates cost more than a dense 4x4 (16 FP64 / amplitude) becomes one GEN2
+// op; its gates are kept as components for the careful path.
 std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
                                const std::vector<LGate>& gates, bool allow_swap,
-                               std::vector<int>& log_of_phys) {
+                               std::vector<int>& log_of_phys, bool block_reorder) {
   std::vector<FOp> out;
   std::vector<int> phys_of(64);
   for (int q = 0; q < 64; ++q) phys_of[q] = q;
-  int qpos[64];
-  for (int q = 0; q < 64; ++q) qpos[q] = -1;
-  for (int p = 0; p < pd.K; ++p) qpos[pd.tile_q[p]] = p;
   const int n = (int)(pd.op_end - pd.op_begin);
-  auto lg_of = [&](int i) -> const LGate& { return gates[pp.ops[pd.op_begin + i].gate]; };
+  auto lg_raw = [&](int li) -> const LGate& { return gates[pp.ops[pd.op_begin + li].gate]; };
+  static const bool fuse2 = [] {
+    const char* e = std::getenv("TQSIM_FUSE2");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<int> ord(n);
+  for (int i = 0; i < n; ++i) ord[i] = i;
+  if (block_reorder && fuse2) ord = block_order(n, lg_raw);
+  auto lg_of = [&](int i) -> const LGate& { return lg_raw(ord[i]); };
+  // error effects of the gates [i, e_end] of a run on slots (s0, S1), pushed to the run end
+  auto make_sites = [&](FOp& f, int i, int e_end, int s0, int S1) {
+    const int slot1 = S1 >= 0 ? S1 : (s0 == 0 ? 1 : 0);
+    std::vector<M4> mats;
+    for (int t = i; t <= e_end; ++t) mats.push_back(op_matrix(lg_of(t), s0, slot1));
+    f.ea = phys_of[s0];
+    f.eb = S1 >= 0 ? phys_of[S1] : -1;
+    M4 R = M4::id();   // product of the gates after t
+    std::vector<ErrSite> sites(e_end - i + 1);
+    for (int t = e_end; t >= i; --t) {
+      const LGate& lg = lg_of(t);
+      ErrSite& es = sites[t - i];
+      es.gate = pp.ops[pd.op_begin + ord[t]].gate;
+      es.local = (uint32_t)ord[t];
+      const M4 Rd = dagger(R);
+      auto slot = [&](int q) { return q == s0 ? 0 : 1; };
+      const int ncode = lg.two ? 15 : 3;
+      for (int c = 1; c <= ncode; ++c) {
+        M4 E = lg.two ? pauli4(c >> 2, slot((int)lg.q0), c & 3, slot((int)lg.q1))
+                      : pauli4(c, slot((int)lg.q0), 0, 1 - slot((int)lg.q0));
+        ErrEff ef = decompose(R.mul(E).mul(Rd));
+        auto to_pos = [&](uint32_t m) {   // local slot masks -> physical qubits after the run
+          uint32_t r = 0;
+          if (m & 1u) r |= 1u << f.ea;
+          if (m & 2u) {
+            if (f.eb < 0) throw Error{TQSIM_EINTERNAL, "error propagation touched the placeholder slot"};
+            r |= 1u << f.eb;
+          }
+          return r;
+        };
+        ef.x = to_pos(ef.x);
+        ef.z = to_pos(ef.z);
+        es.eff.push_back(ef);
+      }
+      R = R.mul(mats[t - i]);
+    }
+    f.sites = std::move(sites);
+  };
+  // one gate as its own op (GEN2 components)
+  auto single = [&](int t) {
+    const LGate& g = lg_of(t);
+    FOp f;
+    f.qa = phys_of[g.q0];
+    if (g.two && g.op == OP_CX) {
+      f.kind = FOp::CX;
+      f.qb = phys_of[g.q1];
+    } else if (g.two) {   // CZ
+      f.kind = FOp::DIAG;
+      f.qb = phys_of[g.q1];
+      f.d[0] = f.d[1] = f.d[2] = 1.0;
+      f.d[3] = -1.0;
+    } else if (is_x_gate(g)) {
+      f.kind = FOp::XPERM;
+    } else if (g.op == OP_DIAG) {
+      f.kind = FOp::DIAG;
+      f.d[0] = cplx(g.m[0], g.m[1]);
+      f.d[1] = cplx(g.m[6], g.m[7]);
+      f.d[2] = f.d[0];
+      f.d[3] = f.d[1];
+    } else {
+      f.kind = FOp::GEN;
+      for (int k = 0; k < 4; ++k) f.m[k] = cplx(g.m[2 * k], g.m[2 * k + 1]);
+    }
+    make_sites(f, t, t, (int)g.q0, g.two ? (int)g.q1 : -1);
+    return f;
+  };
   int i = 0;
   while (i < n) {
     const LGate& g0 = lg_of(i);
@@ -383,6 +553,8 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     int best = P.diagonal() ? i : -1, best_swap = -1;
     M4 bestP = P;
     int bs1 = s1, sw1 = -1;
+    int jmax = i, cost = gate_cost(g0), gens = cost >= 4 ? 1 : 0;
+    M4 Pmax = P;
     for (int j = i + 1; j < n && j < i + 12; ++j) {
       const LGate& gj = lg_of(j);
       int ns1 = s1;
@@ -398,6 +570,10 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
       // as the identity, so the 4x4 is unchanged when s1 becomes a real qubit)
       s1 = ns1;
       P = op_matrix(gj, s0, s1 < 0 ? (s0 == 0 ? 1 : 0) : s1).mul(P);
+      jmax = j;
+      Pmax = P;
+      cost += gate_cost(gj);
+      gens += gate_cost(gj) >= 4 ? 1 : 0;
       if (P.diagonal()) {
         best = j;
         bestP = P;
@@ -409,6 +585,18 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     }
     FOp f;
     int e_end, S1;
+    if (fuse2 && best < 0 && best_swap < 0 && s1 >= 0 && gens >= 2 && cost > 16) {
+      // dense 4x4 on (s0, s1): 16 FP64 per amplitude instead of `cost`
+      f.kind = FOp::GEN2;
+      f.qa = phys_of[s0];
+      f.qb = phys_of[s1];
+      for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) f.m4[r * 4 + c] = Pmax.a[r][c];
+      for (int t = i; t <= jmax; ++t) f.comps.push_back(single(t));
+      out.push_back(f);
+      i = jmax + 1;
+      continue;
+    }
     if (best_swap > best) {   // relabel instead of moving amplitudes
       e_end = best_swap;
       S1 = sw1;
@@ -428,56 +616,11 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
         if (f.d[k] != cplx(1, 0)) trivial = false;
       if (trivial) f.kind = FOp::NOP;
     } else {
-      e_end = i;
-      S1 = g0.two ? (int)g0.q1 : -1;
-      f.qa = phys_of[g0.q0];
-      if (g0.two) {   // CX (CZ is diagonal and handled above)
-        f.kind = FOp::CX;
-        f.qb = phys_of[g0.q1];
-      } else if (is_x_gate(g0)) {
-        f.kind = FOp::XPERM;
-      } else {
-        f.kind = FOp::GEN;
-        for (int k = 0; k < 4; ++k) f.m[k] = cplx(g0.m[2 * k], g0.m[2 * k + 1]);
-      }
+      out.push_back(single(i));
+      ++i;
+      continue;
     }
-    // error sites of the run (careful path): each gate's Pauli pushed to the run end
-    const int slot1 = S1 >= 0 ? S1 : (s0 == 0 ? 1 : 0);
-    std::vector<M4> mats;
-    for (int t = i; t <= e_end; ++t) mats.push_back(op_matrix(lg_of(t), s0, slot1));
-    f.ea = phys_of[s0];
-    f.eb = S1 >= 0 ? phys_of[S1] : -1;
-    M4 R = M4::id();   // product of the gates after t
-    std::vector<ErrSite> sites(e_end - i + 1);
-    for (int t = e_end; t >= i; --t) {
-      const LGate& lg = lg_of(t);
-      ErrSite& es = sites[t - i];
-      es.gate = pp.ops[pd.op_begin + t].gate;
-      es.local = (uint32_t)t;
-      const M4 Rd = dagger(R);
-      auto slot = [&](int q) { return q == s0 ? 0 : 1; };
-      const int ncode = lg.two ? 15 : 3;
-      for (int c = 1; c <= ncode; ++c) {
-        M4 E = lg.two ? pauli4(c >> 2, slot((int)lg.q0), c & 3, slot((int)lg.q1))
-                      : pauli4(c, slot((int)lg.q0), 0, 1 - slot((int)lg.q0));
-        ErrEff ef = decompose(R.mul(E).mul(Rd));
-        // local slot masks -> physical tile positions after the run
-        auto to_pos = [&](uint32_t m) {
-          uint32_t r = 0;
-          if (m & 1u) r |= 1u << f.ea;
-          if (m & 2u) {
-            if (f.eb < 0) throw Error{TQSIM_EINTERNAL, "error propagation touched the placeholder slot"};
-            r |= 1u << f.eb;
-          }
-          return r;
-        };
-        ef.x = to_pos(ef.x);
-        ef.z = to_pos(ef.z);
-        es.eff.push_back(ef);
-      }
-      R = R.mul(mats[t - i]);
-    }
-    f.sites = std::move(sites);
+    make_sites(f, i, e_end, s0, S1);
     out.push_back(f);
     i = e_end + 1;
   }
@@ -661,25 +804,49 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   auto posm = [&](int qa, int qb) { return (1ull << qpos[qa]) | (qb >= 0 ? 1ull << qpos[qb] : 0ull); };
   auto qmk = [&](int qa, int qb) { return (1ull << qa) | (qb >= 0 ? 1ull << qb : 0ull); };
 
+  // Two candidate op lists -- gates in pass order, or regrouped into 2-qubit blocks (more
+  // dense 4x4 fusion) -- each planned into phases; the cheaper one by a per-amplitude
+  // cost model (FP64 ops of the fused ops + a shared-memory exchange per extra phase)
+  // is generated.
   std::vector<int> log_of_phys;
-  const std::vector<FOp> fops = fuse_fast_ops(pd, pp, gates, true, log_of_phys);
-  // diagonal ops need no register slot (index bits are known, jit below)
-  std::vector<PItem> fitems;
-  for (size_t i = 0; i < fops.size(); ++i) {
-    const FOp& f = fops[i];
-    const bool noreg = f.kind == FOp::DIAG || f.kind == FOp::NOP;
-    fitems.push_back({noreg ? 0ull : posm(f.qa, f.qb), qmk(f.qa, f.qb), (int)i});
+  std::vector<FOp> fops;
+  std::vector<PhaseSpec> fast;
+  uint64_t R0 = 0;
+  int store_key[64];   // the store writes tile position p to logical qubit log_of_phys[tile_q[p]]
+  double best_cost = 0.0;
+  for (int cand = 0; cand < 2; ++cand) {
+    std::vector<int> lop;
+    std::vector<FOp> ops = fuse_fast_ops(pd, pp, gates, true, lop, cand == 1);
+    // diagonal ops need no register slot (index bits are known, jit below)
+    std::vector<PItem> items;
+    double fcost = 0.0;
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const FOp& f = ops[i];
+      const bool noreg = f.kind == FOp::DIAG || f.kind == FOp::NOP;
+      items.push_back({noreg ? 0ull : posm(f.qa, f.qb), qmk(f.qa, f.qb), (int)i});
+      fcost += f.kind == FOp::GEN2 ? 16.0 : f.kind == FOp::GEN ? 8.0 : f.kind == FOp::DIAG ? 1.0 : 0.0;
+    }
+    // One phase plan for both paths: the error-free fast path and the careful path,
+    // which runs the same fused ops under a run-time Pauli frame (below).
+    const uint64_t r0 = choose_load_regs(items, K, coal);
+    int skey[64];
+    for (int p = 0; p < K; ++p) skey[p] = lop[pd.tile_q[p]];
+    std::vector<PhaseSpec> ph = plan_phases(items, K, r0, coal, skey);
+    const double cost = fcost + 12.0 * (double)ph.size();
+    if (cand == 0 || cost < best_cost) {
+      best_cost = cost;
+      fops = std::move(ops);
+      fast = std::move(ph);
+      R0 = r0;
+      (void)R0;
+      log_of_phys = lop;
+      for (int p = 0; p < K; ++p) store_key[p] = skey[p];
+    }
   }
-  // One phase plan for both paths: the error-free fast path and the careful path,
-  // which runs the same fused ops under a run-time Pauli frame (below).
-  const uint64_t R0 = choose_load_regs(fitems, K, coal);
   if (out_logical) {   // stored (logical) address bit of every out-of-tile qubit
     out_logical->clear();
     for (int i = 0; i < pd.n_out; ++i) out_logical->push_back((uint8_t)log_of_phys[pd.out_q[i]]);
   }
-  int store_key[64];   // the store writes tile position p to logical qubit log_of_phys[tile_q[p]]
-  for (int p = 0; p < K; ++p) store_key[p] = log_of_phys[pd.tile_q[p]];
-  const std::vector<PhaseSpec> fast = plan_phases(fitems, K, R0, coal, store_key);
   if (const char* e = std::getenv("TQSIM_JIT_DEBUG")) {
     if (e[0] == '1') {
       std::fprintf(stderr, "[tqsim jit] %s: %d ops -> %zu fused ops; %zu phases\n", name.c_str(), nops,
@@ -688,7 +855,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         std::fprintf(stderr, "   phase %zu R=", ph);
         for (int b = 0; b < RBITS; ++b) std::fprintf(stderr, "%d,", pd.tile_q[fast[ph].P.rpos[b]]);
         std::fprintf(stderr, " ops:");
-        static const char* kn[] = {"G", "X", "CX", "D", "NOP"};
+        static const char* kn[] = {"G", "X", "CX", "D", "NOP", "G2"};
         for (int it : fast[ph].items)
           std::fprintf(stderr, " %s(%d,%d)", kn[(int)fops[it].kind], fops[it].qa, fops[it].qb);
         std::fprintf(stderr, "\n");
@@ -714,8 +881,24 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   std::vector<uint32_t> errx((size_t)std::max(nops, 1) * 16, 0u), errz(errx.size(), 0u);
   std::vector<double> gd;
   std::map<std::vector<double>, uint32_t> gd_index;
-  for (const FOp& f : fops)
-    for (const ErrSite& es : f.sites)
+  // every op with error sites (GEN2 components included), in emission order
+  std::vector<const FOp*> site_ops;
+  std::function<void(const FOp&)> collect = [&](const FOp& f) {
+    if (f.kind == FOp::GEN2) {
+      for (const FOp& cf : f.comps) collect(cf);
+      return;
+    }
+    if (!f.sites.empty()) site_ops.push_back(&f);
+  };
+  for (const FOp& f : fops) collect(f);
+  std::map<const FOp*, uint32_t> site_off;   // op -> offset of its sites in SITES
+  std::vector<uint32_t> site_list;
+  for (const FOp* f : site_ops) {
+    site_off[f] = (uint32_t)site_list.size();
+    for (const ErrSite& es : f->sites) site_list.push_back(es.local);
+  }
+  for (const FOp* fp : site_ops)
+    for (const ErrSite& es : fp->sites)
       for (size_t c = 0; c < es.eff.size(); ++c) {
         const ErrEff& ef = es.eff[c];
         if (ef.x >> 30 || ef.z >> 30) throw Error{TQSIM_EINTERNAL, "error frame needs qubits < 30"};
@@ -740,6 +923,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         errx[(size_t)es.local * 16 + c + 1] = wx;
         errz[(size_t)es.local * 16 + c + 1] = wz;
       }
+  o << "static __constant__ unsigned short SITES[" << std::max<size_t>(site_list.size(), 1) << "] = {";
+  for (size_t i = 0; i < site_list.size(); ++i) o << (i ? "," : "") << site_list[i];
+  if (site_list.empty()) o << "0";
+  o << "};\n";
   o << "static __constant__ unsigned short GOFF[" << std::max(nops, 1) << "] = {";
   for (int i = 0; i < nops; ++i) o << (i ? "," : "") << (pp.ops[pd.op_begin + i].gate - pd.slice_begin);
   if (!nops) o << "0";
@@ -934,6 +1121,33 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             oo << "        " << vb << ".y = " << lin(a10.real(), a10.imag(), "x", a11.real(), a11.imag(), "y", true) << "; }\n";
           }
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+        } else if (f.kind == FOp::GEN2) {   // dense 4x4 on two register bits
+          const int ba = rbit(f.qa), bb = rbit(f.qb);
+          fb_flush(ba, fb_gen);
+          fb_flush(bb, fb_gen);
+          std::ostringstream oo;
+          pool.begin_op();
+          for (int k = 0; k < 16; ++k) {
+            if ((k >> ba & 1) || (k >> bb & 1)) continue;
+            int idx[4];
+            std::string v[4], x[4];
+            for (int j = 0; j < 4; ++j) {
+              idx[j] = k | ((j & 1) << ba) | ((j >> 1) << bb);
+              v[j] = g.r(idx[j]);
+              x[j] = "x" + std::to_string(j);
+            }
+            oo << "      { const tq_d2 x0 = " << v[0] << ", x1 = " << v[1] << ", x2 = " << v[2] << ", x3 = " << v[3]
+               << ";\n";
+            for (int r = 0; r < 4; ++r) {
+              cplx c[4];
+              for (int j = 0; j < 4; ++j) c[j] = f.m4[r * 4 + j] * dph[idx[j]];   // pending input phases
+              oo << "        " << v[r] << ".x = " << linN(c, x, 4, false) << ";\n";
+              oo << "        " << v[r] << ".y = " << linN(c, x, 4, true) << ";\n";
+            }
+            oo << "      }\n";
+            for (int j = 0; j < 4; ++j) dph[idx[j]] = cplx(1.0, 0.0);
+          }
+          o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
         } else if (f.kind == FOp::DIAG) {
           const int ra = rbit(f.qa), rb = f.qb >= 0 ? rbit(f.qb) : -2;
           const bool rta = ra < 0, rtb = rb == -1;
@@ -1085,8 +1299,11 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         }
         o << "      }\n";
       };
-      for (int it : specs[ph].items) {
-        const FOp& f = fops[it];
+      std::function<void(const FOp&)> emit_careful = [&](const FOp& f) {
+        if (f.kind == FOp::GEN2) {   // its gates one by one, each with its own errors
+          for (const FOp& cf : f.comps) emit_careful(cf);
+          return;
+        }
 
         if (f.kind == FOp::CX) {
           const int ba = rbit(f.qa), bb = rbit(f.qb);
@@ -1240,19 +1457,18 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         }
         // the run's drawn errors, in gate order (uniform branch; rare)
         if (!f.sites.empty()) {
-          const uint32_t l0 = f.sites.front().local, l1 = f.sites.back().local;
           bool any_gen = false;
           for (const ErrSite& es : f.sites)
             for (const ErrEff& ef : es.eff) any_gen |= ef.generic;
+          std::map<uint32_t, uint32_t> wm;   // bitmap word -> mask of this op's sites
+          for (const ErrSite& es : f.sites) wm[es.local >> 5] |= 1u << (es.local & 31);
           std::ostringstream cond;
           cond << "0u";
-          for (uint32_t w = l0 >> 5; w <= (l1 >> 5); ++w) {
-            uint32_t m = 0;
-            for (uint32_t li = std::max(l0, w * 32); li <= std::min(l1, w * 32 + 31); ++li) m |= 1u << (li & 31);
-            cond << " | (eb" << w << " & " << m << "u)";
-          }
+          for (auto& kv : wm) cond << " | (eb" << kv.first << " & " << kv.second << "u)";
+          const uint32_t so = site_off.at(&f);
           o << "    if (" << cond.str() << ") {\n";
-          o << "      for (tq_u32 li = " << l0 << "u; li <= " << l1 << "u; ++li) {\n";
+          o << "      for (tq_u32 si = " << so << "u; si < " << so + f.sites.size() << "u; ++si) {\n";
+          o << "        const tq_u32 li = SITES[si];\n";
           o << "        if (!((tq_errb[li >> 5] >> (li & 31u)) & 1u)) continue;\n";
           o << "        const tq_u32 c = codes[4u + GOFF[li]];\n";
           o << "        const tq_u32 wx = __ldg(ERRX + li * 16u + c), wz = __ldg(ERRZ + li * 16u + c);\n";
@@ -1271,7 +1487,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           }
           o << "        }\n      }\n    }\n";
         }
-      }
+      };
+      for (int it : specs[ph].items) emit_careful(fops[it]);
     }
     {   // flush the pending phases (run-time factors, then compile-time)
       // product tree T[idx] = gph * prod_{b in L} F_b[bit of idx], idx over the pending bits L
