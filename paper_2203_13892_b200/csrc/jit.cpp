@@ -545,9 +545,15 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     make_sites(f, t, t, (int)g.q0, g.two ? (int)g.q1 : -1);
     return f;
   };
+  // gates touching a qubit off the tile (diagonal units / absorbed SWAPs of the first
+  // pass, passplan.cpp) may only fuse into a DIAG op or a relabeling, never with tile gates
+  auto off_tile = [&](const LGate& g) {
+    return !((pd.tile_mask >> phys_of[g.q0]) & 1) || (g.two && !((pd.tile_mask >> phys_of[g.q1]) & 1));
+  };
   int i = 0;
   while (i < n) {
     const LGate& g0 = lg_of(i);
+    const bool restricted = off_tile(g0);
     int s0 = (int)g0.q0, s1 = g0.two ? (int)g0.q1 : -1;
     M4 P = op_matrix(g0, s0, s1 < 0 ? (s0 == 0 ? 1 : 0) : s1);
     int best = P.diagonal() ? i : -1, best_swap = -1;
@@ -557,6 +563,7 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     M4 Pmax = P;
     for (int j = i + 1; j < n && j < i + 12; ++j) {
       const LGate& gj = lg_of(j);
+      if (!restricted && off_tile(gj)) break;
       int ns1 = s1;
       const int qs[2] = {(int)gj.q0, gj.two ? (int)gj.q1 : -1};
       bool ok = true;
@@ -585,7 +592,9 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     }
     FOp f;
     int e_end, S1;
-    if (fuse2 && best < 0 && best_swap < 0 && s1 >= 0 && gens >= 2 && cost > 16) {
+    if (restricted && best < 0 && best_swap < 0)
+      throw Error{TQSIM_EINTERNAL, "pass planner placed a non-diagonal gate off the tile"};
+    if (!restricted && fuse2 && best < 0 && best_swap < 0 && s1 >= 0 && gens >= 2 && cost > 16) {
       // dense 4x4 on (s0, s1): 16 FP64 per amplitude instead of `cost`
       f.kind = FOp::GEN2;
       f.qa = phys_of[s0];
@@ -823,6 +832,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     for (size_t i = 0; i < ops.size(); ++i) {
       const FOp& f = ops[i];
       const bool noreg = f.kind == FOp::DIAG || f.kind == FOp::NOP;
+      if (!noreg && (qpos[f.qa] < 0 || (f.qb >= 0 && qpos[f.qb] < 0)))
+        throw Error{TQSIM_EINTERNAL, "a register op on a qubit off the tile"};
       items.push_back({noreg ? 0ull : posm(f.qa, f.qb), qmk(f.qa, f.qb), (int)i});
       fcost += f.kind == FOp::GEN2 ? 16.0 : f.kind == FOp::GEN ? 8.0 : f.kind == FOp::DIAG ? 1.0 : 0.0;
     }
@@ -1391,8 +1402,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           auto entry = [&](int bita, int bitb) { return f.d[bita | (bitb << 1)]; };
           auto val = [&](const cplx& v, bool im) { return g_pool->ref(im ? v.imag() : v.real()); };
           // thread bit of qubit q XOR its frame bit (frame-conjugated diagonal: D(i ^ x))
-          auto tbit = [&](int q) {
-            return "(((lth >> " + std::to_string(qpos[q]) + ") ^ (fx >> " + std::to_string(q) + ")) & 1u)";
+          auto tbit = [&](int q) {   // off the tile: the CTA's tile-index bit
+            const std::string ib = qpos[q] >= 0 ? "(lth >> " + std::to_string(qpos[q]) + ")" : "(gtile >> " + std::to_string(q) + ")";
+            return "((" + ib + " ^ (fx >> " + std::to_string(q) + ")) & 1u)";
           };
           if (!rta && !rtb) {   // both register bits: applied now (frame-dependent, no folding)
             std::string ent[8];

@@ -310,3 +310,25 @@ def test_leaf_without_state_store_equals_stored_path(cfg, p):
         nm = NoiseModel(noise.p1, noise.p2, noise.readout_p01, noise.readout_p10)
         ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 11)
         assert_leaves_match(a.leaf_outcomes, ref.leaves)
+
+
+@pytest.mark.parametrize("tile,p", [(7, 0.1), (8, 0.4), (9, 1.0)])
+def test_offtile_diagonal_units(tile, p):
+    """QAOA (CX.RZ.CX) + QFT (lowered CP) on 14 qubits with tiles of 2^7..2^9: the first
+    pass of a level applies diagonal units whose qubits lie off the tile, reading them
+    from the tile index; errors inside those units flip off-tile qubits, which the
+    out-of-place store applies as an address XOR."""
+    from workloads.generators import qaoa_gates, random_3_regular_edges
+    rng = np.random.default_rng(tile * 7 + int(p * 10))
+    n = 14
+    gates = qaoa_gates(n, random_3_regular_edges(n, rng), [0.4, 0.9], [0.3, 0.7]) + qft_gates(n)
+    nm = NoiseModel(p, min(1.0, 2 * p), 0.02, 0.03)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
+    low = OG.lower(gates)
+    recs = T.tqsim_describe_passes(n, gates, noise, 24, [3, 2, 4], opts)
+    qm = lambda g: (1 << low[g][1]) | ((1 << low[g][2]) if low[g][2] >= 0 else 0)
+    offtile = [r for r in recs if qm(r.gate) & ~r.tile_qubit_mask]
+    assert offtile, "no off-tile diagonal unit in the plan"
+    run_and_compare(n, gates, nm, 24, [3, 2, 4], 5 + tile, opts,
+                    dumps=[(0, 0), (0, 2), (1, 4), (2, 23)])

@@ -127,6 +127,24 @@ def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
                 return True
         return False
 
+    def is_diag(g):
+        k, a, c, th, ph, la = low[g]
+        if k in ("cx", "cz"):
+            return k == "cz"
+        m = OG.matrix_1q(k, th, ph, la)
+        return m[0, 1] == 0 and m[1, 0] == 0
+
+    def in_diag_unit(g):   # a diagonal gate, or CX(a,b) D(b) CX(a,b) (lowered RZZ / CP middle)
+        if is_diag(g):
+            return True
+        for s0 in (g - 2, g):
+            if s0 < 0 or s0 + 2 >= len(low):
+                continue
+            x, y, z = low[s0], low[s0 + 1], low[s0 + 2]
+            if x[0] == z[0] == "cx" and x[1:3] == z[1:3] and is_diag(s0 + 1) and y[1] == x[2]:
+                return True
+        return False
+
     pos = {}
     for i, r in enumerate(recs):
         b = plan.boundary_list
@@ -135,9 +153,11 @@ def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
         qm = (1 << a) | ((1 << c) if c >= 0 else 0)
         if qm & ~r.tile_qubit_mask:
             # absorbed SWAP: a store-address relabeling in the first (out-of-place) pass
-            # of its level, on qubits >= 3 (never the leaf run qubits)
-            assert in_swap_triple(r.gate) and r.pass_ == 0 and min(a, c) >= 3, (r.gate, r.pass_)
-        else:
+            # of its level, on qubits >= 3 (never the leaf run qubits); or a diagonal unit
+            # of the first pass reading its off-tile qubits from the tile index
+            assert r.pass_ == 0, (r.gate, r.pass_)
+            assert (in_swap_triple(r.gate) and min(a, c) >= 3) or in_diag_unit(r.gate), r.gate
+        elif not (r.pass_ == 0 and in_diag_unit(r.gate)):
             assert qm & ~r.reg_qubit_mask == 0                       # gate qubits in registers
         assert r.reg_qubit_mask & ~r.tile_qubit_mask == 0            # registers within the tile
         assert bin(r.reg_qubit_mask).count("1") == min(4, max(n, 4))
@@ -214,3 +234,39 @@ def test_jit_compiles_every_variant_on_host():
         k, _, _ = T.tqsim_compile_passes(n, gates, T.noise_arg(0.1, 0.2), 40, [4, 10],
                                          T.default_options(tile_qubits=tq))
         assert k > 0
+
+
+def test_kernel_generator_accepts_every_random_plan():
+    """The code generator (host side, no compile) accepts every pass of random circuits
+    -- CP / RZZ / SWAP-heavy and general -- at every tile width, in particular first
+    passes whose diagonal units sit off the tile (passplan.cpp diag_unit_at)."""
+    from workloads.generators import g1, g2
+    rng = np.random.default_rng(21)
+    noise = T.noise_arg(0.05, 0.1)
+    for it in range(24):
+        n = int(rng.integers(4, 15))
+        if it % 2:
+            gates = random_circuit(n, int(rng.integers(20, 90)), rng)
+        else:   # diagonal-unit heavy
+            gates = []
+            for _ in range(int(rng.integers(10, 40))):
+                a, b = (int(v) for v in rng.choice(n, size=2, replace=False))
+                r = int(rng.integers(0, 4))
+                if r == 0:
+                    gates += [g2("cx", a, b), g1("rz", b, float(rng.uniform(0, 6))), g2("cx", a, b)]
+                elif r == 1:
+                    gates.append(g2("cp", a, b, float(rng.uniform(0, 6))))
+                elif r == 2:
+                    gates.append(g2("swap", a, b))
+                else:
+                    gates.append(g1("rx", a, float(rng.uniform(0, 6))))
+        arities = [3, 2, 4] if it % 3 else None
+        for tile in (4, 6, 8, 10, 12):
+            opts = T.default_options(tile_qubits=tile)
+            recs = T.tqsim_describe_passes(n, gates, noise, 24, arities, opts)
+            npass = {}
+            for r in recs:
+                npass[r.level] = max(npass.get(r.level, 0), r.pass_ + 1)
+            for lv, k in npass.items():
+                for ps in range(k):
+                    assert T.tqsim_pass_source(n, gates, noise, 24, arities, opts, lv, ps)
