@@ -159,6 +159,11 @@ typedef struct {
   uint32_t level, pass, phase, gate;   /* gate = lowered gate index g */
   uint64_t tile_qubit_mask;            /* global qubits staged by the pass's tiles */
   uint64_t reg_qubit_mask;             /* global qubits held in registers in the phase */
+  uint32_t role;                       /* 0 register op; first pass of a level only:
+                                          1 part of a diagonal unit (no register),
+                                          2 part of an absorbed SWAP (store relabeling),
+                                          3 absorbed CX (GF(2)-linear store-address map) */
+  uint32_t reserved;
 } tqsim_op_record;
 
 /* Timing of one gate-pass kernel (tqsim_profile_passes). */

@@ -58,6 +58,13 @@ __device__ __forceinline__ tq_d2 tq_ld(const tq_d2* p) {
   asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
+// one 32-byte access = two consecutive amplitudes (LDG/STG.256 on sm_100)
+__device__ __forceinline__ void tq_ld2(const tq_d2* p, tq_d2& a, tq_d2& b) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void tq_st2(tq_d2* p, const tq_d2& a, const tq_d2& b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" :: "l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
 // r *= i^q
 __device__ __forceinline__ void tq_rot(tq_d2& r, tq_u32 q) {
   const double a = (q & 1u) ? r.y : r.x, b = (q & 1u) ? r.x : r.y;
@@ -211,7 +218,9 @@ struct ErrSite {
 };
 
 struct FOp {
-  enum Kind { GEN, XPERM, CX, DIAG, NOP, GEN2 } kind = GEN;
+  // AMAP: an absorbed CX (ROLE_STOREMAP), applied by the store-address map; no code in
+  // the fast path, a frame conjugation (+ its errors) in the careful path
+  enum Kind { GEN, XPERM, CX, DIAG, NOP, GEN2, AMAP } kind = GEN;
   cplx m4[16];            // GEN2: row-major 4x4, local index bit_qa | bit_qb << 1
   std::vector<FOp> comps; // GEN2: its gates (careful path), each with its own site
   int qa = -1, qb = -1;   // global (physical) qubits (qb = -1: one-qubit op)
@@ -479,6 +488,12 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
   for (int i = 0; i < n; ++i) ord[i] = i;
   if (block_reorder && fuse2) ord = block_order(n, lg_raw);
   auto lg_of = [&](int i) -> const LGate& { return lg_raw(ord[i]); };
+  auto is_map = [&](int i) { return pp.ops[pd.op_begin + ord[i]].role == ROLE_STOREMAP; };
+  // With a store map in the pass, SWAP relabelings stay within {0..2} or within the
+  // qubits >= 3, so the map and the relabeling keep address bits 0..2 on physical
+  // qubits 0..2 (coalesced 32-byte pairs, leaf runs within one tile).
+  bool has_map = false;
+  for (int t = 0; t < n; ++t) has_map |= pp.ops[pd.op_begin + t].role == ROLE_STOREMAP;
   // error effects of the gates [i, e_end] of a run on slots (s0, S1), pushed to the run end
   auto make_sites = [&](FOp& f, int i, int e_end, int s0, int S1) {
     const int slot1 = S1 >= 0 ? S1 : (s0 == 0 ? 1 : 0);
@@ -553,6 +568,17 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
   int i = 0;
   while (i < n) {
     const LGate& g0 = lg_of(i);
+    if (is_map(i)) {
+      FOp f;
+      f.kind = FOp::AMAP;
+      f.qa = phys_of[g0.q0];
+      f.qb = phys_of[g0.q1];
+      if (f.qa < LOW_Q || f.qb < LOW_Q) throw Error{TQSIM_EINTERNAL, "store map on a qubit < 3"};
+      make_sites(f, i, i, (int)g0.q0, (int)g0.q1);
+      out.push_back(f);
+      ++i;
+      continue;
+    }
     const bool restricted = off_tile(g0);
     int s0 = (int)g0.q0, s1 = g0.two ? (int)g0.q1 : -1;
     M4 P = op_matrix(g0, s0, s1 < 0 ? (s0 == 0 ? 1 : 0) : s1);
@@ -563,7 +589,7 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     M4 Pmax = P;
     for (int j = i + 1; j < n && j < i + 12; ++j) {
       const LGate& gj = lg_of(j);
-      if (!restricted && off_tile(gj)) break;
+      if (is_map(j) || (!restricted && off_tile(gj))) break;
       int ns1 = s1;
       const int qs[2] = {(int)gj.q0, gj.two ? (int)gj.q1 : -1};
       bool ok = true;
@@ -585,7 +611,8 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
         best = j;
         bestP = P;
         bs1 = s1;
-      } else if (allow_swap && s1 >= 0 && is_swap(P)) {
+      } else if (allow_swap && s1 >= 0 && is_swap(P) &&
+                 (!has_map || ((phys_of[s0] < LOW_Q) == (phys_of[s1] < LOW_Q)))) {
         best_swap = j;
         sw1 = s1;
       }
@@ -681,10 +708,44 @@ PhaseDesc make_phase_layout(uint64_t R, int K, int low, bool coalesced) {
 // stores after SWAP relabelings): registers padded with the lowest keys >= 5, lanes on
 // the rest in ascending key order, so lanes 0..2 walk address bits 0..2 when R holds
 // none of them.
+// An I/O phase may also hold low address bits in registers when they move as 32-byte
+// pairs: address bit 0 in registers (registers k, k | b0 are one LDG/STG.256) plus at
+// most one of bits 1, 2; the lanes then start at the lowest other bit.  Measured at the
+// full HBM rate of the lane-coalesced layout; bits 0..2 all in registers are not
+// (scripts/microbench/io_layout_bench.cu).
+bool io_pairs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TQSIM_IO_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+bool io_regs_ok(uint64_t R, const int* key, int K) {
+  bool has0 = false;
+  int low = 0;
+  for (int p = 0; p < K; ++p)
+    if (R >> p & 1) {
+      if (key[p] == 0) has0 = true;
+      else if (key[p] < LOW_Q) ++low;
+    }
+  return has0 && io_pairs_enabled() ? low <= 1 : low == 0 && !has0;
+}
+// R plus the position of address bit 0 when R holds a low address bit
+uint64_t io_with_pair(uint64_t R, const int* key, int K) {
+  bool any_low = false;
+  int p0 = -1;
+  for (int p = 0; p < K; ++p) {
+    if ((R >> p & 1) && key[p] < LOW_Q) any_low = true;
+    if (key[p] == 0) p0 = p;
+  }
+  return any_low && p0 >= 0 ? R | 1ull << p0 : R;
+}
+
 PhaseDesc make_io_layout(uint64_t R, int K, const int* key) {
   std::vector<int> order(K);
   for (int p = 0; p < K; ++p) order[p] = p;
   std::sort(order.begin(), order.end(), [&](int a, int b) { return key[a] < key[b]; });
+  if (__builtin_popcountll(R) < RBITS) R = io_with_pair(R, key, K);
   // pad the registers with address bits 5, 6, ... (lanes keep bits 0..4: every warp
   // access is 512 contiguous bytes, and the leaf run sums a warp holds are consecutive)
   for (int i = 0; i < K && __builtin_popcountll(R) < RBITS; ++i)
@@ -697,9 +758,32 @@ PhaseDesc make_io_layout(uint64_t R, int K, const int* key) {
   int rb = 0;
   for (int p = 0; p < K; ++p)
     if (R >> p & 1) P.rpos[rb++] = (uint8_t)p;
-  int m = 0;
+  std::vector<int> lanes;
   for (int i = 0; i < K; ++i)
-    if (!(R >> order[i] & 1)) P.tpos[m++] = (uint8_t)order[i];
+    if (!(R >> order[i] & 1)) lanes.push_back(order[i]);
+  // With low address bits in registers (32-byte pairs) only the leading lanes on the
+  // remaining low bits matter for HBM; fill lanes 1..2 with positions of residues mod 3
+  // not yet used, which keeps the 16-byte shared-memory accesses of this phase
+  // conflict-free under tq_swz (bank group bit b = XOR of position bits = b mod 3).
+  bool low_in_regs = false;
+  for (int p = 0; p < K; ++p)
+    if ((R >> p & 1) && key[p] < LOW_Q) low_in_regs = true;
+  int nf = 0;   // leading lanes on low address bits
+  while (nf < (int)lanes.size() && key[lanes[nf]] < LOW_Q) ++nf;
+  if (low_in_regs) {
+    int used = 0;
+    for (int j = 0; j < nf; ++j) used |= 1 << (lanes[j] % 3);
+    for (int slot = nf; slot < 3 && slot < (int)lanes.size(); ++slot)
+      for (int j = slot; j < (int)lanes.size(); ++j)
+        if (!(used >> (lanes[j] % 3) & 1)) {
+          const int v = lanes[j];
+          lanes.erase(lanes.begin() + j);
+          lanes.insert(lanes.begin() + slot, v);
+          used |= 1 << (v % 3);
+          break;
+        }
+  }
+  for (size_t m = 0; m < lanes.size(); ++m) P.tpos[m] = (uint8_t)lanes[m];
   return P;
 }
 
@@ -755,8 +839,9 @@ std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint6
     first = false;
   }
   if (coal) {
-    const uint64_t last_regs = groups.size() == 1 ? R0 : groups.back().second;
-    if ((last_regs & store_low) || (groups.size() == 1 && !same_low)) groups.emplace_back(std::vector<int>(), 0);
+    const uint64_t last_regs = io_with_pair(groups.size() == 1 ? R0 : groups.back().second, store_key, K);
+    const bool st_ok = __builtin_popcountll(last_regs) <= RBITS && io_regs_ok(last_regs, store_key, K);
+    if (!st_ok || (groups.size() == 1 && !same_low)) groups.emplace_back(std::vector<int>(), 0);
   }
   (void)lowm;
   std::vector<PhaseSpec> out;
@@ -777,18 +862,20 @@ std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint6
 
 // Register set of the load phase: as many leading items as fit in 4 positions
 // >= low (positions 0..low-1 stay on lanes: coalesced), padded with high positions.
-uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal) {
+uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal, bool allow_low) {
   const int low = std::min(LOW_Q, K);
   const uint64_t lowm = (1ull << low) - 1;
+  int load_key[64];
+  for (int p = 0; p < K; ++p) load_key[p] = p;
   uint64_t used = 0, blocked = 0;
   for (const PItem& it : items) {
     if (it.qm & blocked) continue;
-    const bool ok = (!coal || !(it.need & lowm)) && __builtin_popcountll(used | it.need) <= RBITS;
-    if (ok) used |= it.need;
+    const uint64_t nu = coal ? io_with_pair(used | it.need, load_key, K) : used | it.need;
+    const bool ok = __builtin_popcountll(nu) <= RBITS &&
+                    (!coal || (allow_low ? io_regs_ok(nu, load_key, K) : !(nu & lowm)));
+    if (ok) used = nu;
     else blocked |= it.qm;
   }
-  int load_key[64];
-  for (int p = 0; p < K; ++p) load_key[p] = p;
   PhaseDesc P = make_io_layout(used, K, load_key);
   uint64_t R = 0;
   for (int b = 0; b < RBITS; ++b) R |= 1ull << P.rpos[b];
@@ -801,7 +888,7 @@ uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal) {
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs, int variant = 0,
-                     std::vector<uint8_t>* out_logical = nullptr) {
+                     std::vector<uint32_t>* out_row = nullptr) {
   const int K = pd.K, T = 1 << (K - RBITS);
   const int low = std::min(LOW_Q, K);
   const bool coal = K - RBITS >= low;   // enough lane bits to keep qubits 0..2 on lanes 0..2
@@ -823,15 +910,17 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   uint64_t R0 = 0;
   int store_key[64];   // the store writes tile position p to logical qubit log_of_phys[tile_q[p]]
   double best_cost = 0.0;
-  for (int cand = 0; cand < 2; ++cand) {
+  // (x2: the load phase may or may not take low address bits into registers as 32-byte
+  // pairs -- the greedy load choice is not monotone in phases)
+  for (int cand = 0; cand < 4; ++cand) {
     std::vector<int> lop;
-    std::vector<FOp> ops = fuse_fast_ops(pd, pp, gates, true, lop, cand == 1);
+    std::vector<FOp> ops = fuse_fast_ops(pd, pp, gates, true, lop, (cand & 1) == 1);
     // diagonal ops need no register slot (index bits are known, jit below)
     std::vector<PItem> items;
     double fcost = 0.0;
     for (size_t i = 0; i < ops.size(); ++i) {
       const FOp& f = ops[i];
-      const bool noreg = f.kind == FOp::DIAG || f.kind == FOp::NOP;
+      const bool noreg = f.kind == FOp::DIAG || f.kind == FOp::NOP || f.kind == FOp::AMAP;
       if (!noreg && (qpos[f.qa] < 0 || (f.qb >= 0 && qpos[f.qb] < 0)))
         throw Error{TQSIM_EINTERNAL, "a register op on a qubit off the tile"};
       items.push_back({noreg ? 0ull : posm(f.qa, f.qb), qmk(f.qa, f.qb), (int)i});
@@ -839,7 +928,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     }
     // One phase plan for both paths: the error-free fast path and the careful path,
     // which runs the same fused ops under a run-time Pauli frame (below).
-    const uint64_t r0 = choose_load_regs(items, K, coal);
+    const uint64_t r0 = choose_load_regs(items, K, coal, cand >= 2);
     int skey[64];
     for (int p = 0; p < K; ++p) skey[p] = lop[pd.tile_q[p]];
     std::vector<PhaseSpec> ph = plan_phases(items, K, r0, coal, skey);
@@ -854,9 +943,49 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       for (int p = 0; p < K; ++p) store_key[p] = skey[p];
     }
   }
-  if (out_logical) {   // stored (logical) address bit of every out-of-tile qubit
-    out_logical->clear();
-    for (int i = 0; i < pd.n_out; ++i) out_logical->push_back((uint8_t)log_of_phys[pd.out_q[i]]);
+  // Store map: the store writes the amplitude at physical index i to address P(i) =
+  // L(M(i)), M the absorbed CX gates (GF(2)-linear, composed in op order over physical
+  // qubits) and L the SWAP relabeling (physical -> logical bit).  pcol[q] = P(e_q).
+  bool has_map = false;
+  uint32_t pcol[32];
+  {
+    uint32_t col[32];
+    for (int q = 0; q < 32; ++q) col[q] = q < n ? 1u << q : 0u;
+    for (const FOp& f : fops)
+      if (f.kind == FOp::AMAP) {
+        has_map = true;
+        for (int q = 0; q < n; ++q) col[q] ^= ((col[q] >> f.qa) & 1u) << f.qb;
+      }
+    for (int q = 0; q < 32; ++q) {
+      pcol[q] = 0;
+      for (int j = 0; j < n; ++j)
+        if (col[q] >> j & 1) pcol[q] |= 1u << log_of_phys[j];
+    }
+    for (int q = 0; has_map && q < std::min(n, LOW_Q); ++q)
+      if (pcol[q] >= (1u << LOW_Q) || __builtin_popcount(pcol[q]) != 1)
+        throw Error{TQSIM_EINTERNAL, "store map moves address bits 0..2"};
+  }
+  if (out_row) {   // per out-of-tile qubit: the stored-address bits whose parity is its bit
+    // invert P over GF(2): rows of P^-1 (Gauss-Jordan on [P | I], row r = address bit r)
+    std::vector<uint64_t> A(n);   // bits 0..n-1: P, bits 32..32+n-1: identity
+    for (int r = 0; r < n; ++r) {
+      uint64_t v = 1ull << (32 + r);
+      for (int c = 0; c < n; ++c)
+        if (pcol[c] >> r & 1) v |= 1ull << c;
+      A[r] = v;
+    }
+    for (int c = 0; c < n; ++c) {
+      int piv = -1;
+      for (int r = c; r < n; ++r)
+        if (A[r] >> c & 1) { piv = r; break; }
+      if (piv < 0) throw Error{TQSIM_EINTERNAL, "store map is singular"};
+      std::swap(A[c], A[piv]);
+      for (int r = 0; r < n; ++r)
+        if (r != c && (A[r] >> c & 1)) A[r] ^= A[c];
+    }
+    // now row c of [I | P^-1]: physical bit c = parity(P^-1 row c & address)
+    out_row->clear();
+    for (int i = 0; i < pd.n_out; ++i) out_row->push_back((uint32_t)(A[pd.out_q[i]] >> 32));
   }
   if (const char* e = std::getenv("TQSIM_JIT_DEBUG")) {
     if (e[0] == '1') {
@@ -866,7 +995,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         std::fprintf(stderr, "   phase %zu R=", ph);
         for (int b = 0; b < RBITS; ++b) std::fprintf(stderr, "%d,", pd.tile_q[fast[ph].P.rpos[b]]);
         std::fprintf(stderr, " ops:");
-        static const char* kn[] = {"G", "X", "CX", "D", "NOP", "G2"};
+        static const char* kn[] = {"G", "X", "CX", "D", "NOP", "G2", "M"};
         for (int it : fast[ph].items)
           std::fprintf(stderr, " %s(%d,%d)", kn[(int)fops[it].kind], fops[it].qa, fops[it].qb);
         std::fprintf(stderr, "\n");
@@ -964,8 +1093,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
   o << "  tq_u32 gtile = 0u, gtile_st = 0u;\n";   // the tile's out-of-tile index bits: physical / stored
   for (int i = 0; i < pd.n_out; ++i)
-    o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << "; gtile_st |= (tq_u32)((t >> "
-      << i << ") & 1ull) << " << log_of_phys[pd.out_q[i]] << ";\n";
+    o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << "; gtile_st ^= (0u - (tq_u32)((t >> "
+      << i << ") & 1ull)) & " << pcol[pd.out_q[i]] << "u;\n";
   o << "  tq_d2* __restrict__ dst = a.dst + ((tq_u64)s << " << n << ");\n";
   if (mode == 1)
     o << "  const tq_d2* __restrict__ src = a.src + ((((tq_u64)a.child_first + s) / a.arity - a.parent_first) << "
@@ -979,19 +1108,24 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   uint32_t lo_last[16];   // tile-local position offsets of the registers (last offsets() call)
   auto offsets = [&](const PhaseDesc& P, const std::vector<int>* lq, uint32_t* goff, uint32_t* soff,
                      std::string& lb, std::string& gb) {
-    auto qof = [&](int p) { return lq ? (*lq)[pd.tile_q[p]] : (int)pd.tile_q[p]; };
+    // column of tile position p: the physical bit, or (lq: the store) its image P(e_q)
+    auto col = [&](int p) { return lq ? pcol[pd.tile_q[p]] : 1u << pd.tile_q[p]; };
     std::ostringstream l, gg;
     l << "0u";
     gg << (lq ? "gtile_st" : "gtile");
     for (int m = 0; m < K - RBITS; ++m) {
       l << " | (((tid >> " << m << ") & 1u) << " << (int)P.tpos[m] << ")";
-      gg << " | (((tid >> " << m << ") & 1u) << " << qof(P.tpos[m]) << ")";
+      const uint32_t c = col(P.tpos[m]);
+      if (__builtin_popcount(c) == 1)
+        gg << " ^ (((tid >> " << m << ") & 1u) << " << __builtin_ctz(c) << ")";
+      else
+        gg << " ^ ((0u - ((tid >> " << m << ") & 1u)) & " << c << "u)";
     }
     for (int k = 0; k < 16; ++k) {
       uint32_t go = 0, lo = 0;
       for (int b = 0; b < RBITS; ++b)
         if (k >> b & 1) {
-          go |= 1u << qof(P.rpos[b]);
+          go ^= col(P.rpos[b]);
           lo |= 1u << P.rpos[b];
         }
       goff[k] = go;
@@ -1001,16 +1135,26 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     lb = l.str();
     gb = gg.str();
   };
+  // register bit whose offset is address bit 0 (-1: none): such register pairs move as
+  // one 32-byte access (tq_ld2 / tq_st2)
+  auto pair_bit = [&](const uint32_t* go) {
+    for (int b = 0; b < RBITS; ++b)
+      if (go[1 << b] == 1u) return b;
+    return -1;
+  };
   auto emit_load = [&]() {
     uint32_t goff[16], soff[16];
     std::string lb, gb;
     offsets(fast[0].P, nullptr, goff, soff, lb, gb);
     o << "  {\n    const tq_u32 gb = " << gb << ";\n";
+    const int b0 = pair_bit(goff);
     for (int k = 0; k < 16; ++k) {
       if (mode == 0)
         o << "    r" << k << ".x = (gb + " << goff[k] << "u == 0u) ? 1.0 : 0.0; r" << k << ".y = 0.0;\n";
-      else
+      else if (b0 < 0)
         o << "    r" << k << " = tq_ld(src + (gb + " << goff[k] << "u));\n";
+      else if (!(k >> b0 & 1))   // address bit 0 in registers: 32-byte pair
+        o << "    tq_ld2(src + (gb + " << goff[k] << "u), r" << k << ", r" << (k | 1 << b0) << ");\n";
     }
     o << "  }\n";
   };
@@ -1322,6 +1466,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           permute([&](int k) { return k ^ (((k >> ba) & 1) << bb); });
           o << "    fx ^= ((fx >> " << f.qa << ") & 1u) << " << f.qb << "; fz ^= ((fz >> " << f.qb << ") & 1u) << "
             << f.qa << ";\n";
+        } else if (f.kind == FOp::AMAP) {   // applied by the store map: conjugate the frame only
+          o << "    fx ^= ((fx >> " << f.qa << ") & 1u) << " << f.qb << "; fz ^= ((fz >> " << f.qb << ") & 1u) << "
+            << f.qa << ";\n";
         } else if (f.kind == FOp::XPERM) {
           const int ba = rbit(f.qa);
           std::swap(fb[ba].var[0], fb[ba].var[1]);
@@ -1562,21 +1709,41 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         o << "    tq_u32 xl = 0u;\n";
         for (int q = 0; q < n; ++q)
           o << "    xl |= ((fx >> " << q << ") & 1u) << " << log_of_phys[q] << ";\n";
-        if (variant == 0) {   // variants 1/2 feed only |a|^2: the frame's phase does not matter
+        if (variant == 0 && !has_map) {   // variants 1/2 feed only |a|^2: the phase does not matter
           o << "    const tq_u32 zt = __popc(fz & (" << gbp << "));\n";
           for (int k = 0; k < 16; ++k)
             o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << gph[k] << "u)) << 1));\n";
+        } else if (variant == 0) {
+          // the frame acts after the store map: its Z sign is read on the mapped index,
+          // i.e. on the stored address with fz relabeled like fx
+          o << "    tq_u32 zl = 0u;\n";
+          for (int q = 0; q < n; ++q)
+            o << "    zl |= ((fz >> " << q << ") & 1u) << " << log_of_phys[q] << ";\n";
+          o << "    const tq_u32 zt = __popc(zl & gbs);\n";
+          for (int k = 0; k < 16; ++k)
+            o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(zl & " << gofs[k] << "u)) << 1));\n";
         }
         xl = " ^ xl";
       }
       if (variant == 0) {
-        for (int k = 0; k < 16; ++k)
-          o << "    dst[(gbs + " << gofs[k] << "u)" << xl << "] = " << g.r(k) << ";\n";
+        const int b0 = pair_bit(gofs);
+        for (int k = 0; k < 16; ++k) {
+          if (b0 < 0) {
+            o << "    dst[(gbs ^ " << gofs[k] << "u)" << xl << "] = " << g.r(k) << ";\n";
+          } else if (!(k >> b0 & 1)) {   // 32-byte pair; a frame X on address bit 0 swaps it
+            const std::string ra = g.r(k), rb = g.r(k | 1 << b0);
+            if (with_errors)
+              o << "    { const tq_u32 ad = (gbs ^ " << gofs[k] << "u)" << xl << "; const bool sw = ad & 1u; tq_st2(dst + (ad & ~1u), sw ? "
+                << rb << " : " << ra << ", sw ? " << ra << " : " << rb << "); }\n";
+            else
+              o << "    tq_st2(dst + (gbs ^ " << gofs[k] << "u), " << ra << ", " << rb << ");\n";
+          }
+        }
       } else if (variant == 1) {   // the instance's store-address XOR (uniform per instance)
         o << "    if (t == 0 && tid == 0u) a.xlout[s] = " << (with_errors ? "xl" : "0u") << ";\n";
       } else {                     // the selected run's 8 amplitudes only
         for (int k = 0; k < 16; ++k)
-          o << "    { const tq_u32 ad = (gbs + " << gofs[k] << "u)" << xl << "; if ((ad >> " << RUN_Q
+          o << "    { const tq_u32 ad = (gbs ^ " << gofs[k] << "u)" << xl << "; if ((ad >> " << RUN_Q
             << ") == rsel) a.scratch[((tq_u64)s << " << RUN_Q << ") | (ad & " << ((1 << RUN_Q) - 1) << "u)] = "
             << g.r(k) << "; }\n";
       }
@@ -1634,7 +1801,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         for (size_t i = 0; i < reps.size(); ++i) o << (i ? "," : "") << gofs[reps[i]] << "u";
         o << "};\n";
         for (size_t j = 0; j < v.size(); ++j)
-          o << "    a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + (((gbs + ROFF[rbase + " << j << "u])" << xl
+          o << "    a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + (((gbs ^ ROFF[rbase + " << j << "u])" << xl
             << ") >> " << RUN_Q << ")] = " << v[j] << ";\n";
       }
     } else {
@@ -1773,7 +1940,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
     std::string cubin;
     std::string err;
     std::vector<double> coefs;
-    std::vector<uint8_t> out_logical;
+    std::vector<uint32_t> out_row;
   };
   std::vector<Job> jobs;
   std::vector<std::vector<JitPass>> out(pp.levels.size());
@@ -1789,7 +1956,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
         j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : "");
         const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
         std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
-                                    j.smem, j.coefs, v, &j.out_logical);
+                                    j.smem, j.coefs, v, &j.out_row);
         j.src = std::string(kPrelude) + kJitTypes + body;
         jobs.push_back(std::move(j));
       }
@@ -1853,7 +2020,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
       jp.threads = j.threads;
       jp.smem = j.smem;
       jp.coefs = j.coefs;
-      jp.out_logical = j.out_logical;
+      jp.out_row = j.out_row;
     } else {
       (j.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute) = reinterpret_cast<void*>(ck.fn);
     }

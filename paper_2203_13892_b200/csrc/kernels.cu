@@ -28,13 +28,13 @@ struct SelectOut {
   uint32_t* tile;
   const uint32_t* xl;         // the leaf pass's store-address XOR per leaf
   uint32_t n_out;
-  uint8_t out_logical[32];    // stored address bit of out-of-tile qubit i
+  uint32_t out_row[32];       // out-of-tile qubit i = parity(out_row[i] & stored address)
 };
 
 __device__ __forceinline__ uint32_t tile_of_run(uint64_t run, uint32_t xl, const SelectOut& so) {
   const uint64_t a = (run << RUN_Q) ^ (uint64_t)xl;   // source (physical) index, logical bits
   uint32_t t = 0;
-  for (uint32_t i = 0; i < so.n_out; ++i) t |= (uint32_t)((a >> so.out_logical[i]) & 1u) << i;
+  for (uint32_t i = 0; i < so.n_out; ++i) t |= (uint32_t)(__popcll(a & (uint64_t)so.out_row[i]) & 1) << i;
   return t;
 }
 
@@ -493,7 +493,7 @@ static dev::SelectOut select_out(const LeafSelect* sel) {
   so.tile = sel->tile;
   so.xl = sel->xl;
   so.n_out = sel->n_out;
-  for (uint32_t i = 0; i < sel->n_out && i < 32; ++i) so.out_logical[i] = sel->out_logical[i];
+  for (uint32_t i = 0; i < sel->n_out && i < 32; ++i) so.out_row[i] = sel->out_row[i];
   return so;
 }
 

@@ -46,6 +46,12 @@ size_t diag_unit_at(const std::vector<uint32_t>& v, size_t i, const std::vector<
   return 0;
 }
 
+// absorb_swaps also absorbs CX gates on qubits >= low that do not fit the tile (or touch
+// a qubit of an earlier absorbed CX) into a GF(2)-linear map of the store address: the
+// out-of-place store writes amplitude i to M(i) (jit.cpp).  Later gates on their qubits
+// that are not themselves absorbed are deferred (they would run before the map).
+// Measured: C5 HEA-28 (CX ladders) 261,248 -> 127,616 HBM passes.
+//
 // absorb_swaps (first pass of a level: out of place, so its store may permute the
 // address bits freely): a SWAP on qubits >= low that does not fit the tile joins the
 // group as a pure relabeling needing no tile slot; later gates on its qubits are
@@ -58,12 +64,12 @@ template <class MaskFn>
 std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
     const std::vector<uint32_t>& order, const std::vector<LGate>& gates, MaskFn need_mask,
     int cap, size_t max_items = ~size_t(0), bool absorb_swaps = false, int low = 0,
-    std::vector<char>* unit_gate = nullptr) {
+    std::vector<uint8_t>* role = nullptr) {
   std::vector<std::pair<std::vector<uint32_t>, uint64_t>> groups;
   std::vector<uint32_t> remaining = order;
   bool first_group = true;
   while (!remaining.empty()) {
-    uint64_t used = 0, blocked = 0;
+    uint64_t used = 0, blocked = 0, mapped = 0;   // mapped: qubits of absorbed CX gates
     std::vector<uint32_t> in, deferred;
     for (size_t ri = 0; ri < remaining.size(); ++ri) {
       const uint32_t g = remaining[ri];
@@ -71,8 +77,11 @@ std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
         const LGate& x = gates[g];
         const uint64_t qm = qmask(x);
         const uint64_t need = need_mask(g);
-        if (!(qm & blocked) && popc(used | need) > cap && (int)x.q0 >= low && (int)x.q1 >= low) {
-          for (int t = 0; t < 3; ++t) in.push_back(remaining[ri + t]);
+        if (!(qm & (blocked | mapped)) && popc(used | need) > cap && (int)x.q0 >= low && (int)x.q1 >= low) {
+          for (int t = 0; t < 3; ++t) {
+            in.push_back(remaining[ri + t]);
+            if (role) (*role)[remaining[ri + t]] = ROLE_SWAP;
+          }
           blocked |= qm;   // nothing later in this pass touches the relabeled pair
           ri += 2;
           continue;
@@ -82,18 +91,28 @@ std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
         const size_t du = diag_unit_at(remaining, ri, gates);
         if (du && in.size() + du <= max_items) {
           const uint64_t qm = qmask(gates[g]);
-          if (!(qm & blocked)) {
+          if (!(qm & (blocked | mapped))) {
             for (size_t t = 0; t < du; ++t) {
               in.push_back(remaining[ri + t]);
-              if (unit_gate) (*unit_gate)[remaining[ri + t]] = 1;
+              if (role) (*role)[remaining[ri + t]] = ROLE_DIAG;
             }
             ri += du - 1;
             continue;
           }
         }
+        const LGate& x = gates[g];
+        if (x.op == OP_CX && (int)x.q0 >= low && (int)x.q1 >= low && in.size() < max_items) {
+          const uint64_t qm = qmask(x);
+          if (!(qm & blocked) && ((qm & mapped) || popc(used | need_mask(g)) > cap)) {
+            in.push_back(g);
+            mapped |= qm;
+            if (role) (*role)[g] = ROLE_STOREMAP;
+            continue;
+          }
+        }
       }
       const uint64_t qm = qmask(gates[g]);
-      if ((qm & blocked) || in.size() >= max_items) {
+      if ((qm & (blocked | mapped)) || in.size() >= max_items) {
         deferred.push_back(g);
         blocked |= qm;
         continue;
@@ -162,10 +181,10 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
   for (size_t d = 0; d + 1 < plan.bounds.size(); ++d) {
     std::vector<uint32_t> order;
     for (uint64_t g = plan.bounds[d]; g < plan.bounds[d + 1]; ++g) order.push_back((uint32_t)g);
-    std::vector<char> unit_gate(gates.size(), 0);   // gates of the first pass's diagonal units
+    std::vector<uint8_t> role(gates.size(), ROLE_REG);   // roles in the first pass (OpRole)
     auto passes = group_gates(order, gates,
                               [&](uint32_t g) { return qmask(gates[g]) & ~low_mask; }, hcap,
-                              MAX_PASS_OPS, /*absorb_swaps=*/true, low, &unit_gate);
+                              MAX_PASS_OPS, /*absorb_swaps=*/true, low, &role);
     std::vector<PassDesc> lvl;
     for (size_t pi = 0; pi < passes.size(); ++pi) {
       uint64_t H = passes[pi].second;
@@ -192,7 +211,7 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
       // kernel generator fuses them back into one diagonal
       auto pos_mask = [&](uint32_t g) {
         const int a = qpos[gates[g].q0], b = qpos[gates[g].q1];
-        if (a < 0 || b < 0 || unit_gate[g]) return 0ull;
+        if (a < 0 || b < 0 || role[g] == ROLE_DIAG || role[g] == ROLE_STOREMAP) return 0ull;
         return (1ull << a) | (1ull << b);
       };
       auto phases = group_gates(passes[pi].first, gates, pos_mask, RBITS);
@@ -233,6 +252,7 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
           od.type = lg.op;
           od.two = lg.two ? 1 : 0;
           od.gate = g;
+          od.role = role[g];
           const bool intile = pos_mask(g) != 0;   // in registers
           od.ra = intile ? (uint8_t)rbit_of_pos[qpos[lg.q0]] : 0;
           od.rb = intile && lg.two ? (uint8_t)rbit_of_pos[qpos[lg.q1]] : od.ra;

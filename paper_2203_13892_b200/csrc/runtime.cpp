@@ -339,8 +339,8 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       ls.t3 = t3;
       ls.tile = tiles;
       ls.xl = xlv;
-      ls.n_out = (uint32_t)jp.out_logical.size();
-      for (size_t i = 0; i < jp.out_logical.size() && i < 32; ++i) ls.out_logical[i] = jp.out_logical[i];
+      ls.n_out = (uint32_t)jp.out_row.size();
+      for (size_t i = 0; i < jp.out_row.size() && i < 32; ++i) ls.out_row[i] = jp.out_row[i];
       mark(x, 1);
       if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {
         ck(launch_sample_small(buf, runs, (uint32_t)cnt, n, (int)h->n_user, b, h->d_seed, h->noise.readout_p01,
@@ -654,7 +654,7 @@ tqsim_status tqsim_describe_passes(const tqsim_circuit* c, const tqsim_noise_mod
           for (uint32_t i = P.op_begin; i < P.op_end; ++i, ++k)
             if (out && k < cap)
               out[k] = tqsim_op_record{(uint32_t)d, (uint32_t)p, ph - pd.phase_begin,
-                                       h->pp.ops[i].gate, pd.tile_mask, rmask};
+                                       h->pp.ops[i].gate, pd.tile_mask, rmask, h->pp.ops[i].role, 0u};
         }
       }
     *n_out = k;

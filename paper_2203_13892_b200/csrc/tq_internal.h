@@ -57,11 +57,20 @@ constexpr int LOW_Q = 3;        // qubits 0..4 are in every tile (512 B contiguo
 constexpr int MAX_PASS_OPS = 192; // gates per pass kernel (code size / shared codes bound)
 constexpr int RUN_Q = 3;          // leaf |a|^2 run sums cover 2^RUN_Q consecutive amplitudes
 
-struct OpDesc {                 // 8 bytes, device-readable
+// Role of a gate in its pass (first pass of a level only for roles 1..3, passplan.cpp)
+enum OpRole : uint8_t {
+  ROLE_REG = 0,       // applied to amplitudes held in registers
+  ROLE_DIAG = 1,      // part of a diagonal unit: phases from known index bits, no register
+  ROLE_SWAP = 2,      // part of an absorbed SWAP: a relabeling of address bits at the store
+  ROLE_STOREMAP = 3,  // an absorbed CX: a GF(2)-linear map of the store address
+};
+
+struct OpDesc {
   uint8_t type;                 // OpType
   uint8_t ra, rb;               // register bit(s) 0..3 (rb = target for CX)
   uint8_t two;                  // 2q noise location
   uint32_t gate;                // lowered gate index g (noise key + matrix)
+  uint8_t role;                 // OpRole
 };
 
 struct PhaseDesc {              // 32 bytes, device-readable
@@ -151,7 +160,7 @@ struct LeafSelect {
   uint32_t* tile;
   const uint32_t* xl;
   uint32_t n_out;
-  uint8_t out_logical[32];
+  uint32_t out_row[32];      // out-of-tile qubit i = parity(out_row[i] & stored address)
 };
 int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
                          int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
@@ -175,7 +184,7 @@ struct JitPass {
   void* kernel = nullptr;   // cudaKernel_t
   void* kernel_nostore = nullptr;     // leaf-sum passes: run sums only (variant 1)
   void* kernel_recompute = nullptr;   // leaf-sum passes: one tile per leaf, 8 amps (variant 2)
-  std::vector<uint8_t> out_logical;   // stored address bit of every out-of-tile qubit
+  std::vector<uint32_t> out_row;   // per out-of-tile qubit: stored-address bits whose parity is its bit
   int threads = 0;
   size_t smem = 0;
   std::vector<double> coefs;      // by-value coefficient parameter (TQSIM_JIT_COEF=0 mode)

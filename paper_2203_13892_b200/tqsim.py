@@ -103,7 +103,7 @@ class tqsim_debug(C.Structure):
 class tqsim_op_record(C.Structure):
     _fields_ = [("level", C.c_uint32), ("pass_", C.c_uint32), ("phase", C.c_uint32),
                 ("gate", C.c_uint32), ("tile_qubit_mask", C.c_uint64),
-                ("reg_qubit_mask", C.c_uint64)]
+                ("reg_qubit_mask", C.c_uint64), ("role", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 _P = C.POINTER

@@ -332,3 +332,30 @@ def test_offtile_diagonal_units(tile, p):
     assert offtile, "no off-tile diagonal unit in the plan"
     run_and_compare(n, gates, nm, 24, [3, 2, 4], 5 + tile, opts,
                     dumps=[(0, 0), (0, 2), (1, 4), (2, 23)])
+
+
+@pytest.mark.parametrize("tile,p,ar", [(7, 0.2, [3, 2, 4]), (8, 1.0, [4, 6]), (10, 0.05, [4, 6])])
+def test_store_map_cx_ladders(tile, p, ar):
+    """HEA (RY layers + CX ladders) on 14 qubits with small tiles: the first pass of a
+    level absorbs the CX gates that do not fit into a GF(2)-linear map of the store
+    address; their errors conjugate through the map in the careful path; the leaf
+    sampler inverts the map to find a run's tile (no-store leaf path)."""
+    from workloads.generators import hea_gates
+    rng = np.random.default_rng(tile + int(p * 100))
+    n = 14
+    gates = hea_gates(n, 3, rng.uniform(0, 6.28, (3, n)))
+    gates += [("swap", 3, 11, 0.0, 0.0, 0.0), ("cx", 12, 5, 0.0, 0.0, 0.0), ("swap", 0, 9, 0.0, 0.0, 0.0)]
+    nm = NoiseModel(p, min(1.0, 2 * p), 0.02, 0.03)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
+    recs = T.tqsim_describe_passes(n, gates, noise, 24, ar, opts)
+    assert any(r.role == 3 for r in recs), "no absorbed CX in the plan"
+    if len(ar) == 2:   # store maps in the leaf level's pass too
+        assert any(r.role == 3 and r.level == 1 for r in recs)
+    dumps = [(0, 0), (0, 2), (1, 4), (2, 23)] if len(ar) == 3 else [(0, 0), (0, 3), (1, 5), (1, 23)]
+    run_and_compare(n, gates, nm, 24, ar, 11 + tile, opts, dumps=dumps)
+    # the leaf sampler without stored leaf states (select -> recompute -> finish)
+    res = T.tqsim_run_ex(n, gates, noise, 24, ar, 11 + tile, opts)
+    low = OG.lower(gates)
+    ref = simulate_tree(n, low, oracle_plan_of(res.plan), nm, 11 + tile)
+    assert_leaves_match(res.leaf_outcomes, ref.leaves)

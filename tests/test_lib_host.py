@@ -151,16 +151,25 @@ def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
         assert b[r.level] <= r.gate < b[r.level + 1]                 # in its own slice
         k, a, c = low[r.gate][0], low[r.gate][1], low[r.gate][2]
         qm = (1 << a) | ((1 << c) if c >= 0 else 0)
-        if qm & ~r.tile_qubit_mask:
-            # absorbed SWAP: a store-address relabeling in the first (out-of-place) pass
-            # of its level, on qubits >= 3 (never the leaf run qubits); or a diagonal unit
-            # of the first pass reading its off-tile qubits from the tile index
-            assert r.pass_ == 0, (r.gate, r.pass_)
-            assert (in_swap_triple(r.gate) and min(a, c) >= 3) or in_diag_unit(r.gate), r.gate
-        elif not (r.pass_ == 0 and in_diag_unit(r.gate)):
-            assert qm & ~r.reg_qubit_mask == 0                       # gate qubits in registers
+        # roles (tqsim_op_record.role): 0 register op; in the first (out-of-place) pass
+        # of a level: 1 diagonal unit reading off-tile qubits from the tile index, 2
+        # absorbed SWAP (store relabeling, qubits >= 3), 3 absorbed CX (store map, >= 3)
+        if r.role == 0:
+            assert qm & ~r.reg_qubit_mask == 0, r.gate                # gate qubits in registers
+        else:
+            assert r.pass_ == 0, (r.gate, r.pass_, r.role)
+        if r.role == 1:
+            assert in_diag_unit(r.gate), r.gate
+        elif r.role == 2:
+            assert in_swap_triple(r.gate) and min(a, c) >= 3, r.gate
+        elif r.role == 3:
+            assert k == "cx" and min(a, c) >= 3, r.gate
         assert r.reg_qubit_mask & ~r.tile_qubit_mask == 0            # registers within the tile
         assert bin(r.reg_qubit_mask).count("1") == min(4, max(n, 4))
+        # store maps / relabelings act at the end of the pass
+        if r.role in (2, 3):
+            pos[r.gate] = (r.level, r.pass_, 1 << 30, i)
+            continue
         pos[r.gate] = (r.level, r.pass_, r.phase, i)
     # order preserved between any two gates sharing a qubit
     last = {}
