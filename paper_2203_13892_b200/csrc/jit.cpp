@@ -490,10 +490,10 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
   auto lg_of = [&](int i) -> const LGate& { return lg_raw(ord[i]); };
   auto is_map = [&](int i) { return pp.ops[pd.op_begin + ord[i]].role == ROLE_STOREMAP; };
   // With a store map in the pass, SWAP relabelings stay within {0..2} or within the
-  // qubits >= 3, so the map and the relabeling keep address bits 0..2 on physical
-  // qubits 0..2 (coalesced 32-byte pairs, leaf runs within one tile).
+  // qubits >= 3, so address bits 0..2 stay on physical qubits 0..2.
   bool has_map = false;
   for (int t = 0; t < n; ++t) has_map |= pp.ops[pd.op_begin + t].role == ROLE_STOREMAP;
+  bool lowhigh_relabel = false;
   // error effects of the gates [i, e_end] of a run on slots (s0, S1), pushed to the run end
   auto make_sites = [&](FOp& f, int i, int e_end, int s0, int S1) {
     const int slot1 = S1 >= 0 ? S1 : (s0 == 0 ? 1 : 0);
@@ -573,7 +573,7 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
       f.kind = FOp::AMAP;
       f.qa = phys_of[g0.q0];
       f.qb = phys_of[g0.q1];
-      if (f.qa < LOW_Q || f.qb < LOW_Q) throw Error{TQSIM_EINTERNAL, "store map on a qubit < 3"};
+      if (f.qb >= LOW_Q && f.qa < LOW_Q) throw Error{TQSIM_EINTERNAL, "store map from a low control to a high target"};
       make_sites(f, i, i, (int)g0.q0, (int)g0.q1);
       out.push_back(f);
       ++i;
@@ -636,6 +636,7 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     if (best_swap > best) {   // relabel instead of moving amplitudes
       e_end = best_swap;
       S1 = sw1;
+      lowhigh_relabel |= (phys_of[s0] < LOW_Q) != (phys_of[sw1] < LOW_Q);
       std::swap(phys_of[s0], phys_of[sw1]);
       f.kind = FOp::NOP;
       f.qa = phys_of[s0];   // the pair of physical qubits the relabeling exchanges
@@ -659,6 +660,23 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     make_sites(f, i, e_end, s0, S1);
     out.push_back(f);
     i = e_end + 1;
+  }
+  // Trailing CX ops -- no later op of the pass (other than store maps and relabelings)
+  // touches their qubits -- whose target is < 3 or whose control is >= 3 also become
+  // store maps: they then need no registers (fewer phases).  The stored high address
+  // bits stay functions of the physical high bits (whole 128-byte lines, leaf runs in
+  // one tile).  Not with a low/high relabeling in the pass (address bits 0..2 must stay
+  // on physical qubits 0..2 under a map).
+  if (!lowhigh_relabel) {
+    uint64_t touched = 0;
+    for (int t = (int)out.size() - 1; t >= 0; --t) {
+      FOp& f = out[t];
+      if (f.kind == FOp::AMAP || f.kind == FOp::NOP) continue;
+      uint64_t qm = 1ull << f.qa;
+      if (f.qb >= 0) qm |= 1ull << f.qb;
+      if (f.kind == FOp::CX && !(qm & touched) && (f.qb < LOW_Q || f.qa >= LOW_Q)) f.kind = FOp::AMAP;
+      else touched |= qm;
+    }
   }
   log_of_phys.assign(64, 0);
   for (int q = 0; q < 64; ++q) log_of_phys[phys_of[q]] = q;
@@ -962,7 +980,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         if (col[q] >> j & 1) pcol[q] |= 1u << log_of_phys[j];
     }
     for (int q = 0; has_map && q < std::min(n, LOW_Q); ++q)
-      if (pcol[q] >= (1u << LOW_Q) || __builtin_popcount(pcol[q]) != 1)
+      if (pcol[q] >= (1u << LOW_Q) || !pcol[q])
         throw Error{TQSIM_EINTERNAL, "store map moves address bits 0..2"};
   }
   if (out_row) {   // per out-of-tile qubit: the stored-address bits whose parity is its bit
@@ -1137,7 +1155,11 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   };
   // register bit whose offset is address bit 0 (-1: none): such register pairs move as
   // one 32-byte access (tq_ld2 / tq_st2)
-  auto pair_bit = [&](const uint32_t* go) {
+  // (store: only when address bit 0 is the image of one physical bit alone)
+  int bit0_cols = 0;
+  for (int q = 0; q < n; ++q) bit0_cols += pcol[q] & 1u;
+  auto pair_bit = [&](const uint32_t* go, bool store) {
+    if (store && bit0_cols != 1) return -1;
     for (int b = 0; b < RBITS; ++b)
       if (go[1 << b] == 1u) return b;
     return -1;
@@ -1147,7 +1169,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     std::string lb, gb;
     offsets(fast[0].P, nullptr, goff, soff, lb, gb);
     o << "  {\n    const tq_u32 gb = " << gb << ";\n";
-    const int b0 = pair_bit(goff);
+    const int b0 = pair_bit(goff, false);
     for (int k = 0; k < 16; ++k) {
       if (mode == 0)
         o << "    r" << k << ".x = (gb + " << goff[k] << "u == 0u) ? 1.0 : 0.0; r" << k << ".y = 0.0;\n";
@@ -1726,7 +1748,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         xl = " ^ xl";
       }
       if (variant == 0) {
-        const int b0 = pair_bit(gofs);
+        const int b0 = pair_bit(gofs, true);
         for (int k = 0; k < 16; ++k) {
           if (b0 < 0) {
             o << "    dst[(gbs ^ " << gofs[k] << "u)" << xl << "] = " << g.r(k) << ";\n";

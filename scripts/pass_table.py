@@ -15,6 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
     ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--shard", default="0/1", help="r/w: this shard of the tree only")
     args = ap.parse_args()
     import torch
     import paper_2203_13892_b200.tqsim as T
@@ -22,19 +23,20 @@ def main():
     w = load_config(args.config)
     n, gates, noise, shots, ar = T.workload_args(w)
     h = T.tqsim_create(n, gates, noise, shots, ar, T.default_options(tile_qubits=args.tile))
-    ws = torch.empty(h.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    rk, wd = (int(v) for v in args.shard.split("/"))
+    ws = torch.empty(h.workspace_bytes(rk, wd), dtype=torch.uint8, device="cuda")
     out = torch.zeros(h.plan.n_outcomes, dtype=torch.int32, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
-    h.execute(1, 0, 1, st, ws.data_ptr(), ws.numel(), out.data_ptr())
+    h.execute(1, rk, wd, st, ws.data_ptr(), ws.numel(), out.data_ptr())
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for s in range(3):
-        h.execute(2 + s, 0, 1, st, ws.data_ptr(), ws.numel(), out.data_ptr())
+    for s in range(1 if wd > 1 else 3):
+        h.execute(2 + s, rk, wd, st, ws.data_ptr(), ws.numel(), out.data_ptr())
     e1.record()
     torch.cuda.synchronize()
-    step = e0.elapsed_time(e1) / 3
-    rows = h.profile_passes(1, 0, 1, st, ws.data_ptr(), ws.numel(), out.data_ptr())
+    step = e0.elapsed_time(e1) / (1 if wd > 1 else 3)
+    rows = h.profile_passes(1, rk, wd, st, ws.data_ptr(), ws.numel(), out.data_ptr())
     tot = 0.0
     print("%-5s %-4s %6s %10s %10s %8s %9s" % ("level", "pass", "states", "launch/tr", "ms/launch", "GB/s", "ms/tree"))
     for r in rows:
