@@ -573,7 +573,8 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
       f.kind = FOp::AMAP;
       f.qa = phys_of[g0.q0];
       f.qb = phys_of[g0.q1];
-      if (f.qb >= LOW_Q && f.qa < LOW_Q) throw Error{TQSIM_EINTERNAL, "store map from a low control to a high target"};
+      if (f.qa < LOW_Q && f.qb >= LOW_Q && pd.leaf_sums)
+        throw Error{TQSIM_EINTERNAL, "absorbed CX from a low control in the leaf-sum pass"};
       make_sites(f, i, i, (int)g0.q0, (int)g0.q1);
       out.push_back(f);
       ++i;
@@ -662,11 +663,12 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     i = e_end + 1;
   }
   // Trailing CX ops -- no later op of the pass (other than store maps and relabelings)
-  // touches their qubits -- whose target is < 3 or whose control is >= 3 also become
-  // store maps: they then need no registers (fewer phases).  The stored high address
-  // bits stay functions of the physical high bits (whole 128-byte lines, leaf runs in
-  // one tile).  Not with a low/high relabeling in the pass (address bits 0..2 must stay
-  // on physical qubits 0..2 under a map).
+  // touches their qubits -- also become store maps: they then need no registers (fewer
+  // phases).  In the leaf-sum pass only those whose target is < 3 or whose control is
+  // >= 3, so the stored high address bits stay functions of the physical high bits
+  // (leaf runs in one tile); elsewhere a low control only splits 128-byte lines into
+  // 32-byte-complete halves.  Not with a low/high relabeling in the pass (address bits
+  // 0..2 must stay on physical qubits 0..2 under a map).
   if (!lowhigh_relabel) {
     uint64_t touched = 0;
     for (int t = (int)out.size() - 1; t >= 0; --t) {
@@ -674,7 +676,8 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
       if (f.kind == FOp::AMAP || f.kind == FOp::NOP) continue;
       uint64_t qm = 1ull << f.qa;
       if (f.qb >= 0) qm |= 1ull << f.qb;
-      if (f.kind == FOp::CX && !(qm & touched) && (f.qb < LOW_Q || f.qa >= LOW_Q)) f.kind = FOp::AMAP;
+      if (f.kind == FOp::CX && !(qm & touched) && (f.qb < LOW_Q || f.qa >= LOW_Q || !pd.leaf_sums))
+        f.kind = FOp::AMAP;
       else touched |= qm;
     }
   }
@@ -979,7 +982,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       for (int j = 0; j < n; ++j)
         if (col[q] >> j & 1) pcol[q] |= 1u << log_of_phys[j];
     }
-    for (int q = 0; has_map && q < std::min(n, LOW_Q); ++q)
+    for (int q = 0; has_map && pd.leaf_sums && q < std::min(n, LOW_Q); ++q)
       if (pcol[q] >= (1u << LOW_Q) || !pcol[q])
         throw Error{TQSIM_EINTERNAL, "store map moves address bits 0..2"};
   }

@@ -46,7 +46,7 @@ size_t diag_unit_at(const std::vector<uint32_t>& v, size_t i, const std::vector<
   return 0;
 }
 
-// absorb_swaps also absorbs CX gates on qubits >= low that do not fit the tile (or touch
+// absorb_swaps also absorbs CX gates that do not fit the tile (or touch
 // a qubit of an earlier absorbed CX) into a GF(2)-linear map of the store address: the
 // out-of-place store writes amplitude i to M(i) (jit.cpp).  Later gates on their qubits
 // that are not themselves absorbed are deferred (they would run before the map).
@@ -64,7 +64,7 @@ template <class MaskFn>
 std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
     const std::vector<uint32_t>& order, const std::vector<LGate>& gates, MaskFn need_mask,
     int cap, size_t max_items = ~size_t(0), bool absorb_swaps = false, int low = 0,
-    std::vector<uint8_t>* role = nullptr) {
+    std::vector<uint8_t>* role = nullptr, bool leaf_level = false) {
   std::vector<std::pair<std::vector<uint32_t>, uint64_t>> groups;
   std::vector<uint32_t> remaining = order;
   bool first_group = true;
@@ -101,7 +101,11 @@ std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
           }
         }
         const LGate& x = gates[g];
-        if (x.op == OP_CX && (int)x.q0 >= low && (int)x.q1 >= low && in.size() < max_items) {
+        // (target < low: a permutation inside 128-byte lines; control < low <= target:
+        // splits lines into 32-byte-complete halves, and a leaf run over two tiles, so
+        // not at the leaf level)
+        const bool mappable = (int)x.q1 < low || (int)x.q0 >= low || !leaf_level;
+        if (x.op == OP_CX && mappable && in.size() < max_items) {
           const uint64_t qm = qmask(x);
           if (!(qm & blocked) && ((qm & mapped) || popc(used | need_mask(g)) > cap)) {
             in.push_back(g);
@@ -184,7 +188,8 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
     std::vector<uint8_t> role(gates.size(), ROLE_REG);   // roles in the first pass (OpRole)
     auto passes = group_gates(order, gates,
                               [&](uint32_t g) { return qmask(gates[g]) & ~low_mask; }, hcap,
-                              MAX_PASS_OPS, /*absorb_swaps=*/true, low, &role);
+                              MAX_PASS_OPS, /*absorb_swaps=*/true, low, &role,
+                              /*leaf_level=*/d + 2 == plan.bounds.size());
     std::vector<PassDesc> lvl;
     for (size_t pi = 0; pi < passes.size(); ++pi) {
       uint64_t H = passes[pi].second;

@@ -153,7 +153,7 @@ def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
         qm = (1 << a) | ((1 << c) if c >= 0 else 0)
         # roles (tqsim_op_record.role): 0 register op; in the first (out-of-place) pass
         # of a level: 1 diagonal unit reading off-tile qubits from the tile index, 2
-        # absorbed SWAP (store relabeling, qubits >= 3), 3 absorbed CX (store map, >= 3)
+        # absorbed SWAP (store relabeling, qubits >= 3), 3 absorbed CX (store map)
         if r.role == 0:
             assert qm & ~r.reg_qubit_mask == 0, r.gate                # gate qubits in registers
         else:
@@ -162,8 +162,8 @@ def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
             assert in_diag_unit(r.gate), r.gate
         elif r.role == 2:
             assert in_swap_triple(r.gate) and min(a, c) >= 3, r.gate
-        elif r.role == 3:
-            assert k == "cx" and min(a, c) >= 3, r.gate
+        elif r.role == 3:   # control a, target c; a low control only above the leaf level
+            assert k == "cx" and (c < 3 or a >= 3 or r.level + 1 < plan.n_levels), r.gate
         assert r.reg_qubit_mask & ~r.tile_qubit_mask == 0            # registers within the tile
         assert bin(r.reg_qubit_mask).count("1") == min(4, max(n, 4))
         # store maps / relabelings act at the end of the pass
