@@ -669,6 +669,17 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
   // (leaf runs in one tile); elsewhere a low control only splits 128-byte lines into
   // 32-byte-complete halves.  Not with a low/high relabeling in the pass (address bits
   // 0..2 must stay on physical qubits 0..2 under a map).
+  // The composed map must keep the columns of physical qubits 0, 1 (and 2 in the
+  // leaf-sum pass) within address bits 0..2: lanes on qubits 0..1 then still store
+  // 64-byte-contiguous groups (measured: fully scattered 16-byte stores run at ~60% of
+  // the HBM rate, scripts/microbench/io_layout_bench.cu).
+  auto map_ok = [&]() {
+    uint32_t col[3] = {1u, 2u, 4u};
+    for (const FOp& f : out)
+      if (f.kind == FOp::AMAP)
+        for (int q = 0; q < 3; ++q) col[q] ^= ((col[q] >> f.qa) & 1u) << f.qb;
+    return col[0] < 8u && col[1] < 8u && (!pd.leaf_sums || col[2] < 8u);
+  };
   if (!lowhigh_relabel) {
     uint64_t touched = 0;
     for (int t = (int)out.size() - 1; t >= 0; --t) {
@@ -676,11 +687,15 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
       if (f.kind == FOp::AMAP || f.kind == FOp::NOP) continue;
       uint64_t qm = 1ull << f.qa;
       if (f.qb >= 0) qm |= 1ull << f.qb;
-      if (f.kind == FOp::CX && !(qm & touched) && (f.qb < LOW_Q || f.qa >= LOW_Q || !pd.leaf_sums))
+      if (f.kind == FOp::CX && !(qm & touched)) {
         f.kind = FOp::AMAP;
-      else touched |= qm;
+        if (map_ok()) continue;
+        f.kind = FOp::CX;
+      }
+      touched |= qm;
     }
   }
+  if (!map_ok()) throw Error{TQSIM_EINTERNAL, "absorbed CX maps split the 64-byte store groups"};
   log_of_phys.assign(64, 0);
   for (int q = 0; q < 64; ++q) log_of_phys[phys_of[q]] = q;
   return out;
@@ -986,6 +1001,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       if (pcol[q] >= (1u << LOW_Q) || !pcol[q])
         throw Error{TQSIM_EINTERNAL, "store map moves address bits 0..2"};
   }
+  bool store_moves = false;   // some amplitude is stored at an address other than its own
+  for (int q = 0; q < n; ++q) store_moves |= pcol[q] != (1u << q);
   if (out_row) {   // per out-of-tile qubit: the stored-address bits whose parity is its bit
     // invert P over GF(2): rows of P^-1 (Gauss-Jordan on [P | I], row r = address bit r)
     std::vector<uint64_t> A(n);   // bits 0..n-1: P, bits 32..32+n-1: identity
@@ -1719,6 +1736,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
     }
     if (last) {
+      // In place with a single phase, a thread's loads and stores meet no barrier: when
+      // the store addresses differ from the loaded ones (a relabeling or store map, or
+      // the careful path's frame XOR) another warp may not have loaded them yet.
+      if (mode == 2 && nph == 1 && (with_errors || store_moves)) o << "    __syncthreads();\n";
       // fast path: physical tile qubit tile_q[p] holds logical qubit log_of_phys[tile_q[p]]
       uint32_t gofs[16], sofs[16];
       std::string lbx, gbl;

@@ -101,10 +101,10 @@ std::vector<std::pair<std::vector<uint32_t>, uint64_t>> group_gates(
           }
         }
         const LGate& x = gates[g];
-        // (target < low: a permutation inside 128-byte lines; control < low <= target:
-        // splits lines into 32-byte-complete halves, and a leaf run over two tiles, so
-        // not at the leaf level)
-        const bool mappable = (int)x.q1 < low || (int)x.q0 >= low || !leaf_level;
+        // (target < low: a permutation inside 128-byte lines; control low - 1 = 2 <= target:
+        // splits lines into 64-byte halves, and a leaf run over two tiles, so not at the
+        // leaf level; controls 0, 1 would scatter the stores)
+        const bool mappable = (int)x.q1 < low || (int)x.q0 >= low || ((int)x.q0 == low - 1 && !leaf_level);
         if (x.op == OP_CX && mappable && in.size() < max_items) {
           const uint64_t qm = qmask(x);
           if (!(qm & blocked) && ((qm & mapped) || popc(used | need_mask(g)) > cap)) {

@@ -163,7 +163,7 @@ def _check_pass_invariants(n, gates, noise, shots, arities=None, options=None):
         elif r.role == 2:
             assert in_swap_triple(r.gate) and min(a, c) >= 3, r.gate
         elif r.role == 3:   # control a, target c; a low control only above the leaf level
-            assert k == "cx" and (c < 3 or a >= 3 or r.level + 1 < plan.n_levels), r.gate
+            assert k == "cx" and (c < 3 or a >= 3 or (a == 2 and r.level + 1 < plan.n_levels)), r.gate
         assert r.reg_qubit_mask & ~r.tile_qubit_mask == 0            # registers within the tile
         assert bin(r.reg_qubit_mask).count("1") == min(4, max(n, 4))
         # store maps / relabelings act at the end of the pass
