@@ -1205,11 +1205,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // case) run the fused fast path, the others apply each keyed Pauli after its gate
   o << "  const unsigned char* __restrict__ codes = a.rows + (tq_u64)s * " << CROW << "u;\n";
   o << "  const tq_u32 emask = __ldg(reinterpret_cast<const unsigned int*>(codes));\n";
-  o << "  if (!((emask >> " << std::min<uint32_t>(pd.pass_index, 31) << ") & 1u)) {\n";
+  o << "  const bool errs = (emask >> " << std::min<uint32_t>(pd.pass_index, 31) << ") & 1u;\n";
 
-  auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors) {
+  auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors, int ph_only) {
   const int nph = (int)specs.size();
   for (int ph = 0; ph < nph; ++ph) {
+    if (ph != ph_only) continue;
     const PhaseDesc& P = specs[ph].P;
     const bool last = ph == nph - 1;
     g.reset_map();
@@ -1857,17 +1858,35 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  }\n";
   }
   };
-  emit_phases(fast, false);
-  o << "  } else {\n";
+  // Per phase, CTA-uniform: the error-free fast code while the Pauli frame is trivial
+  // and no op of the phase drew an error, else the careful code (the frame carries
+  // across phases; both leave the tile in the same canonical shared-memory layout).
   // bitmap of the pass ops whose gate drew an error
-  o << "  if (tid < " << NW << "u) tq_errb[tid] = 0u;\n  __syncthreads();\n";
-  o << "  for (tq_u32 li = tid; li < " << nops << "u; li += " << T << "u)\n"
-    << "    if (codes[4u + GOFF[li]] != 0) atomicOr(&tq_errb[li >> 5], 1u << (li & 31u));\n";
-  o << "  __syncthreads();\n";
-  for (int w = 0; w < NW; ++w) o << "  const tq_u32 eb" << w << " = tq_errb[" << w << "];\n";
-  o << "  tq_u32 fx = 0u, fz = 0u, fk = 0u;\n";
-  emit_phases(fast, true);
+  for (int w = 0; w < NW; ++w) o << "  tq_u32 eb" << w << " = 0u;\n";
+  o << "  if (errs) {\n";
+  o << "    if (tid < " << NW << "u) tq_errb[tid] = 0u;\n    __syncthreads();\n";
+  o << "    for (tq_u32 li = tid; li < " << nops << "u; li += " << T << "u)\n"
+    << "      if (codes[4u + GOFF[li]] != 0) atomicOr(&tq_errb[li >> 5], 1u << (li & 31u));\n";
+  o << "    __syncthreads();\n";
+  for (int w = 0; w < NW; ++w) o << "    eb" << w << " = tq_errb[" << w << "];\n";
   o << "  }\n";
+  o << "  tq_u32 fx = 0u, fz = 0u, fk = 0u;\n";
+  for (int ph = 0; ph < (int)fast.size(); ++ph) {
+    std::vector<uint32_t> pm(NW, 0u);   // error sites of the phase's ops
+    std::function<void(const FOp&)> mark = [&](const FOp& f) {
+      for (const FOp& cf : f.comps) mark(cf);
+      for (const ErrSite& es : f.sites) pm[es.local >> 5] |= 1u << (es.local & 31);
+    };
+    for (int it : fast[ph].items) mark(fops[it]);
+    o << "  if ((fx | fz | fk) == 0u";
+    for (int w = 0; w < NW; ++w)
+      if (pm[w]) o << " && !(eb" << w << " & " << pm[w] << "u)";
+    o << ") {\n";
+    emit_phases(fast, false, ph);
+    o << "  } else {\n";
+    emit_phases(fast, true, ph);
+    o << "  }\n";
+  }
   o << "}\n";
   g_pool = nullptr;
   coefs = pool.vals;
