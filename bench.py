@@ -19,7 +19,7 @@ roofline  gate-pass kernels: algorithmic bytes / CUDA-event time of every distin
           kernel (5 back-to-back launches on its in-tree operands, tqsim_profile_passes),
           weighted by its launches per tree, vs MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline  the oracle (oracle/, numpy, 1 thread) on a bounded sample of the
-          same workload (one top-level subtree), rank 0 only.
+          same workload (the first leaves of its DFS, ~20 s), rank 0 only.
 """
 from __future__ import annotations
 
@@ -112,28 +112,58 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(w, sample_top: int = 1):
-    """The oracle as it stands (numpy, 1 thread) on a bounded sample of the workload."""
+def cpu_baseline(w, budget_s: float = 20.0):
+    """The oracle as it stands (numpy, 1 thread) on a bounded sample of the workload: the
+    oracle's own slice / leaf functions (oracle/tree.py) driven in the same DFS order as
+    oracle.tree.simulate_tree (state reuse), stopped at the first leaf after `budget_s`
+    seconds.  Widths above 22 qubits are not sampled (one oracle slice takes minutes)."""
     from threadpoolctl import threadpool_limits
 
     from oracle import gates as OG
     from oracle.planner import dcp_plan, fixed_plan
-    from oracle.tree import NoiseModel, error_rates, simulate_tree
+    from oracle.statevector import zero_state
+    from oracle.tree import NoiseModel, error_rates, run_slice, sample_leaf
 
+    n = w.circuit.n_qubits
+    if n > 22:
+        return {"value": None, "unit": "shots/s", "cores": 1, "kind": "oracle",
+                "sample": "not sampled: %d qubits (one oracle slice takes minutes on one core)" % n}
     low = OG.lower(w.circuit.gates)
     nm = NoiseModel(w.p1, w.p2, w.readout_p01, w.readout_p10)
     if w.arities:
         plan = fixed_plan(len(low), w.arities)
     else:
-        plan = dcp_plan(error_rates(low, nm), w.shots, w.circuit.n_qubits, w.copy_cost_gates)
+        plan = dcp_plan(error_rates(low, nm), w.shots, n, w.copy_cost_gates)
+    A, B, L = plan.arities, plan.boundaries, len(plan.arities)
+    leaves = 0
+
+    class Done(Exception):
+        pass
+
     with threadpool_limits(1):
         t0 = time.perf_counter()
-        res = simulate_tree(w.circuit.n_qubits, low, plan, nm, w.seed, top_range=(0, sample_top))
+
+        def node(d, j, parent):
+            nonlocal leaves
+            psi = run_slice(parent.copy(), n, low, B[d], B[d + 1], j, w.seed, nm)
+            if d == L - 1:
+                sample_leaf(psi, n, j, w.seed, nm)
+                leaves += 1
+                if time.perf_counter() - t0 > budget_s:
+                    raise Done
+                return
+            for br in range(A[d + 1]):
+                node(d + 1, j * A[d + 1] + br, psi)
+
+        try:
+            for j0 in range(A[0]):
+                node(0, j0, zero_state(n))
+        except Done:
+            pass
         dt = time.perf_counter() - t0
-    n = len(res.leaves)
-    return {"value": n / dt, "unit": "shots/s", "cores": 1, "kind": "oracle",
-            "sample": "%d of %d top-level subtrees (%d leaves) of %s, full tree DFS, %.1f s"
-                      % (sample_top, plan.arities[0], n, w.name, dt)}
+    return {"value": leaves / dt, "unit": "shots/s", "cores": 1, "kind": "oracle",
+            "sample": "first %d leaves (DFS order, state reuse) of the %d-leaf tree of %s, %.1f s"
+                      % (leaves, plan.n_outcomes, w.name, dt)}
 
 
 def run_reference(args, w, rank, world):
@@ -144,7 +174,10 @@ def run_reference(args, w, rank, world):
     vals = []
     cb = None
     for s in range(args.steps):
-        cb = cpu_baseline(w)
+        cb = cpu_baseline(w, budget_s=10.0)
+        if cb["value"] is None:
+            print(json.dumps({"impl": "reference", "unavailable": cb["sample"]}), flush=True)
+            return
         vals.append(cb["value"])
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "shots/s",
