@@ -39,6 +39,9 @@ struct tqsim_handle {
   // with the same workspace / outcome buffers / shard; seed-independent (read from d_seed)
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t capture_stream = nullptr;
+  // the leaf branch of the captured tree (see run_level: pipelined penultimate level)
+  cudaStream_t leaf_stream = nullptr;
+  cudaEvent_t pipe_ev[5] = {};   // level done [2], leaf done [2], join
   std::vector<uint64_t> graph_key;
   tqsim_stats graph_stats{};
   std::vector<uint8_t> h_tables;  // host copy: [two flags | pass index] per lowered gate
@@ -109,6 +112,7 @@ void require_device() {
 struct Layout {
   std::vector<uint64_t> cap;       // states per level batch
   std::vector<uint64_t> off;       // byte offset of level buffer
+  uint64_t off2 = 0;               // second buffer of the penultimate level (pipelined leaf)
   uint64_t runs_off = 0, sums_off = 0, rows_off = 0, total = 0;
   std::vector<uint64_t> lvl_count;      // the shard's instances per level
   std::vector<uint64_t> rows_lvl_off;   // byte offset of each level's noise rows (in the rows region)
@@ -147,6 +151,10 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
     for (size_t d = 0; d < levels; ++d) {
       l.off.push_back(off);
       off = align_up(off + l.cap[d] * S);
+    }
+    if (levels >= 2) {   // double buffer of the penultimate level
+      l.off2 = off;
+      off = align_up(off + l.cap[levels - 2] * S);
     }
     l.runs_off = off;
     off = align_up(off + l.cap.back() * (8ull << (n - RUN_Q)));
@@ -212,6 +220,15 @@ struct Exec {
   Layout L;
   uint32_t* d_out;
   std::vector<uint64_t> lvl_first;   // global id of the shard's first instance per level
+  // Pipelined penultimate level (captured tree only): its batches alternate between two
+  // buffers; each batch's leaf work runs on a second stream, so the FP64-bound leaf passes
+  // of batch k overlap the HBM-bound passes of batch k+1.
+  bool pipe = false;
+  cudaStream_t st2 = nullptr;
+  const cudaEvent_t* ev = nullptr;   // level done [0..1], leaf done [2..3], join [4]
+  uint64_t kD = 0;
+  bool slot_used[2] = {false, false};
+  bool leaf_issued = false;
 };
 
 std::vector<uint64_t> level_firsts(const tqsim_handle* h, uint64_t t0) {
@@ -261,13 +278,15 @@ void dump_if_requested(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, const char
   }
 }
 
-void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_first) {
+void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_first,
+               const char* parent_buf = nullptr) {
   tqsim_handle* h = x.h;
   const int n = h->n_sim;
   const uint32_t levels = (uint32_t)h->plan.arities.size();
   const uint64_t cap = x.L.cap[d];
   char* buf = x.ws + x.L.off[d];
-  const char* pbuf = d > 0 ? x.ws + x.L.off[d - 1] : nullptr;
+  const char* pbuf = parent_buf ? parent_buf : d > 0 ? x.ws + x.L.off[d - 1] : nullptr;
+  const bool piped = x.pipe && d + 2 == levels;
   const auto& passes = h->pp.levels[d];
   const uint32_t slice_begin = (uint32_t)h->plan.bounds[d];
   const uint32_t slice_len = (uint32_t)(h->plan.bounds[d + 1] - slice_begin);
@@ -275,6 +294,12 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   (void)slice_begin;
   for (uint64_t b = i0; b < i1; b += cap) {
     const uint64_t cnt = std::min(cap, i1 - b);
+    int slot = 0;
+    if (piped) {   // this batch's buffer: free once the leaf work of batch k-2 is done
+      slot = (int)(x.kD++ & 1);
+      buf = x.ws + (slot ? x.L.off2 : x.L.off[d]);
+      if (x.slot_used[slot]) ckc(cudaStreamWaitEvent(x.st, x.ev[2 + slot], 0), "pipe wait");
+    }
     // the batch's noise rows (row a3), drawn for the whole shard at the start of the tree
     uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d]) +
                     (b - x.lvl_first[d]) * row_bytes;
@@ -398,6 +423,16 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
                                          (8ull << (x.L.chunk_log2 - RUN_Q)) + (16ull << RUN_Q));
       }
       h->stats.leaves += cnt;
+    } else if (piped) {
+      const uint64_t A = h->plan.arities[d + 1];
+      ckc(cudaEventRecord(x.ev[slot], x.st), "pipe record");
+      ckc(cudaStreamWaitEvent(x.st2, x.ev[slot], 0), "pipe fork");
+      std::swap(x.st, x.st2);
+      run_level(x, d + 1, b * A, (b + cnt) * A, b, buf);
+      std::swap(x.st, x.st2);
+      ckc(cudaEventRecord(x.ev[2 + slot], x.st2), "pipe record");
+      x.slot_used[slot] = true;
+      x.leaf_issued = true;
     } else {
       const uint64_t A = h->plan.arities[d + 1];
       run_level(x, d + 1, b * A, (b + cnt) * A, b);
@@ -431,6 +466,10 @@ void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
   h->stats.kernel_launches++;
   h->stats.noise_launches++;
   run_level(x, 0, t0, t1, 0);
+  if (x.pipe && x.leaf_issued) {   // join the leaf branch
+    ckc(cudaEventRecord(x.ev[4], x.st2), "pipe join record");
+    ckc(cudaStreamWaitEvent(x.st, x.ev[4], 0), "pipe join");
+  }
 }
 
 // per-gate device tables: 2q flag (noise class) and pass index (error bitmask bit)
@@ -511,6 +550,24 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
         ckc(cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking), "capture stream");
       Exec xc = x;
       xc.st = h->capture_stream;
+      static const bool pipe_on = [] {
+        const char* e = std::getenv("TQSIM_PIPE");
+        return !(e && e[0] == '0');
+      }();
+      if (pipe_on && h->plan.arities.size() >= 2) {
+        if (!h->leaf_stream) {
+          // highest priority: as CTAs of the running HBM-bound pass retire, the block
+          // scheduler fills the freed slots with the FP64-bound leaf CTAs (node priorities
+          // kept by the graph: cudaGraphInstantiateFlagUseNodePriority)
+          int lo = 0, hi = 0;
+          ckc(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+          ckc(cudaStreamCreateWithPriority(&h->leaf_stream, cudaStreamNonBlocking, hi), "leaf stream");
+          for (cudaEvent_t& e : h->pipe_ev) ckc(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "pipe event");
+        }
+        xc.pipe = true;
+        xc.st2 = h->leaf_stream;
+        xc.ev = h->pipe_ev;
+      }
       ckc(cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
       cudaGraph_t g = nullptr;
       try {
@@ -521,7 +578,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
         throw;
       }
       ckc(cudaStreamEndCapture(h->capture_stream, &g), "end capture");
-      const cudaError_t e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+      const cudaError_t e = cudaGraphInstantiate(&h->graph_exec, g, cudaGraphInstantiateFlagUseNodePriority);
       cudaGraphDestroy(g);
       ckc(e, "graph instantiate");
       h->graph_key = key;
@@ -752,6 +809,9 @@ void tqsim_destroy(tqsim_handle* h) {
   if (h->d_seed) cudaFree(h->d_seed);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
+  if (h->leaf_stream) cudaStreamDestroy(h->leaf_stream);
+  for (cudaEvent_t e : h->pipe_ev)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   delete h;
 }
