@@ -348,6 +348,25 @@ M4 dagger(const M4& m) {
 
 bool near(const cplx& a, const cplx& b) { return std::abs(a - b) < 1e-13; }
 
+// exact 0 / +-1 for components within rounding of them (phases composed at generation time)
+cplx snap(cplx v) {
+  auto s1 = [](double x) {
+    for (double t : {0.0, 1.0, -1.0})
+      if (std::abs(x - t) < 1e-14) return t;
+    return x;
+  };
+  return cplx(s1(v.real()), s1(v.imag()));
+}
+
+// real 2x2 whose entries are +-c (H, and H up to signs)
+bool hadamard_like(const cplx* m) {
+  const double c = std::abs(m[0].real());
+  if (c == 0.0) return false;
+  for (int e = 0; e < 4; ++e)
+    if (m[e].imag() != 0.0 || std::abs(m[e].real()) != c) return false;
+  return true;
+}
+
 // E' = R E R^dagger (monomial) -> Pauli-type i^k X^x Z^z or generic D X^x, local masks
 ErrEff decompose(const M4& M) {
   ErrEff e;
@@ -1301,6 +1320,37 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           std::swap(fb[ba].var[0], fb[ba].var[1]);
           std::swap(fb[ba].one[0], fb[ba].one[1]);
           permute([&](int k) { return k ^ (1 << ba); });
+        } else if (f.kind == FOp::GEN && hadamard_like(f.m)) {
+          // c * (+-1 entries), e.g. H: a butterfly of adds.  The pair's pending phases
+          // stay pending when equal (the gate commutes with a common factor), else the
+          // second input is multiplied by the ratio; c and the signs join the pending
+          // phases (applied once at the phase end, or folded into a later gate).
+          const int ba = rbit(f.qa);
+          fb_flush(ba, fb_gen);
+          std::ostringstream oo;
+          pool.begin_op();
+          const double c = std::abs(f.m[0].real());
+          double sg[4];
+          for (int e = 0; e < 4; ++e) sg[e] = f.m[e].real() > 0 ? 1.0 : -1.0;
+          for (int k = 0; k < 16; ++k) {
+            if (k >> ba & 1) continue;
+            const int k1 = k | 1 << ba;
+            const std::string va = g.r(k), vb = g.r(k1);
+            const cplx p = dph[k];
+            const cplx q = snap(dph[k1] / p);
+            if (q != cplx(1.0, 0.0))   // (zero parts skipped: a factor +-i is a swap with a sign)
+              oo << "      { const tq_d2 y = " << vb << "; " << vb << ".x = " << lin(q.real(), q.imag(), "y", 0, 0, "y", false)
+                 << "; " << vb << ".y = " << lin(q.real(), q.imag(), "y", 0, 0, "y", true) << "; }\n";
+            // out_r = s_r0 * (x + (s_r1 / s_r0) y)
+            const char* op0 = sg[1] * sg[0] > 0 ? " + " : " - ";
+            const char* op1 = sg[3] * sg[2] > 0 ? " + " : " - ";
+            oo << "      { const tq_d2 x = " << va << ", y = " << vb << "; " << va << ".x = x.x" << op0 << "y.x; " << va
+               << ".y = x.y" << op0 << "y.y; " << vb << ".x = x.x" << op1 << "y.x; " << vb << ".y = x.y" << op1
+               << "y.y; }\n";
+            dph[k] = p * (sg[0] * c);
+            dph[k1] = p * (sg[2] * c);
+          }
+          o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
         } else if (f.kind == FOp::GEN) {
           const int ba = rbit(f.qa);
           fb_flush(ba, fb_gen);
@@ -1694,10 +1744,14 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     }
     {   // flush the pending phases (run-time factors, then compile-time)
       // product tree T[idx] = gph * prod_{b in L} F_b[bit of idx], idx over the pending bits L
+      // The leaf variants 1/2 feed only |a|^2: in their last phase the pending run-time
+      // factors (diagonal entries: unit modulus) are dropped and the compile-time ones
+      // reduce to their modulus.
+      const bool mag_only = last && variant != 0;
       std::vector<int> L;
-      for (int b = 0; b < RBITS; ++b)
+      for (int b = 0; b < RBITS && !mag_only; ++b)
         if (fb[b].on) L.push_back(b);
-      std::vector<std::string> Tn(1, gph_on ? std::string("gph") : std::string());
+      std::vector<std::string> Tn(1, gph_on && !mag_only ? std::string("gph") : std::string());
       int tcount = 0;
       for (size_t li = 0; li < L.size(); ++li) {
         std::vector<std::string> nt(Tn.size() * 2);
@@ -1728,11 +1782,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       std::ostringstream oo;
       pool.begin_op();
       for (int k = 0; k < 16; ++k) {
-        if (dph[k] == cplx(1.0, 0.0)) continue;
+        const cplx d = mag_only ? snap(cplx(std::abs(dph[k]), 0.0)) : dph[k];
+        if (d == cplx(1.0, 0.0)) continue;
         const std::string v = g.r(k);
         oo << "      { const tq_d2 x = " << v << "; " << v << ".x = "
-           << lin(dph[k].real(), dph[k].imag(), "x", 0, 0, "x", false) << "; " << v << ".y = "
-           << lin(dph[k].real(), dph[k].imag(), "x", 0, 0, "x", true) << "; }\n";
+           << lin(d.real(), d.imag(), "x", 0, 0, "x", false) << "; " << v << ".y = "
+           << lin(d.real(), d.imag(), "x", 0, 0, "x", true) << "; }\n";
       }
       o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
     }
