@@ -358,6 +358,30 @@ cplx snap(cplx v) {
   return cplx(s1(v.real()), s1(v.imag()));
 }
 
+// ZYZ form of a 2x2 unitary: m = e^{ia} diag(1, e^{if}) [[c, -s], [s, c]] diag(1, e^{il}),
+// c, s >= 0.  ea = e^{ia}, eaf = e^{i(a+f)}, el = e^{il}.  False when m is not of this
+// form to 1e-12 (not unitary up to a phase) or is diagonal / anti-diagonal-free.
+struct Zyz {
+  double c = 0, s = 0;
+  cplx ea, eaf, el;
+};
+bool zyz_of(const cplx* m, Zyz& z) {
+  z.c = std::abs(m[0]);
+  z.s = std::abs(m[2]);
+  if (z.s < 1e-12 || std::abs(z.c * z.c + z.s * z.s - 1.0) > 1e-12) return false;
+  z.eaf = m[2] / z.s;
+  if (z.c > 1e-12) {
+    z.ea = m[0] / z.c;
+  } else {
+    z.ea = cplx(1.0, 0.0);
+    z.c = 0.0;
+  }
+  z.el = (-m[1] / z.s) / z.ea;
+  const cplx m11 = z.eaf * z.el * z.c;
+  if (std::abs(m11 - m[3]) > 1e-12 || std::abs(std::abs(z.el) - 1.0) > 1e-12) return false;
+  return true;
+}
+
 // real 2x2 whose entries are +-c (H, and H up to signs)
 bool hadamard_like(const cplx* m) {
   const double c = std::abs(m[0].real());
@@ -1309,6 +1333,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       // Diagonals on (thread bit, register bit b) accumulate into per-thread factors
       // F_b[0], F_b[1] (one per value of logical register bit b), applied once -- at
       // the phase end through a product tree, or before an op that mixes bit b.
+      Zyz zyz;
       for (int it : specs[ph].items) {
         const FOp& f = fops[it];
         if (f.kind == FOp::CX) {
@@ -1349,6 +1374,39 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
                << "y.y; }\n";
             dph[k] = p * (sg[0] * c);
             dph[k1] = p * (sg[2] * c);
+          }
+          o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+        } else if (f.kind == FOp::GEN && zyz_of(f.m, zyz)) {
+          // U = e^{ia} diag(1, e^{if}) [[c, -s], [s, c]] diag(1, e^{il}): the right phase joins
+          // the second input's pending phase (a ratio multiply when the pair's phases then
+          // differ), the left phases and the larger of c, s join the outputs' pending phases,
+          // and the core is [[1, -t], [t, 1]] or [[u, -1], [1, u]] (|t|, |u| <= 1): one FMA per
+          // output component instead of two to four (RX, RY, U3 cores).
+          const int ba = rbit(f.qa);
+          fb_flush(ba, fb_gen);
+          std::ostringstream oo;
+          pool.begin_op();
+          const bool by_c = std::abs(zyz.c) >= std::abs(zyz.s);
+          const double r = by_c ? zyz.s / zyz.c : zyz.c / zyz.s, sc = by_c ? zyz.c : zyz.s;
+          for (int k = 0; k < 16; ++k) {
+            if (k >> ba & 1) continue;
+            const int k1 = k | 1 << ba;
+            const std::string va = g.r(k), vb = g.r(k1);
+            const cplx p = dph[k];
+            const cplx q = snap(zyz.el * dph[k1] / p);
+            if (q != cplx(1.0, 0.0))
+              oo << "      { const tq_d2 y = " << vb << "; " << vb << ".x = " << lin(q.real(), q.imag(), "y", 0, 0, "y", false)
+                 << "; " << vb << ".y = " << lin(q.real(), q.imag(), "y", 0, 0, "y", true) << "; }\n";
+            const std::string R = g_pool->ref(r), NR = g_pool->ref(-r);
+            oo << "      { const tq_d2 x = " << va << ", y = " << vb << ";\n";
+            if (by_c)   // (x - t y, t x + y)
+              oo << "        " << va << ".x = fma(" << NR << ", y.x, x.x); " << va << ".y = fma(" << NR << ", y.y, x.y); "
+                 << vb << ".x = fma(" << R << ", x.x, y.x); " << vb << ".y = fma(" << R << ", x.y, y.y); }\n";
+            else        // (u x - y, x + u y)
+              oo << "        " << va << ".x = fma(" << R << ", x.x, -y.x); " << va << ".y = fma(" << R << ", x.y, -y.y); "
+                 << vb << ".x = fma(" << R << ", y.x, x.x); " << vb << ".y = fma(" << R << ", y.y, x.y); }\n";
+            dph[k] = snap(p * zyz.ea * sc);
+            dph[k1] = snap(p * zyz.eaf * sc);
           }
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
         } else if (f.kind == FOp::GEN) {
