@@ -310,7 +310,7 @@ def main():
             note = ("tqsim_run per step: host circuit in (validated, hashed; the prepared plan and its "
                     "specialized kernels are reused from the library's plan cache after the first call), "
                     "h2d = per-gate noise-class and pass tables (2 B / lowered gate) + kernel parameters, "
-                    "d2h = leaf outcomes (uint32), host histogram")
+                    "d2h = leaf outcomes (uint32) into page-locked memory, host histogram (C; returned as arrays, the dict view of Result.counts is built on first access)")
             h2d = 2 * n_low + 96 * launches_per_step
         else:
             note = ("distributed.ShardRunner per step on every rank: the shard (replayed CUDA graph), "

@@ -45,6 +45,7 @@ struct tqsim_handle {
   std::vector<uint64_t> graph_key;
   tqsim_stats graph_stats{};
   std::vector<uint8_t> h_tables;  // host copy: [two flags | pass index] per lowered gate
+  uint8_t* h_tables_pinned = nullptr;   // the same bytes in page-locked memory (async H2D)
   tqsim_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -187,6 +188,8 @@ std::mutex g_arena_mu;
 void* g_arena = nullptr;
 size_t g_arena_size = 0;
 cudaStream_t g_stream = nullptr;   // tqsim_run's stream (created once)
+void* g_pinned = nullptr;          // tqsim_run's page-locked outcome buffer
+size_t g_pinned_size = 0;
 
 // Prepared-handle cache of tqsim_run (the plan cache of FFT-style libraries): lowering,
 // DCP, pass plan and the run-time specialized kernels of a (circuit, noise, shots,
@@ -475,8 +478,16 @@ void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
 // per-gate device tables: 2q flag (noise class) and pass index (error bitmask bit)
 void upload_gate_tables(tqsim_handle* h, cudaStream_t st) {
   const size_t G = h->h_tables.size() / 2;
-  ckc(cudaMemcpyAsync(h->d_two, h->h_tables.data(), G, cudaMemcpyHostToDevice, st), "upload two");
-  ckc(cudaMemcpyAsync(h->d_pass_of, h->h_tables.data() + G, G, cudaMemcpyHostToDevice, st), "upload pass_of");
+  const uint8_t* src = h->h_tables.data();
+  if (st) {   // page-locked staging (tqsim_run: every call uploads its tables)
+    if (!h->h_tables_pinned) {
+      ckc(cudaMallocHost(reinterpret_cast<void**>(&h->h_tables_pinned), std::max<size_t>(2 * G, 1)), "cudaMallocHost");
+      std::memcpy(h->h_tables_pinned, src, 2 * G);
+    }
+    src = h->h_tables_pinned;
+  }
+  ckc(cudaMemcpyAsync(h->d_two, src, G, cudaMemcpyHostToDevice, st), "upload two");
+  ckc(cudaMemcpyAsync(h->d_pass_of, src + G, G, cudaMemcpyHostToDevice, st), "upload pass_of");
 }
 
 tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,
@@ -621,15 +632,26 @@ void build_result(tqsim_handle* h, const std::vector<uint32_t>& outs, double wal
   r->plan = h->cplan;
   r->stats = h->stats;
   r->wall_s = wall;
-  std::vector<uint32_t> sorted = outs;
-  std::sort(sorted.begin(), sorted.end());
   std::vector<uint64_t> bits, counts;
-  for (size_t i = 0; i < sorted.size();) {
-    size_t j = i;
-    while (j < sorted.size() && sorted[j] == sorted[i]) ++j;
-    bits.push_back(sorted[i]);
-    counts.push_back(j - i);
-    i = j;
+  if (h->n_user <= 24 && (1ull << h->n_user) <= 8 * std::max<size_t>(outs.size(), 1)) {
+    // counting histogram over the 2^n outcomes (ascending bitstrings, as the sort gives)
+    std::vector<uint32_t> hist(1ull << h->n_user, 0u);
+    for (uint32_t v : outs) ++hist[v];
+    for (size_t v = 0; v < hist.size(); ++v)
+      if (hist[v]) {
+        bits.push_back(v);
+        counts.push_back(hist[v]);
+      }
+  } else {
+    std::vector<uint32_t> sorted = outs;
+    std::sort(sorted.begin(), sorted.end());
+    for (size_t i = 0; i < sorted.size();) {
+      size_t j = i;
+      while (j < sorted.size() && sorted[j] == sorted[i]) ++j;
+      bits.push_back(sorted[i]);
+      counts.push_back(j - i);
+      i = j;
+    }
   }
   r->n_distinct = bits.size();
   r->bitstrings = static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, bits.size()) * 8));
@@ -807,6 +829,7 @@ void tqsim_destroy(tqsim_handle* h) {
   if (h->d_two) cudaFree(h->d_two);
   if (h->d_pass_of) cudaFree(h->d_pass_of);
   if (h->d_seed) cudaFree(h->d_seed);
+  if (h->h_tables_pinned) cudaFreeHost(h->h_tables_pinned);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   if (h->leaf_stream) cudaStreamDestroy(h->leaf_stream);
@@ -970,9 +993,17 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, u
       uint32_t* d_out = reinterpret_cast<uint32_t*>(base + out_off);
       ckc(cudaMemsetAsync(d_out, 0, nout * 4, st), "memset outcomes");
       execute(h, seed, 0, 1, st, base, ws, d_out);
-      std::vector<uint32_t> outs(nout);
-      ckc(cudaMemcpyAsync(outs.data(), d_out, nout * 4, cudaMemcpyDeviceToHost, st), "D2H outcomes");
+      if (g_pinned_size < nout * 4) {   // page-locked landing buffer of the outcomes
+        if (g_pinned) cudaFreeHost(g_pinned);
+        g_pinned = nullptr;
+        g_pinned_size = 0;
+        ckc(cudaMallocHost(&g_pinned, nout * 4), "cudaMallocHost outcomes");
+        g_pinned_size = nout * 4;
+      }
+      ckc(cudaMemcpyAsync(g_pinned, d_out, nout * 4, cudaMemcpyDeviceToHost, st), "D2H outcomes");
       ckc(cudaStreamSynchronize(st), "stream sync");
+      const uint32_t* po = static_cast<const uint32_t*>(g_pinned);
+      std::vector<uint32_t> outs(po, po + nout);
       h->debug = nullptr;
       const double wall =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();

@@ -9,7 +9,6 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -370,14 +369,26 @@ def tqsim_create(*args, **kw) -> Handle:
     return Handle(*args, **kw)
 
 
-@dataclass
 class Result:
-    plan: tqsim_plan
-    counts: Dict[int, int]
-    leaf_outcomes: np.ndarray
-    wall_s: float
-    stats: tqsim_stats
-    dumps: Optional[np.ndarray] = None
+    """A run's outcome: the plan, the histogram (`bitstrings`, `counts_array`, ascending;
+    `counts` is the same as a dict, built on first access), the leaf-ordered outcomes,
+    wall time, run statistics and (debug) dumped states."""
+
+    def __init__(self, plan, bitstrings, counts_array, leaf_outcomes, wall_s, stats, dumps=None):
+        self.plan = plan
+        self.bitstrings = bitstrings
+        self.counts_array = counts_array
+        self.leaf_outcomes = leaf_outcomes
+        self.wall_s = wall_s
+        self.stats = stats
+        self.dumps = dumps
+        self._counts = None
+
+    @property
+    def counts(self) -> Dict[int, int]:
+        if self._counts is None:
+            self._counts = dict(zip(self.bitstrings.tolist(), self.counts_array.tolist()))
+        return self._counts
 
 
 def tqsim_run_ex(n_qubits, gates, noise, n_shots, arities=None, seed=0, options=None,
@@ -403,9 +414,8 @@ def tqsim_run_ex(n_qubits, gates, noise, n_shots, arities=None, seed=0, options=
         n = res.plan.n_outcomes
         leaf = np.ctypeslib.as_array(res.leaf_outcomes, shape=(n,)).copy()
         nd = res.n_distinct
-        bits = np.ctypeslib.as_array(res.bitstrings, shape=(max(nd, 1),))[:nd]
-        cnts = np.ctypeslib.as_array(res.counts, shape=(max(nd, 1),))[:nd]
-        counts = {int(b): int(c) for b, c in zip(bits, cnts)}
+        bits = np.ctypeslib.as_array(res.bitstrings, shape=(max(nd, 1),))[:nd].copy()
+        cnts = np.ctypeslib.as_array(res.counts, shape=(max(nd, 1),))[:nd].copy()
         plan = tqsim_plan.from_buffer_copy(res.plan)
         stats = tqsim_stats.from_buffer_copy(res.stats)
         wall = float(res.wall_s)
@@ -414,7 +424,7 @@ def tqsim_run_ex(n_qubits, gates, noise, n_shots, arities=None, seed=0, options=
     states = None
     if host is not None:
         states = host[..., 0] + 1j * host[..., 1]
-    return Result(plan, counts, leaf, wall, stats, states)
+    return Result(plan, bits, cnts, leaf, wall, stats, states)
 
 
 def tqsim_run(n_qubits, gates, noise, n_shots, arities=None, seed=0) -> Result:
@@ -430,10 +440,9 @@ def tqsim_run(n_qubits, gates, noise, n_shots, arities=None, seed=0) -> Result:
         n = res.plan.n_outcomes
         leaf = np.ctypeslib.as_array(res.leaf_outcomes, shape=(n,)).copy()
         nd = res.n_distinct
-        bits = np.ctypeslib.as_array(res.bitstrings, shape=(max(nd, 1),))[:nd]
-        cnts = np.ctypeslib.as_array(res.counts, shape=(max(nd, 1),))[:nd]
-        out = Result(tqsim_plan.from_buffer_copy(res.plan),
-                     dict(zip(bits.tolist(), cnts.tolist())), leaf, float(res.wall_s),
+        bits = np.ctypeslib.as_array(res.bitstrings, shape=(max(nd, 1),))[:nd].copy()
+        cnts = np.ctypeslib.as_array(res.counts, shape=(max(nd, 1),))[:nd].copy()
+        out = Result(tqsim_plan.from_buffer_copy(res.plan), bits, cnts, leaf, float(res.wall_s),
                      tqsim_stats.from_buffer_copy(res.stats))
     finally:
         lib().tqsim_result_free(r)
