@@ -50,6 +50,7 @@ struct TqJitArgs {
   const unsigned char* rows; tq_u32 row_bytes;   // noise rows of the batch (launch_noise_rows)
   // leaf measurement without the state store (variants 1/2, see gen_pass)
   const tq_u32* tiles; const tq_u32* runsel; tq_d2* scratch; tq_u32* xlout;
+  tq_u32 dedup;   // leaf level without stored states: skip error-free duplicate siblings
 };
 // 16-byte global load the compiler may not sink below the error-branch: the tile loads
 // are issued before the (dependent) noise-row mask load is waited on
@@ -87,6 +88,7 @@ struct HostJitArgs {   // mirrors TqJitArgs
   const uint32_t* runsel;
   void* scratch;
   uint32_t* xlout;
+  uint32_t dedup;
 };
 
 std::string hexd(double v) {
@@ -1172,6 +1174,20 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const tq_u32 s = (tq_u32)bid;\n  const tq_u64 t = a.tiles[s];\n  const tq_u32 rsel = a.runsel[s];\n";
   else
     o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
+  if (variant != 2) {
+    // Leaf level, states not stored: a child with no error in the whole slice has the
+    // same state as every error-free sibling (same parent, same gates), so only the first
+    // error-free sibling of the batch computes it; the sampler reads its run sums
+    // (tq_dedup_rep, kernels.cu).  The skipped child's store-address XOR is 0.
+    o << "  if (a.dedup && *reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)s * a.row_bytes) == 0u) {\n"
+      << "    const tq_u64 j = a.child_first + s, g0 = j - j % a.arity;\n"
+      << "    for (tq_u32 q = g0 > a.child_first ? (tq_u32)(g0 - a.child_first) : 0u; q < s; ++q)\n"
+      << "      if (*reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)q * a.row_bytes) == 0u) {\n"
+      << "        if (t == 0 && tid == 0u && a.xlout) a.xlout[s] = 0u;\n"
+      << "        return;\n"
+      << "      }\n"
+      << "  }\n";
+  }
   o << "  tq_u32 gtile = 0u, gtile_st = 0u;\n";   // the tile's out-of-tile index bits: physical / stored
   for (int i = 0; i < pd.n_out; ++i)
     o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << "; gtile_st ^= (0u - (tq_u32)((t >> "
@@ -1180,7 +1196,17 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   if (mode == 1)
     o << "  const tq_d2* __restrict__ src = a.src + ((((tq_u64)a.child_first + s) / a.arity - a.parent_first) << "
       << n << ");\n";
-  else if (mode == 2)
+  else if (mode == 2 && variant == 2) {
+    // recompute of a leaf whose state was not computed (an error-free duplicate): its
+    // representative's slot holds the same state
+    o << "  tq_u32 sr = s;\n"
+      << "  if (a.dedup && *reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)s * a.row_bytes) == 0u) {\n"
+      << "    const tq_u64 j = a.child_first + s, g0 = j - j % a.arity;\n"
+      << "    for (tq_u32 q = g0 > a.child_first ? (tq_u32)(g0 - a.child_first) : 0u; q < s; ++q)\n"
+      << "      if (*reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)q * a.row_bytes) == 0u) { sr = q; break; }\n"
+      << "  }\n"
+      << "  const tq_d2* src = a.dst + ((tq_u64)sr << " << n << ");\n";
+  } else if (mode == 2)
     o << "  const tq_d2* src = dst;\n";
   o << "  tq_d2 r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, r10, r11, r12, r13, r14, r15;\n";
 
@@ -2211,7 +2237,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
                 L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes,
-                L.tiles, L.runsel, L.scratch, L.xlout};
+                L.tiles, L.runsel, L.scratch, L.xlout, L.dedup};
   const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute;
   if (!kern) return (int)cudaErrorInvalidDeviceFunction;
   const uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;

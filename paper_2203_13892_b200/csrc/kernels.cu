@@ -29,7 +29,19 @@ struct SelectOut {
   const uint32_t* xl;         // the leaf pass's store-address XOR per leaf
   uint32_t n_out;
   uint32_t out_row[32];       // out-of-tile qubit i = parity(out_row[i] & stored address)
+  const uint8_t* rows;        // dedup: the batch's noise rows (error mask = first u32)
+  uint32_t row_bytes, arity, dedup;
 };
+
+// The leaf whose run sums leaf s reads: itself, or -- no error in its slice -- the first
+// error-free sibling in the batch (the gate passes computed only that one; same state).
+__device__ __forceinline__ uint32_t tq_dedup_rep(const SelectOut& so, uint64_t leaf_first, uint32_t s) {
+  if (!so.dedup || *reinterpret_cast<const uint32_t*>(so.rows + (uint64_t)s * so.row_bytes) != 0u) return s;
+  const uint64_t j = leaf_first + s, g0 = j - j % so.arity;
+  for (uint32_t q = g0 > leaf_first ? (uint32_t)(g0 - leaf_first) : 0u; q < s; ++q)
+    if (*reinterpret_cast<const uint32_t*>(so.rows + (uint64_t)q * so.row_bytes) == 0u) return q;
+  return s;
+}
 
 __device__ __forceinline__ uint32_t tile_of_run(uint64_t run, uint32_t xl, const SelectOut& so) {
   const uint64_t a = (run << RUN_Q) ^ (uint64_t)xl;   // source (physical) index, logical bits
@@ -88,10 +100,13 @@ __device__ __forceinline__ int block_first(bool pred, int* sh) {
 // chunk = 2^chunk_log2 amplitudes = 2^(chunk_log2 - RUN_Q) runs.
 __global__ void __launch_bounds__(MT) chunk_sums_kernel(const double* __restrict__ runs, uint32_t n,
                                                         uint32_t chunk_log2,
-                                                        double* __restrict__ sums) {
+                                                        double* __restrict__ sums, uint64_t leaf_first,
+                                                        const __grid_constant__ SelectOut so) {
   __shared__ double red[MT / 32];
   const uint32_t rpc = 1u << (chunk_log2 - RUN_Q);   // runs per chunk
   const uint64_t bid = blockIdx.x;                   // = state * n_chunks + chunk
+  const uint32_t st = (uint32_t)(bid >> (n - chunk_log2));
+  if (tq_dedup_rep(so, leaf_first, st) != st) return;   // a duplicate: its representative's sums
   const double* p = runs + bid * rpc;
   double acc = 0.0;
   for (uint32_t i = threadIdx.x; i < rpc; i += MT) acc += p[i];
@@ -174,7 +189,8 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
   const uint64_t leaf = leaf_first + s;
   const uint64_t nc = 1ull << (n - chunk_log2);
   const uint32_t rpc = 1u << (chunk_log2 - RUN_Q);
-  const double* cs = sums + (uint64_t)s * nc;
+  const uint32_t sr = tq_dedup_rep(so, leaf_first, s);   // whose run / chunk sums to read
+  const double* cs = sums + (uint64_t)sr * nc;
   const double u = tq_measure_uniform(leaf, seed);
 
   // total = sum of chunk sums (block reduction in a fixed order)
@@ -187,7 +203,7 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
   // level 1: chunk;  level 2: 8-amplitude run inside the chunk;  level 3: amplitude
   double before1 = 0.0, before2 = 0.0;
   const uint64_t chunk = block_search(cs, nc, target, &before1, wsum, &first_sh, &pick_sh, &before_sh);
-  const double* rs = runs + ((uint64_t)s << (n - RUN_Q)) + chunk * rpc;
+  const double* rs = runs + ((uint64_t)sr << (n - RUN_Q)) + chunk * rpc;
   const uint64_t run = block_search(rs, rpc, target - before1, &before2, wsum, &first_sh, &pick_sh,
                                     &before_sh);
   if (threadIdx.x == 0 && so.runsel) {   // select phase only (the leaf state was not stored)
@@ -262,7 +278,7 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
   const uint64_t leaf = leaf_first + s;
   const uint32_t R = 1u << (n - RUN_Q);
   const uint32_t seg = (R + W - 1) / W;
-  const double* rs = runs + ((uint64_t)s << (n - RUN_Q));
+  const double* rs = runs + ((uint64_t)tq_dedup_rep(so, leaf_first, s) << (n - RUN_Q));
   const uint32_t s0 = w * seg, s1 = min(R, s0 + seg);
   double part = 0.0;
   for (uint32_t i = s0 + lane; i < s1; i += 32u) part += rs[i];
@@ -476,12 +492,13 @@ int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t s
   return (int)cudaGetLastError();
 }
 
+static dev::SelectOut select_out(const LeafSelect* sel);
 int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
-                      double* sums, void* stream) {
+                      double* sums, void* stream, const LeafSelect* sel, uint64_t leaf_first) {
   const uint64_t grid = (uint64_t)batch << (n_sim - chunk_log2);
   if (grid == 0) return 0;
   dev::chunk_sums_kernel<<<(unsigned)grid, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
-      runsums, (uint32_t)n_sim, (uint32_t)chunk_log2, sums);
+      runsums, (uint32_t)n_sim, (uint32_t)chunk_log2, sums, leaf_first, select_out(sel));
   return (int)cudaGetLastError();
 }
 
@@ -494,6 +511,10 @@ static dev::SelectOut select_out(const LeafSelect* sel) {
   so.xl = sel->xl;
   so.n_out = sel->n_out;
   for (uint32_t i = 0; i < sel->n_out && i < 32; ++i) so.out_row[i] = sel->out_row[i];
+  so.rows = sel->rows;
+  so.row_bytes = sel->row_bytes;
+  so.arity = sel->arity ? sel->arity : 1u;
+  so.dedup = sel->dedup;
   return so;
 }
 

@@ -335,6 +335,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       const bool runsums_only = nostore && passes[p].leaf_sums;
       pl.variant = runsums_only ? 1u : 0u;
       pl.xlout = xlv;
+      pl.dedup = nostore ? 1u : 0u;   // leaf level (nostore implies leaf): error-free siblings once
       mark(x, 0);
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
       mark(x, 0);
@@ -368,6 +369,10 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       ls.tile = tiles;
       ls.xl = xlv;
       ls.n_out = (uint32_t)jp.out_row.size();
+      ls.rows = rows;
+      ls.row_bytes = row_bytes;
+      ls.arity = h->plan.arities[d];
+      ls.dedup = 1;
       for (size_t i = 0; i < jp.out_row.size() && i < 32; ++i) ls.out_row[i] = jp.out_row[i];
       mark(x, 1);
       if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {
@@ -378,7 +383,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
         h->stats.measure_launches += 1;
         h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8;
       } else {
-        ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
+        ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st, &ls, b), "chunk sums launch");
         ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, h->d_seed,
                          h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st, &ls),
            "sample select launch");
@@ -886,6 +891,30 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
       // the level's first batch's noise rows (drawn by the run above)
       uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d]);
       (void)slice_begin;
+      // leaf level: as in the tree, error-free duplicate siblings are skipped; count the
+      // computed children (and their distinct parents) for the algorithmic bytes
+      const bool leaf = d + 1 == h->pp.levels.size() && !(h->debug && h->debug->n_dumps);
+      uint64_t comp = cnt, comp_par = 0;
+      {
+        std::vector<uint8_t> hr(cnt * row_bytes);
+        ckc(cudaMemcpy(hr.data(), rows, hr.size(), cudaMemcpyDeviceToHost), "rows D2H");
+        auto em = [&](uint64_t q) { uint32_t v; std::memcpy(&v, &hr[q * row_bytes], 4); return v; };
+        const uint64_t A = h->plan.arities[d];
+        uint64_t last_par = ~0ull;
+        comp = 0;
+        for (uint64_t q = 0; q < cnt; ++q) {
+          bool dup = false;
+          if (leaf && em(q) == 0) {
+            const uint64_t j = first + q, g0 = j - j % A;
+            for (uint64_t r = g0 > first ? g0 - first : 0; r < q && !dup; ++r) dup = em(r) == 0;
+          }
+          if (dup) continue;
+          ++comp;
+          const uint64_t par = (first + q) / A;
+          if (par != last_par) ++comp_par;
+          last_par = par;
+        }
+      }
       for (size_t p = 0; p < h->pp.levels[d].size(); ++p) {
         PassLaunch pl{};
         pl.src_mode = p > 0 ? 2u : (d == 0 ? 0u : 1u);
@@ -905,6 +934,7 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
         // as in the tree: the leaf's last pass stores run sums only
         pl.variant = pd.leaf_sums ? 1u : 0u;
         pl.xlout = reinterpret_cast<uint32_t*>(x.ws + x.L.sel_off + 2 * align_up(4 * x.L.cap.back()));
+        pl.dedup = leaf ? 1u : 0u;
         ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");   // warm
         ckc(cudaEventRecord(e0, st), "record");
         for (uint32_t i = 0; i < reps; ++i) ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");
@@ -912,13 +942,10 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
         ckc(cudaEventSynchronize(e1), "sync");
         float ms = 0.f;
         ckc(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
-        const uint64_t amps = cnt << n;
+        const uint64_t amps = comp << n;   // computed children only (leaf dedup)
         double bytes = pl.variant == 1 ? (double)amps : (double)amps * 16;
         if (pl.src_mode == 2) bytes += (double)amps * 16;
-        else if (pl.src_mode == 1) {
-          const uint64_t A = pl.arity, parents = (first + cnt - 1) / A - first / A + 1;
-          bytes += (double)(parents << n) * 16;
-        }
+        else if (pl.src_mode == 1) bytes += (double)(comp_par << n) * 16;
         if (out && k < cap) {
           tqsim_pass_timing& o = out[k];
           o.level = (uint32_t)d;

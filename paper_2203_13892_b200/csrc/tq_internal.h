@@ -125,6 +125,7 @@ struct PassLaunch {
   const uint32_t* runsel;       // variant 2: selected run per leaf
   void* scratch;                // variant 2: 8 amplitudes per leaf (double2)
   uint32_t* xlout;              // variant 1: store-address XOR per leaf
+  uint32_t dedup;               // leaf level, no state store: skip error-free duplicate siblings
 };
 
 // Noise rows of one level batch (row a3): per instance a row of row_bytes bytes,
@@ -151,8 +152,9 @@ int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const 
                           uint64_t total_instances, const uint64_t* d_seed, double p1, double p2,
                           uint8_t* d_rows, void* stream);
 
+struct LeafSelect;
 int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chunk_log2,
-                      double* sums, void* stream);
+                      double* sums, void* stream, const LeafSelect* sel = nullptr, uint64_t leaf_first = 0);
 // leaf sampling without a stored leaf state (select -> recompute one tile -> finish)
 struct LeafSelect {
   uint32_t* runsel;
@@ -161,6 +163,9 @@ struct LeafSelect {
   const uint32_t* xl;
   uint32_t n_out;
   uint32_t out_row[32];      // out-of-tile qubit i = parity(out_row[i] & stored address)
+  // duplicate error-free siblings (see the gate passes): read the representative's sums
+  const uint8_t* rows = nullptr;
+  uint32_t row_bytes = 0, arity = 1, dedup = 0;
 };
 int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
                          int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,

@@ -359,3 +359,29 @@ def test_store_map_cx_ladders(tile, p, ar):
     low = OG.lower(gates)
     ref = simulate_tree(n, low, oracle_plan_of(res.plan), nm, 11 + tile)
     assert_leaves_match(res.leaf_outcomes, ref.leaves)
+
+
+@pytest.mark.parametrize("n,ar,blog,tile", [(19, [2, 3, 4], 0, 0), (12, [3, 5, 3], 15, 6),
+                                            (16, [2, 7], 19, 0), (14, [4, 4], 0, 7)])
+def test_leaf_dedup_equals_stored_path(n, ar, blog, tile):
+    """Error-free sibling leaves share one computed state (only the first error-free
+    sibling of a batch runs the leaf passes; the sampler reads its run sums): outcomes
+    equal the stored-state path bit for bit, through the chunk-sum sampler (n = 19) and
+    with sibling groups cut by batch boundaries (batch of 2^blog amplitudes, arity 3 / 7),
+    and with several leaf passes (small tiles: the recompute reads the representative's
+    in-place slot)."""
+    rng = np.random.default_rng(n + len(ar))
+    gates = random_circuit(n, 60, rng)
+    noise = T.noise_arg(0.003, 0.01, 0.02, 0.03)   # most leaves error-free: many duplicates
+    shots = int(np.prod(ar))
+    opts = T.default_options(batch_log2_amps=blog, tile_qubits=tile)
+    recs = T.tqsim_describe_passes(n, gates, noise, shots, ar, opts)
+    if tile:
+        assert max(r.pass_ for r in recs if r.level == len(ar) - 1) >= 1   # multi-pass leaf level
+    a = T.tqsim_run_ex(n, gates, noise, shots, ar, 5, opts)                          # dedup
+    b = T.tqsim_run_ex(n, gates, noise, shots, ar, 5, opts, [(len(ar) - 1, 0)])      # stored
+    assert np.array_equal(a.leaf_outcomes, b.leaf_outcomes)
+    nm = NoiseModel(0.003, 0.01, 0.02, 0.03)
+    if n <= 16:
+        ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 5)
+        assert_leaves_match(a.leaf_outcomes, ref.leaves)
