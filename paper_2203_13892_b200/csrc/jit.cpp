@@ -50,7 +50,9 @@ struct TqJitArgs {
   const unsigned char* rows; tq_u32 row_bytes;   // noise rows of the batch (launch_noise_rows)
   // leaf measurement without the state store (variants 1/2, see gen_pass)
   const tq_u32* tiles; const tq_u32* runsel; tq_d2* scratch; tq_u32* xlout;
-  tq_u32 dedup;   // leaf level without stored states: skip error-free duplicate siblings
+  tq_u32 dedup;   // no stored states asked for: skip error-free duplicate siblings
+  // the parent batch's dedup (fan-out reads a skipped parent's representative)
+  const unsigned char* prows; tq_u32 prow_bytes, parity, pdedup;
 };
 // 16-byte global load the compiler may not sink below the error-branch: the tile loads
 // are issued before the (dependent) noise-row mask load is waited on
@@ -89,6 +91,8 @@ struct HostJitArgs {   // mirrors TqJitArgs
   void* scratch;
   uint32_t* xlout;
   uint32_t dedup;
+  const void* prows;
+  uint32_t prow_bytes, parity, pdedup;
 };
 
 std::string hexd(double v) {
@@ -1183,7 +1187,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       << "    const tq_u64 j = a.child_first + s, g0 = j - j % a.arity;\n"
       << "    for (tq_u32 q = g0 > a.child_first ? (tq_u32)(g0 - a.child_first) : 0u; q < s; ++q)\n"
       << "      if (*reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)q * a.row_bytes) == 0u) {\n"
-      << "        if (t == 0 && tid == 0u && a.xlout) a.xlout[s] = 0u;\n"
+      << (variant == 1 ? "        if (t == 0 && tid == 0u) a.xlout[s] = 0u;\n" : "")
       << "        return;\n"
       << "      }\n"
       << "  }\n";
@@ -1193,9 +1197,14 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << "; gtile_st ^= (0u - (tq_u32)((t >> "
       << i << ") & 1ull)) & " << pcol[pd.out_q[i]] << "u;\n";
   o << "  tq_d2* __restrict__ dst = a.dst + ((tq_u64)s << " << n << ");\n";
-  if (mode == 1)
-    o << "  const tq_d2* __restrict__ src = a.src + ((((tq_u64)a.child_first + s) / a.arity - a.parent_first) << "
-      << n << ");\n";
+  if (mode == 1)   // fan-out src: the parent, or (skipped duplicate parent) its representative
+    o << "  tq_u64 pj = ((tq_u64)a.child_first + s) / a.arity;\n"
+      << "  if (a.pdedup && *reinterpret_cast<const tq_u32*>(a.prows + (pj - a.parent_first) * a.prow_bytes) == 0u) {\n"
+      << "    const tq_u64 g0 = pj - pj % a.parity;\n"
+      << "    for (tq_u64 q = g0 > a.parent_first ? g0 : a.parent_first; q < pj; ++q)\n"
+      << "      if (*reinterpret_cast<const tq_u32*>(a.prows + (q - a.parent_first) * a.prow_bytes) == 0u) { pj = q; break; }\n"
+      << "  }\n"
+      << "  const tq_d2* __restrict__ src = a.src + ((pj - a.parent_first) << " << n << ");\n";
   else if (mode == 2 && variant == 2) {
     // recompute of a leaf whose state was not computed (an error-free duplicate): its
     // representative's slot holds the same state
@@ -2237,7 +2246,8 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
                 L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes,
-                L.tiles, L.runsel, L.scratch, L.xlout, L.dedup};
+                L.tiles, L.runsel, L.scratch, L.xlout, L.dedup, L.prows, L.prow_bytes,
+                L.parity ? L.parity : 1u, L.pdedup};
   const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute;
   if (!kern) return (int)cudaErrorInvalidDeviceFunction;
   const uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;

@@ -232,6 +232,7 @@ struct Exec {
   uint64_t kD = 0;
   bool slot_used[2] = {false, false};
   bool leaf_issued = false;
+  uint64_t pcnt[64] = {};   // instances of the current batch per level (dedup needs >= 2)
 };
 
 std::vector<uint64_t> level_firsts(const tqsim_handle* h, uint64_t t0) {
@@ -297,6 +298,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   (void)slice_begin;
   for (uint64_t b = i0; b < i1; b += cap) {
     const uint64_t cnt = std::min(cap, i1 - b);
+    x.pcnt[d] = cnt;
     int slot = 0;
     if (piped) {   // this batch's buffer: free once the leaf work of batch k-2 is done
       slot = (int)(x.kD++ & 1);
@@ -335,7 +337,17 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       const bool runsums_only = nostore && passes[p].leaf_sums;
       pl.variant = runsums_only ? 1u : 0u;
       pl.xlout = xlv;
-      pl.dedup = nostore ? 1u : 0u;   // leaf level (nostore implies leaf): error-free siblings once
+      // error-free siblings computed once (no state dumps asked for: nobody reads a skipped
+      // slot except through the redirects of the next level's fan-out and the sampler)
+      const bool dedup = !(h->debug && h->debug->n_dumps);
+      pl.dedup = dedup && cnt > 1 ? 1u : 0u;   // (a batch of one has no duplicates)
+      if (d > 0 && dedup && x.pcnt[d - 1] > 1) {
+        const uint32_t prb = noise_row_bytes((uint32_t)(h->plan.bounds[d] - h->plan.bounds[d - 1]));
+        pl.prows = x.ws + x.L.rows_off + x.L.rows_lvl_off[d - 1] + (parent_first - x.lvl_first[d - 1]) * prb;
+        pl.prow_bytes = prb;
+        pl.parity = h->plan.arities[d - 1];
+        pl.pdedup = 1;
+      }
       mark(x, 0);
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
       mark(x, 0);
@@ -891,28 +903,46 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
       // the level's first batch's noise rows (drawn by the run above)
       uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d]);
       (void)slice_begin;
-      // leaf level: as in the tree, error-free duplicate siblings are skipped; count the
-      // computed children (and their distinct parents) for the algorithmic bytes
-      const bool leaf = d + 1 == h->pp.levels.size() && !(h->debug && h->debug->n_dumps);
+      // as in the tree, error-free duplicate siblings are skipped (and a fan-out reads a
+      // skipped parent's representative); count the computed children and the distinct
+      // parent states they read for the algorithmic bytes
+      const bool leaf = !(h->debug && h->debug->n_dumps);   // dedup on
+      const uint64_t A = h->plan.arities[d];
+      const uint64_t pfirst = d > 0 ? first / A : 0;
+      const uint32_t prb = d > 0 ? noise_row_bytes((uint32_t)(h->plan.bounds[d] - h->plan.bounds[d - 1])) : 0;
+      const uint8_t* prows = d > 0 ? reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d - 1]) : nullptr;
       uint64_t comp = cnt, comp_par = 0;
       {
         std::vector<uint8_t> hr(cnt * row_bytes);
         ckc(cudaMemcpy(hr.data(), rows, hr.size(), cudaMemcpyDeviceToHost), "rows D2H");
-        auto em = [&](uint64_t q) { uint32_t v; std::memcpy(&v, &hr[q * row_bytes], 4); return v; };
-        const uint64_t A = h->plan.arities[d];
-        uint64_t last_par = ~0ull;
+        const uint64_t pcnt = d > 0 ? (first + cnt - 1) / A - pfirst + 1 : 0;
+        std::vector<uint8_t> hp(pcnt * prb);
+        if (d > 0) ckc(cudaMemcpy(hp.data(), prows, hp.size(), cudaMemcpyDeviceToHost), "rows D2H");
+        auto em = [&](const std::vector<uint8_t>& v, uint32_t rb, uint64_t q) {
+          uint32_t w;
+          std::memcpy(&w, &v[q * rb], 4);
+          return w;
+        };
+        // representative of instance q (batch-relative) of a batch starting at f, arity a
+        auto rep_of = [&](const std::vector<uint8_t>& v, uint32_t rb, uint64_t f, uint64_t a, uint64_t q) {
+          if (!leaf || v.size() <= rb || em(v, rb, q) != 0) return q;   // (batch of one: no dedup)
+          const uint64_t j = f + q, g0 = j - j % a;
+          for (uint64_t r = g0 > f ? g0 - f : 0; r < q; ++r)
+            if (em(v, rb, r) == 0) return r;
+          return q;
+        };
+        std::vector<char> seen(pcnt, 0);
         comp = 0;
         for (uint64_t q = 0; q < cnt; ++q) {
-          bool dup = false;
-          if (leaf && em(q) == 0) {
-            const uint64_t j = first + q, g0 = j - j % A;
-            for (uint64_t r = g0 > first ? g0 - first : 0; r < q && !dup; ++r) dup = em(r) == 0;
-          }
-          if (dup) continue;
+          if (rep_of(hr, row_bytes, first, A, q) != q) continue;
           ++comp;
-          const uint64_t par = (first + q) / A;
-          if (par != last_par) ++comp_par;
-          last_par = par;
+          if (d > 0) {
+            const uint64_t pq = rep_of(hp, prb, pfirst, h->plan.arities[d - 1], (first + q) / A - pfirst);
+            if (!seen[pq]) {
+              seen[pq] = 1;
+              ++comp_par;
+            }
+          }
         }
       }
       for (size_t p = 0; p < h->pp.levels[d].size(); ++p) {
@@ -934,7 +964,13 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
         // as in the tree: the leaf's last pass stores run sums only
         pl.variant = pd.leaf_sums ? 1u : 0u;
         pl.xlout = reinterpret_cast<uint32_t*>(x.ws + x.L.sel_off + 2 * align_up(4 * x.L.cap.back()));
-        pl.dedup = leaf ? 1u : 0u;
+        pl.dedup = leaf && cnt > 1 ? 1u : 0u;
+        if (d > 0 && leaf && std::min<uint64_t>(x.L.cap[d - 1], inst / A) > 1) {
+          pl.prows = prows;
+          pl.prow_bytes = prb;
+          pl.parity = h->plan.arities[d - 1];
+          pl.pdedup = 1;
+        }
         ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");   // warm
         ckc(cudaEventRecord(e0, st), "record");
         for (uint32_t i = 0; i < reps; ++i) ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");

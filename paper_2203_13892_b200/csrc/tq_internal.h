@@ -125,7 +125,9 @@ struct PassLaunch {
   const uint32_t* runsel;       // variant 2: selected run per leaf
   void* scratch;                // variant 2: 8 amplitudes per leaf (double2)
   uint32_t* xlout;              // variant 1: store-address XOR per leaf
-  uint32_t dedup;               // leaf level, no state store: skip error-free duplicate siblings
+  uint32_t dedup;               // no state store: skip error-free duplicate siblings
+  const void* prows;            // the parent batch's noise rows (fan-out redirect when pdedup)
+  uint32_t prow_bytes, parity, pdedup;
 };
 
 // Noise rows of one level batch (row a3): per instance a row of row_bytes bytes,

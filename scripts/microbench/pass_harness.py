@@ -42,6 +42,7 @@ int main() {
   a.child_first = 0; a.parent_first = 0; a.arity = mode == 1 ? arity : 1; a.batch = batch;
   a.runsum = runsum; a.rows = rows; a.row_bytes = crow;
   unsigned* xlout; CK(cudaMalloc(&xlout, batch * 4)); a.xlout = xlout; a.tiles = nullptr; a.runsel = nullptr; a.scratch = nullptr;
+  a.dedup = 0; a.prows = nullptr; a.prow_bytes = 0; a.parity = 1; a.pdedup = 0;
   TqCoef cf = {};
   const size_t smem = SMEM;
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(tq_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -103,7 +104,7 @@ def main():
         open(args.src_out, "w").write(src)
     thr = int(re.search(r"__launch_bounds__\((\d+),", src).group(1))
     K = thr.bit_length() - 1 + 4
-    mode = 1 if "/ a.arity - a.parent_first" in src else (2 if "const tq_d2* src = dst;" in src else 0)
+    mode = 1 if "tq_u64 pj = " in src or "/ a.arity - a.parent_first" in src else (2 if "const tq_d2* src = dst;" in src else 0)
     smem = (16 << K) if "extern __shared__ tq_d2 tile[]" in src else 0
     crow = int(re.search(r"a\.rows \+ \(tq_u64\)s \* (\d+)u", src).group(1))
     goff0 = int(re.search(r"GOFF\[\d+\] = \{(\d+)", src).group(1))
