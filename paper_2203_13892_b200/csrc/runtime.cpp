@@ -137,7 +137,11 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
   const int n = h->n_sim;
   const uint64_t S = 16ull << n;
   const int tl = h->opts.batch_log2_amps ? (int)h->opts.batch_log2_amps : 26;
-  const uint64_t target = tl >= n ? (1ull << (tl - n)) : 1ull;
+  // >= 2 states per batch by default: sibling pairs share a batch, so error-free
+  // duplicates are computed once (measured C5 shard: 8.7 -> 5.5 s); the budget loop
+  // below halves the caps again when the buffers would not fit
+  const uint64_t target = std::max<uint64_t>(tl >= n ? (1ull << (tl - n)) : 1ull,
+                                             h->opts.batch_log2_amps ? 1ull : 2ull);
   const size_t levels = h->plan.arities.size();
   uint64_t per = std::max<uint64_t>(top_count, 1);
   for (size_t d = 0; d < levels; ++d) {
