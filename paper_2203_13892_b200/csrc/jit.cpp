@@ -50,9 +50,8 @@ struct TqJitArgs {
   const unsigned char* rows; tq_u32 row_bytes;   // noise rows of the batch (launch_noise_rows)
   // leaf measurement without the state store (variants 1/2, see gen_pass)
   const tq_u32* tiles; const tq_u32* runsel; tq_d2* scratch; tq_u32* xlout;
-  tq_u32 dedup;   // no stored states asked for: skip error-free duplicate siblings
-  // the parent batch's dedup (fan-out reads a skipped parent's representative)
-  const unsigned char* prows; tq_u32 prow_bytes, parity, pdedup;
+  // dedup maps (launch_dedup_map) of the batch and of the parent batch, or null
+  const tq_u32* rep; const tq_u32* prep;
 };
 // 16-byte global load the compiler may not sink below the error-branch: the tile loads
 // are issued before the (dependent) noise-row mask load is waited on
@@ -90,9 +89,8 @@ struct HostJitArgs {   // mirrors TqJitArgs
   const uint32_t* runsel;
   void* scratch;
   uint32_t* xlout;
-  uint32_t dedup;
-  const void* prows;
-  uint32_t prow_bytes, parity, pdedup;
+  const uint32_t* rep;
+  const uint32_t* prep;
 };
 
 std::string hexd(double v) {
@@ -1179,17 +1177,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   else
     o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
   if (variant != 2) {
-    // Leaf level, states not stored: a child with no error in the whole slice has the
-    // same state as every error-free sibling (same parent, same gates), so only the first
-    // error-free sibling of the batch computes it; the sampler reads its run sums
-    // (tq_dedup_rep, kernels.cu).  The skipped child's store-address XOR is 0.
-    o << "  if (a.dedup && *reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)s * a.row_bytes) == 0u) {\n"
-      << "    const tq_u64 j = a.child_first + s, g0 = j - j % a.arity;\n"
-      << "    for (tq_u32 q = g0 > a.child_first ? (tq_u32)(g0 - a.child_first) : 0u; q < s; ++q)\n"
-      << "      if (*reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)q * a.row_bytes) == 0u) {\n"
-      << (variant == 1 ? "        if (t == 0 && tid == 0u) a.xlout[s] = 0u;\n" : "")
-      << "        return;\n"
-      << "      }\n"
+    // An instance that shares its representative's state (dedup map, launch_dedup_map:
+    // no error in its slice, same effective parent) is not computed; readers go through
+    // the map.  A skipped leaf's store-address XOR is 0.
+    o << "  if (a.rep && a.rep[s] != s) {\n"
+      << (variant == 1 ? "    if (t == 0 && tid == 0u) a.xlout[s] = 0u;\n" : "")
+      << "    return;\n"
       << "  }\n";
   }
   o << "  tq_u32 gtile = 0u, gtile_st = 0u;\n";   // the tile's out-of-tile index bits: physical / stored
@@ -1198,22 +1191,13 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       << i << ") & 1ull)) & " << pcol[pd.out_q[i]] << "u;\n";
   o << "  tq_d2* __restrict__ dst = a.dst + ((tq_u64)s << " << n << ");\n";
   if (mode == 1)   // fan-out src: the parent, or (skipped duplicate parent) its representative
-    o << "  tq_u64 pj = ((tq_u64)a.child_first + s) / a.arity;\n"
-      << "  if (a.pdedup && *reinterpret_cast<const tq_u32*>(a.prows + (pj - a.parent_first) * a.prow_bytes) == 0u) {\n"
-      << "    const tq_u64 g0 = pj - pj % a.parity;\n"
-      << "    for (tq_u64 q = g0 > a.parent_first ? g0 : a.parent_first; q < pj; ++q)\n"
-      << "      if (*reinterpret_cast<const tq_u32*>(a.prows + (q - a.parent_first) * a.prow_bytes) == 0u) { pj = q; break; }\n"
-      << "  }\n"
-      << "  const tq_d2* __restrict__ src = a.src + ((pj - a.parent_first) << " << n << ");\n";
+    o << "  tq_u64 pj = ((tq_u64)a.child_first + s) / a.arity - a.parent_first;\n"
+      << "  if (a.prep) pj = a.prep[pj];\n"
+      << "  const tq_d2* __restrict__ src = a.src + (pj << " << n << ");\n";
   else if (mode == 2 && variant == 2) {
     // recompute of a leaf whose state was not computed (an error-free duplicate): its
     // representative's slot holds the same state
-    o << "  tq_u32 sr = s;\n"
-      << "  if (a.dedup && *reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)s * a.row_bytes) == 0u) {\n"
-      << "    const tq_u64 j = a.child_first + s, g0 = j - j % a.arity;\n"
-      << "    for (tq_u32 q = g0 > a.child_first ? (tq_u32)(g0 - a.child_first) : 0u; q < s; ++q)\n"
-      << "      if (*reinterpret_cast<const tq_u32*>(a.rows + (tq_u64)q * a.row_bytes) == 0u) { sr = q; break; }\n"
-      << "  }\n"
+    o << "  const tq_u32 sr = a.rep ? a.rep[s] : s;\n"
       << "  const tq_d2* src = a.dst + ((tq_u64)sr << " << n << ");\n";
   } else if (mode == 2)
     o << "  const tq_d2* src = dst;\n";
@@ -2246,8 +2230,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
                 L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes,
-                L.tiles, L.runsel, L.scratch, L.xlout, L.dedup, L.prows, L.prow_bytes,
-                L.parity ? L.parity : 1u, L.pdedup};
+                L.tiles, L.runsel, L.scratch, L.xlout, L.rep, L.prep};
   const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute;
   if (!kern) return (int)cudaErrorInvalidDeviceFunction;
   const uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;

@@ -29,18 +29,13 @@ struct SelectOut {
   const uint32_t* xl;         // the leaf pass's store-address XOR per leaf
   uint32_t n_out;
   uint32_t out_row[32];       // out-of-tile qubit i = parity(out_row[i] & stored address)
-  const uint8_t* rows;        // dedup: the batch's noise rows (error mask = first u32)
-  uint32_t row_bytes, arity, dedup;
+  const uint32_t* rep;        // dedup map of the leaf batch (null: every leaf computed)
 };
 
-// The leaf whose run sums leaf s reads: itself, or -- no error in its slice -- the first
-// error-free sibling in the batch (the gate passes computed only that one; same state).
+// The leaf whose run sums leaf s reads (the dedup map: the gate passes computed only it)
 __device__ __forceinline__ uint32_t tq_dedup_rep(const SelectOut& so, uint64_t leaf_first, uint32_t s) {
-  if (!so.dedup || *reinterpret_cast<const uint32_t*>(so.rows + (uint64_t)s * so.row_bytes) != 0u) return s;
-  const uint64_t j = leaf_first + s, g0 = j - j % so.arity;
-  for (uint32_t q = g0 > leaf_first ? (uint32_t)(g0 - leaf_first) : 0u; q < s; ++q)
-    if (*reinterpret_cast<const uint32_t*>(so.rows + (uint64_t)q * so.row_bytes) == 0u) return q;
-  return s;
+  (void)leaf_first;
+  return so.rep ? so.rep[s] : s;
 }
 
 __device__ __forceinline__ uint32_t tile_of_run(uint64_t run, uint32_t xl, const SelectOut& so) {
@@ -460,6 +455,62 @@ __global__ void __launch_bounds__(256) noise_rows_all_kernel(
   if (lane == 0) *reinterpret_cast<uint32_t*>(row) = mask;
 }
 
+// Dedup map of every level of the shard (one CTA, levels in order: a level's map reads its
+// parent level's).  Batches are formed as run_level forms them: level 0 in caps from the
+// shard's first instance, level d+1 in caps from (parent batch start) * arity.  An instance
+// with an error in its slice is computed (rep = itself).  An error-free instance shares the
+// state of the first error-free child, in its batch, of its parent's representative P*
+// (different parents with the same representative hold the same state), else of the first
+// error-free sibling in its batch, else it is computed; the chosen instance is computed by
+// the same rule.
+__global__ void __launch_bounds__(1024) dedup_map_kernel(const uint8_t* __restrict__ rows,
+                                                         const __grid_constant__ NoiseLevels L,
+                                                         uint32_t* __restrict__ rep, uint32_t* __restrict__ pos) {
+  for (uint32_t d = 0; d < L.n_levels; ++d) {
+    const NoiseLevel& lv = L.lv[d];
+    const uint8_t* rw = rows + lv.rows_off;
+    auto em = [&](uint64_t j) { return *reinterpret_cast<const uint32_t*>(rw + (j - lv.inst_first) * lv.row_bytes); };
+    const uint64_t A = lv.arity;
+    for (uint64_t idx = threadIdx.x; idx < lv.count; idx += blockDim.x) {
+      const uint64_t j = lv.inst_first + idx;
+      uint64_t bs, P = 0, Ps = 0, cfirst;
+      if (d == 0) {
+        bs = lv.inst_first + ((j - lv.inst_first) / lv.cap) * lv.cap;
+        cfirst = lv.inst_first;   // level-0 siblings: the shard's level-0 instances
+      } else {
+        const NoiseLevel& pl = L.lv[d - 1];
+        P = j / A;
+        const uint64_t pidx = P - pl.inst_first;
+        const uint64_t pbs = P - pos[pl.map_off + pidx];
+        const uint64_t rs = pbs * A;
+        bs = rs + ((j - rs) / lv.cap) * lv.cap;
+        Ps = pbs + rep[pl.map_off + pidx];
+        cfirst = P * A;
+      }
+      pos[lv.map_off + idx] = (uint32_t)(j - bs);
+      uint64_t r = j;
+      if (em(j) == 0u) {
+        bool found = false;
+        if (d > 0 && Ps != P)   // children of the parent's representative
+          for (uint64_t c = (Ps * A > bs ? Ps * A : bs); c < Ps * A + A && c < j; ++c)
+            if (em(c) == 0u) {
+              r = c;
+              found = true;
+              break;
+            }
+        if (!found)
+          for (uint64_t c = (cfirst > bs ? cfirst : bs); c < j; ++c)
+            if (em(c) == 0u) {
+              r = c;
+              break;
+            }
+      }
+      rep[lv.map_off + idx] = (uint32_t)(r - bs);
+    }
+    __syncthreads();
+  }
+}
+
 // The run's seed in device memory: the tree's launches (a replayed CUDA graph) read it
 __global__ void set_seed_kernel(uint64_t* d_seed, uint64_t seed) { *d_seed = seed; }
 
@@ -473,6 +524,12 @@ int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const 
   const uint64_t threads = total_instances * 32;
   dev::noise_rows_all_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       d_two, d_pass_of, L, total_instances, d_seed, p1, p2, d_rows);
+  return (int)cudaGetLastError();
+}
+
+int launch_dedup_map(const uint8_t* d_rows, const NoiseLevels& L, uint32_t* d_rep, uint32_t* d_pos,
+                     void* stream) {
+  dev::dedup_map_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(d_rows, L, d_rep, d_pos);
   return (int)cudaGetLastError();
 }
 
@@ -511,10 +568,7 @@ static dev::SelectOut select_out(const LeafSelect* sel) {
   so.xl = sel->xl;
   so.n_out = sel->n_out;
   for (uint32_t i = 0; i < sel->n_out && i < 32; ++i) so.out_row[i] = sel->out_row[i];
-  so.rows = sel->rows;
-  so.row_bytes = sel->row_bytes;
-  so.arity = sel->arity ? sel->arity : 1u;
-  so.dedup = sel->dedup;
+  so.rep = sel->rep;
   return so;
 }
 

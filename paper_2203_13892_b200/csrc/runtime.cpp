@@ -117,6 +117,9 @@ struct Layout {
   uint64_t runs_off = 0, sums_off = 0, rows_off = 0, total = 0;
   std::vector<uint64_t> lvl_count;      // the shard's instances per level
   std::vector<uint64_t> rows_lvl_off;   // byte offset of each level's noise rows (in the rows region)
+  uint64_t map_off = 0;                 // dedup maps: rep then pos, u32 per instance of the shard
+  std::vector<uint64_t> map_lvl;        // entry offset of each level's map
+  uint64_t map_entries = 0;
   uint64_t sel_off = 0;                 // leaf select / recompute buffers (per leaf of a batch):
                                         // runsel u32, tile u32, xl u32, t3 f64, 8 amplitudes
   int chunk_log2 = 0;
@@ -174,6 +177,14 @@ Layout layout(const tqsim_handle* h, uint64_t top_count) {
                                                                          h->plan.bounds[d])));
     }
     off = align_up(off + rows);
+    l.map_off = off;
+    l.map_lvl.clear();
+    l.map_entries = 0;
+    for (size_t d = 0; d < levels; ++d) {
+      l.map_lvl.push_back(l.map_entries);
+      l.map_entries += l.lvl_count[d];
+    }
+    off = align_up(off + 8 * l.map_entries);
     l.sel_off = off;
     off = align_up(off + l.cap.back() * (4 + 4 + 4 + 8 + (16ull << RUN_Q)) + 4 * ALIGN);
     l.total = off;
@@ -236,7 +247,8 @@ struct Exec {
   uint64_t kD = 0;
   bool slot_used[2] = {false, false};
   bool leaf_issued = false;
-  uint64_t pcnt[64] = {};   // instances of the current batch per level (dedup needs >= 2)
+  uint64_t pcnt[64] = {};   // instances of the current batch per level
+  bool dedup = false;       // dedup maps built for this tree (no state dumps asked for)
 };
 
 std::vector<uint64_t> level_firsts(const tqsim_handle* h, uint64_t t0) {
@@ -341,16 +353,12 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       const bool runsums_only = nostore && passes[p].leaf_sums;
       pl.variant = runsums_only ? 1u : 0u;
       pl.xlout = xlv;
-      // error-free siblings computed once (no state dumps asked for: nobody reads a skipped
-      // slot except through the redirects of the next level's fan-out and the sampler)
-      const bool dedup = !(h->debug && h->debug->n_dumps);
-      pl.dedup = dedup && cnt > 1 ? 1u : 0u;   // (a batch of one has no duplicates)
-      if (d > 0 && dedup && x.pcnt[d - 1] > 1) {
-        const uint32_t prb = noise_row_bytes((uint32_t)(h->plan.bounds[d] - h->plan.bounds[d - 1]));
-        pl.prows = x.ws + x.L.rows_off + x.L.rows_lvl_off[d - 1] + (parent_first - x.lvl_first[d - 1]) * prb;
-        pl.prow_bytes = prb;
-        pl.parity = h->plan.arities[d - 1];
-        pl.pdedup = 1;
+      // shared states computed once (dedup maps; nobody reads a skipped slot except through
+      // the maps: the next level's fan-out, the sampler, the recompute)
+      if (x.dedup) {
+        const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
+        if (cnt > 1) pl.rep = maps + x.L.map_lvl[d] + (b - x.lvl_first[d]);
+        if (d > 0 && x.pcnt[d - 1] > 1) pl.prep = maps + x.L.map_lvl[d - 1] + (parent_first - x.lvl_first[d - 1]);
       }
       mark(x, 0);
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
@@ -385,10 +393,9 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       ls.tile = tiles;
       ls.xl = xlv;
       ls.n_out = (uint32_t)jp.out_row.size();
-      ls.rows = rows;
-      ls.row_bytes = row_bytes;
-      ls.arity = h->plan.arities[d];
-      ls.dedup = 1;
+      ls.rep = x.dedup && cnt > 1 ? reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off) + x.L.map_lvl[d] +
+                                         (b - x.lvl_first[d])
+                                   : nullptr;
       for (size_t i = 0; i < jp.out_row.size() && i < 32; ++i) ls.out_row[i] = jp.out_row[i];
       mark(x, 1);
       if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {
@@ -479,6 +486,9 @@ void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
     lv.slice_begin = (uint32_t)h->plan.bounds[d];
     lv.slice_len = (uint32_t)(h->plan.bounds[d + 1] - h->plan.bounds[d]);
     lv.row_bytes = noise_row_bytes(lv.slice_len);
+    lv.map_off = x.L.map_lvl[d];
+    lv.cap = x.L.cap[d];
+    lv.arity = h->plan.arities[d];
     total += lv.count;
   }
   NL.n_levels = (uint32_t)levels;
@@ -489,6 +499,14 @@ void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
   mark(x, 2);
   h->stats.kernel_launches++;
   h->stats.noise_launches++;
+  x.dedup = !(h->debug && h->debug->n_dumps);
+  if (x.dedup) {
+    uint32_t* maps = reinterpret_cast<uint32_t*>(x.ws + x.L.map_off);
+    ck(launch_dedup_map(reinterpret_cast<const uint8_t*>(x.ws + x.L.rows_off), NL, maps, maps + x.L.map_entries,
+                        x.st),
+       "dedup map launch");
+    h->stats.kernel_launches++;
+  }
   run_level(x, 0, t0, t1, 0);
   if (x.pipe && x.leaf_issued) {   // join the leaf branch
     ckc(cudaEventRecord(x.ev[4], x.st2), "pipe join record");
@@ -907,41 +925,30 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
       // the level's first batch's noise rows (drawn by the run above)
       uint8_t* rows = reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d]);
       (void)slice_begin;
-      // as in the tree, error-free duplicate siblings are skipped (and a fan-out reads a
-      // skipped parent's representative); count the computed children and the distinct
-      // parent states they read for the algorithmic bytes
-      const bool leaf = !(h->debug && h->debug->n_dumps);   // dedup on
+      // as in the tree, instances sharing a representative's state are skipped and a
+      // fan-out reads a skipped parent's representative (the dedup maps the run above
+      // built); count the computed instances and the distinct parent states they read
+      const bool dd = !(h->debug && h->debug->n_dumps);
       const uint64_t A = h->plan.arities[d];
-      const uint64_t pfirst = d > 0 ? first / A : 0;
-      const uint32_t prb = d > 0 ? noise_row_bytes((uint32_t)(h->plan.bounds[d] - h->plan.bounds[d - 1])) : 0;
-      const uint8_t* prows = d > 0 ? reinterpret_cast<uint8_t*>(x.ws + x.L.rows_off + x.L.rows_lvl_off[d - 1]) : nullptr;
+      const uint64_t pcnt_batch = d > 0 ? std::min<uint64_t>(x.L.cap[d - 1], inst / A) : 0;
+      const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
+      const uint32_t* rep_d = dd && cnt > 1 ? maps + x.L.map_lvl[d] : nullptr;
+      const uint32_t* rep_p = dd && d > 0 && pcnt_batch > 1 ? maps + x.L.map_lvl[d - 1] : nullptr;
       uint64_t comp = cnt, comp_par = 0;
       {
-        std::vector<uint8_t> hr(cnt * row_bytes);
-        ckc(cudaMemcpy(hr.data(), rows, hr.size(), cudaMemcpyDeviceToHost), "rows D2H");
-        const uint64_t pcnt = d > 0 ? (first + cnt - 1) / A - pfirst + 1 : 0;
-        std::vector<uint8_t> hp(pcnt * prb);
-        if (d > 0) ckc(cudaMemcpy(hp.data(), prows, hp.size(), cudaMemcpyDeviceToHost), "rows D2H");
-        auto em = [&](const std::vector<uint8_t>& v, uint32_t rb, uint64_t q) {
-          uint32_t w;
-          std::memcpy(&w, &v[q * rb], 4);
-          return w;
-        };
-        // representative of instance q (batch-relative) of a batch starting at f, arity a
-        auto rep_of = [&](const std::vector<uint8_t>& v, uint32_t rb, uint64_t f, uint64_t a, uint64_t q) {
-          if (!leaf || v.size() <= rb || em(v, rb, q) != 0) return q;   // (batch of one: no dedup)
-          const uint64_t j = f + q, g0 = j - j % a;
-          for (uint64_t r = g0 > f ? g0 - f : 0; r < q; ++r)
-            if (em(v, rb, r) == 0) return r;
-          return q;
-        };
-        std::vector<char> seen(pcnt, 0);
+        std::vector<uint32_t> hr(cnt), hp(pcnt_batch);
+        for (uint64_t q = 0; q < cnt; ++q) hr[q] = (uint32_t)q;
+        for (uint64_t q = 0; q < pcnt_batch; ++q) hp[q] = (uint32_t)q;
+        if (rep_d) ckc(cudaMemcpy(hr.data(), rep_d, cnt * 4, cudaMemcpyDeviceToHost), "map D2H");
+        if (rep_p) ckc(cudaMemcpy(hp.data(), rep_p, pcnt_batch * 4, cudaMemcpyDeviceToHost), "map D2H");
+        const uint64_t pfirst = d > 0 ? first / A : 0;
+        std::vector<char> seen(pcnt_batch, 0);
         comp = 0;
         for (uint64_t q = 0; q < cnt; ++q) {
-          if (rep_of(hr, row_bytes, first, A, q) != q) continue;
+          if (hr[q] != q) continue;
           ++comp;
           if (d > 0) {
-            const uint64_t pq = rep_of(hp, prb, pfirst, h->plan.arities[d - 1], (first + q) / A - pfirst);
+            const uint64_t pq = hp[(first + q) / A - pfirst];
             if (!seen[pq]) {
               seen[pq] = 1;
               ++comp_par;
@@ -968,13 +975,8 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
         // as in the tree: the leaf's last pass stores run sums only
         pl.variant = pd.leaf_sums ? 1u : 0u;
         pl.xlout = reinterpret_cast<uint32_t*>(x.ws + x.L.sel_off + 2 * align_up(4 * x.L.cap.back()));
-        pl.dedup = leaf && cnt > 1 ? 1u : 0u;
-        if (d > 0 && leaf && std::min<uint64_t>(x.L.cap[d - 1], inst / A) > 1) {
-          pl.prows = prows;
-          pl.prow_bytes = prb;
-          pl.parity = h->plan.arities[d - 1];
-          pl.pdedup = 1;
-        }
+        pl.rep = rep_d;
+        pl.prep = rep_p;
         ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");   // warm
         ckc(cudaEventRecord(e0, st), "record");
         for (uint32_t i = 0; i < reps; ++i) ck(launch_jit_pass(h->jit[d][p], pd, pl, st), "gate pass launch");

@@ -125,9 +125,8 @@ struct PassLaunch {
   const uint32_t* runsel;       // variant 2: selected run per leaf
   void* scratch;                // variant 2: 8 amplitudes per leaf (double2)
   uint32_t* xlout;              // variant 1: store-address XOR per leaf
-  uint32_t dedup;               // no state store: skip error-free duplicate siblings
-  const void* prows;            // the parent batch's noise rows (fan-out redirect when pdedup)
-  uint32_t prow_bytes, parity, pdedup;
+  const uint32_t* rep;          // dedup map of the batch (null: every instance computed)
+  const uint32_t* prep;         // dedup map of the parent batch (fan-out reads prep[parent])
 };
 
 // Noise rows of one level batch (row a3): per instance a row of row_bytes bytes,
@@ -144,12 +143,22 @@ struct NoiseLevel {
   uint64_t count;        // the shard's instances at this level
   uint64_t rows_off;     // byte offset of the level's rows in the rows region
   uint32_t slice_begin, slice_len, row_bytes, pad;
+  // dedup map (launch_dedup_map): entry offset of the level in the rep / pos arrays,
+  // the level's batch cap and arity
+  uint64_t map_off;
+  uint64_t cap;
+  uint32_t arity, pad2;
 };
 constexpr int NOISE_MAX_LEVELS = 64;
 struct NoiseLevels {
   NoiseLevel lv[NOISE_MAX_LEVELS];
   uint32_t n_levels;
 };
+// Per instance of every level of the shard: rep = batch-relative index of the instance
+// whose computed state it shares (itself unless it drew no error and an earlier instance of
+// its batch with the same effective parent did not either), pos = its batch-relative index.
+int launch_dedup_map(const uint8_t* d_rows, const NoiseLevels& L, uint32_t* d_rep, uint32_t* d_pos,
+                     void* stream);
 int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const NoiseLevels& L,
                           uint64_t total_instances, const uint64_t* d_seed, double p1, double p2,
                           uint8_t* d_rows, void* stream);
@@ -165,9 +174,8 @@ struct LeafSelect {
   const uint32_t* xl;
   uint32_t n_out;
   uint32_t out_row[32];      // out-of-tile qubit i = parity(out_row[i] & stored address)
-  // duplicate error-free siblings (see the gate passes): read the representative's sums
-  const uint8_t* rows = nullptr;
-  uint32_t row_bytes = 0, arity = 1, dedup = 0;
+  // dedup map of the leaf batch: read the representative's sums (null: none)
+  const uint32_t* rep = nullptr;
 };
 int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
                          int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,

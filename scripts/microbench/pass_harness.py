@@ -42,7 +42,7 @@ int main() {
   a.child_first = 0; a.parent_first = 0; a.arity = mode == 1 ? arity : 1; a.batch = batch;
   a.runsum = runsum; a.rows = rows; a.row_bytes = crow;
   unsigned* xlout; CK(cudaMalloc(&xlout, batch * 4)); a.xlout = xlout; a.tiles = nullptr; a.runsel = nullptr; a.scratch = nullptr;
-  a.dedup = 0; a.prows = nullptr; a.prow_bytes = 0; a.parity = 1; a.pdedup = 0;
+  a.rep = nullptr; a.prep = nullptr;
   TqCoef cf = {};
   const size_t smem = SMEM;
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(tq_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
