@@ -463,15 +463,15 @@ __global__ void __launch_bounds__(256) noise_rows_all_kernel(
 // (different parents with the same representative hold the same state), else of the first
 // error-free sibling in its batch, else it is computed; the chosen instance is computed by
 // the same rule.
-__global__ void __launch_bounds__(1024) dedup_map_kernel(const uint8_t* __restrict__ rows,
-                                                         const __grid_constant__ NoiseLevels L,
-                                                         uint32_t* __restrict__ rep, uint32_t* __restrict__ pos) {
-  for (uint32_t d = 0; d < L.n_levels; ++d) {
+__device__ __forceinline__ void dedup_map_level(const uint8_t* __restrict__ rows, const NoiseLevels& L,
+                                                uint32_t d, uint64_t idx0, uint64_t stride,
+                                                uint32_t* __restrict__ rep, uint32_t* __restrict__ pos) {
+  {
     const NoiseLevel& lv = L.lv[d];
     const uint8_t* rw = rows + lv.rows_off;
     auto em = [&](uint64_t j) { return *reinterpret_cast<const uint32_t*>(rw + (j - lv.inst_first) * lv.row_bytes); };
     const uint64_t A = lv.arity;
-    for (uint64_t idx = threadIdx.x; idx < lv.count; idx += blockDim.x) {
+    for (uint64_t idx = idx0; idx < lv.count; idx += stride) {
       const uint64_t j = lv.inst_first + idx;
       uint64_t bs, P = 0, Ps = 0, cfirst;
       if (d == 0) {
@@ -507,8 +507,26 @@ __global__ void __launch_bounds__(1024) dedup_map_kernel(const uint8_t* __restri
       }
       rep[lv.map_off + idx] = (uint32_t)(r - bs);
     }
+  }
+}
+
+// all levels, one CTA (levels in order)
+__global__ void __launch_bounds__(1024) dedup_map_kernel(const uint8_t* __restrict__ rows,
+                                                         const __grid_constant__ NoiseLevels L,
+                                                         uint32_t* __restrict__ rep, uint32_t* __restrict__ pos) {
+  for (uint32_t d = 0; d < L.n_levels; ++d) {
+    dedup_map_level(rows, L, d, threadIdx.x, blockDim.x, rep, pos);
     __syncthreads();
   }
+}
+
+// one level, one thread per instance (a chain of these on a side stream runs ahead of
+// the tree's levels)
+__global__ void __launch_bounds__(256) dedup_map_level_kernel(const uint8_t* __restrict__ rows,
+                                                              const __grid_constant__ NoiseLevels L, uint32_t d,
+                                                              uint32_t* __restrict__ rep, uint32_t* __restrict__ pos) {
+  dedup_map_level(rows, L, d, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x,
+                  rep, pos);
 }
 
 // The run's seed in device memory: the tree's launches (a replayed CUDA graph) read it
@@ -530,6 +548,15 @@ int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const 
 int launch_dedup_map(const uint8_t* d_rows, const NoiseLevels& L, uint32_t* d_rep, uint32_t* d_pos,
                      void* stream) {
   dev::dedup_map_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(d_rows, L, d_rep, d_pos);
+  return (int)cudaGetLastError();
+}
+
+int launch_dedup_map_level(const uint8_t* d_rows, const NoiseLevels& L, uint32_t d, uint32_t* d_rep,
+                           uint32_t* d_pos, void* stream) {
+  const uint64_t cnt = L.lv[d].count;
+  if (cnt == 0) return 0;
+  const unsigned grid = (unsigned)std::min<uint64_t>((cnt + 255) / 256, 4096);
+  dev::dedup_map_level_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_rows, L, d, d_rep, d_pos);
   return (int)cudaGetLastError();
 }
 

@@ -42,6 +42,7 @@ struct tqsim_handle {
   // the leaf branch of the captured tree (see run_level: pipelined penultimate level)
   cudaStream_t leaf_stream = nullptr;
   cudaEvent_t pipe_ev[5] = {};   // level done [2], leaf done [2], join
+  std::vector<cudaEvent_t> map_ev; // per level: its dedup map is built (side-stream chain)
   std::vector<uint64_t> graph_key;
   tqsim_stats graph_stats{};
   std::vector<uint8_t> h_tables;  // host copy: [two flags | pass index] per lowered gate
@@ -249,6 +250,8 @@ struct Exec {
   bool leaf_issued = false;
   uint64_t pcnt[64] = {};   // instances of the current batch per level
   bool dedup = false;       // dedup maps built for this tree (no state dumps asked for)
+  const cudaEvent_t* map_ev = nullptr;   // side-stream map chain: level d's map is ready
+  bool map_waited[64] = {};
 };
 
 std::vector<uint64_t> level_firsts(const tqsim_handle* h, uint64_t t0) {
@@ -307,6 +310,10 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   char* buf = x.ws + x.L.off[d];
   const char* pbuf = parent_buf ? parent_buf : d > 0 ? x.ws + x.L.off[d - 1] : nullptr;
   const bool piped = x.pipe && d + 2 == levels;
+  if (x.map_ev && !x.map_waited[d]) {   // this level's dedup map (side-stream chain)
+    ckc(cudaStreamWaitEvent(x.st, x.map_ev[d], 0), "map wait");
+    x.map_waited[d] = true;
+  }
   const auto& passes = h->pp.levels[d];
   const uint32_t slice_begin = (uint32_t)h->plan.bounds[d];
   const uint32_t slice_len = (uint32_t)(h->plan.bounds[d + 1] - slice_begin);
@@ -502,10 +509,26 @@ void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
   x.dedup = !(h->debug && h->debug->n_dumps);
   if (x.dedup) {
     uint32_t* maps = reinterpret_cast<uint32_t*>(x.ws + x.L.map_off);
-    ck(launch_dedup_map(reinterpret_cast<const uint8_t*>(x.ws + x.L.rows_off), NL, maps, maps + x.L.map_entries,
-                        x.st),
-       "dedup map launch");
-    h->stats.kernel_launches++;
+    const uint8_t* rws = reinterpret_cast<const uint8_t*>(x.ws + x.L.rows_off);
+    if (x.pipe) {   // per-level kernels on the side stream, ahead of the levels that wait on them
+      while (h->map_ev.size() < levels) {
+        cudaEvent_t e;
+        ckc(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "map event");
+        h->map_ev.push_back(e);
+      }
+      ckc(cudaEventRecord(x.ev[4], x.st), "map fork");
+      ckc(cudaStreamWaitEvent(x.st2, x.ev[4], 0), "map fork wait");
+      for (size_t d = 0; d < levels; ++d) {
+        ck(launch_dedup_map_level(rws, NL, (uint32_t)d, maps, maps + x.L.map_entries, x.st2), "dedup map launch");
+        ckc(cudaEventRecord(h->map_ev[d], x.st2), "map record");
+        h->stats.kernel_launches++;
+      }
+      x.map_ev = h->map_ev.data();
+      x.leaf_issued = true;   // the side stream joins at the end
+    } else {
+      ck(launch_dedup_map(rws, NL, maps, maps + x.L.map_entries, x.st), "dedup map launch");
+      h->stats.kernel_launches++;
+    }
   }
   run_level(x, 0, t0, t1, 0);
   if (x.pipe && x.leaf_issued) {   // join the leaf branch
@@ -874,6 +897,7 @@ void tqsim_destroy(tqsim_handle* h) {
   if (h->leaf_stream) cudaStreamDestroy(h->leaf_stream);
   for (cudaEvent_t e : h->pipe_ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->map_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   delete h;
 }

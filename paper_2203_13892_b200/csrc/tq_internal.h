@@ -159,6 +159,8 @@ struct NoiseLevels {
 // its batch with the same effective parent did not either), pos = its batch-relative index.
 int launch_dedup_map(const uint8_t* d_rows, const NoiseLevels& L, uint32_t* d_rep, uint32_t* d_pos,
                      void* stream);
+int launch_dedup_map_level(const uint8_t* d_rows, const NoiseLevels& L, uint32_t d, uint32_t* d_rep,
+                           uint32_t* d_pos, void* stream);
 int launch_noise_rows_all(const uint8_t* d_two, const uint8_t* d_pass_of, const NoiseLevels& L,
                           uint64_t total_instances, const uint64_t* d_seed, double p1, double p2,
                           uint8_t* d_rows, void* stream);
