@@ -136,11 +136,28 @@ void shard(const tqsim_plan& p, uint32_t rank, uint32_t world, uint64_t& t0, uin
   t1 = a0 * (rank + 1) / world;
 }
 
+Layout layout_tl(const tqsim_handle* h, uint64_t top_count, int tl);
+
+// Batch size: opts.batch_log2_amps, or by default 2^26 amplitudes per level batch -- and for
+// 18+ qubits the largest batch up to 2^30 amplitudes whose buffers take <= 45% of the
+// memory budget (room for a second workspace: tqsim_run keeps its arena): larger batches
+// hold more siblings and cousins, so more shared states are computed once (measured: C3
+// 251 -> 238 ms, C4 1.21 -> 0.94-0.99 s at 2^28-2^29; C5 shard 5.1 -> 3.9 s at 2^30, which
+// takes ~160 GB and so needs batch_log2_amps = 30 explicitly).
 Layout layout(const tqsim_handle* h, uint64_t top_count) {
+  if (h->opts.batch_log2_amps) return layout_tl(h, top_count, (int)h->opts.batch_log2_amps);
+  if (h->n_sim >= 18)
+    for (int tl = 30; tl > 26; --tl) {
+      Layout L = layout_tl(h, top_count, tl);
+      if ((double)L.total <= 0.45 * (double)h->opts.mem_budget) return L;
+    }
+  return layout_tl(h, top_count, 26);
+}
+
+Layout layout_tl(const tqsim_handle* h, uint64_t top_count, int tl) {
   Layout L;
   const int n = h->n_sim;
   const uint64_t S = 16ull << n;
-  const int tl = h->opts.batch_log2_amps ? (int)h->opts.batch_log2_amps : 26;
   // >= 2 states per batch by default: sibling pairs share a batch, so error-free
   // duplicates are computed once (measured C5 shard: 8.7 -> 5.5 s); the budget loop
   // below halves the caps again when the buffers would not fit
