@@ -282,6 +282,11 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* circuit, const tqsim_noise_model*
                           tqsim_result** out);
 void tqsim_result_free(tqsim_result* r);
 
+/* [host] Release what tqsim_run / tqsim_run_ex keep between calls: the prepared-handle
+ * (plan) cache, the device workspace arena and the page-locked outcome buffer.  The next
+ * call plans and allocates again.  Not concurrent with a running tqsim_run. */
+void tqsim_release_run_cache(void);
+
 /* [gpu] B200 state-copy cost in gate units (§3.3, fig:copy-overhead; SURVEY
  * §8(f) #2): *copy_ms = device-to-device copy of a 1 GiB batch of n-qubit states,
  * *gate_ms = the engine's time per gate application on the same batch (seeded probe

@@ -1134,6 +1134,18 @@ tqsim_status tqsim_run(const tqsim_circuit* c, const tqsim_noise_model* nm, uint
   return tqsim_run_ex(c, nm, n_shots, tree_arities, n_levels, seed, nullptr, nullptr, out);
 }
 
+void tqsim_release_run_cache(void) {
+  std::lock_guard<std::mutex> lock(g_arena_mu);
+  for (auto& e : g_hcache) tqsim_destroy(e.h);
+  g_hcache.clear();
+  if (g_arena) cudaFree(g_arena);
+  g_arena = nullptr;
+  g_arena_size = 0;
+  if (g_pinned) cudaFreeHost(g_pinned);
+  g_pinned = nullptr;
+  g_pinned_size = 0;
+}
+
 void tqsim_result_free(tqsim_result* r) {
   if (!r) return;
   std::free(r->bitstrings);

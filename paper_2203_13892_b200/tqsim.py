@@ -145,6 +145,7 @@ _SIGS = {
                                _P(C.c_uint32), C.c_uint32, C.c_uint64, _P(tqsim_options),
                                _P(tqsim_debug), _P(_P(tqsim_result))]),
     "tqsim_result_free": (None, [_P(tqsim_result)]),
+    "tqsim_release_run_cache": (None, []),
     "tqsim_debug_philox": (C.c_int, [_P(C.c_uint32), C.c_uint64, _P(C.c_uint32)]),
     "tqsim_debug_noise_table": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64,
                                           C.c_uint64, _P(C.c_uint8)]),
@@ -447,6 +448,11 @@ def tqsim_run(n_qubits, gates, noise, n_shots, arities=None, seed=0) -> Result:
     finally:
         lib().tqsim_result_free(r)
     return out
+
+
+def tqsim_release_run_cache() -> None:
+    """Free tqsim_run's plan cache, workspace arena and page-locked buffer."""
+    lib().tqsim_release_run_cache()
 
 
 def tqsim_debug_philox(words: np.ndarray) -> np.ndarray:

@@ -60,6 +60,8 @@ def test_c4_beta0_all_leaves_closed_form():
 
 def test_c5_ry0_shard_sparse_oracle():
     torch = pytest.importorskip("torch")
+    T.tqsim_release_run_cache()        # earlier tests' tqsim_run arena (tens of GB)
+    torch.cuda.empty_cache()
     w = make_variant("c5_hea28_ry0")
     n, gates, noise, shots, ar = T.workload_args(w)
     h = T.tqsim_create(n, gates, noise, shots, ar)

@@ -385,3 +385,15 @@ def test_leaf_dedup_equals_stored_path(n, ar, blog, tile):
     if n <= 16:
         ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 5)
         assert_leaves_match(a.leaf_outcomes, ref.leaves)
+
+
+def test_release_run_cache_then_run_again():
+    """tqsim_release_run_cache frees the plan cache, arena and pinned buffer; the next
+    tqsim_run plans and allocates again and gives the same outcomes."""
+    w = load_config("c1_qft5")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    a = T.tqsim_run(n, gates, noise, shots, ar, 3)
+    T.tqsim_release_run_cache()
+    b = T.tqsim_run(n, gates, noise, shots, ar, 3)
+    assert np.array_equal(a.leaf_outcomes, b.leaf_outcomes)
+    assert a.counts == b.counts
