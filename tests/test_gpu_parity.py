@@ -397,3 +397,19 @@ def test_release_run_cache_then_run_again():
     b = T.tqsim_run(n, gates, noise, shots, ar, 3)
     assert np.array_equal(a.leaf_outcomes, b.leaf_outcomes)
     assert a.counts == b.counts
+
+
+@pytest.mark.parametrize("tile,p", [(0, 0.002), (6, 0.01), (9, 0.05), (11, 0.002)])
+def test_random_circuits_dedup_vs_oracle(tile, p):
+    """Random circuits (every gate kind, SWAP / CP / CX ladders) through the default path --
+    no state dumps, so shared states are computed once (dedup maps) and the leaves are
+    sampled without stored states -- against the oracle's outcomes."""
+    rng = np.random.default_rng(500 + tile)
+    for it in range(3):
+        n = int(rng.integers(5, 15))
+        gates = random_circuit(n, int(rng.integers(30, 90)), rng)
+        nm = NoiseModel(p, 2 * p, 0.02, 0.03)
+        arities = [[3, 2, 4], [4, 4, 2], [2, 3, 2, 2]][it]
+        shots = int(np.prod(arities))
+        opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 3)
+        run_and_compare(n, gates, nm, shots, arities, 900 + it, opts)
