@@ -1656,6 +1656,43 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             if (v & 2) { u[1] = -u[1]; u[2] = -u[2]; }
             for (int i = 0; i < 4; ++i) V[v][i] = u[i];
           }
+          bool hl = true;
+          for (int v = 0; v < 4; ++v) hl = hl && hadamard_like(V[v]) && std::abs(V[v][0].real()) == std::abs(V[0][0].real());
+          if (hl) {
+            // Hadamard-like: V_v = diag(s00, s10) h [[1, a], [1, b]] (a = s01 s00, b = s11 s10):
+            // registers get the add/sub butterfly, h joins the (uniform) pending phases, and
+            // diag(s00, s10) = s00 Z^[s10 != s00] joins the frame (fk += 2, fz ^= e_q)
+            const double h = std::abs(V[0][0].real());
+            double sa[4], sb[4];
+            int gneg[4], zfl[4];
+            for (int v = 0; v < 4; ++v) {
+              const double s00 = V[v][0].real() > 0 ? 1 : -1, s01 = V[v][1].real() > 0 ? 1 : -1;
+              const double s10 = V[v][2].real() > 0 ? 1 : -1, s11 = V[v][3].real() > 0 ? 1 : -1;
+              sa[v] = s01 * s00;
+              sb[v] = s11 * s10;
+              gneg[v] = s00 < 0 ? 1 : 0;
+              zfl[v] = s10 != s00 ? 1 : 0;
+            }
+            std::ostringstream oo;
+            oo << "      const tq_u32 v = ((fx >> " << f.qa << ") & 1u) | (((fz >> " << f.qa << ") & 1u) << 1);\n";
+            auto sel4 = [&](const double* t) {
+              std::ostringstream e;
+              e << "((v & 2u) ? ((v & 1u) ? " << t[3] << ".0 : " << t[2] << ".0) : ((v & 1u) ? " << t[1] << ".0 : " << t[0] << ".0))";
+              return e.str();
+            };
+            auto bits4 = [&](const int* t) { return (unsigned)(t[0] | t[1] << 1 | t[2] << 2 | t[3] << 3); };
+            oo << "      const double sa = " << sel4(sa) << ", sb = " << sel4(sb) << ";\n";
+            oo << "      fk += ((" << bits4(gneg) << "u >> v) & 1u) << 1;\n";
+            oo << "      fz ^= ((" << bits4(zfl) << "u >> v) & 1u) << " << f.qa << ";\n";
+            for (int k = 0; k < 16; ++k) {
+              if (k >> ba & 1) continue;
+              const std::string va = g.r(k), vb = g.r(k | 1 << ba);
+              oo << "      { const tq_d2 x = " << va << ", y = " << vb << "; " << va << ".x = fma(sa, y.x, x.x); " << va
+                 << ".y = fma(sa, y.y, x.y); " << vb << ".x = fma(sb, y.x, x.x); " << vb << ".y = fma(sb, y.y, x.y); }\n";
+            }
+            for (int k = 0; k < 16; ++k) dph[k] *= h;   // uniform: commutes with every later op
+            o << "    {\n" << oo.str() << "    }\n";
+          } else {
           pool.begin_op();
           std::ostringstream oo;
           oo << "      const tq_u32 v = ((fx >> " << f.qa << ") & 1u) | (((fz >> " << f.qa << ") & 1u) << 1);\n";
@@ -1712,6 +1749,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             oo << "        " << vb << ".y = " << linx(2, "x", 3, "y", true) << "; }\n";
           }
           o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
+          }
         } else if (f.kind == FOp::DIAG) {
           pool.begin_op();
           const int ra = rbit(f.qa), rb = f.qb >= 0 ? rbit(f.qb) : -2;
