@@ -352,6 +352,21 @@ M4 dagger(const M4& m) {
 
 bool near(const cplx& a, const cplx& b) { return std::abs(a - b) < 1e-13; }
 
+// The four frame variants of a one-qubit matrix are c [[1, s u], [s w, 1]] with one sign s
+// per variant (RX, RY; c real, |u|, |w| <= 1)
+bool sign_variants(const cplx V[4][4]) {
+  const cplx c = V[0][0];
+  if (c.imag() != 0.0 || c.real() <= 0.0) return false;
+  if (std::abs(V[0][1]) > c.real() || std::abs(V[0][2]) > c.real()) return false;
+  for (int v = 0; v < 4; ++v) {
+    if (V[v][0] != c || V[v][3] != c) return false;
+    const bool same = std::abs(V[v][1] - V[0][1]) < 1e-15 && std::abs(V[v][2] - V[0][2]) < 1e-15;
+    const bool flip = std::abs(V[v][1] + V[0][1]) < 1e-15 && std::abs(V[v][2] + V[0][2]) < 1e-15;
+    if (!same && !flip) return false;
+  }
+  return true;
+}
+
 // exact 0 / +-1 for components within rounding of them (phases composed at generation time)
 cplx snap(cplx v) {
   auto s1 = [](double x) {
@@ -1692,6 +1707,38 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             }
             for (int k = 0; k < 16; ++k) dph[k] *= h;   // uniform: commutes with every later op
             o << "    {\n" << oo.str() << "    }\n";
+          } else if (sign_variants(V)) {
+            // V_v = c [[1, sg_v u], [sg_v w, 1]] (RX, RY: the frame only flips the sign of the
+            // off-diagonal): one FMA per output component per nonzero part of u / w, c joins
+            // the (uniform) pending phases
+            const double c = V[0][0].real();
+            const cplx u = V[0][1] / c, w = V[0][2] / c;
+            unsigned neg = 0;
+            for (int v = 0; v < 4; ++v)
+              if (std::abs(V[v][1] + V[0][1]) < 1e-15 && std::abs(V[0][1]) > 0) neg |= 1u << v;
+            pool.begin_op();
+            std::ostringstream oo;
+            oo << "      const tq_u32 v = ((fx >> " << f.qa << ") & 1u) | (((fz >> " << f.qa << ") & 1u) << 1);\n";
+            oo << "      const double sg = ((" << neg << "u >> v) & 1u) ? -1.0 : 1.0;\n";
+            auto term = [&](double cv, const std::string& src, std::string& e) {   // e += sg*cv*src
+              if (cv == 0.0) return;
+              e = "fma(sg * " + g_pool->ref(cv) + ", " + src + ", " + e + ")";
+            };
+            for (int k = 0; k < 16; ++k) {
+              if (k >> ba & 1) continue;
+              const std::string va = g.r(k), vb = g.r(k | 1 << ba);
+              std::string a0 = "x.x", a1 = "x.y", b0 = "y.x", b1 = "y.y";
+              // out0 = x + sg u y: re += u.re y.x - u.im y.y, im += u.re y.y + u.im y.x
+              term(u.real(), "y.x", a0); term(-u.imag(), "y.y", a0);
+              term(u.real(), "y.y", a1); term(u.imag(), "y.x", a1);
+              // out1 = y + sg w x
+              term(w.real(), "x.x", b0); term(-w.imag(), "x.y", b0);
+              term(w.real(), "x.y", b1); term(w.imag(), "x.x", b1);
+              oo << "      { const tq_d2 x = " << va << ", y = " << vb << "; " << va << ".x = " << a0 << "; " << va
+                 << ".y = " << a1 << "; " << vb << ".x = " << b0 << "; " << vb << ".y = " << b1 << "; }\n";
+            }
+            for (int k = 0; k < 16; ++k) dph[k] *= c;
+            o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
           } else {
           pool.begin_op();
           std::ostringstream oo;
