@@ -94,6 +94,11 @@ typedef struct {
   uint32_t tile_qubits;       /* HBM-pass tile width K (4..13); 0 = auto (12) */
   uint32_t batch_log2_amps;   /* target amplitudes per level batch = 2^v; 0 = auto (26) */
   uint32_t profile;           /* 1 = time every kernel launch with CUDA events (tqsim_stats) */
+  uint32_t no_dedup;          /* 0 (default) = an error-free instance whose effective parent
+                                 state equals an earlier instance's of its batch shares that
+                                 instance's computed state (bit-identical);
+                                 1 = every node instance of the tree is computed */
+  uint32_t reserved;          /* 0 */
 } tqsim_options;
 
 /* The tree plan (§3.1): level d executes lowered gates
@@ -131,6 +136,12 @@ typedef struct {
   uint64_t leaves;                  /* leaves sampled by this shard */
   uint64_t noise_launches;          /* noise-row kernels (one per level batch) */
   double noise_ms;                  /* sum of noise-row launch durations (profile=1 only) */
+  /* Work actually executed (error-free duplicates skipped, options.no_dedup = 0).  Filled by
+   * tqsim_profile_tree and by tqsim_run_ex / tqsim_run (which synchronize); tqsim_execute
+   * (asynchronous) leaves them 0. */
+  uint64_t computed_node_executions;
+  uint64_t computed_gate_amp_updates;
+  uint64_t computed_pass_bytes;     /* algorithmic bytes of the computed instances' passes */
 } tqsim_stats;
 
 typedef struct {
@@ -143,15 +154,25 @@ typedef struct {
   tqsim_stats stats;
 } tqsim_result;
 
-/* Optional state dumps for parity tests: the state of node (level, instance)
- * after its subcircuit (after the last gate and its Pauli, before measurement)
- * is copied to dump_host + i * 2 * 2^n doubles (interleaved re, im). */
+/* Optional debug outputs for parity tests (§2.3 sampling, R9).
+ * State dumps: the state of node (level, instance) after its subcircuit (after the last
+ * gate and its Pauli, before measurement) is copied to dump_host + i * 2 * 2^n doubles
+ * (interleaved re, im).  Requesting dumps switches the run to the stored-state path
+ * (every instance computed, leaf states stored).
+ * Per-leaf sampler outputs (host arrays of plan.n_outcomes entries, either may be NULL;
+ * they do NOT change the execution path -- dedup maps and the no-store leaf sampler stay
+ * on): leaf_u[l] = the u53 uniform of leaf l (R9), leaf_flagged[l] = 1 iff u*total lies
+ * within 1e-9 of C(x-1) or C(x) for the sampled x (the draw a rounding difference could
+ * move), leaf_total[l] = sum |a|^2 of the leaf state as the sampler summed it. */
 typedef struct {
   uint32_t n_dumps;
   uint32_t reserved;
   const uint32_t* dump_levels;
   const uint64_t* dump_instances;
   double* dump_host;
+  double* leaf_u;
+  uint8_t* leaf_flagged;
+  double* leaf_total;
 } tqsim_debug;
 
 /* Operation record of the pass plan (for host-side invariant tests). */
@@ -229,9 +250,10 @@ tqsim_status tqsim_pass_source(const tqsim_circuit* circuit, const tqsim_noise_m
                                const tqsim_options* opts, uint32_t level, uint32_t pass, char* out,
                                uint64_t cap, uint64_t* n_out);
 
-/* [host] Shard of rank/world: level-0 instances
- * [top_begin, top_end) = [floor(A0*r/W), floor(A0*(r+1)/W)), whose leaves are
- * the contiguous range [leaf_begin, leaf_end). */
+/* [host] Shard of rank/world (see tqsim_shard_levels): the level-0
+ * instances [top_begin, top_end) the rank runs (ancestors of its split-level range,
+ * recomputed when the split is below level 0) and its contiguous leaf range
+ * [leaf_begin, leaf_end).  When world divides A_0 this is [A0*r/W, A0*(r+1)/W). */
 tqsim_status tqsim_shard_range(const tqsim_plan* plan, uint32_t rank, uint32_t world,
                                uint64_t* top_begin, uint64_t* top_end, uint64_t* leaf_begin,
                                uint64_t* leaf_end);
@@ -268,6 +290,39 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
                                   void* stream, void* d_workspace, uint64_t workspace_bytes,
                                   uint32_t* d_leaf_outcomes, uint32_t reps, tqsim_pass_timing* out,
                                   uint64_t cap, uint64_t* n_out);
+
+/* In-tree timing of the tree's kernels, aggregated per (kind, level, pass) (tqsim_profile_tree). */
+typedef struct {
+  uint32_t kind;              /* 0 gate pass (tq_pass_l<level>_p<pass>), 1 leaf measurement of the
+                                 level (select + leaf recompute + finish kernels), 2 noise rows */
+  uint32_t level, pass;
+  uint32_t reserved;
+  uint64_t launches;
+  uint64_t states;            /* node instances the launches covered (their grids) */
+  uint64_t computed_states;   /* instances actually computed (dedup representatives) */
+  double ms;                  /* sum of the launches' CUDA-event durations (serialised, in tree order) */
+  double alg_bytes;           /* algorithmic HBM bytes of the computed instances */
+  double nominal_bytes;       /* the same counted for every instance (SURVEY §8(d) per-unit figure) */
+  double fp64_per_amp;        /* kind 0: FP64 operations per amplitude of the fast path (cost model) */
+} tqsim_kernel_timing;
+
+/* [gpu] Run the shard once with every launch bracketed by CUDA events on `stream` (no graph,
+ * no pipelining: the kernels run in tree order, one at a time) and report each kernel
+ * family's summed device time with the work it did (the roofline input of bench.py).
+ * Synchronous.  out: capacity `cap` records (NULL / 0 to query *n_out). */
+tqsim_status tqsim_profile_tree(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world,
+                                void* stream, void* d_workspace, uint64_t workspace_bytes,
+                                uint32_t* d_leaf_outcomes, tqsim_kernel_timing* out, uint64_t cap,
+                                uint64_t* n_out);
+
+/* [host] The shard's instance range at every level: the tree is split at
+ * level *split_level, the first level whose instance count is a multiple of world (else
+ * the first with >= 16 * world instances, else the leaf level); rank owns level-split
+ * instances [I*rank/world, I*(rank+1)/world) and all their descendants, and recomputes
+ * their ancestors.  lo, hi: arrays of plan->n_levels entries (host); the rank's level-d
+ * instances are [lo[d], hi[d]). */
+tqsim_status tqsim_shard_levels(const tqsim_plan* plan, uint32_t rank, uint32_t world,
+                                uint32_t* split_level, uint64_t* lo, uint64_t* hi);
 
 /* [gpu] The north_star call: host circuit in, host histogram out (allocates
  * its own workspace, synchronous).  tree_arities NULL = auto (DCP). */

@@ -986,7 +986,7 @@ uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal, boo
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs, int variant = 0,
-                     std::vector<uint32_t>* out_row = nullptr) {
+                     std::vector<uint32_t>* out_row = nullptr, double* fp64_out = nullptr) {
   const int K = pd.K, T = 1 << (K - RBITS);
   const int low = std::min(LOW_Q, K);
   const bool coal = K - RBITS >= low;   // enough lane bits to keep qubits 0..2 on lanes 0..2
@@ -1033,6 +1033,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     const double cost = fcost + 12.0 * (double)ph.size();
     if (cand == 0 || cost < best_cost) {
       best_cost = cost;
+      if (fp64_out) *fp64_out = fcost;
       fops = std::move(ops);
       fast = std::move(ph);
       R0 = r0;
@@ -1167,7 +1168,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   for (size_t i = 0; i < site_list.size(); ++i) o << (i ? "," : "") << site_list[i];
   if (site_list.empty()) o << "0";
   o << "};\n";
-  o << "static __constant__ unsigned short GOFF[" << std::max(nops, 1) << "] = {";
+  // gate offsets inside the slice (a slice may exceed 65,535 lowered gates: flat plans)
+  o << "static __constant__ " << (pd.slice_len > 65535u ? "tq_u32" : "unsigned short") << " GOFF["
+    << std::max(nops, 1) << "] = {";
   for (int i = 0; i < nops; ++i) o << (i ? "," : "") << (pp.ops[pd.op_begin + i].gate - pd.slice_begin);
   if (!nops) o << "0";
   o << "};\nstatic __device__ const tq_u32 ERRX[" << errx.size() << "] = {";
@@ -2223,6 +2226,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
     std::string err;
     std::vector<double> coefs;
     std::vector<uint32_t> out_row;
+    double fp64 = 0.0;
   };
   std::vector<Job> jobs;
   std::vector<std::vector<JitPass>> out(pp.levels.size());
@@ -2238,7 +2242,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
         j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : "");
         const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
         std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
-                                    j.smem, j.coefs, v, &j.out_row);
+                                    j.smem, j.coefs, v, &j.out_row, &j.fp64);
         j.src = std::string(kPrelude) + kJitTypes + body;
         jobs.push_back(std::move(j));
       }
@@ -2303,6 +2307,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
       jp.smem = j.smem;
       jp.coefs = j.coefs;
       jp.out_row = j.out_row;
+      jp.fp64_per_amp = j.fp64;
     } else {
       (j.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute) = reinterpret_cast<void*>(ck.fn);
     }

@@ -30,7 +30,17 @@ struct SelectOut {
   uint32_t n_out;
   uint32_t out_row[32];       // out-of-tile qubit i = parity(out_row[i] & stored address)
   const uint32_t* rep;        // dedup map of the leaf batch (null: every leaf computed)
+  // debug outputs (tqsim_debug; null = not requested), indexed by global leaf id
+  double* dbg_u;
+  double* dbg_total;
+  uint8_t* dbg_flag;
 };
+
+// R9: the draw is flagged when u*total lies within 1e-9 of C(x-1) or C(x).  t = target
+// relative to the run start, c0 / c1 = the run's cumulative sums before / after x.
+__device__ __forceinline__ uint8_t tq_flag(double t, double c0, double c1) {
+  return (uint8_t)((t - c0 < 1e-9) || (c1 - t < 1e-9));
+}
 
 // The leaf whose run sums leaf s reads (the dedup map: the gate passes computed only it)
 __device__ __forceinline__ uint32_t tq_dedup_rep(const SelectOut& so, uint64_t leaf_first, uint32_t s) {
@@ -195,6 +205,8 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
   if (threadIdx.x == 0) total_sh = tot;
   __syncthreads();
   const double target = u * total_sh;
+  if (threadIdx.x == 0 && so.dbg_u) so.dbg_u[leaf] = u;
+  if (threadIdx.x == 0 && so.dbg_total) so.dbg_total[leaf] = total_sh;
   // level 1: chunk;  level 2: 8-amplitude run inside the chunk;  level 3: amplitude
   double before1 = 0.0, before2 = 0.0;
   const uint64_t chunk = block_search(cs, nc, target, &before1, wsum, &first_sh, &pick_sh, &before_sh);
@@ -212,16 +224,22 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
     const double t3 = target - before1 - before2;
     const uint64_t base = ((chunk * rpc + run) << RUN_Q);
     const cd* ap = states + ((uint64_t)s << n) + base;
-    double acc = 0.0;
+    double acc = 0.0, c0 = 0.0, c1 = 0.0;
     int x = -1, lastnz = -1;
     for (int e = 0; e < (1 << RUN_Q); ++e) {
       const cd v = ap[e];
       const double pr = v.x * v.x + v.y * v.y;
       if (pr > 0.0) lastnz = e;
+      if (x < 0) c0 = acc;
       acc += pr;
-      if (x < 0 && acc > t3) x = e;
+      if (x < 0 && acc > t3) {
+        x = e;
+        c1 = acc;
+      }
     }
+    uint8_t flag = x < 0 ? 1 : tq_flag(t3, c0, c1);
     if (x < 0) x = lastnz >= 0 ? lastnz : 0;   // rounding: the last non-zero amplitude of the run
+    if (so.dbg_flag) so.dbg_flag[leaf] = flag;
     const uint32_t xi = (uint32_t)(base + (uint64_t)x);
     // readout (R11): bit b flips iff word (b&3) of Philox(ctr=(b>>2, leaf, 2, 0)) * 2^-32 < p
     uint32_t mask = 0;
@@ -283,7 +301,10 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
   // every warp walks the W segment totals (identical order -> identical decision)
   double total = 0.0;
   for (uint32_t i = 0; i < W; ++i) total += wtot[i];
-  const double target = tq_measure_uniform(leaf, seed) * total;
+  const double u = tq_measure_uniform(leaf, seed);
+  const double target = u * total;
+  if (threadIdx.x == 0 && so.dbg_u) so.dbg_u[leaf] = u;
+  if (threadIdx.x == 0 && so.dbg_total) so.dbg_total[leaf] = total;
   double before = 0.0;
   int ws = -1, wlast = 0;
   for (uint32_t i = 0; i < W; ++i) {
@@ -337,15 +358,20 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
   }
   const uint64_t abase = (uint64_t)run << RUN_Q;
   const cd* ap = states + ((uint64_t)s << n) + abase;
-  double c = 0.0;
+  double c = 0.0, c0 = 0.0, c1 = 0.0;
   int x = -1, lastamp = -1;
   for (int e = 0; e < (1 << RUN_Q); ++e) {
     const cd v = ap[e];
     const double pr = v.x * v.x + v.y * v.y;
     if (pr > 0.0) lastamp = e;
+    if (x < 0) c0 = c;
     c += pr;
-    if (x < 0 && c > t3) x = e;
+    if (x < 0 && c > t3) {
+      x = e;
+      c1 = c;
+    }
   }
+  if (so.dbg_flag) so.dbg_flag[leaf] = x < 0 ? 1 : tq_flag(t3, c0, c1);
   if (x < 0) x = lastamp >= 0 ? lastamp : 0;
   const uint32_t xi = (uint32_t)(abase + (uint64_t)x);
   out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
@@ -358,22 +384,28 @@ __global__ void __launch_bounds__(MT) sample_finish_kernel(const cd* __restrict_
                                                            const double* __restrict__ t3s, uint32_t batch,
                                                            uint32_t n_user, uint64_t leaf_first,
                                                            const uint64_t* __restrict__ seedp, double p01,
-                                                           double p10, uint32_t* __restrict__ out) {
+                                                           double p10, uint32_t* __restrict__ out,
+                                                           uint8_t* __restrict__ dbg_flag) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= batch) return;
   const uint64_t seed = *seedp;
   const uint64_t leaf = leaf_first + s;
   const double t3 = t3s[s];
   const cd* ap = scratch + ((uint64_t)s << RUN_Q);
-  double c = 0.0;
+  double c = 0.0, c0 = 0.0, c1 = 0.0;
   int x = -1, lastamp = -1;
   for (int e = 0; e < (1 << RUN_Q); ++e) {
     const cd v = ap[e];
     const double pr = v.x * v.x + v.y * v.y;
     if (pr > 0.0) lastamp = e;
+    if (x < 0) c0 = c;
     c += pr;
-    if (x < 0 && c > t3) x = e;
+    if (x < 0 && c > t3) {
+      x = e;
+      c1 = c;
+    }
   }
+  if (dbg_flag) dbg_flag[leaf] = x < 0 ? 1 : tq_flag(t3, c0, c1);
   if (x < 0) x = lastamp >= 0 ? lastamp : 0;
   const uint32_t xi = (uint32_t)(((uint64_t)runsel[s] << RUN_Q) + (uint64_t)x);
   out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
@@ -482,7 +514,9 @@ __device__ __forceinline__ void dedup_map_level(const uint8_t* __restrict__ rows
         P = j / A;
         const uint64_t pidx = P - pl.inst_first;
         const uint64_t pbs = P - pos[pl.map_off + pidx];
-        const uint64_t rs = pbs * A;
+        // the parent batch's children start at pbs * A, clipped to the shard's first
+        // instance of this level (a shard split below level 0 recomputes its ancestors)
+        const uint64_t rs = pbs * A > lv.inst_first ? pbs * A : lv.inst_first;
         bs = rs + ((j - rs) / lv.cap) * lv.cap;
         Ps = pbs + rep[pl.map_off + pidx];
         cfirst = P * A;
@@ -589,6 +623,9 @@ int launch_chunk_sums(const double* runsums, uint32_t batch, int n_sim, int chun
 static dev::SelectOut select_out(const LeafSelect* sel) {
   dev::SelectOut so{};
   if (!sel) return so;
+  so.dbg_u = sel->dbg_u;
+  so.dbg_total = sel->dbg_total;
+  so.dbg_flag = sel->dbg_flag;
   so.runsel = sel->runsel;
   so.t3 = sel->t3;
   so.tile = sel->tile;
@@ -611,11 +648,11 @@ int launch_sample(const void* states, const double* runsums, const double* sums,
 
 int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
                          int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
-                         uint32_t* d_out, void* stream) {
+                         uint32_t* d_out, void* stream, uint8_t* d_flag) {
   if (batch == 0) return 0;
   dev::sample_finish_kernel<<<(batch + dev::MT - 1) / dev::MT, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const dev::cd*>(scratch), runsel, t3, batch, (uint32_t)n_user, leaf_first, d_seed, p01, p10,
-      d_out);
+      d_out, d_flag);
   return (int)cudaGetLastError();
 }
 

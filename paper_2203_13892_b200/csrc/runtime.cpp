@@ -15,7 +15,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <new>
 
 #include "tq_internal.h"
@@ -53,6 +56,18 @@ struct tqsim_handle {
   std::vector<std::pair<int, size_t>> ev_marks;   // (kind 0 pass / 1 measure / 2 noise, event index)
   const tqsim_debug* debug = nullptr;
   cudaStream_t debug_stream = nullptr;
+  // per-leaf sampler debug outputs (device, global leaf id; set by tqsim_run_ex for one call)
+  double* d_dbg_u = nullptr;
+  double* d_dbg_total = nullptr;
+  uint8_t* d_dbg_flag = nullptr;
+  // tqsim_profile_tree: one tag per event interval (kind, level, pass, batch start, count)
+  struct Tag {
+    int kind;
+    uint32_t level, pass;
+    uint64_t b, cnt;
+  };
+  std::vector<Tag> ev_tags;
+  bool tag_launches = false;
 };
 
 namespace tq {
@@ -129,14 +144,58 @@ struct Layout {
 constexpr uint64_t ALIGN = 256;
 inline uint64_t align_up(uint64_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
 
-void shard(const tqsim_plan& p, uint32_t rank, uint32_t world, uint64_t& t0, uint64_t& t1) {
+// Shard of rank r of W: the tree is split at the split level d*, the first
+// level whose instance count I is a multiple of W (else the first with I >= 16 W, else the
+// leaf level); rank r owns the level-d* instances [I r / W, I (r+1) / W) and everything
+// below them, and recomputes the few ancestors above them (instances are keyed, so a
+// recomputed ancestor is bit-identical on every rank).  lo[d], hi[d]: the rank's
+// contiguous instance range at level d.
+struct ShardRange {
+  uint32_t split = 0;
+  std::vector<uint64_t> lo, hi;
+  uint64_t count(size_t d) const { return hi[d] - lo[d]; }
+  bool empty() const { return hi.empty() || hi[0] <= lo[0]; }
+};
+
+ShardRange shard_levels(const tqsim_plan& p, uint32_t rank, uint32_t world) {
   if (world < 1 || rank >= world) throw Error{TQSIM_EINVAL, "rank must be < world, world >= 1"};
-  const uint64_t a0 = p.arities[0];
-  t0 = a0 * rank / world;
-  t1 = a0 * (rank + 1) / world;
+  const uint32_t L = p.n_levels;
+  std::vector<uint64_t> inst(L);
+  uint64_t v = 1;
+  for (uint32_t d = 0; d < L; ++d) inst[d] = v *= p.arities[d];
+  uint32_t ds = L - 1;
+  bool found = false;
+  for (uint32_t d = 0; d < L && !found; ++d)
+    if (inst[d] % world == 0) ds = d, found = true;
+  for (uint32_t d = 0; d < L && !found; ++d)
+    if (inst[d] >= 16ull * world) ds = d, found = true;
+  ShardRange r;
+  r.split = ds;
+  r.lo.assign(L, 0);
+  r.hi.assign(L, 0);
+  r.lo[ds] = inst[ds] * rank / world;
+  r.hi[ds] = inst[ds] * (rank + 1) / world;
+  if (r.hi[ds] > r.lo[ds]) {
+    for (uint32_t d = ds; d-- > 0;) {   // ancestors (recomputed)
+      r.lo[d] = r.lo[d + 1] / p.arities[d + 1];
+      r.hi[d] = (r.hi[d + 1] + p.arities[d + 1] - 1) / p.arities[d + 1];
+    }
+    for (uint32_t d = ds + 1; d < L; ++d) {
+      r.lo[d] = r.lo[d - 1] * p.arities[d];
+      r.hi[d] = r.hi[d - 1] * p.arities[d];
+    }
+  }
+  return r;
 }
 
-Layout layout_tl(const tqsim_handle* h, uint64_t top_count, int tl);
+// level-0 range [t0, t1) of the shard (used for the public range query)
+void shard(const tqsim_plan& p, uint32_t rank, uint32_t world, uint64_t& t0, uint64_t& t1) {
+  const ShardRange r = shard_levels(p, rank, world);
+  t0 = r.lo[0];
+  t1 = r.hi[0];
+}
+
+Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl);
 
 // Batch size: opts.batch_log2_amps, or by default 2^26 amplitudes per level batch -- and for
 // 18+ qubits the largest batch up to 2^30 amplitudes whose buffers take <= 45% of the
@@ -144,17 +203,17 @@ Layout layout_tl(const tqsim_handle* h, uint64_t top_count, int tl);
 // hold more siblings and cousins, so more shared states are computed once (measured: C3
 // 251 -> 238 ms, C4 1.21 -> 0.94-0.99 s at 2^28-2^29; C5 shard 5.1 -> 3.9 s at 2^30, which
 // takes ~160 GB and so needs batch_log2_amps = 30 explicitly).
-Layout layout(const tqsim_handle* h, uint64_t top_count) {
-  if (h->opts.batch_log2_amps) return layout_tl(h, top_count, (int)h->opts.batch_log2_amps);
+Layout layout(const tqsim_handle* h, const ShardRange& sr) {
+  if (h->opts.batch_log2_amps) return layout_tl(h, sr, (int)h->opts.batch_log2_amps);
   if (h->n_sim >= 18)
     for (int tl = 30; tl > 26; --tl) {
-      Layout L = layout_tl(h, top_count, tl);
+      Layout L = layout_tl(h, sr, tl);
       if ((double)L.total <= 0.45 * (double)h->opts.mem_budget) return L;
     }
-  return layout_tl(h, top_count, 26);
+  return layout_tl(h, sr, 26);
 }
 
-Layout layout_tl(const tqsim_handle* h, uint64_t top_count, int tl) {
+Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl) {
   Layout L;
   const int n = h->n_sim;
   const uint64_t S = 16ull << n;
@@ -164,11 +223,10 @@ Layout layout_tl(const tqsim_handle* h, uint64_t top_count, int tl) {
   const uint64_t target = std::max<uint64_t>(tl >= n ? (1ull << (tl - n)) : 1ull,
                                              h->opts.batch_log2_amps ? 1ull : 2ull);
   const size_t levels = h->plan.arities.size();
-  uint64_t per = std::max<uint64_t>(top_count, 1);
   for (size_t d = 0; d < levels; ++d) {
-    if (d > 0) per *= h->plan.arities[d];
+    const uint64_t per = sr.count(d);
     L.cap.push_back(std::max<uint64_t>(1, std::min(per, target)));
-    L.lvl_count.push_back(top_count ? per : 0);
+    L.lvl_count.push_back(per);
   }
   L.chunk_log2 = std::min(n, 12);
   auto total_of = [&](Layout& l) {
@@ -256,6 +314,7 @@ struct Exec {
   Layout L;
   uint32_t* d_out;
   std::vector<uint64_t> lvl_first;   // global id of the shard's first instance per level
+  std::vector<uint64_t> lvl_end;     // one past the shard's last instance per level
   // Pipelined penultimate level (captured tree only): its batches alternate between two
   // buffers; each batch's leaf work runs on a second stream, so the FP64-bound leaf passes
   // of batch k overlap the HBM-bound passes of batch k+1.
@@ -271,14 +330,9 @@ struct Exec {
   bool map_waited[64] = {};
 };
 
-std::vector<uint64_t> level_firsts(const tqsim_handle* h, uint64_t t0) {
-  std::vector<uint64_t> f;
-  uint64_t v = t0;
-  for (size_t d = 0; d < h->plan.arities.size(); ++d) {
-    if (d > 0) v *= h->plan.arities[d];
-    f.push_back(v);
-  }
-  return f;
+Exec make_exec(tqsim_handle* h, uint64_t seed, cudaStream_t st, void* ws, const ShardRange& sr, uint32_t* d_out) {
+  Exec x{h, seed, st, static_cast<char*>(ws), layout(h, sr), d_out, sr.lo, sr.hi};
+  return x;
 }
 
 cudaEvent_t next_event(tqsim_handle* h) {
@@ -290,8 +344,10 @@ cudaEvent_t next_event(tqsim_handle* h) {
   return h->ev_pool[h->ev_used++];
 }
 
-void mark(Exec& x, int kind) {
+void mark(Exec& x, int kind, uint32_t level = 0, uint32_t pass = 0, uint64_t b = 0, uint64_t cnt = 0) {
   if (!x.h->opts.profile) return;
+  if (x.h->tag_launches && (x.h->ev_marks.size() & 1) == 0)   // an interval opens
+    x.h->ev_tags.push_back(tqsim_handle::Tag{kind, level, pass, b, cnt});
   static const bool sync = [] {
     const char* e = std::getenv("TQSIM_PROFILE_SYNC");
     return e && e[0] == '1';
@@ -384,9 +440,9 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
         if (cnt > 1) pl.rep = maps + x.L.map_lvl[d] + (b - x.lvl_first[d]);
         if (d > 0 && x.pcnt[d - 1] > 1) pl.prep = maps + x.L.map_lvl[d - 1] + (parent_first - x.lvl_first[d - 1]);
       }
-      mark(x, 0);
+      mark(x, 0, d, (uint32_t)p, b, cnt);
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
-      mark(x, 0);
+      mark(x, 0, d, (uint32_t)p, b, cnt);
       h->stats.kernel_launches++;
       h->stats.pass_launches++;
       if (passes[p].leaf_sums) last = pl;
@@ -421,7 +477,10 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
                                          (b - x.lvl_first[d])
                                    : nullptr;
       for (size_t i = 0; i < jp.out_row.size() && i < 32; ++i) ls.out_row[i] = jp.out_row[i];
-      mark(x, 1);
+      ls.dbg_u = h->d_dbg_u;
+      ls.dbg_total = h->d_dbg_total;
+      ls.dbg_flag = nullptr;   // the finish kernel flags the draw
+      mark(x, 1, d, 0, b, cnt);
       if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {
         ck(launch_sample_small(buf, runs, (uint32_t)cnt, n, (int)h->n_user, b, h->d_seed, h->noise.readout_p01,
                                h->noise.readout_p10, x.d_out, x.st, &ls),
@@ -446,9 +505,9 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       rc.scratch = scratch;
       ck(launch_jit_pass(jp, passes[lp], rc, x.st), "leaf recompute launch");
       ck(launch_sample_finish(scratch, runsel, t3, (uint32_t)cnt, (int)h->n_user, b, h->d_seed,
-                              h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
+                              h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st, h->d_dbg_flag),
          "sample finish launch");
-      mark(x, 1);
+      mark(x, 1, d, 0, b, cnt);
       h->stats.kernel_launches += 2;
       h->stats.measure_launches += 2;
       // the recomputed tile per leaf (read its share of the source + 8 amplitudes written)
@@ -457,10 +516,14 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     } else if (leaf) {
       double* sums = reinterpret_cast<double*>(x.ws + x.L.sums_off);
       const double* runs = reinterpret_cast<const double*>(x.ws + x.L.runs_off);
-      mark(x, 1);
+      LeafSelect dbg{};   // stored-state path: only the debug outputs
+      dbg.dbg_u = h->d_dbg_u;
+      dbg.dbg_total = h->d_dbg_total;
+      dbg.dbg_flag = h->d_dbg_flag;
+      mark(x, 1, d, 0, b, cnt);
       if (n - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {   // one kernel: all run sums of each leaf
         ck(launch_sample_small(buf, runs, (uint32_t)cnt, n, (int)h->n_user, b, h->d_seed,
-                               h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
+                               h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st, &dbg),
            "sample launch");
         h->stats.kernel_launches += 1;
         h->stats.measure_launches += 1;
@@ -468,7 +531,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       } else {
         ck(launch_chunk_sums(runs, (uint32_t)cnt, n, x.L.chunk_log2, sums, x.st), "chunk sums launch");
         ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, x.L.chunk_log2, b, h->d_seed,
-                         h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st),
+                         h->noise.readout_p01, h->noise.readout_p10, x.d_out, x.st, &dbg),
            "sample launch");
         h->stats.kernel_launches += 2;
         h->stats.measure_launches += 2;
@@ -477,26 +540,27 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
                                   cnt * ((8ull << (n - x.L.chunk_log2)) +
                                          (8ull << (x.L.chunk_log2 - RUN_Q)) + (16ull << RUN_Q));
       }
+      mark(x, 1, d, 0, b, cnt);
       h->stats.leaves += cnt;
     } else if (piped) {
       const uint64_t A = h->plan.arities[d + 1];
       ckc(cudaEventRecord(x.ev[slot], x.st), "pipe record");
       ckc(cudaStreamWaitEvent(x.st2, x.ev[slot], 0), "pipe fork");
       std::swap(x.st, x.st2);
-      run_level(x, d + 1, b * A, (b + cnt) * A, b, buf);
+      run_level(x, d + 1, std::max(b * A, x.lvl_first[d + 1]), std::min((b + cnt) * A, x.lvl_end[d + 1]), b, buf);
       std::swap(x.st, x.st2);
       ckc(cudaEventRecord(x.ev[2 + slot], x.st2), "pipe record");
       x.slot_used[slot] = true;
       x.leaf_issued = true;
     } else {
       const uint64_t A = h->plan.arities[d + 1];
-      run_level(x, d + 1, b * A, (b + cnt) * A, b);
+      run_level(x, d + 1, std::max(b * A, x.lvl_first[d + 1]), std::min((b + cnt) * A, x.lvl_end[d + 1]), b);
     }
   }
 }
 
 // Every noise row of the shard (all levels) in one launch, then the tree.
-void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
+void run_tree(Exec& x) {
   tqsim_handle* h = x.h;
   NoiseLevels NL{};
   const size_t levels = h->plan.arities.size();
@@ -523,7 +587,7 @@ void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
   mark(x, 2);
   h->stats.kernel_launches++;
   h->stats.noise_launches++;
-  x.dedup = !(h->debug && h->debug->n_dumps);
+  x.dedup = !(h->debug && h->debug->n_dumps) && !h->opts.no_dedup;
   if (x.dedup) {
     uint32_t* maps = reinterpret_cast<uint32_t*>(x.ws + x.L.map_off);
     const uint8_t* rws = reinterpret_cast<const uint8_t*>(x.ws + x.L.rows_off);
@@ -547,7 +611,7 @@ void run_tree(Exec& x, uint64_t t0, uint64_t t1) {
       h->stats.kernel_launches++;
     }
   }
-  run_level(x, 0, t0, t1, 0);
+  run_level(x, 0, x.lvl_first[0], x.lvl_end[0], 0);
   if (x.pipe && x.leaf_issued) {   // join the leaf branch
     ckc(cudaEventRecord(x.ev[4], x.st2), "pipe join record");
     ckc(cudaStreamWaitEvent(x.st, x.ev[4], 0), "pipe join");
@@ -615,24 +679,26 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
              void* ws, uint64_t ws_bytes, uint32_t* d_out) {
   if (!h) throw Error{TQSIM_EINVAL, "handle is NULL"};
   if (!d_out) throw Error{TQSIM_EINVAL, "d_leaf_outcomes is NULL"};
-  uint64_t t0, t1;
-  shard(h->cplan, rank, world, t0, t1);
-  Exec x{h, seed, st, static_cast<char*>(ws), layout(h, t1 - t0), d_out, level_firsts(h, t0)};
+  const ShardRange sr = shard_levels(h->cplan, rank, world);
+  Exec x = make_exec(h, seed, st, ws, sr, d_out);
   if (!ws || ws_bytes < x.L.total) throw Error{TQSIM_ECAPACITY, "workspace too small"};
   if (reinterpret_cast<uintptr_t>(ws) % ALIGN) throw Error{TQSIM_EINVAL, "workspace not 256-byte aligned"};
   h->stats = tqsim_stats{};
   h->ev_used = 0;
   h->ev_marks.clear();
+  h->ev_tags.clear();
   ck(launch_set_seed(h->d_seed, seed, st), "seed launch");
   static const bool graphs = [] {
     const char* e = std::getenv("TQSIM_GRAPH");
     return !(e && e[0] == '0');
   }();
   const bool dumps = h->debug && h->debug->n_dumps;
-  if (t1 > t0 && graphs && !h->opts.profile && !dumps) {
+  if (!sr.empty() && graphs && !h->opts.profile && !dumps) {
     // replay the captured tree: one graph launch instead of one host launch per kernel
     const std::vector<uint64_t> key = {reinterpret_cast<uint64_t>(ws), ws_bytes, reinterpret_cast<uint64_t>(d_out),
-                                       rank, world};
+                                       rank, world, reinterpret_cast<uint64_t>(h->d_dbg_u),
+                                       reinterpret_cast<uint64_t>(h->d_dbg_total),
+                                       reinterpret_cast<uint64_t>(h->d_dbg_flag)};
     if (!h->graph_exec || h->graph_key != key) {
       if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
       h->graph_exec = nullptr;
@@ -661,7 +727,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
       ckc(cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
       cudaGraph_t g = nullptr;
       try {
-        run_tree(xc, t0, t1);
+        run_tree(xc);
       } catch (...) {
         cudaStreamEndCapture(h->capture_stream, &g);
         if (g) cudaGraphDestroy(g);
@@ -679,7 +745,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
     ckc(cudaGraphLaunch(h->graph_exec, st), "graph launch");
     return;
   }
-  if (t1 > t0) run_tree(x, t0, t1);
+  if (!sr.empty()) run_tree(x);
   h->stats.kernel_launches += 1;     // the seed kernel
   if (h->opts.profile) {
     ckc(cudaStreamSynchronize(st), "profile sync");
@@ -703,6 +769,84 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
       }
     }
   }
+}
+
+// Work the tree actually executed (DESIGN.md §7 "shared states computed once"): per batch
+// of every level, formed exactly as run_level forms them, the instances that were computed
+// (dedup representatives; every instance when dedup is off) and the distinct parent states
+// their fan-out pass read.  Reads the dedup maps back from the workspace (synchronous).
+struct BatchWork {
+  uint64_t comp = 0, parents = 0;
+};
+using WorkMap = std::map<std::pair<uint32_t, uint64_t>, BatchWork>;
+
+WorkMap computed_work(const tqsim_handle* h, const ShardRange& sr, const Layout& L, const char* ws, bool dedup) {
+  std::vector<uint32_t> maps;
+  if (dedup && L.map_entries) {
+    maps.resize(2 * L.map_entries);
+    ckc(cudaMemcpy(maps.data(), ws + L.map_off, 8 * L.map_entries, cudaMemcpyDeviceToHost), "maps D2H");
+  }
+  const size_t levels = h->plan.arities.size();
+  WorkMap out;
+  auto rep = [&](uint32_t d, uint64_t j) -> uint64_t {   // global id of j's representative
+    if (!dedup) return j;
+    const uint64_t idx = L.map_lvl[d] + (j - sr.lo[d]);
+    return j - maps[L.map_entries + idx] + maps[idx];
+  };
+  std::function<void(uint32_t, uint64_t, uint64_t)> walk = [&](uint32_t d, uint64_t i0, uint64_t i1) {
+    for (uint64_t b = i0; b < i1; b += L.cap[d]) {
+      const uint64_t cnt = std::min(L.cap[d], i1 - b);
+      BatchWork w;
+      std::vector<uint64_t> par;
+      for (uint64_t j = b; j < b + cnt; ++j) {
+        if (cnt > 1 && rep(d, j) != j) continue;
+        ++w.comp;
+        if (d > 0) {
+          const uint64_t P = j / h->plan.arities[d];
+          par.push_back(rep(d - 1, P));
+        }
+      }
+      std::sort(par.begin(), par.end());
+      w.parents = (uint64_t)(std::unique(par.begin(), par.end()) - par.begin());
+      out[{d, b}] = w;
+      if (d + 1 < levels) {
+        const uint64_t A = h->plan.arities[d + 1];
+        walk(d + 1, std::max(b * A, sr.lo[d + 1]), std::min((b + cnt) * A, sr.hi[d + 1]));
+      }
+    }
+  };
+  if (!sr.empty()) walk(0, sr.lo[0], sr.hi[0]);
+  return out;
+}
+
+// algorithmic bytes of pass p of level d over `comp` computed states reading `parents`
+// distinct parent states: in place 32 B / amplitude; fan-out 16 B written
+// + 16 B per amplitude of each parent read; root 16 B written; the leaf's run-sums-only
+// pass writes 1 B / amplitude instead of 16.
+double pass_alg_bytes(const tqsim_handle* h, uint32_t d, size_t p, uint64_t comp, uint64_t parents, bool nostore) {
+  const double amps = (double)comp * (double)(1ull << h->n_sim);
+  const bool runsums_only = nostore && h->pp.levels[d][p].leaf_sums;
+  double bytes = runsums_only ? amps : amps * 16.0;
+  if (p > 0) bytes += amps * 16.0;
+  else if (d > 0) bytes += (double)parents * (double)(1ull << h->n_sim) * 16.0;
+  return bytes;
+}
+
+void fill_computed(tqsim_handle* h, const ShardRange& sr, const Layout& L, const char* ws) {
+  const bool dumps = h->debug && h->debug->n_dumps;
+  const bool dedup = !dumps && !h->opts.no_dedup;
+  const WorkMap wm = computed_work(h, sr, L, ws, dedup);
+  tqsim_stats& st = h->stats;
+  st.computed_node_executions = st.computed_gate_amp_updates = st.computed_pass_bytes = 0;
+  double bytes = 0.0;
+  for (const auto& kv : wm) {
+    const uint32_t d = kv.first.first;
+    const BatchWork& w = kv.second;
+    st.computed_node_executions += w.comp;
+    st.computed_gate_amp_updates += (w.comp * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
+    for (size_t p = 0; p < h->pp.levels[d].size(); ++p) bytes += pass_alg_bytes(h, d, p, w.comp, w.parents, !dumps);
+  }
+  st.computed_pass_bytes = (uint64_t)bytes;
 }
 
 void build_result(tqsim_handle* h, const std::vector<uint32_t>& outs, double wall, tqsim_result** out) {
@@ -869,14 +1013,11 @@ tqsim_status tqsim_shard_range(const tqsim_plan* p, uint32_t rank, uint32_t worl
                                uint64_t* leaf_end) {
   return guarded([&] {
     if (!p || p->n_levels < 1) throw Error{TQSIM_EINVAL, "plan is NULL or empty"};
-    uint64_t t0, t1;
-    shard(*p, rank, world, t0, t1);
-    uint64_t below = 1;
-    for (uint32_t d = 1; d < p->n_levels; ++d) below *= p->arities[d];
-    if (top_begin) *top_begin = t0;
-    if (top_end) *top_end = t1;
-    if (leaf_begin) *leaf_begin = t0 * below;
-    if (leaf_end) *leaf_end = t1 * below;
+    const ShardRange r = shard_levels(*p, rank, world);
+    if (top_begin) *top_begin = r.lo[0];
+    if (top_end) *top_end = r.hi[0];
+    if (leaf_begin) *leaf_begin = r.lo.back();
+    if (leaf_end) *leaf_end = r.hi.back();
   });
 }
 
@@ -923,9 +1064,7 @@ tqsim_status tqsim_workspace_bytes(const tqsim_handle* h, uint32_t rank, uint32_
                                    uint64_t* bytes) {
   return guarded([&] {
     if (!h || !bytes) throw Error{TQSIM_EINVAL, "NULL argument"};
-    uint64_t t0, t1;
-    shard(h->cplan, rank, world, t0, t1);
-    *bytes = layout(h, t1 - t0).total;
+    *bytes = layout(h, shard_levels(h->cplan, rank, world)).total;
   });
 }
 
@@ -949,17 +1088,17 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
     // one real run: every level buffer holds states of the tree (batch 0 of each level)
     execute(h, seed, rank, world, st, d_workspace, workspace_bytes, d_leaf_outcomes);
     ckc(cudaStreamSynchronize(st), "sync");
-    uint64_t t0, t1;
-    shard(h->cplan, rank, world, t0, t1);
-    Exec x{h, seed, st, static_cast<char*>(d_workspace), layout(h, t1 - t0), d_leaf_outcomes, level_firsts(h, t0)};
+    const ShardRange sr = shard_levels(h->cplan, rank, world);
+    Exec x = make_exec(h, seed, st, d_workspace, sr, d_leaf_outcomes);
     ckc(cudaEventCreate(&e0), "event");
     ckc(cudaEventCreate(&e1), "event");
     const int n = h->n_sim;
-    uint64_t k = 0, inst = t1 - t0;
+    uint64_t k = 0;
     for (size_t d = 0; d < h->pp.levels.size(); ++d) {
-      if (d > 0) inst *= h->plan.arities[d];
+      const uint64_t inst = sr.count(d);
+      if (inst == 0) continue;
       const uint64_t cnt = std::min<uint64_t>(x.L.cap[d], inst);
-      const uint64_t first = d == 0 ? t0 : (t0 * (inst / (t1 - t0)));   // first instance of the shard
+      const uint64_t first = sr.lo[d];   // first instance of the shard
       const uint32_t slice_begin = (uint32_t)h->plan.bounds[d];
       const uint32_t slice_len = (uint32_t)(h->plan.bounds[d + 1] - slice_begin);
       const uint32_t row_bytes = noise_row_bytes(slice_len);
@@ -969,9 +1108,9 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
       // as in the tree, instances sharing a representative's state are skipped and a
       // fan-out reads a skipped parent's representative (the dedup maps the run above
       // built); count the computed instances and the distinct parent states they read
-      const bool dd = !(h->debug && h->debug->n_dumps);
+      const bool dd = !(h->debug && h->debug->n_dumps) && !h->opts.no_dedup;
       const uint64_t A = h->plan.arities[d];
-      const uint64_t pcnt_batch = d > 0 ? std::min<uint64_t>(x.L.cap[d - 1], inst / A) : 0;
+      const uint64_t pcnt_batch = d > 0 ? std::min<uint64_t>(x.L.cap[d - 1], sr.count(d - 1)) : 0;
       const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
       const uint32_t* rep_d = dd && cnt > 1 ? maps + x.L.map_lvl[d] : nullptr;
       const uint32_t* rep_p = dd && d > 0 && pcnt_batch > 1 ? maps + x.L.map_lvl[d - 1] : nullptr;
@@ -1049,6 +1188,72 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
   return r;
 }
 
+tqsim_status tqsim_shard_levels(const tqsim_plan* p, uint32_t rank, uint32_t world, uint32_t* split_level,
+                                uint64_t* lo, uint64_t* hi) {
+  return guarded([&] {
+    if (!p || p->n_levels < 1) throw Error{TQSIM_EINVAL, "plan is NULL or empty"};
+    const ShardRange r = shard_levels(*p, rank, world);
+    if (split_level) *split_level = r.split;
+    for (uint32_t d = 0; d < p->n_levels; ++d) {
+      if (lo) lo[d] = r.lo[d];
+      if (hi) hi[d] = r.hi[d];
+    }
+  });
+}
+
+tqsim_status tqsim_profile_tree(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, void* stream,
+                                void* d_workspace, uint64_t workspace_bytes, uint32_t* d_leaf_outcomes,
+                                tqsim_kernel_timing* out, uint64_t cap, uint64_t* n_out) {
+  uint32_t prof0 = 0;
+  const tqsim_status r = guarded([&] {
+    if (!h || !n_out) throw Error{TQSIM_EINVAL, "NULL argument"};
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof0 = h->opts.profile;
+    h->opts.profile = 1;
+    h->tag_launches = true;
+    execute(h, seed, rank, world, st, d_workspace, workspace_bytes, d_leaf_outcomes);   // synchronizes
+    const ShardRange sr = shard_levels(h->cplan, rank, world);
+    const Layout lay = layout(h, sr);
+    const bool dedup = !(h->debug && h->debug->n_dumps) && !h->opts.no_dedup;
+    const WorkMap wm = computed_work(h, sr, lay, static_cast<const char*>(d_workspace), dedup);
+    fill_computed(h, sr, lay, static_cast<const char*>(d_workspace));
+    std::map<std::tuple<int, uint32_t, uint32_t>, tqsim_kernel_timing> agg;
+    for (size_t i = 0; i + 1 < h->ev_marks.size(); i += 2) {
+      const tqsim_handle::Tag& tg = h->ev_tags.at(i / 2);
+      float ms = 0.f;
+      ckc(cudaEventElapsedTime(&ms, h->ev_pool[h->ev_marks[i].second], h->ev_pool[h->ev_marks[i + 1].second]),
+          "elapsed");
+      tqsim_kernel_timing& k = agg[std::make_tuple(tg.kind, tg.level, tg.pass)];
+      k.kind = (uint32_t)tg.kind;
+      k.level = tg.level;
+      k.pass = tg.pass;
+      k.launches += 1;
+      k.ms += ms;
+      if (tg.kind != 0) continue;
+      k.states += tg.cnt;
+      k.fp64_per_amp = h->jit[tg.level][tg.pass].fp64_per_amp;
+      auto it = wm.find({tg.level, tg.b});
+      const BatchWork w = it != wm.end() ? it->second : BatchWork{tg.cnt, 0};
+      k.computed_states += w.comp;
+      k.alg_bytes += pass_alg_bytes(h, tg.level, tg.pass, w.comp, w.parents, !(h->debug && h->debug->n_dumps));
+      const uint64_t A = h->plan.arities[tg.level];
+      const uint64_t par = tg.level > 0 ? (tg.b + tg.cnt - 1) / A - tg.b / A + 1 : 0;
+      k.nominal_bytes += pass_alg_bytes(h, tg.level, tg.pass, tg.cnt, par, !(h->debug && h->debug->n_dumps));
+    }
+    uint64_t k = 0;
+    for (const auto& kv : agg) {
+      if (out && k < cap) out[k] = kv.second;
+      ++k;
+    }
+    *n_out = k;
+  });
+  if (h) {
+    h->opts.profile = prof0;
+    h->tag_launches = false;
+  }
+  return r;
+}
+
 tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, uint64_t n_shots,
                           const uint32_t* arities, uint32_t n_levels, uint64_t seed,
                           const tqsim_options* o, const tqsim_debug* debug, tqsim_result** out) {
@@ -1090,14 +1295,23 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, u
     cudaStream_t st = nullptr;
     try {
       h->debug = debug;
-      uint64_t t0, t1;
-      shard(h->cplan, 0, 1, t0, t1);
-      const uint64_t ws = layout(h, t1 - t0).total;
+      const ShardRange sr = shard_levels(h->cplan, 0, 1);
+      const Layout lay = layout(h, sr);
+      const uint64_t ws = lay.total;
       const uint64_t nout = h->cplan.n_outcomes;
       const uint64_t out_off = align_up(ws);
-      char* base = static_cast<char*>(arena_get(out_off + nout * 4));
+      // per-leaf sampler debug outputs (u53, total, boundary flag), when asked for
+      const bool want_u = debug && (debug->leaf_u || debug->leaf_total || debug->leaf_flagged);
+      const uint64_t dbg_off = align_up(out_off + nout * 4);
+      const uint64_t arena_bytes = want_u ? dbg_off + align_up(nout * 8) * 2 + nout : out_off + nout * 4;
+      char* base = static_cast<char*>(arena_get(arena_bytes));
       if (!g_stream) ckc(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking), "cudaStreamCreate");
       st = g_stream;
+      if (want_u) {
+        h->d_dbg_u = reinterpret_cast<double*>(base + dbg_off);
+        h->d_dbg_total = reinterpret_cast<double*>(base + dbg_off + align_up(nout * 8));
+        h->d_dbg_flag = reinterpret_cast<uint8_t*>(base + dbg_off + 2 * align_up(nout * 8));
+      }
       // this call's per-gate tables (2q flags, pass index) from the host circuit
       upload_gate_tables(h, st);
       uint32_t* d_out = reinterpret_cast<uint32_t*>(base + out_off);
@@ -1114,12 +1328,24 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, u
       ckc(cudaStreamSynchronize(st), "stream sync");
       const uint32_t* po = static_cast<const uint32_t*>(g_pinned);
       std::vector<uint32_t> outs(po, po + nout);
+      if (want_u) {
+        if (debug->leaf_u) ckc(cudaMemcpy(debug->leaf_u, h->d_dbg_u, nout * 8, cudaMemcpyDeviceToHost), "D2H u");
+        if (debug->leaf_total)
+          ckc(cudaMemcpy(debug->leaf_total, h->d_dbg_total, nout * 8, cudaMemcpyDeviceToHost), "D2H total");
+        if (debug->leaf_flagged)
+          ckc(cudaMemcpy(debug->leaf_flagged, h->d_dbg_flag, nout, cudaMemcpyDeviceToHost), "D2H flags");
+      }
+      h->d_dbg_u = h->d_dbg_total = nullptr;
+      h->d_dbg_flag = nullptr;
+      fill_computed(h, sr, lay, base);   // work executed (dedup representatives), maps read back
       h->debug = nullptr;
       const double wall =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       build_result(h, outs, wall, out);
     } catch (...) {
       h->debug = nullptr;
+      h->d_dbg_u = h->d_dbg_total = nullptr;
+      h->d_dbg_flag = nullptr;
       for (size_t i = 0; i < g_hcache.size(); ++i)   // a failed handle is not reused
         if (g_hcache[i].h == h) g_hcache.erase(g_hcache.begin() + i);
       tqsim_destroy(h);
@@ -1230,9 +1456,7 @@ tqsim_status tqsim_profile_copy_cost(uint32_t n_qubits, uint32_t n_probe_gates, 
     o.profile = 1;
     const uint32_t ar[2] = {1, (uint32_t)B};
     h = create_handle(&c, &nm, B, ar, 2, &o, true);
-    uint64_t t0, t1;
-    shard(h->cplan, 0, 1, t0, t1);
-    const Layout L = layout(h, t1 - t0);
+    const Layout L = layout(h, shard_levels(h->cplan, 0, 1));
     cudaFree(a);
     a = nullptr;
     ckc(cudaMalloc(&a, L.total + h->cplan.n_outcomes * 4 + ALIGN), "cudaMalloc workspace");

@@ -34,7 +34,7 @@ std::vector<LGate> lower(const tqsim_circuit* c);
 struct Options {
   double copy_cost_gates = 10.0, z = 1.96, eps = 0.05;
   uint64_t mem_budget = 180000000000ull;
-  uint32_t topup = 0, tile_qubits = 0, batch_log2_amps = 0, profile = 0;
+  uint32_t topup = 0, tile_qubits = 0, batch_log2_amps = 0, profile = 0, no_dedup = 0;
 };
 Options options_from(const tqsim_options* o);
 
@@ -178,10 +178,14 @@ struct LeafSelect {
   uint32_t out_row[32];      // out-of-tile qubit i = parity(out_row[i] & stored address)
   // dedup map of the leaf batch: read the representative's sums (null: none)
   const uint32_t* rep = nullptr;
+  // debug outputs by global leaf id (tqsim_debug leaf_u / leaf_total / leaf_flagged), or null
+  double* dbg_u = nullptr;
+  double* dbg_total = nullptr;
+  uint8_t* dbg_flag = nullptr;
 };
 int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
                          int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
-                         uint32_t* d_out, void* stream);
+                         uint32_t* d_out, void* stream, uint8_t* d_flag = nullptr);
 int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
                   int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, const uint64_t* d_seed,
                   double p01, double p10, uint32_t* d_out, void* stream, const LeafSelect* sel = nullptr);
@@ -205,6 +209,7 @@ struct JitPass {
   int threads = 0;
   size_t smem = 0;
   std::vector<double> coefs;      // by-value coefficient parameter (TQSIM_JIT_COEF=0 mode)
+  double fp64_per_amp = 0.0;      // FP64 operations per amplitude of the fast path (cost model)
 };
 std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vector<LGate>& gates,
                                             double* compile_seconds);

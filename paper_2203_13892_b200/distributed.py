@@ -1,13 +1,16 @@
 """Top-level branch sharding over GPUs.
 
-One process per GPU (torchrun).  Rank r of W runs the level-0 instances
-[floor(A0 r / W), floor(A0 (r+1) / W)) of the tree -- a contiguous range of
-leaves -- through tqsim_execute on its own device, writing only its leaves of a
-zero-initialised uint32 leaf-outcome array; one all_reduce(SUM) over NCCL
-(NVLink) combines the disjoint ranges, and the histogram is built from the
-combined array.  Top-level subtrees share nothing but the root |0..0>, so there
-is no other data-path collective.  torch is used only for device memory,
-streams and the process group.
+One process per GPU (torchrun).  The tree is split at the first level whose
+instance count W divides (tqsim_shard_levels; level 0 when W | A_0): rank r runs
+the split-level instances [I r / W, I (r+1) / W), everything below them, and
+the few ancestors above them (recomputed: keyed noise makes them identical on
+every rank) -- a contiguous range of leaves -- through tqsim_execute on its own
+device, writing only its leaves of a zero-initialised uint32 leaf-outcome
+array; one all_reduce(SUM) over NCCL (NVLink) combines the disjoint ranges, and
+the histogram is built from the combined array.  Subtrees of different
+split-level instances share only recomputed ancestors, so there is no other
+data-path collective.  torch is used only for device memory, streams and the
+process group.
 """
 from __future__ import annotations
 
@@ -47,10 +50,13 @@ class ShardRunner:
         self.leaf_range = T.tqsim_shard_range(handle.plan, rank, world)[2:]
 
     def run(self, seed: int, group=None, stream=None):
-        """Enqueue the shard and the combining all_reduce; returns the device outcome array."""
+        """Enqueue the shard and the combining all_reduce; returns the device outcome array.
+        Everything (zeroing, the shard's kernels, the NCCL all_reduce) is ordered on one
+        stream: `stream` if given (made current for the call), else the current stream."""
         import torch
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.out.zero_()
-        self.h.execute(seed, self.rank, self.world, st.cuda_stream, self.ws.data_ptr(),
-                       self.ws.numel(), self.out.data_ptr())
-        return combine(self.out, group)
+        with torch.cuda.stream(st):
+            self.out.zero_()
+            self.h.execute(seed, self.rank, self.world, st.cuda_stream, self.ws.data_ptr(),
+                           self.ws.numel(), self.out.data_ptr())
+            return combine(self.out, group)

@@ -51,7 +51,7 @@ class tqsim_options(C.Structure):
     _fields_ = [("copy_cost_gates", C.c_double), ("z", C.c_double), ("eps", C.c_double),
                 ("mem_budget_bytes", C.c_uint64), ("topup", C.c_uint32),
                 ("tile_qubits", C.c_uint32), ("batch_log2_amps", C.c_uint32),
-                ("profile", C.c_uint32)]
+                ("profile", C.c_uint32), ("no_dedup", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class tqsim_plan(C.Structure):
@@ -77,13 +77,22 @@ class tqsim_stats(C.Structure):
                 ("measure_launches", C.c_uint64), ("node_executions", C.c_uint64),
                 ("gate_amp_updates", C.c_uint64), ("pass_bytes", C.c_uint64),
                 ("measure_bytes", C.c_uint64), ("pass_ms", C.c_double), ("measure_ms", C.c_double),
-                ("leaves", C.c_uint64), ("noise_launches", C.c_uint64), ("noise_ms", C.c_double)]
+                ("leaves", C.c_uint64), ("noise_launches", C.c_uint64), ("noise_ms", C.c_double),
+                ("computed_node_executions", C.c_uint64), ("computed_gate_amp_updates", C.c_uint64),
+                ("computed_pass_bytes", C.c_uint64)]
 
 
 class tqsim_pass_timing(C.Structure):
     _fields_ = [("level", C.c_uint32), ("pass_", C.c_uint32), ("states_per_launch", C.c_uint32),
                 ("reserved", C.c_uint32), ("launches_per_tree", C.c_double),
                 ("ms_per_launch", C.c_double), ("alg_bytes_per_launch", C.c_double)]
+
+
+class tqsim_kernel_timing(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("level", C.c_uint32), ("pass_", C.c_uint32),
+                ("reserved", C.c_uint32), ("launches", C.c_uint64), ("states", C.c_uint64),
+                ("computed_states", C.c_uint64), ("ms", C.c_double), ("alg_bytes", C.c_double),
+                ("nominal_bytes", C.c_double), ("fp64_per_amp", C.c_double)]
 
 
 class tqsim_result(C.Structure):
@@ -96,7 +105,8 @@ class tqsim_result(C.Structure):
 class tqsim_debug(C.Structure):
     _fields_ = [("n_dumps", C.c_uint32), ("reserved", C.c_uint32),
                 ("dump_levels", C.POINTER(C.c_uint32)), ("dump_instances", C.POINTER(C.c_uint64)),
-                ("dump_host", C.POINTER(C.c_double))]
+                ("dump_host", C.POINTER(C.c_double)), ("leaf_u", C.POINTER(C.c_double)),
+                ("leaf_flagged", C.POINTER(C.c_uint8)), ("leaf_total", C.POINTER(C.c_double))]
 
 
 class tqsim_op_record(C.Structure):
@@ -114,6 +124,11 @@ _SIGS = {
     "tqsim_profile_passes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
                                        C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,
                                        _P(tqsim_pass_timing), C.c_uint64, _P(C.c_uint64)]),
+    "tqsim_profile_tree": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
+                                     C.c_void_p, C.c_uint64, C.c_void_p, _P(tqsim_kernel_timing),
+                                     C.c_uint64, _P(C.c_uint64)]),
+    "tqsim_shard_levels": (C.c_int, [_P(tqsim_plan), C.c_uint32, C.c_uint32, _P(C.c_uint32),
+                                     _P(C.c_uint64), _P(C.c_uint64)]),
     "tqsim_parse_qasm": (C.c_int, [C.c_char_p, _P(tqsim_gate), C.c_uint64, _P(C.c_uint64),
                                    _P(C.c_uint32), _P(C.c_uint32)]),
     "tqsim_profile_copy_cost": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, _P(C.c_double),
@@ -302,6 +317,15 @@ def tqsim_shard_range(plan: tqsim_plan, rank: int, world: int) -> Tuple[int, int
     return tuple(int(x.value) for x in v)
 
 
+def tqsim_shard_levels(plan: tqsim_plan, rank: int, world: int):
+    """(split_level, lo[], hi[]): the rank's instance range [lo[d], hi[d]) at every level."""
+    L = int(plan.n_levels)
+    sp = C.c_uint32()
+    lo, hi = (C.c_uint64 * L)(), (C.c_uint64 * L)()
+    _check(lib().tqsim_shard_levels(C.byref(plan), rank, world, C.byref(sp), lo, hi))
+    return int(sp.value), [int(v) for v in lo], [int(v) for v in hi]
+
+
 class Handle:
     """tqsim_create / tqsim_execute / tqsim_destroy."""
 
@@ -346,6 +370,17 @@ class Handle:
         _check(lib().tqsim_profile_passes(*args, out, n.value, C.byref(n)))
         return [out[i] for i in range(n.value)]
 
+    def profile_tree(self, seed: int, rank: int, world: int, stream: int, d_workspace: int,
+                     workspace_bytes: int, d_leaf_outcomes: int):
+        """In-tree CUDA-event timing of every kernel family (tqsim_profile_tree)."""
+        n = C.c_uint64()
+        args = (self.h, int(seed), rank, world, C.c_void_p(stream), C.c_void_p(d_workspace),
+                int(workspace_bytes), C.c_void_p(d_leaf_outcomes))
+        _check(lib().tqsim_profile_tree(*args, None, 0, C.byref(n)))
+        out = (tqsim_kernel_timing * max(1, n.value))()
+        _check(lib().tqsim_profile_tree(*args, out, n.value, C.byref(n)))
+        return [out[i] for i in range(n.value)]
+
     def noise_table(self, seed: int, level: int, inst_begin: int, count: int) -> np.ndarray:
         p = self.plan
         slen = p.boundaries[level + 1] - p.boundaries[level]
@@ -375,8 +410,12 @@ class Result:
     `counts` is the same as a dict, built on first access), the leaf-ordered outcomes,
     wall time, run statistics and (debug) dumped states."""
 
-    def __init__(self, plan, bitstrings, counts_array, leaf_outcomes, wall_s, stats, dumps=None):
+    def __init__(self, plan, bitstrings, counts_array, leaf_outcomes, wall_s, stats, dumps=None,
+                 leaf_u=None, leaf_flagged=None, leaf_total=None):
         self.plan = plan
+        self.leaf_u = leaf_u                  # debug: per-leaf u53 uniform (R9)
+        self.leaf_flagged = leaf_flagged      # debug: draw within 1e-9 of a CDF boundary
+        self.leaf_total = leaf_total          # debug: sum |a|^2 as the sampler summed it
         self.bitstrings = bitstrings
         self.counts_array = counts_array
         self.leaf_outcomes = leaf_outcomes
@@ -393,19 +432,33 @@ class Result:
 
 
 def tqsim_run_ex(n_qubits, gates, noise, n_shots, arities=None, seed=0, options=None,
-                 dumps: Sequence[Tuple[int, int]] = ()) -> Result:
+                 dumps: Sequence[Tuple[int, int]] = (), leaf_debug: bool = False) -> Result:
+    """tqsim_run with options; `dumps` = [(level, instance)] state dumps (stored-state path);
+    leaf_debug=True also returns the per-leaf u53 / flag / total (default path kept)."""
     ca = CircuitArg(n_qubits, gates)
     a, L = _arities(arities)
     dbg = None
     host = None
+    lu = lf = lt = None
+    if dumps or leaf_debug:
+        dbg = tqsim_debug()
     if dumps:
         lv = (C.c_uint32 * len(dumps))(*[int(d) for d, _ in dumps])
         ins = (C.c_uint64 * len(dumps))(*[int(j) for _, j in dumps])
         host = np.zeros((len(dumps), 2 ** n_qubits, 2), dtype=np.float64)
-        dbg = tqsim_debug(len(dumps), 0, C.cast(lv, C.POINTER(C.c_uint32)),
-                          C.cast(ins, C.POINTER(C.c_uint64)),
-                          host.ctypes.data_as(C.POINTER(C.c_double)))
+        dbg.n_dumps = len(dumps)
+        dbg.dump_levels = C.cast(lv, C.POINTER(C.c_uint32))
+        dbg.dump_instances = C.cast(ins, C.POINTER(C.c_uint64))
+        dbg.dump_host = host.ctypes.data_as(C.POINTER(C.c_double))
         dbg._keep = (lv, ins)
+    if leaf_debug:
+        nout = tqsim_plan_circuit(n_qubits, gates, noise, n_shots, arities, options).n_outcomes
+        lu = np.zeros(nout, dtype=np.float64)
+        lt = np.zeros(nout, dtype=np.float64)
+        lf = np.zeros(nout, dtype=np.uint8)
+        dbg.leaf_u = lu.ctypes.data_as(C.POINTER(C.c_double))
+        dbg.leaf_total = lt.ctypes.data_as(C.POINTER(C.c_double))
+        dbg.leaf_flagged = lf.ctypes.data_as(C.POINTER(C.c_uint8))
     r = C.POINTER(tqsim_result)()
     _check(lib().tqsim_run_ex(C.byref(ca.c), C.byref(noise), int(n_shots), a, L, int(seed),
                               C.byref(options) if options else None,
@@ -425,7 +478,8 @@ def tqsim_run_ex(n_qubits, gates, noise, n_shots, arities=None, seed=0, options=
     states = None
     if host is not None:
         states = host[..., 0] + 1j * host[..., 1]
-    return Result(plan, bits, cnts, leaf, wall, stats, states)
+    return Result(plan, bits, cnts, leaf, wall, stats, states, lu,
+                  lf.astype(bool) if lf is not None else None, lt)
 
 
 def tqsim_run(n_qubits, gates, noise, n_shots, arities=None, seed=0) -> Result:
