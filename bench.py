@@ -373,18 +373,30 @@ def main():
     hbm_peak, peak_src, sm_max = peaks()
     fp64_peak = N_SM * FP64_DFMA_PER_CLK_SM * sm_max * 1e6 / 1e12          # T DFMA/s
     amps = 1 << n
+    top_name = "tq_pass_l%d_p%d" % (top.level, top.pass_)
+    # ncu evidence of the same tree (profiles/ncu_<workload>.json, profiles/ncu_join.py):
+    # DRAM bytes per launch and FP64 pipe instructions (DFMA + DADD + DMUL) per computed
+    # amplitude of each kernel family; without it the FP64 work is the code generator's model
+    ncu = None
+    npath = os.path.join(ROOT, "profiles", "ncu_%s.json" % w.name)
+    if os.path.exists(npath):
+        with open(npath) as f:
+            ncu = {r["kernel"]: r for r in json.load(f)["families"]}
+    top_ncu = ncu.get(top_name) if ncu else None
+    fp64_per_amp = top_ncu["fp64_inst_per_computed_amp"] if top_ncu and top_ncu.get(
+        "fp64_inst_per_computed_amp") else top.fp64_per_amp
+    fp64_src = ("ncu-measured FP64 thread instructions per computed amplitude (%s)" % os.path.basename(npath)
+                if top_ncu else "code-generator cost model (FP64 ops per amplitude, fast path)")
     top_gbs = top.alg_bytes / (top.ms * 1e-3) / 1e9
-    top_fp64 = top.fp64_per_amp * top.computed_states * amps / (top.ms * 1e-3) / 1e12
+    top_fp64 = fp64_per_amp * top.computed_states * amps / (top.ms * 1e-3) / 1e12
     fam_gbs = pass_bytes / (pass_ms * 1e-3) / 1e9
     # which roof binds the top kernel: the larger of its time at the HBM peak and at the FP64 peak
     t_hbm = top.alg_bytes / (hbm_peak * 1e9)
-    t_fp64 = top.fp64_per_amp * top.computed_states * amps / (fp64_peak * 1e12)
+    t_fp64 = fp64_per_amp * top.computed_states * amps / (fp64_peak * 1e12)
     bound = "hbm" if t_hbm >= t_fp64 else "alu"
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_%s.json" % w.name)
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f)
+    traffic = {"dram_bytes_per_launch": top_ncu["dram_bytes_per_launch"],
+               "source": "ncu launch list of one tree, %s family (%s)" % (top_name, os.path.basename(npath))} \
+        if top_ncu and top_ncu.get("dram_bytes_per_launch") else None
     roofline = {
         "bound": bound,
         "achieved": top_gbs if bound == "hbm" else top_fp64,
@@ -393,7 +405,7 @@ def main():
         "frac": (top_gbs / hbm_peak) if bound == "hbm" else (top_fp64 / fp64_peak),
         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
         "traffic_source": traffic.get("source") if traffic else None,
-        "kernel": "tq_pass_l%d_p%d" % (top.level, top.pass_),
+        "kernel": top_name,
         "peak_source": peak_src if bound == "hbm" else
         "derived: 148 SMs x 64 DFMA/clk x %.0f MHz (DESIGN.md §6.1)" % sm_max,
         "method": "tqsim_profile_tree: every launch of one tree bracketed by CUDA events on the launching "
@@ -405,6 +417,7 @@ def main():
         "computed_states": top.computed_states, "states": top.states,
         "hbm_gbs": top_gbs, "hbm_frac": top_gbs / hbm_peak,
         "fp64_tdfma_s": top_fp64, "fp64_frac": top_fp64 / fp64_peak, "fp64_peak_tdfma_s": fp64_peak,
+        "fp64_work_source": fp64_src, "fp64_inst_per_computed_amp": fp64_per_amp,
         "share_of_tree": top.ms / tree_ms if tree_ms else None,
         "pass_family": {"ms_per_step": pass_ms, "alg_gbs": fam_gbs, "frac": fam_gbs / hbm_peak,
                         "alg_bytes": pass_bytes, "nominal_bytes": pass_nominal,
