@@ -80,10 +80,22 @@ typedef struct {
  * probability p1 one of X,Y,Z uniformly; after every 2q gate, with probability
  * p2 one of the 15 non-II Pauli pairs uniformly.  Readout error (R11):
  * each measured bit flips 0->1 with readout_p01 and 1->0 with readout_p10.
- * All in [0, 1]. */
+ * All in [0, 1].
+ * Non-Pauli channels (§4.3.2, Table 2; readings R31-R37): after every lowered
+ * gate and its depolarizing Pauli, on each qubit the gate acts on, thermal relaxation
+ * (t1 > 0: amplitude damping with 1 - exp(-t/t1) then phase damping with
+ * 1 - exp(-2t/t2 + t/t1), t = gate_time_1q / gate_time_2q, requires t2 <= 2 t1),
+ * amplitude damping (amp_damping = gamma) and phase damping (phase_damping = lambda),
+ * each unravelled as a keyed quantum trajectory (R34-R35).  Any of them enabled selects
+ * the Kraus engine: the state of every trajectory resident in one CTA's shared memory,
+ * n_qubits <= 13 (TQSIM_EINVAL otherwise).  0 = off. */
 typedef struct {
   double p1, p2, readout_p01, readout_p10;
+  double amp_damping, phase_damping;
+  double t1, t2, gate_time_1q, gate_time_2q;   /* seconds */
 } tqsim_noise_model;
+
+#define TQSIM_KRAUS_MAX_QUBITS 13
 
 typedef struct {
   double copy_cost_gates;     /* first-slice length m = round(.) (R14); default 10 */

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -68,6 +69,9 @@ struct tqsim_handle {
   };
   std::vector<Tag> ev_tags;
   bool tag_launches = false;
+  // Kraus engine (non-Pauli channels, kraus.cu): the lowered gate table in HBM
+  bool kraus = false;
+  tq::KGate* d_kgates = nullptr;
 };
 
 namespace tq {
@@ -113,6 +117,11 @@ void validate_noise(const tqsim_noise_model* nm) {
   const double v[4] = {nm->p1, nm->p2, nm->readout_p01, nm->readout_p10};
   for (double p : v)
     if (!(p >= 0.0 && p <= 1.0)) throw Error{TQSIM_EINVAL, "probabilities must be in [0, 1]"};
+  if (!(nm->amp_damping >= 0.0 && nm->amp_damping < 1.0) || !(nm->phase_damping >= 0.0 && nm->phase_damping < 1.0))
+    throw Error{TQSIM_EINVAL, "amp_damping / phase_damping must be in [0, 1)"};
+  if (!(nm->t1 >= 0.0)) throw Error{TQSIM_EINVAL, "t1 must be >= 0"};
+  if (nm->t1 > 0.0 && !(nm->t2 > 0.0 && nm->t2 <= 2.0 * nm->t1 && nm->gate_time_1q >= 0.0 && nm->gate_time_2q >= 0.0))
+    throw Error{TQSIM_EINVAL, "thermal relaxation needs 0 < t2 <= 2 t1 and gate times >= 0"};
 }
 
 void require_device() {
@@ -136,6 +145,7 @@ struct Layout {
   uint64_t map_off = 0;                 // dedup maps: rep then pos, u32 per instance of the shard
   std::vector<uint64_t> map_lvl;        // entry offset of each level's map
   uint64_t map_entries = 0;
+  std::vector<uint64_t> kflag_off;      // Kraus engine: per level, one path-flag byte per batch slot
   uint64_t sel_off = 0;                 // leaf select / recompute buffers (per leaf of a batch):
                                         // runsel u32, tile u32, xl u32, t3 f64, 8 amplitudes
   int chunk_log2 = 0;
@@ -261,6 +271,11 @@ Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl) {
       l.map_entries += l.lvl_count[d];
     }
     off = align_up(off + 8 * l.map_entries);
+    l.kflag_off.clear();
+    for (size_t d = 0; d < levels; ++d) {
+      l.kflag_off.push_back(off);
+      off = align_up(off + (h->kraus ? l.cap[d] : 0));
+    }
     l.sel_off = off;
     off = align_up(off + l.cap.back() * (4 + 4 + 4 + 8 + (16ull << RUN_Q)) + 4 * ALIGN);
     l.total = off;
@@ -559,8 +574,73 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
   }
 }
 
+// Kraus engine (kraus.cu): level batches as run_level forms them; one CTA per instance runs
+// the whole slice with the state in shared memory; leaves are sampled in the same kernel.
+void run_level_kraus(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_first) {
+  tqsim_handle* h = x.h;
+  const uint32_t levels = (uint32_t)h->plan.arities.size();
+  const tqsim_noise_model& nm = h->noise;
+  for (uint64_t b = i0; b < i1; b += x.L.cap[d]) {
+    const uint64_t cnt = std::min(x.L.cap[d], i1 - b);
+    KrausArgs a{};
+    a.gates = h->d_kgates;
+    a.src = d > 0 ? x.ws + x.L.off[d - 1] : nullptr;
+    a.dst = x.ws + x.L.off[d];
+    a.src_flag = d > 0 ? reinterpret_cast<const uint8_t*>(x.ws + x.L.kflag_off[d - 1]) : nullptr;
+    a.dst_flag = reinterpret_cast<uint8_t*>(x.ws + x.L.kflag_off[d]);
+    a.child_first = b;
+    a.parent_first = parent_first;
+    a.arity = h->plan.arities[d];
+    a.g0 = (uint32_t)h->plan.bounds[d];
+    a.g1 = (uint32_t)h->plan.bounds[d + 1];
+    a.n = (uint32_t)h->n_user;
+    a.n_user = h->n_user;
+    a.mode = d > 0 ? 1u : 0u;
+    a.leaf = d + 1 == levels ? 1u : 0u;
+    a.seedp = h->d_seed;
+    a.p1 = nm.p1;
+    a.p2 = nm.p2;
+    a.p01 = nm.readout_p01;
+    a.p10 = nm.readout_p10;
+    if (nm.t1 > 0.0) {   // R32: TR = AD(1 - e^{-t/T1}) then PD(1 - e^{-2t/T2 + t/T1}), t per gate class
+      a.ch_mask |= 1u;
+      const double t[2] = {nm.gate_time_1q, nm.gate_time_2q};
+      for (int c = 0; c < 2; ++c) {
+        a.trg[c] = 1.0 - std::exp(-t[c] / nm.t1);
+        a.trl[c] = 1.0 - std::exp(-2.0 * t[c] / nm.t2 + t[c] / nm.t1);
+      }
+    }
+    if (nm.amp_damping > 0.0) a.ch_mask |= 2u, a.ad = nm.amp_damping;
+    if (nm.phase_damping > 0.0) a.ch_mask |= 4u, a.pd = nm.phase_damping;
+    a.out = x.d_out;
+    a.dbg_u = h->d_dbg_u;
+    a.dbg_total = h->d_dbg_total;
+    a.dbg_flag = h->d_dbg_flag;
+    mark(x, 3, d, 0, b, cnt);
+    ck(launch_kraus_slice(a, (uint32_t)cnt, x.st), "kraus slice launch");
+    mark(x, 3, d, 0, b, cnt);
+    h->stats.kernel_launches++;
+    h->stats.pass_launches++;
+    h->stats.node_executions += cnt;
+    h->stats.gate_amp_updates += (cnt * (a.g1 - a.g0)) << h->n_user;
+    // one parent read per instance, the state written (not at a leaf): shared memory otherwise
+    h->stats.pass_bytes += (cnt << h->n_user) * ((d > 0 ? 16 : 0) + (a.leaf ? 0 : 16));
+    dump_if_requested(x, d, b, cnt, x.ws + x.L.off[d]);
+    if (a.leaf) {
+      h->stats.leaves += cnt;
+    } else {
+      const uint64_t A = h->plan.arities[d + 1];
+      run_level_kraus(x, d + 1, std::max(b * A, x.lvl_first[d + 1]), std::min((b + cnt) * A, x.lvl_end[d + 1]), b);
+    }
+  }
+}
+
 // Every noise row of the shard (all levels) in one launch, then the tree.
 void run_tree(Exec& x) {
+  if (x.h->kraus) {
+    run_level_kraus(x, 0, x.lvl_first[0], x.lvl_end[0], 0);
+    return;
+  }
   tqsim_handle* h = x.h;
   NoiseLevels NL{};
   const size_t levels = h->plan.arities.size();
@@ -644,6 +724,10 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     h->gates = lower(c);
     h->opts = opts;
     h->noise = *nm;
+    h->kraus = kraus_enabled(*nm);
+    if (h->kraus && c->n_qubits > TQSIM_KRAUS_MAX_QUBITS)
+      throw Error{TQSIM_EINVAL, "non-Pauli channels (amplitude / phase damping, thermal relaxation) run in the "
+                                "shared-memory Kraus engine: n_qubits must be <= 13"};
     h->plan = make_plan(h->gates, c->n_qubits, nm, n_shots, arities, n_levels, opts);
     h->pp = make_pass_plan(h->gates, c->n_qubits, h->plan, opts);
     h->n_sim = h->pp.n_sim;
@@ -664,8 +748,23 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
             h->h_tables[G + h->pp.ops[oi].gate] = (uint8_t)std::min<uint32_t>(pd.pass_index, 31);
       upload_gate_tables(h, nullptr);
       ckc(cudaStreamSynchronize(nullptr), "upload gate tables");
-      // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
-      h->jit = jit_build(h->pp, h->gates, &h->compile_s);
+      if (h->kraus) {   // the Kraus engine reads the lowered gates from HBM (kraus.cu)
+        std::vector<KGate> kg(h->gates.size());
+        for (size_t g = 0; g < h->gates.size(); ++g) {
+          const LGate& l = h->gates[g];
+          kg[g].two = l.two ? 1u : 0u;
+          kg[g].op = l.op;
+          kg[g].q0 = l.q0;
+          kg[g].q1 = l.q1;
+          for (int k = 0; k < 8; ++k) kg[g].m[k] = l.m[k];
+        }
+        ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_kgates), sizeof(KGate) * std::max<size_t>(kg.size(), 1)),
+            "cudaMalloc kraus gates");
+        ckc(cudaMemcpy(h->d_kgates, kg.data(), sizeof(KGate) * kg.size(), cudaMemcpyHostToDevice), "kraus gates");
+      } else {
+        // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
+        h->jit = jit_build(h->pp, h->gates, &h->compile_s);
+      }
 
     }
   } catch (...) {
@@ -693,7 +792,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
     return !(e && e[0] == '0');
   }();
   const bool dumps = h->debug && h->debug->n_dumps;
-  if (!sr.empty() && graphs && !h->opts.profile && !dumps) {
+  if (!sr.empty() && graphs && !h->opts.profile && !dumps && !h->kraus) {
     // replay the captured tree: one graph launch instead of one host launch per kernel
     const std::vector<uint64_t> key = {reinterpret_cast<uint64_t>(ws), ws_bytes, reinterpret_cast<uint64_t>(d_out),
                                        rank, world, reinterpret_cast<uint64_t>(h->d_dbg_u),
@@ -824,6 +923,11 @@ WorkMap computed_work(const tqsim_handle* h, const ShardRange& sr, const Layout&
 // + 16 B per amplitude of each parent read; root 16 B written; the leaf's run-sums-only
 // pass writes 1 B / amplitude instead of 16.
 double pass_alg_bytes(const tqsim_handle* h, uint32_t d, size_t p, uint64_t comp, uint64_t parents, bool nostore) {
+  if (h->kraus) {   // Kraus engine: one kernel per level; parent read + state write (none at a leaf)
+    if (p > 0) return 0.0;
+    const double amps = (double)comp * (double)(1ull << h->n_user);
+    return amps * ((d > 0 ? 16.0 : 0.0) + (d + 1 == h->plan.arities.size() ? 0.0 : 16.0));
+  }
   const double amps = (double)comp * (double)(1ull << h->n_sim);
   const bool runsums_only = nostore && h->pp.levels[d][p].leaf_sums;
   double bytes = runsums_only ? amps : amps * 16.0;
@@ -834,7 +938,7 @@ double pass_alg_bytes(const tqsim_handle* h, uint32_t d, size_t p, uint64_t comp
 
 void fill_computed(tqsim_handle* h, const ShardRange& sr, const Layout& L, const char* ws) {
   const bool dumps = h->debug && h->debug->n_dumps;
-  const bool dedup = !dumps && !h->opts.no_dedup;
+  const bool dedup = !dumps && !h->opts.no_dedup && !h->kraus;
   const WorkMap wm = computed_work(h, sr, L, ws, dedup);
   tqsim_stats& st = h->stats;
   st.computed_node_executions = st.computed_gate_amp_updates = st.computed_pass_bytes = 0;
@@ -844,7 +948,8 @@ void fill_computed(tqsim_handle* h, const ShardRange& sr, const Layout& L, const
     const BatchWork& w = kv.second;
     st.computed_node_executions += w.comp;
     st.computed_gate_amp_updates += (w.comp * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
-    for (size_t p = 0; p < h->pp.levels[d].size(); ++p) bytes += pass_alg_bytes(h, d, p, w.comp, w.parents, !dumps);
+    const size_t np = h->kraus ? 1 : h->pp.levels[d].size();
+    for (size_t p = 0; p < np; ++p) bytes += pass_alg_bytes(h, d, p, w.comp, w.parents, !dumps);
   }
   st.computed_pass_bytes = (uint64_t)bytes;
 }
@@ -1049,6 +1154,7 @@ void tqsim_destroy(tqsim_handle* h) {
   if (h->d_two) cudaFree(h->d_two);
   if (h->d_pass_of) cudaFree(h->d_pass_of);
   if (h->d_seed) cudaFree(h->d_seed);
+  if (h->d_kgates) cudaFree(h->d_kgates);
   if (h->h_tables_pinned) cudaFreeHost(h->h_tables_pinned);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
@@ -1094,7 +1200,7 @@ tqsim_status tqsim_profile_passes(tqsim_handle* h, uint64_t seed, uint32_t rank,
     ckc(cudaEventCreate(&e1), "event");
     const int n = h->n_sim;
     uint64_t k = 0;
-    for (size_t d = 0; d < h->pp.levels.size(); ++d) {
+    for (size_t d = 0; d < h->pp.levels.size() && !h->kraus; ++d) {
       const uint64_t inst = sr.count(d);
       if (inst == 0) continue;
       const uint64_t cnt = std::min<uint64_t>(x.L.cap[d], inst);
@@ -1214,7 +1320,7 @@ tqsim_status tqsim_profile_tree(tqsim_handle* h, uint64_t seed, uint32_t rank, u
     execute(h, seed, rank, world, st, d_workspace, workspace_bytes, d_leaf_outcomes);   // synchronizes
     const ShardRange sr = shard_levels(h->cplan, rank, world);
     const Layout lay = layout(h, sr);
-    const bool dedup = !(h->debug && h->debug->n_dumps) && !h->opts.no_dedup;
+    const bool dedup = !(h->debug && h->debug->n_dumps) && !h->opts.no_dedup && !h->kraus;
     const WorkMap wm = computed_work(h, sr, lay, static_cast<const char*>(d_workspace), dedup);
     fill_computed(h, sr, lay, static_cast<const char*>(d_workspace));
     std::map<std::tuple<int, uint32_t, uint32_t>, tqsim_kernel_timing> agg;
@@ -1229,9 +1335,9 @@ tqsim_status tqsim_profile_tree(tqsim_handle* h, uint64_t seed, uint32_t rank, u
       k.pass = tg.pass;
       k.launches += 1;
       k.ms += ms;
-      if (tg.kind != 0) continue;
+      if (tg.kind != 0 && tg.kind != 3) continue;
       k.states += tg.cnt;
-      k.fp64_per_amp = h->jit[tg.level][tg.pass].fp64_per_amp;
+      if (tg.kind == 0) k.fp64_per_amp = h->jit[tg.level][tg.pass].fp64_per_amp;
       auto it = wm.find({tg.level, tg.b});
       const BatchWork w = it != wm.end() ? it->second : BatchWork{tg.cnt, 0};
       k.computed_states += w.comp;

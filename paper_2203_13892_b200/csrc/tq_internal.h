@@ -200,6 +200,33 @@ int launch_noise_table(const uint8_t* d_two, uint32_t slice_begin, uint32_t slic
                        uint8_t* d_out);
 const char* cuda_error_string(int code);
 
+// ---------------------------------------------------------------- Kraus engine (kraus.cu)
+struct KGate {                  // a lowered gate for the Kraus engine (device table)
+  uint32_t two, op, q0, q1;     // op: OpType (OP_CX / OP_CZ for 2q)
+  double m[8];                  // 1q: 2x2 complex row major (re, im)
+};
+struct KrausArgs {
+  const KGate* gates;
+  const void* src;              // parent level batch (mode 1)
+  void* dst;                    // this level batch (non-leaf)
+  const uint8_t* src_flag;      // parent's path flag (R36)
+  uint8_t* dst_flag;
+  uint64_t child_first, parent_first;
+  uint32_t arity, g0, g1, n, n_user, mode, leaf, ch_mask;   // ch_mask: 1 TR, 2 AD, 4 PD
+  const uint64_t* seedp;
+  double p1, p2, p01, p10;
+  double trg[2], trl[2];        // TR amplitude / phase damping parameters per gate class (1q, 2q)
+  double ad, pd;
+  uint32_t* out;
+  double* dbg_u;
+  double* dbg_total;
+  uint8_t* dbg_flag;
+};
+int launch_kraus_slice(const KrausArgs& a, uint32_t batch, void* stream);
+inline bool kraus_enabled(const tqsim_noise_model& nm) {
+  return nm.amp_damping > 0.0 || nm.phase_damping > 0.0 || nm.t1 > 0.0;
+}
+
 // ---------------------------------------------------------------- JIT pass kernels (jit.cpp)
 struct JitPass {
   void* kernel = nullptr;   // cudaKernel_t

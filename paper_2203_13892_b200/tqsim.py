@@ -44,7 +44,9 @@ class tqsim_circuit(C.Structure):
 
 class tqsim_noise_model(C.Structure):
     _fields_ = [("p1", C.c_double), ("p2", C.c_double), ("readout_p01", C.c_double),
-                ("readout_p10", C.c_double)]
+                ("readout_p10", C.c_double), ("amp_damping", C.c_double), ("phase_damping", C.c_double),
+                ("t1", C.c_double), ("t2", C.c_double), ("gate_time_1q", C.c_double),
+                ("gate_time_2q", C.c_double)]
 
 
 class tqsim_options(C.Structure):
@@ -205,8 +207,14 @@ class CircuitArg:
         self.c = tqsim_circuit(int(n_qubits), 0, len(gates), C.cast(arr, C.POINTER(tqsim_gate)))
 
 
-def noise_arg(p1: float, p2: float, p01: float = 0.0, p10: float = 0.0) -> tqsim_noise_model:
-    return tqsim_noise_model(float(p1), float(p2), float(p01), float(p10))
+def noise_arg(p1: float, p2: float, p01: float = 0.0, p10: float = 0.0, amp_damping: float = 0.0,
+              phase_damping: float = 0.0, t1: float = 0.0, t2: float = 0.0, gate_time_1q: float = 0.0,
+              gate_time_2q: float = 0.0) -> tqsim_noise_model:
+    """Depolarizing p1 / p2, readout p01 / p10, and the non-Pauli channels (amplitude / phase
+    damping, thermal relaxation T1 / T2 with gate times), 0 = off."""
+    return tqsim_noise_model(float(p1), float(p2), float(p01), float(p10), float(amp_damping),
+                             float(phase_damping), float(t1), float(t2), float(gate_time_1q),
+                             float(gate_time_2q))
 
 
 def default_options(**kw) -> tqsim_options:
