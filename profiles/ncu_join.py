@@ -51,9 +51,14 @@ def main():
              "fp64_pipe_pct": a["pipe_pct_x_ns"] / a["ns"] if a["ns"] else None}
         f = fam.get(key[1:]) if key[0] == "pass" else None
         if f:
-            r.update({"alg_bytes": f["alg_bytes"], "dram_over_alg": a["dram"] / f["alg_bytes"] if f["alg_bytes"] else None,
-                      "computed_states": f["computed_states"],
-                      "fp64_inst_per_computed_amp": a["fp64"] / (f["computed_states"] * 2 ** n) if f["computed_states"] else None,
+            # the launch list may cover only part of the tree: compare per-launch averages
+            cover = a["launches"] / f["launches"]
+            alg_cov = f["alg_bytes"] * cover
+            comp_cov = f["computed_states"] * cover
+            r.update({"tree_launches": f["launches"], "coverage": cover,
+                      "alg_bytes_per_launch": f["alg_bytes"] / f["launches"],
+                      "dram_over_alg": a["dram"] / alg_cov if alg_cov else None,
+                      "fp64_inst_per_computed_amp": a["fp64"] / (comp_cov * 2 ** n) if comp_cov else None,
                       "fp64_model_per_amp": f["fp64_per_amp_model"],
                       "dram_bytes_per_launch": a["dram"] / a["launches"]})
         out["families"].append(r)

@@ -10,4 +10,5 @@ from .generators import (  # noqa: F401
     GATE_KINDS, Circuit, Workload, qft_gates, basis_prep_gates, brickwork_gates,
     random_3_regular_edges, qaoa_gates, hea_gates, ghz_gates, load_config,
     config_names, make_config, make_variant, monomial_brickwork_gates, random_circuit,
+    inverse_qft_gates, qpe_gates, bv_gates,
 )

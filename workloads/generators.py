@@ -166,6 +166,44 @@ def hea_gates(n: int, layers: int, angles: np.ndarray) -> List[Gate]:
     return out
 
 
+def inverse_qft_gates(qubits: Sequence[int]) -> List[Gate]:
+    """The textbook QFT on `qubits` (qft_gates' order: H(j), CP(pi/2^(j-m)) control m target
+    j, then the SWAPs), reversed with negated angles."""
+    m = len(qubits)
+    fwd: List[Gate] = []
+    for j in range(m - 1, -1, -1):
+        fwd.append(g1("h", qubits[j]))
+        for k in range(j - 1, -1, -1):
+            fwd.append(g2("cp", qubits[k], qubits[j], math.pi / (2 ** (j - k))))
+    for i in range(m // 2):
+        fwd.append(g2("swap", qubits[i], qubits[m - 1 - i]))
+    return [(k, a, b, -th, ph, la) for (k, a, b, th, ph, la) in reversed(fwd)]
+
+
+def qpe_gates(n_count: int, phase: float) -> List[Gate]:
+    """Quantum phase estimation of U = P(2 pi phase) on its eigenstate |1> (the paper's QPE_9:
+    8 counting qubits + 1 target, phase 1/3, "cannot be exactly represented by a 9-bit
+    fixed-point number", P:647-648): counting qubits 0..n_count-1, target n_count;
+    X(target), H(counting), CP(2 pi phase 2^k) control k -> target, inverse QFT(counting).
+    The counting register then reads ~ phase * 2^n_count."""
+    t = n_count
+    out: List[Gate] = [g1("x", t)] + [g1("h", q) for q in range(n_count)]
+    for k in range(n_count):
+        out.append(g2("cp", k, t, 2 * math.pi * phase * (2 ** k)))
+    return out + inverse_qft_gates(list(range(n_count)))
+
+
+def bv_gates(n: int, hidden: int) -> List[Gate]:
+    """Bernstein-Vazirani on n qubits (n-1 data + ancilla n-1; the paper's BV_10 with the
+    hidden string all ones): X + H on the ancilla, H on the data, CX(data_i -> ancilla)
+    for every set bit of `hidden`, H on all -- the ideal output is the single bitstring
+    hidden + 2^(n-1) (the ancilla returns to |1>)."""
+    a = n - 1
+    out: List[Gate] = [g1("x", a), g1("h", a)] + [g1("h", q) for q in range(a)]
+    out += [g2("cx", q, a) for q in range(a) if (hidden >> q) & 1]
+    return out + [g1("h", q) for q in range(n)]
+
+
 def random_circuit(n: int, n_gates: int, rng: np.random.Generator,
                    kinds: Sequence[str] = GATE_KINDS) -> List[Gate]:
     """Random gate list over every kind (for parity/unit tests)."""
