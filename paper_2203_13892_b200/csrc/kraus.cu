@@ -259,11 +259,11 @@ __global__ void __launch_bounds__(KT) kraus_slice_kernel(const __grid_constant__
     }
     __syncthreads();
   }
-  if (!a.leaf) {   // the node's state for its children
+  if (!a.leaf || a.store_leaf) {   // the node's state for its children (or a leaf's, for dumps)
     kd2* __restrict__ dst = reinterpret_cast<kd2*>(a.dst) + ((uint64_t)s << n);
     for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) dst[i] = psi[i];
     if (threadIdx.x == 0 && a.dst_flag) a.dst_flag[s] = (uint8_t)sh.flag;
-    return;
+    if (!a.leaf) return;
   }
   // leaf (§2.3, R9): thread t owns amplitudes [t C, (t+1) C); block scan of the chunk sums
   const uint32_t T = blockDim.x, C = (N + T - 1) / T;

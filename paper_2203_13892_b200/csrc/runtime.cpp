@@ -597,6 +597,7 @@ void run_level_kraus(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t par
     a.n_user = h->n_user;
     a.mode = d > 0 ? 1u : 0u;
     a.leaf = d + 1 == levels ? 1u : 0u;
+    a.store_leaf = h->debug && h->debug->n_dumps ? 1u : 0u;
     a.seedp = h->d_seed;
     a.p1 = nm.p1;
     a.p2 = nm.p2;

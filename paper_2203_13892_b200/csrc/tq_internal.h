@@ -213,6 +213,7 @@ struct KrausArgs {
   uint8_t* dst_flag;
   uint64_t child_first, parent_first;
   uint32_t arity, g0, g1, n, n_user, mode, leaf, ch_mask;   // ch_mask: 1 TR, 2 AD, 4 PD
+  uint32_t store_leaf;          // leaf level: also store the state (state dumps)
   const uint64_t* seedp;
   double p1, p2, p01, p10;
   double trg[2], trl[2];        // TR amplitude / phase damping parameters per gate class (1q, 2q)
