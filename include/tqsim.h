@@ -131,7 +131,8 @@ typedef struct {
   uint64_t flat_gate_amp_updates;   /* n_outcomes * n_lowered_gates * 2^n */
   uint64_t hbm_passes;              /* sum_d instances_d * passes(slice d) */
   uint32_t tile_qubits;             /* K: amplitudes per gate-pass tile = 2^K (auto or options) */
-  uint32_t reserved0;
+  uint32_t trail_top_bits;          /* conditional leaf sampling: the leaf index's
+                                       top bits selected first from marginals (0 = off) */
 } tqsim_plan;
 
 /* Execution statistics of the last tqsim_execute on a handle. */

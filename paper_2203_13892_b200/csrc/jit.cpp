@@ -986,7 +986,7 @@ uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal, boo
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs, int variant = 0,
-                     std::vector<uint32_t>* out_row = nullptr, double* fp64_out = nullptr) {
+                     std::vector<uint32_t>* out_row = nullptr, double* fp64_out = nullptr, int proj_m = 0) {
   const int K = pd.K, T = 1 << (K - RBITS);
   const int low = std::min(LOW_Q, K);
   const bool coal = K - RBITS >= low;   // enough lane bits to keep qubits 0..2 on lanes 0..2
@@ -1194,6 +1194,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const tq_u32 s = (tq_u32)bid;\n  const tq_u64 t = a.tiles[s];\n  const tq_u32 rsel = a.runsel[s];\n";
   else
     o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
+  if (variant == 3)   // the leaf's chosen top bits (the select kernel's chunk)
+    o << "  const tq_u32 hsel = a.runsel[s];\n";
   if (variant != 2) {
     // An instance that shares its representative's state (dedup map, launch_dedup_map:
     // no error in its slice, same effective parent) is not computed; readers go through
@@ -1285,7 +1287,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // case) run the fused fast path, the others apply each keyed Pauli after its gate
   o << "  const unsigned char* __restrict__ codes = a.rows + (tq_u64)s * " << CROW << "u;\n";
   o << "  const tq_u32 emask = __ldg(reinterpret_cast<const unsigned int*>(codes));\n";
-  o << "  const bool errs = (emask >> " << std::min<uint32_t>(pd.pass_index, 31) << ") & 1u;\n";
+  if (pd.mask_any)   // trail passes: any error in the slice (their bits are not in the row mask)
+    o << "  const bool errs = emask != 0u;\n";
+  else
+    o << "  const bool errs = (emask >> " << std::min<uint32_t>(pd.pass_index, 31) << ") & 1u;\n";
 
   auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors, int ph_only) {
   const int nph = (int)specs.size();
@@ -1912,7 +1917,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       // The leaf variants 1/2 feed only |a|^2: in their last phase the pending run-time
       // factors (diagonal entries: unit modulus) are dropped and the compile-time ones
       // reduce to their modulus.
-      const bool mag_only = last && variant != 0;
+      const bool mag_only = last && variant != 0 && variant != 3;
       std::vector<int> L;
       for (int b = 0; b < RBITS && !mag_only; ++b)
         if (fb[b].on) L.push_back(b);
@@ -1976,11 +1981,11 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         o << "    tq_u32 xl = 0u;\n";
         for (int q = 0; q < n; ++q)
           o << "    xl |= ((fx >> " << q << ") & 1u) << " << log_of_phys[q] << ";\n";
-        if (variant == 0 && !has_map) {   // variants 1/2 feed only |a|^2: the phase does not matter
+        if ((variant == 0 || variant == 3) && !has_map) {   // variants 1/2 feed only |a|^2: the phase does not matter
           o << "    const tq_u32 zt = __popc(fz & (" << gbp << "));\n";
           for (int k = 0; k < 16; ++k)
             o << "    tq_rot(" << g.r(k) << ", fk + ((zt + __popc(fz & " << gph[k] << "u)) << 1));\n";
-        } else if (variant == 0) {
+        } else if (variant == 0 || variant == 3) {
           // the frame acts after the store map: its Z sign is read on the mapped index,
           // i.e. on the stored address with fz relabeled like fx
           o << "    tq_u32 zl = 0u;\n";
@@ -2006,6 +2011,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
               o << "    tq_st2(dst + (gbs ^ " << gofs[k] << "u), " << ra << ", " << rb << ");\n";
           }
         }
+      } else if (variant == 3) {   // projection: the amplitudes whose top bits equal the leaf's choice
+        const int n2 = n - proj_m;
+        for (int k = 0; k < 16; ++k)
+          o << "    { const tq_u32 ad = (gbs ^ " << gofs[k] << "u)" << xl << "; if ((ad >> " << n2
+            << ") == hsel) a.scratch[((tq_u64)s << " << n2 << ") | (ad & " << ((1u << n2) - 1u) << "u)] = "
+            << g.r(k) << "; }\n";
       } else if (variant == 1) {   // the instance's store-address XOR (uniform per instance)
         o << "    if (t == 0 && tid == 0u) a.xlout[s] = " << (with_errors ? "xl" : "0u") << ";\n";
       } else {                     // the selected run's 8 amplitudes only
@@ -2014,7 +2025,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
             << ") == rsel) a.scratch[((tq_u64)s << " << RUN_Q << ") | (ad & " << ((1 << RUN_Q) - 1) << "u)] = "
             << g.r(k) << "; }\n";
       }
-      if (pd.leaf_sums && variant != 2) {
+      if (pd.leaf_sums && variant != 2 && variant != 3) {
         // |a|^2 sums of the 8-amplitude runs (qubits 0..2): reduce over the register bits
         // holding positions 0..2, then butterfly-shuffle over the lane bits holding the
         // rest (the store layout puts the lowest non-register positions on lanes 0..4).
@@ -2187,6 +2198,26 @@ void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint6
                        gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, names.back(), th, sm, cf, v));
       }
     }
+  if (pp.trail.on) {   // the conditional leaf sampling kernels (jit_build's trail jobs)
+    const TrailPlan& tp = pp.trail;
+    for (int v : {1, 3}) {
+      names.push_back("tq_trail_a_v" + std::to_string(v));
+      int th;
+      size_t sm;
+      std::vector<double> cf;
+      srcs.push_back(std::string(kPrelude) + kJitTypes +
+                     gen_pass(tp.a, pp, gates, pp.n_sim, 1, names.back(), th, sm, cf, v, nullptr, nullptr, tp.m));
+    }
+    for (size_t p = 0; p < tp.b.size(); ++p)
+      for (int v : p + 1 == tp.b.size() ? std::vector<int>{1, 2} : std::vector<int>{0}) {
+        names.push_back("tq_trail_b" + std::to_string(p) + "_v" + std::to_string(v));
+        int th;
+        size_t sm;
+        std::vector<double> cf;
+        srcs.push_back(std::string(kPrelude) + kJitTypes +
+                       gen_pass(tp.b[p], pp, gates, tp.n2, 2, names.back(), th, sm, cf, v));
+      }
+  }
   std::vector<std::string> errs(srcs.size());
   std::vector<size_t> sizes(srcs.size(), 0);
   std::atomic<size_t> next{0};
@@ -2215,9 +2246,10 @@ void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint6
 }
 
 std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vector<LGate>& gates,
-                                            double* compile_seconds) {
+                                            double* compile_seconds, JitTrail* trail) {
   struct Job {
     size_t d, p;
+    int which = 0;   // 0 level pass, 1 trail pass A, 2 trail stage-2 pass p
     int variant;
     std::string name, src;
     int threads;
@@ -2247,6 +2279,37 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
         jobs.push_back(std::move(j));
       }
     }
+  }
+  if (trail && pp.trail.on) {   // conditional leaf sampling (passplan.cpp plan_trail)
+    const TrailPlan& tp = pp.trail;
+    for (int v : {1, 3}) {       // pass A: run sums (marginals) / projection onto the chosen top bits
+      Job j;
+      j.which = 1;
+      j.d = pp.levels.size() - 1;
+      j.p = 0;
+      j.variant = v;
+      j.name = "tq_trail_a_v" + std::to_string(v);
+      std::string body = gen_pass(tp.a, pp, gates, pp.n_sim, 1, j.name, j.threads, j.smem, j.coefs, v, &j.out_row,
+                                  &j.fp64, tp.m);
+      j.src = std::string(kPrelude) + kJitTypes + body;
+      jobs.push_back(std::move(j));
+    }
+    for (size_t p = 0; p < tp.b.size(); ++p) {
+      const bool last = p + 1 == tp.b.size();
+      for (int v : last ? std::vector<int>{1, 2} : std::vector<int>{0}) {
+        Job j;
+        j.which = 2;
+        j.d = pp.levels.size() - 1;
+        j.p = p;
+        j.variant = v;
+        j.name = "tq_trail_b" + std::to_string(p) + "_v" + std::to_string(v);
+        std::string body = gen_pass(tp.b[p], pp, gates, tp.n2, 2, j.name, j.threads, j.smem, j.coefs, v, &j.out_row,
+                                    &j.fp64);
+        j.src = std::string(kPrelude) + kJitTypes + body;
+        jobs.push_back(std::move(j));
+      }
+    }
+    trail->b.assign(tp.b.size(), JitPass{});
   }
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<size_t> todo;
@@ -2300,7 +2363,21 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (Job& j : jobs) {
     const CompiledKernel& ck = g_cache.at(j.src);
-    JitPass& jp = out[j.d][j.p];
+    JitPass& jp = j.which == 0 ? out[j.d][j.p] : j.which == 1 ? trail->a : trail->b[j.p];
+    if (j.variant == 3) {   // trail projection: its own launch parameters
+      jp.kernel_project = reinterpret_cast<void*>(ck.fn);
+      jp.threads_project = j.threads;
+      jp.smem_project = j.smem;
+      jp.coefs_project = j.coefs;
+      continue;
+    }
+    if (j.which != 0 && j.variant == 1) {   // trail kernels without a variant 0: launch parameters
+      jp.threads = j.threads;
+      jp.smem = j.smem;
+      jp.coefs = j.coefs;
+      jp.out_row = j.out_row;
+      jp.fp64_per_amp = j.fp64;
+    }
     if (j.variant == 0) {
       jp.kernel = reinterpret_cast<void*>(ck.fn);
       jp.threads = j.threads;
@@ -2321,14 +2398,18 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
                 L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes,
                 L.tiles, L.runsel, L.scratch, L.xlout, L.rep, L.prep};
-  const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore : jp.kernel_recompute;
+  const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore
+                   : L.variant == 2 ? jp.kernel_recompute : jp.kernel_project;
   if (!kern) return (int)cudaErrorInvalidDeviceFunction;
   const uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;
   static const double zero = 0.0;
-  void* args[] = {&a, const_cast<double*>(jp.coefs.empty() ? &zero : jp.coefs.data())};
-  return (int)cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(jp.threads), args, jp.smem,
+  const std::vector<double>& cf = L.variant == 3 ? jp.coefs_project : jp.coefs;
+  void* args[] = {&a, const_cast<double*>(cf.empty() ? &zero : cf.data())};
+  const int threads = L.variant == 3 ? jp.threads_project : jp.threads;
+  const size_t smem = L.variant == 3 ? jp.smem_project : jp.smem;
+  return (int)cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), args, smem,
                                static_cast<cudaStream_t>(stream));
 }
 

@@ -34,6 +34,13 @@ struct SelectOut {
   double* dbg_u;
   double* dbg_total;
   uint8_t* dbg_flag;
+  // conditional leaf sampling: stage 1 writes the chosen chunk (the top bits)
+  // and the residual target; stage 2 samples the rest with that target and ORs the top bits
+  uint32_t* hsel;
+  double* htarget;
+  const double* tgt;
+  const uint32_t* hi;
+  uint32_t hi_shift;
 };
 
 // R9: the draw is flagged when u*total lies within 1e-9 of C(x-1) or C(x).  t = target
@@ -204,12 +211,19 @@ __global__ void __launch_bounds__(MT) sample_kernel(const cd* __restrict__ state
   const double tot = block_sum(loc, wsum);
   if (threadIdx.x == 0) total_sh = tot;
   __syncthreads();
-  const double target = u * total_sh;
-  if (threadIdx.x == 0 && so.dbg_u) so.dbg_u[leaf] = u;
-  if (threadIdx.x == 0 && so.dbg_total) so.dbg_total[leaf] = total_sh;
+  const double target = so.tgt ? so.tgt[s] : u * total_sh;   // stage 2: the residual target
+  if (threadIdx.x == 0 && so.dbg_u && !so.tgt) so.dbg_u[leaf] = u;
+  if (threadIdx.x == 0 && so.dbg_total && !so.tgt) so.dbg_total[leaf] = total_sh;
   // level 1: chunk;  level 2: 8-amplitude run inside the chunk;  level 3: amplitude
   double before1 = 0.0, before2 = 0.0;
   const uint64_t chunk = block_search(cs, nc, target, &before1, wsum, &first_sh, &pick_sh, &before_sh);
+  if (so.hsel) {   // stage 1 of the conditional sampling: the chunk = the leaf's top bits
+    if (threadIdx.x == 0) {
+      so.hsel[s] = (uint32_t)chunk;
+      so.htarget[s] = target - before1;
+    }
+    return;
+  }
   const double* rs = runs + ((uint64_t)sr << (n - RUN_Q)) + chunk * rpc;
   const uint64_t run = block_search(rs, rpc, target - before1, &before2, wsum, &first_sh, &pick_sh,
                                     &before_sh);
@@ -302,9 +316,9 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
   double total = 0.0;
   for (uint32_t i = 0; i < W; ++i) total += wtot[i];
   const double u = tq_measure_uniform(leaf, seed);
-  const double target = u * total;
-  if (threadIdx.x == 0 && so.dbg_u) so.dbg_u[leaf] = u;
-  if (threadIdx.x == 0 && so.dbg_total) so.dbg_total[leaf] = total;
+  const double target = so.tgt ? so.tgt[s] : u * total;   // stage 2: the residual target
+  if (threadIdx.x == 0 && so.dbg_u && !so.tgt) so.dbg_u[leaf] = u;
+  if (threadIdx.x == 0 && so.dbg_total && !so.tgt) so.dbg_total[leaf] = total;
   double before = 0.0;
   int ws = -1, wlast = 0;
   for (uint32_t i = 0; i < W; ++i) {
@@ -373,7 +387,8 @@ __global__ void __launch_bounds__(MT) sample_small_kernel(const cd* __restrict__
   }
   if (so.dbg_flag) so.dbg_flag[leaf] = x < 0 ? 1 : tq_flag(t3, c0, c1);
   if (x < 0) x = lastamp >= 0 ? lastamp : 0;
-  const uint32_t xi = (uint32_t)(abase + (uint64_t)x);
+  uint32_t xi = (uint32_t)(abase + (uint64_t)x);
+  if (so.hi) xi |= so.hi[s] << so.hi_shift;
   out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
 }
 
@@ -385,7 +400,8 @@ __global__ void __launch_bounds__(MT) sample_finish_kernel(const cd* __restrict_
                                                            uint32_t n_user, uint64_t leaf_first,
                                                            const uint64_t* __restrict__ seedp, double p01,
                                                            double p10, uint32_t* __restrict__ out,
-                                                           uint8_t* __restrict__ dbg_flag) {
+                                                           uint8_t* __restrict__ dbg_flag,
+                                                           const uint32_t* __restrict__ hi, uint32_t hi_shift) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= batch) return;
   const uint64_t seed = *seedp;
@@ -407,7 +423,8 @@ __global__ void __launch_bounds__(MT) sample_finish_kernel(const cd* __restrict_
   }
   if (dbg_flag) dbg_flag[leaf] = x < 0 ? 1 : tq_flag(t3, c0, c1);
   if (x < 0) x = lastamp >= 0 ? lastamp : 0;
-  const uint32_t xi = (uint32_t)(((uint64_t)runsel[s] << RUN_Q) + (uint64_t)x);
+  uint32_t xi = (uint32_t)(((uint64_t)runsel[s] << RUN_Q) + (uint64_t)x);
+  if (hi) xi |= hi[s] << hi_shift;   // conditional sampling: the stage-1 top bits
   out[leaf] = xi ^ readout_flips(xi, n_user, leaf, seed, p01, p10);
 }
 
@@ -626,6 +643,11 @@ static dev::SelectOut select_out(const LeafSelect* sel) {
   so.dbg_u = sel->dbg_u;
   so.dbg_total = sel->dbg_total;
   so.dbg_flag = sel->dbg_flag;
+  so.hsel = sel->hsel;
+  so.htarget = sel->htarget;
+  so.tgt = sel->tgt;
+  so.hi = sel->hi;
+  so.hi_shift = sel->hi_shift;
   so.runsel = sel->runsel;
   so.t3 = sel->t3;
   so.tile = sel->tile;
@@ -648,11 +670,11 @@ int launch_sample(const void* states, const double* runsums, const double* sums,
 
 int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
                          int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
-                         uint32_t* d_out, void* stream, uint8_t* d_flag) {
+                         uint32_t* d_out, void* stream, uint8_t* d_flag, const uint32_t* d_hi, uint32_t hi_shift) {
   if (batch == 0) return 0;
   dev::sample_finish_kernel<<<(batch + dev::MT - 1) / dev::MT, dev::MT, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const dev::cd*>(scratch), runsel, t3, batch, (uint32_t)n_user, leaf_first, d_seed, p01, p10,
-      d_out, d_flag);
+      d_out, d_flag, d_hi, hi_shift);
   return (int)cudaGetLastError();
 }
 

@@ -12,6 +12,7 @@
 // with which it shares no qubit (they commute); the Pauli error of a gate is
 // applied together with the gate, so "noise after its gate" holds.
 #include <algorithm>
+#include <cstdlib>
 
 #include "tq_internal.h"
 
@@ -172,6 +173,161 @@ PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, cons
 }
 
 namespace {
+// One HBM pass: the tile {0..low-1} ∪ H (padded with the lowest unused high qubits), its
+// register phases over the pass's gates (RBITS register positions each), appended to pp.
+PassDesc build_pass(PassPlan& pp, const std::vector<LGate>& gates, int K, int n, int low, uint64_t H,
+                    const std::vector<uint32_t>& group, const std::vector<uint8_t>& role, uint32_t slice_begin,
+                    uint32_t slice_len, uint32_t pass_index, bool leaf_sums) {
+  const uint64_t low_mask = (1ull << low) - 1;
+  const int hcap = K - low;
+  for (int q = low; q < n && popc(H) < hcap; ++q)   // pad with the lowest unused high qubits
+    if (!(H >> q & 1)) H |= 1ull << q;
+  PassDesc pd;
+  pd.K = K;
+  pd.slice_begin = slice_begin;
+  pd.pass_index = pass_index;
+  pd.slice_len = slice_len;
+  int pos = 0;
+  int qpos[64];
+  for (int q = 0; q < 64; ++q) qpos[q] = -1;
+  for (int q = 0; q < low; ++q) { pd.tile_q[pos] = (uint8_t)q; qpos[q] = pos++; }
+  for (int q = low; q < n; ++q)
+    if (H >> q & 1) { pd.tile_q[pos] = (uint8_t)q; qpos[q] = pos++; }
+  pd.tile_mask = low_mask | H;
+  pd.n_out = 0;
+  for (int q = 0; q < n; ++q)
+    if (!(pd.tile_mask >> q & 1)) pd.out_q[pd.n_out++] = (uint8_t)q;
+  // phases over tile positions
+  // absorbed SWAP relabelings (non-tile qubits) and diagonal units need no register
+  // slot; a unit's gates thereby stay consecutive in the op list, which is how the
+  // kernel generator fuses them back into one diagonal
+  auto pos_mask = [&](uint32_t g) {
+    const int a = qpos[gates[g].q0], b = qpos[gates[g].q1];
+    if (a < 0 || b < 0 || role[g] == ROLE_DIAG || role[g] == ROLE_STOREMAP) return 0ull;
+    return (1ull << a) | (1ull << b);
+  };
+  auto phases = group_gates(group, gates, pos_mask, RBITS);
+  pd.phase_begin = (uint32_t)pp.phases.size();
+  pd.op_begin = (uint32_t)pp.ops.size();
+  for (size_t ph = 0; ph < phases.size(); ++ph) {
+    uint64_t R = phases[ph].second;
+    for (int p = K - 1; p >= 0 && popc(R) < RBITS; --p)   // pad with high positions
+      if (!(R >> p & 1) && p >= low) R |= 1ull << p;
+    for (int p = 0; p < K && popc(R) < RBITS; ++p)
+      if (!(R >> p & 1)) R |= 1ull << p;
+    PhaseDesc pdsc{};
+    int rb = 0, rbit_of_pos[MAX_K];
+    for (int p = 0; p < K; ++p)
+      if (R >> p & 1) { pdsc.rpos[rb] = (uint8_t)p; rbit_of_pos[p] = rb++; }
+    // thread-bit -> position map
+    std::vector<int> nonr;
+    for (int p = 0; p < K; ++p)
+      if (!(R >> p & 1)) nonr.push_back(p);
+    const bool global_phase = ph == 0 || ph + 1 == phases.size();
+    std::vector<int> tmap;
+    if (!global_phase && nonr.size() >= 3) {
+      // lanes 0..2 on positions of distinct residue mod 3 -> conflict-free 16-byte
+      // shared-memory accesses under the XOR swizzle of kernels.cu
+      std::vector<int> rest = nonr;
+      for (int r = 0; r < 3; ++r)
+        for (size_t i = 0; i < rest.size(); ++i)
+          if (rest[i] % 3 == r) { tmap.push_back(rest[i]); rest.erase(rest.begin() + i); break; }
+      tmap.insert(tmap.end(), rest.begin(), rest.end());
+    } else {
+      tmap = nonr;
+    }
+    for (size_t m = 0; m < tmap.size(); ++m) pdsc.tpos[m] = (uint8_t)tmap[m];
+    pdsc.op_begin = (uint32_t)pp.ops.size();
+    for (uint32_t g : phases[ph].first) {
+      const LGate& lg = gates[g];
+      OpDesc od{};
+      od.type = lg.op;
+      od.two = lg.two ? 1 : 0;
+      od.gate = g;
+      od.role = role[g];
+      const bool intile = pos_mask(g) != 0;   // in registers
+      od.ra = intile ? (uint8_t)rbit_of_pos[qpos[lg.q0]] : 0;
+      od.rb = intile && lg.two ? (uint8_t)rbit_of_pos[qpos[lg.q1]] : od.ra;
+      pp.ops.push_back(od);
+    }
+    pdsc.op_end = (uint32_t)pp.ops.size();
+    pp.phases.push_back(pdsc);
+  }
+  // The leaf level's last pass also writes |a|^2 sums of 2^RUN_Q-amplitude runs
+  // (qubits 0..RUN_Q-1) for the sampler (jit.cpp).
+  pd.leaf_sums = leaf_sums;
+  pd.phase_end = (uint32_t)pp.phases.size();
+  pd.op_end = (uint32_t)pp.ops.size();
+  return pd;
+}
+
+// Conditional sampling through the leaf slice's trailing layer: split the
+// leaf slice into A = every gate touching G1 = the top m = K - low qubits, plus every
+// diagonal unit, and B = the rest (gates on qubits < n - m only).  If every B gate can move
+// after the A gates it precedes (no shared qubit) and A fits one pass over the tile
+// {0..low-1} ∪ G1, the leaf is sampled as: marginals over the top bits from A alone (B is
+// unitary on the other qubits), then the conditional (n-m)-qubit state of the chosen top
+// bits, B applied to it, and the rest of the index by the same inverse CDF.
+void plan_trail(PassPlan& pp, const std::vector<LGate>& gates, const Plan& plan, int n, int K, int low) {
+  const size_t L = plan.arities.size();
+  const int m = K - low, n2 = n - m;
+  if (L < 2 || m < 1 || n2 < low + 2 || pp.levels[L - 1].size() < 2) return;
+  const uint32_t b0 = (uint32_t)plan.bounds[L - 1], b1 = (uint32_t)plan.bounds[L];
+  std::vector<uint32_t> order;
+  for (uint32_t g = b0; g < b1; ++g) order.push_back(g);
+  const uint64_t G1 = ((1ull << m) - 1) << n2, tile = G1 | ((1ull << low) - 1);
+  std::vector<uint8_t> role(gates.size(), ROLE_REG);
+  std::vector<char> inA(order.size(), 0);
+  for (size_t i = 0; i < order.size();) {
+    const size_t du = diag_unit_at(order, i, gates);
+    if (du) {
+      for (size_t t = 0; t < du; ++t) {
+        inA[i + t] = 1;
+        role[order[i + t]] = ROLE_DIAG;
+      }
+      i += du;
+      continue;
+    }
+    const uint64_t qm = qmask(gates[order[i]]);
+    if (qm & G1) {
+      if (qm & ~tile) return;   // a non-diagonal gate coupling G1 to a qubit off the tile
+      inA[i] = 1;
+    }
+    ++i;
+  }
+  std::vector<uint32_t> A, B;
+  uint64_t bq = 0;   // qubits of the B gates seen so far
+  for (size_t i = 0; i < order.size(); ++i) {
+    const uint64_t qm = qmask(gates[order[i]]);
+    if (inA[i]) {
+      if (qm & bq) return;   // an A gate after a B gate on a shared qubit: B cannot move past it
+      A.push_back(order[i]);
+    } else {
+      B.push_back(order[i]);
+      bq |= qm;
+    }
+  }
+  if (B.empty() || A.size() > (size_t)MAX_PASS_OPS) return;
+  TrailPlan t;
+  t.on = true;
+  t.m = m;
+  t.n2 = n2;
+  t.a = build_pass(pp, gates, K, n, low, G1, A, role, b0, b1 - b0, 0, true);
+  t.a.mask_any = true;
+  const int K2 = std::min(K, n2);
+  const uint64_t low_mask = (1ull << low) - 1;
+  std::vector<uint8_t> role2(gates.size(), ROLE_REG);
+  auto groups = group_gates(B, gates, [&](uint32_t g) { return qmask(gates[g]) & ~low_mask; }, K2 - low,
+                            MAX_PASS_OPS);
+  for (size_t pi = 0; pi < groups.size(); ++pi) {
+    PassDesc pd = build_pass(pp, gates, K2, n2, low, groups[pi].second, groups[pi].first, role2, b0, b1 - b0,
+                             (uint32_t)(1 + pi), pi + 1 == groups.size());
+    pd.mask_any = true;
+    t.b.push_back(pd);
+  }
+  pp.trail = std::move(t);
+}
+
 PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan, int K) {
   PassPlan pp;
   const int n = std::max<int>((int)n_qubits, RBITS);
@@ -191,90 +347,14 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
                               MAX_PASS_OPS, /*absorb_swaps=*/true, low, &role,
                               /*leaf_level=*/d + 2 == plan.bounds.size());
     std::vector<PassDesc> lvl;
-    for (size_t pi = 0; pi < passes.size(); ++pi) {
-      uint64_t H = passes[pi].second;
-      for (int q = low; q < n && popc(H) < hcap; ++q)   // pad with the lowest unused high qubits
-        if (!(H >> q & 1)) H |= 1ull << q;
-      PassDesc pd;
-      pd.K = K;
-      pd.slice_begin = (uint32_t)plan.bounds[d];
-      pd.pass_index = (uint32_t)pi;
-      pd.slice_len = (uint32_t)(plan.bounds[d + 1] - plan.bounds[d]);
-      int pos = 0;
-      int qpos[64];
-      for (int q = 0; q < 64; ++q) qpos[q] = -1;
-      for (int q = 0; q < low; ++q) { pd.tile_q[pos] = (uint8_t)q; qpos[q] = pos++; }
-      for (int q = low; q < n; ++q)
-        if (H >> q & 1) { pd.tile_q[pos] = (uint8_t)q; qpos[q] = pos++; }
-      pd.tile_mask = low_mask | H;
-      pd.n_out = 0;
-      for (int q = 0; q < n; ++q)
-        if (!(pd.tile_mask >> q & 1)) pd.out_q[pd.n_out++] = (uint8_t)q;
-      // phases over tile positions
-      // absorbed SWAP relabelings (non-tile qubits) and diagonal units need no register
-      // slot; a unit's gates thereby stay consecutive in the op list, which is how the
-      // kernel generator fuses them back into one diagonal
-      auto pos_mask = [&](uint32_t g) {
-        const int a = qpos[gates[g].q0], b = qpos[gates[g].q1];
-        if (a < 0 || b < 0 || role[g] == ROLE_DIAG || role[g] == ROLE_STOREMAP) return 0ull;
-        return (1ull << a) | (1ull << b);
-      };
-      auto phases = group_gates(passes[pi].first, gates, pos_mask, RBITS);
-      pd.phase_begin = (uint32_t)pp.phases.size();
-      pd.op_begin = (uint32_t)pp.ops.size();
-      for (size_t ph = 0; ph < phases.size(); ++ph) {
-        uint64_t R = phases[ph].second;
-        for (int p = K - 1; p >= 0 && popc(R) < RBITS; --p)   // pad with high positions
-          if (!(R >> p & 1) && p >= low) R |= 1ull << p;
-        for (int p = 0; p < K && popc(R) < RBITS; ++p)
-          if (!(R >> p & 1)) R |= 1ull << p;
-        PhaseDesc pdsc{};
-        int rb = 0, rbit_of_pos[MAX_K];
-        for (int p = 0; p < K; ++p)
-          if (R >> p & 1) { pdsc.rpos[rb] = (uint8_t)p; rbit_of_pos[p] = rb++; }
-        // thread-bit -> position map
-        std::vector<int> nonr;
-        for (int p = 0; p < K; ++p)
-          if (!(R >> p & 1)) nonr.push_back(p);
-        const bool global_phase = ph == 0 || ph + 1 == phases.size();
-        std::vector<int> tmap;
-        if (!global_phase && nonr.size() >= 3) {
-          // lanes 0..2 on positions of distinct residue mod 3 -> conflict-free 16-byte
-          // shared-memory accesses under the XOR swizzle of kernels.cu
-          std::vector<int> rest = nonr;
-          for (int r = 0; r < 3; ++r)
-            for (size_t i = 0; i < rest.size(); ++i)
-              if (rest[i] % 3 == r) { tmap.push_back(rest[i]); rest.erase(rest.begin() + i); break; }
-          tmap.insert(tmap.end(), rest.begin(), rest.end());
-        } else {
-          tmap = nonr;
-        }
-        for (size_t m = 0; m < tmap.size(); ++m) pdsc.tpos[m] = (uint8_t)tmap[m];
-        pdsc.op_begin = (uint32_t)pp.ops.size();
-        for (uint32_t g : phases[ph].first) {
-          const LGate& lg = gates[g];
-          OpDesc od{};
-          od.type = lg.op;
-          od.two = lg.two ? 1 : 0;
-          od.gate = g;
-          od.role = role[g];
-          const bool intile = pos_mask(g) != 0;   // in registers
-          od.ra = intile ? (uint8_t)rbit_of_pos[qpos[lg.q0]] : 0;
-          od.rb = intile && lg.two ? (uint8_t)rbit_of_pos[qpos[lg.q1]] : od.ra;
-          pp.ops.push_back(od);
-        }
-        pdsc.op_end = (uint32_t)pp.ops.size();
-        pp.phases.push_back(pdsc);
-      }
-      // The leaf level's last pass also writes |a|^2 sums of 2^RUN_Q-amplitude runs
-      // (qubits 0..RUN_Q-1) for the sampler (jit.cpp).
-      if (d + 2 == plan.bounds.size() && pi + 1 == passes.size()) pd.leaf_sums = true;
-      pd.phase_end = (uint32_t)pp.phases.size();
-      pd.op_end = (uint32_t)pp.ops.size();
-      lvl.push_back(pd);
-    }
+    for (size_t pi = 0; pi < passes.size(); ++pi)
+      lvl.push_back(build_pass(pp, gates, K, n, low, passes[pi].second, passes[pi].first, role,
+                               (uint32_t)plan.bounds[d], (uint32_t)(plan.bounds[d + 1] - plan.bounds[d]),
+                               (uint32_t)pi, d + 2 == plan.bounds.size() && pi + 1 == passes.size()));
     pp.levels.push_back(std::move(lvl));
   }
+  if (const char* e = std::getenv("TQSIM_TRAIL"); !(e && e[0] == '0'))
+    plan_trail(pp, gates, plan, n, K, low);
   return pp;
 }
 }  // namespace

@@ -35,6 +35,7 @@ struct tqsim_handle {
   tqsim_plan cplan{};
   std::vector<uint64_t> inst;
   std::vector<std::vector<tq::JitPass>> jit;   // specialized pass kernels [level][pass]
+  tq::JitTrail jit_trail;                      // conditional leaf sampling kernels (pp.trail)
   double compile_s = 0.0;
   uint8_t* d_two = nullptr;
   uint8_t* d_pass_of = nullptr;   // per lowered gate: index of its pass in its level (<= 31)
@@ -146,6 +147,8 @@ struct Layout {
   std::vector<uint64_t> map_lvl;        // entry offset of each level's map
   uint64_t map_entries = 0;
   std::vector<uint64_t> kflag_off;      // Kraus engine: per level, one path-flag byte per batch slot
+  // conditional leaf sampling (pp.trail): projected states, their run sums, stage-1 outputs
+  uint64_t psi_off = 0, runs2_off = 0, hsel_off = 0, htgt_off = 0;
   uint64_t sel_off = 0;                 // leaf select / recompute buffers (per leaf of a batch):
                                         // runsel u32, tile u32, xl u32, t3 f64, 8 amplitudes
   int chunk_log2 = 0;
@@ -276,6 +279,17 @@ Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl) {
       l.kflag_off.push_back(off);
       off = align_up(off + (h->kraus ? l.cap[d] : 0));
     }
+    if (h->pp.trail.on) {
+      const uint64_t capl = l.cap.back(), n2 = (uint64_t)h->pp.trail.n2;
+      l.psi_off = off;
+      off = align_up(off + (capl << n2) * 16);
+      l.runs2_off = off;
+      off = align_up(off + capl * (8ull << (n2 - RUN_Q)));
+      l.hsel_off = off;
+      off = align_up(off + capl * 4);
+      l.htgt_off = off;
+      off = align_up(off + capl * 8);
+    }
     l.sel_off = off;
     off = align_up(off + l.cap.back() * (4 + 4 + 4 + 8 + (16ull << RUN_Q)) + 4 * ALIGN);
     l.total = off;
@@ -389,6 +403,154 @@ void dump_if_requested(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, const char
   }
 }
 
+// Conditional leaf sampling of one leaf batch [b, b+cnt) (passplan.cpp
+// plan_trail).  The inverse CDF over the index (R9) is taken top bits first: the marginals of
+// the top m bits need only the A gates (the B gates act on the other qubits and are unitary
+// there), so
+//   1. pass A (fan-out + A gates) writes run sums, summed into 2^m chunk sums = marginals;
+//   2. stage-1 select: the chunk (top bits) holding u*total and the residual target;
+//   3. pass A again, storing only the amplitudes of the chosen top bits (projection, every
+//      leaf -- a shared state has per-leaf top bits) -> an n2-qubit state per leaf;
+//   4. the B passes on those states (the last writes run sums);
+//   5. stage-2 select with the residual target -> recompute the run's tile -> finish
+//      (outcome = top bits << n2 | rest, readout flips on every bit).
+// Same outcome as sampling the full leaf state (the same inverse CDF, same u) up to rounding
+// (draws within 1e-9 of a boundary are flagged, R9); the leaf state is never materialised.
+void run_leaf_trail(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, uint64_t parent_first, const char* pbuf,
+                    char* buf, const uint8_t* rows, uint32_t row_bytes) {
+  tqsim_handle* h = x.h;
+  const TrailPlan& tp = h->pp.trail;
+  const JitTrail& jt = h->jit_trail;
+  const int n = h->n_sim, n2 = tp.n2;
+  const uint64_t capl = x.L.cap.back();
+  char* sel = x.ws + x.L.sel_off;
+  uint32_t* runsel = reinterpret_cast<uint32_t*>(sel);
+  uint32_t* tiles = reinterpret_cast<uint32_t*>(sel + align_up(4 * capl));
+  uint32_t* xlv = reinterpret_cast<uint32_t*>(sel + 2 * align_up(4 * capl));
+  double* t3 = reinterpret_cast<double*>(sel + 3 * align_up(4 * capl));
+  void* scratch = sel + 3 * align_up(4 * capl) + align_up(8 * capl);
+  double* runs = reinterpret_cast<double*>(x.ws + x.L.runs_off);
+  double* sums = reinterpret_cast<double*>(x.ws + x.L.sums_off);
+  char* psi = x.ws + x.L.psi_off;
+  double* runs2 = reinterpret_cast<double*>(x.ws + x.L.runs2_off);
+  uint32_t* hsel = reinterpret_cast<uint32_t*>(x.ws + x.L.hsel_off);
+  double* htgt = reinterpret_cast<double*>(x.ws + x.L.htgt_off);
+  const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
+  const uint32_t* rep = x.dedup && cnt > 1 ? maps + x.L.map_lvl[d] + (b - x.lvl_first[d]) : nullptr;
+  const uint32_t* prep = x.dedup && d > 0 && x.pcnt[d - 1] > 1
+                             ? maps + x.L.map_lvl[d - 1] + (parent_first - x.lvl_first[d - 1]) : nullptr;
+  const uint64_t A = h->plan.arities[d];
+  const uint64_t parents = (b + cnt - 1) / A - b / A + 1;
+  PassLaunch pl{};
+  pl.src_mode = 1u;
+  pl.src = pbuf;
+  pl.dst = buf;
+  pl.child_first = b;
+  pl.parent_first = parent_first;
+  pl.arity = (uint32_t)A;
+  pl.batch = (uint32_t)cnt;
+  pl.seed = x.seed;
+  pl.p1 = h->noise.p1;
+  pl.p2 = h->noise.p2;
+  pl.rows = rows;
+  pl.row_bytes = row_bytes;
+  pl.prep = prep;
+  // 1. pass A: run sums of the computed (representative) leaves
+  pl.variant = 1u;
+  pl.runsum = runs;
+  pl.xlout = xlv;
+  pl.rep = rep;
+  mark(x, 0, d, 0, b, cnt);
+  ck(launch_jit_pass(jt.a, tp.a, pl, x.st), "trail pass A launch");
+  mark(x, 0, d, 0, b, cnt);
+  h->stats.pass_bytes += (cnt << n) * 1 + (parents << n) * 16;
+  // 2. chunk sums over the top bits (marginals) and the stage-1 select
+  LeafSelect s1{};
+  s1.rep = rep;
+  s1.hsel = hsel;
+  s1.htarget = htgt;
+  s1.dbg_u = h->d_dbg_u;
+  s1.dbg_total = h->d_dbg_total;
+  mark(x, 1, d, 0, b, cnt);
+  ck(launch_chunk_sums(runs, (uint32_t)cnt, n, n2, sums, x.st, &s1, b), "trail chunk sums launch");
+  ck(launch_sample(buf, runs, sums, (uint32_t)cnt, n, (int)h->n_user, n2, b, h->d_seed, h->noise.readout_p01,
+                   h->noise.readout_p10, x.d_out, x.st, &s1),
+     "trail select launch");
+  mark(x, 1, d, 0, b, cnt);
+  // 3. projection onto the chosen top bits (every leaf: a shared state has per-leaf choices)
+  PassLaunch pb = pl;
+  pb.variant = 3u;
+  pb.rep = nullptr;
+  pb.runsel = hsel;
+  pb.scratch = psi;
+  mark(x, 0, d, 100, b, cnt);
+  ck(launch_jit_pass(jt.a, tp.a, pb, x.st), "trail projection launch");
+  mark(x, 0, d, 100, b, cnt);
+  h->stats.pass_bytes += (parents << n) * 16 + (cnt << n2) * 16;
+  // 4. the B passes on the projected n2-qubit states, in place
+  PassLaunch last{};
+  for (size_t p = 0; p < tp.b.size(); ++p) {
+    PassLaunch q = pl;
+    q.src_mode = 2u;
+    q.src = psi;
+    q.dst = psi;
+    q.prep = nullptr;
+    q.rep = nullptr;
+    q.child_first = b;
+    const bool lastp = p + 1 == tp.b.size();
+    q.variant = lastp ? 1u : 0u;
+    q.runsum = runs2;
+    q.xlout = xlv;
+    mark(x, 0, d, 101 + (uint32_t)p, b, cnt);
+    ck(launch_jit_pass(jt.b[p], tp.b[p], q, x.st), "trail stage-2 pass launch");
+    mark(x, 0, d, 101 + (uint32_t)p, b, cnt);
+    h->stats.pass_bytes += (cnt << n2) * (lastp ? 17 : 32);
+    if (lastp) last = q;
+  }
+  h->stats.kernel_launches += 4 + tp.b.size();
+  h->stats.pass_launches += 2 + tp.b.size();
+  // 5. stage 2: the rest of the index from the residual target; recompute; finish
+  const JitPass& jl = jt.b.back();
+  LeafSelect s2{};
+  s2.runsel = runsel;
+  s2.t3 = t3;
+  s2.tile = tiles;
+  s2.xl = xlv;
+  s2.n_out = (uint32_t)jl.out_row.size();
+  for (size_t i = 0; i < jl.out_row.size() && i < 32; ++i) s2.out_row[i] = jl.out_row[i];
+  s2.tgt = htgt;
+  s2.hi = hsel;
+  s2.hi_shift = (uint32_t)n2;
+  mark(x, 1, d, 1, b, cnt);
+  if (n2 - RUN_Q <= SMALL_SAMPLE_RUNS_LOG2) {
+    ck(launch_sample_small(psi, runs2, (uint32_t)cnt, n2, (int)h->n_user, b, h->d_seed, h->noise.readout_p01,
+                           h->noise.readout_p10, x.d_out, x.st, &s2),
+       "trail stage-2 select launch");
+    h->stats.kernel_launches += 1;
+  } else {
+    const int c2 = std::min(n2, 12);
+    ck(launch_chunk_sums(runs2, (uint32_t)cnt, n2, c2, sums, x.st, &s2, b), "trail stage-2 chunk sums");
+    ck(launch_sample(psi, runs2, sums, (uint32_t)cnt, n2, (int)h->n_user, c2, b, h->d_seed, h->noise.readout_p01,
+                     h->noise.readout_p10, x.d_out, x.st, &s2),
+       "trail stage-2 select launch");
+    h->stats.kernel_launches += 2;
+  }
+  PassLaunch rc = last;
+  rc.variant = 2;
+  rc.tiles = tiles;
+  rc.runsel = runsel;
+  rc.scratch = scratch;
+  ck(launch_jit_pass(jl, tp.b.back(), rc, x.st), "trail leaf recompute launch");
+  ck(launch_sample_finish(scratch, runsel, t3, (uint32_t)cnt, (int)h->n_user, b, h->d_seed, h->noise.readout_p01,
+                          h->noise.readout_p10, x.d_out, x.st, h->d_dbg_flag, hsel, (uint32_t)n2),
+     "trail sample finish launch");
+  mark(x, 1, d, 1, b, cnt);
+  h->stats.kernel_launches += 2;
+  h->stats.measure_launches += 5;
+  h->stats.measure_bytes += (cnt << (n - RUN_Q)) * 8 + cnt * ((16ull << tp.b.back().K) + (16ull << RUN_Q) * 2);
+  h->stats.leaves += cnt;
+}
+
 void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_first,
                const char* parent_buf = nullptr) {
   tqsim_handle* h = x.h;
@@ -429,6 +591,12 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     uint32_t* xlv = reinterpret_cast<uint32_t*>(sel + 2 * align_up(4 * capl));
     double* t3 = reinterpret_cast<double*>(sel + 3 * align_up(4 * capl));
     void* scratch = sel + 3 * align_up(4 * capl) + align_up(8 * capl);
+    if (leaf && nostore && h->pp.trail.on) {   // conditional leaf sampling (default path)
+      run_leaf_trail(x, d, b, cnt, parent_first, pbuf, buf, rows, row_bytes);
+      h->stats.node_executions += cnt;
+      h->stats.gate_amp_updates += (cnt * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
+      continue;
+    }
     PassLaunch last{};
     for (size_t p = 0; p < passes.size(); ++p) {
       PassLaunch pl{};
@@ -735,6 +903,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     h->inst = instances(h->plan);
     fill_plan(h->plan, c->n_qubits, h->gates.size(), h->pp.passes_total(h->inst), &h->cplan);
     h->cplan.tile_qubits = h->pp.levels.empty() || h->pp.levels[0].empty() ? 0u : (uint32_t)h->pp.levels[0][0].K;
+    h->cplan.trail_top_bits = h->pp.trail.on && !h->kraus ? (uint32_t)h->pp.trail.m : 0u;
     if (need_gpu) {
       require_device();
       const size_t G = std::max<size_t>(h->gates.size(), 1);
@@ -764,7 +933,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
         ckc(cudaMemcpy(h->d_kgates, kg.data(), sizeof(KGate) * kg.size(), cudaMemcpyHostToDevice), "kraus gates");
       } else {
         // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
-        h->jit = jit_build(h->pp, h->gates, &h->compile_s);
+        h->jit = jit_build(h->pp, h->gates, &h->compile_s, &h->jit_trail);
       }
 
     }
@@ -937,6 +1106,20 @@ double pass_alg_bytes(const tqsim_handle* h, uint32_t d, size_t p, uint64_t comp
   return bytes;
 }
 
+// Conditional leaf sampling (run_leaf_trail): algorithmic bytes of its kernels over a leaf
+// batch of `cnt` leaves, `comp` of them computed, reading `parents` (computed) / `parents_all`
+// distinct parent states.  pass 0 = A (run sums), 100 = projection, 101 + p = stage-2 pass p.
+double trail_alg_bytes(const tqsim_handle* h, uint32_t pass, uint64_t cnt, uint64_t comp, uint64_t parents,
+                       uint64_t parents_all) {
+  const double S = (double)(1ull << h->n_sim), S2 = (double)(1ull << h->pp.trail.n2);
+  if (pass == 0) return (double)comp * S + (double)parents * S * 16.0;
+  if (pass == 100) return (double)parents_all * S * 16.0 + (double)cnt * S2 * 16.0;
+  const bool lastp = pass - 101 + 1 == h->pp.trail.b.size();
+  return (double)cnt * S2 * (lastp ? 17.0 : 32.0);
+}
+
+bool trail_active(const tqsim_handle* h) { return h->pp.trail.on && !(h->debug && h->debug->n_dumps); }
+
 void fill_computed(tqsim_handle* h, const ShardRange& sr, const Layout& L, const char* ws) {
   const bool dumps = h->debug && h->debug->n_dumps;
   const bool dedup = !dumps && !h->opts.no_dedup && !h->kraus;
@@ -949,6 +1132,15 @@ void fill_computed(tqsim_handle* h, const ShardRange& sr, const Layout& L, const
     const BatchWork& w = kv.second;
     st.computed_node_executions += w.comp;
     st.computed_gate_amp_updates += (w.comp * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
+    if (d + 1 == h->plan.arities.size() && trail_active(h)) {
+      const uint64_t A = h->plan.arities[d], b = kv.first.second;
+      const uint64_t cnt = std::min(L.cap[d], sr.hi[d] - b);
+      const uint64_t pall = (b + cnt - 1) / A - b / A + 1;
+      bytes += trail_alg_bytes(h, 0, cnt, w.comp, w.parents, pall) + trail_alg_bytes(h, 100, cnt, w.comp, w.parents, pall);
+      for (size_t p = 0; p < h->pp.trail.b.size(); ++p)
+        bytes += trail_alg_bytes(h, 101 + (uint32_t)p, cnt, w.comp, w.parents, pall);
+      continue;
+    }
     const size_t np = h->kraus ? 1 : h->pp.levels[d].size();
     for (size_t p = 0; p < np; ++p) bytes += pass_alg_bytes(h, d, p, w.comp, w.parents, !dumps);
   }
@@ -1338,9 +1530,20 @@ tqsim_status tqsim_profile_tree(tqsim_handle* h, uint64_t seed, uint32_t rank, u
       k.ms += ms;
       if (tg.kind != 0 && tg.kind != 3) continue;
       k.states += tg.cnt;
-      if (tg.kind == 0) k.fp64_per_amp = h->jit[tg.level][tg.pass].fp64_per_amp;
       auto it = wm.find({tg.level, tg.b});
       const BatchWork w = it != wm.end() ? it->second : BatchWork{tg.cnt, 0};
+      if (tg.kind == 0 && tg.level + 1 == h->plan.arities.size() && trail_active(h)) {   // trail kernels
+        const uint64_t A = h->plan.arities[tg.level];
+        const uint64_t pall = (tg.b + tg.cnt - 1) / A - tg.b / A + 1;
+        const uint64_t comp = tg.pass == 0 ? w.comp : tg.cnt;
+        k.computed_states += comp;
+        k.alg_bytes += trail_alg_bytes(h, tg.pass, tg.cnt, w.comp, w.parents, pall);
+        k.nominal_bytes += trail_alg_bytes(h, tg.pass, tg.cnt, tg.cnt, pall, pall);
+        k.fp64_per_amp = tg.pass == 0 || tg.pass == 100 ? h->jit_trail.a.fp64_per_amp
+                                                         : h->jit_trail.b[tg.pass - 101].fp64_per_amp;
+        continue;
+      }
+      if (tg.kind == 0) k.fp64_per_amp = h->jit[tg.level][tg.pass].fp64_per_amp;
       k.computed_states += w.comp;
       k.alg_bytes += pass_alg_bytes(h, tg.level, tg.pass, w.comp, w.parents, !(h->debug && h->debug->n_dumps));
       const uint64_t A = h->plan.arities[tg.level];

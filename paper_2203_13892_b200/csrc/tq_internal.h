@@ -93,6 +93,16 @@ struct PassDesc {
   uint32_t slice_begin = 0;     // first lowered gate of the level's slice
   uint32_t pass_index = 0;      // index of this pass within its level
   uint32_t slice_len = 0;       // gates of the level's slice
+  bool mask_any = false;        // take the careful path when any gate of the slice erred
+                                // (trail passes: their gates' pass bits are not in the row mask)
+};
+
+// Conditional leaf sampling through the trailing layer (passplan.cpp plan_trail)
+struct TrailPlan {
+  bool on = false;
+  int m = 0, n2 = 0;            // G1 = the top m qubits; stage-2 width n2 = n - m
+  PassDesc a;                   // pass A over {0..2} ∪ G1: run sums (variant 1) / projection (variant 3)
+  std::vector<PassDesc> b;      // stage-2 passes on the projected n2-qubit states (last: run sums)
 };
 
 struct PassPlan {
@@ -100,6 +110,7 @@ struct PassPlan {
   std::vector<std::vector<PassDesc>> levels;   // per level, its passes
   std::vector<PhaseDesc> phases;
   std::vector<OpDesc> ops;
+  TrailPlan trail;                       // leaf level: conditional sampling (default path)
   uint64_t passes_total(const std::vector<uint64_t>& inst) const;
 };
 
@@ -182,10 +193,18 @@ struct LeafSelect {
   double* dbg_u = nullptr;
   double* dbg_total = nullptr;
   uint8_t* dbg_flag = nullptr;
+  // conditional leaf sampling: stage-1 outputs (chunk = top bits, residual target) /
+  // stage-2 inputs (target override, top bits ORed into the outcome at hi_shift)
+  uint32_t* hsel = nullptr;
+  double* htarget = nullptr;
+  const double* tgt = nullptr;
+  const uint32_t* hi = nullptr;
+  uint32_t hi_shift = 0;
 };
 int launch_sample_finish(const void* scratch, const uint32_t* runsel, const double* t3, uint32_t batch,
                          int n_user, uint64_t leaf_first, const uint64_t* d_seed, double p01, double p10,
-                         uint32_t* d_out, void* stream, uint8_t* d_flag = nullptr);
+                         uint32_t* d_out, void* stream, uint8_t* d_flag = nullptr,
+                         const uint32_t* d_hi = nullptr, uint32_t hi_shift = 0);
 int launch_sample(const void* states, const double* runsums, const double* sums, uint32_t batch,
                   int n_sim, int n_user, int chunk_log2, uint64_t leaf_first, const uint64_t* d_seed,
                   double p01, double p10, uint32_t* d_out, void* stream, const LeafSelect* sel = nullptr);
@@ -238,9 +257,18 @@ struct JitPass {
   size_t smem = 0;
   std::vector<double> coefs;      // by-value coefficient parameter (TQSIM_JIT_COEF=0 mode)
   double fp64_per_amp = 0.0;      // FP64 operations per amplitude of the fast path (cost model)
+  // trail pass A: the projection kernel (variant 3) and its launch parameters
+  void* kernel_project = nullptr;
+  int threads_project = 0;
+  size_t smem_project = 0;
+  std::vector<double> coefs_project;
+};
+struct JitTrail {                  // kernels of PassPlan::trail
+  JitPass a;                       // kernel_nostore = run sums (v1), kernel_project = projection (v3)
+  std::vector<JitPass> b;          // stage-2 passes (the last: kernel_nostore v1, kernel_recompute v2)
 };
 std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vector<LGate>& gates,
-                                            double* compile_seconds);
+                                            double* compile_seconds, JitTrail* trail = nullptr);
 void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint64_t* n_kernels,
                       uint64_t* cubin_bytes);
 std::string jit_source(const PassPlan& pp, const std::vector<LGate>& gates, size_t level,

@@ -416,3 +416,37 @@ def test_random_circuits_dedup_vs_oracle(tile, p):
         shots = int(np.prod(arities))
         opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 3)
         run_and_compare(n, gates, nm, shots, arities, 900 + it, opts)
+
+
+@pytest.mark.parametrize("n,tile,p,ar", [(14, 7, 0.05, [3, 2, 4]), (14, 8, 1.0, [3, 2, 4]), (12, 6, 0.002, [4, 6]),
+                                         (13, 0, 0.2, [2, 3, 4]), (20, 4, 0.01, [2, 3])])
+def test_conditional_leaf_sampling_vs_oracle(n, tile, p, ar):
+    """Leaf slices ending in a single-qubit layer (QAOA mixers) are sampled top bits first
+    (marginals of the top bits from the gates touching them, then the
+    conditional state of the chosen bits): the outcomes equal the oracle's full-state
+    inverse CDF and the stored-state path's, with errors in every kernel (p up to 1), dedup
+    maps (p = 0.002), and the stage-2 chunk sampler (n = 20, one top bit)."""
+    from workloads.generators import qaoa_gates, random_3_regular_edges
+    rng = np.random.default_rng(n * 10 + tile)
+    edges = random_3_regular_edges(n, rng) if n % 2 == 0 else [(q, (q + 1) % n) for q in range(n)]
+    gates = qaoa_gates(n, edges, list(rng.uniform(0, 3, 2)), list(rng.uniform(0, 3, 2)))
+    nm = NoiseModel(p, min(1.0, 2 * p), 0.02, 0.03)
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    shots = int(np.prod(ar))
+    plan = T.tqsim_plan_circuit(n, gates, noise, shots, ar, opts)
+    assert plan.trail_top_bits > 0, "the plan does not use conditional leaf sampling"
+    a = T.tqsim_run_ex(n, gates, noise, shots, ar, 21, opts, (), leaf_debug=True)           # conditional
+    b = T.tqsim_run_ex(n, gates, noise, shots, ar, 21, opts, [(len(ar) - 1, 0)])             # stored path
+    ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 21)
+    flagged = {l for l, r in ref.leaves.items() if r.flagged}
+    for l, r in ref.leaves.items():
+        assert a.leaf_u[l] == r.u
+        if l in flagged:
+            continue
+        assert int(a.leaf_outcomes[l]) == r.outcome, (l, int(a.leaf_outcomes[l]), r.outcome)
+        assert int(b.leaf_outcomes[l]) == r.outcome
+        assert not a.leaf_flagged[l]
+    nd = T.tqsim_run_ex(n, gates, noise, shots, ar, 21, T.default_options(tile_qubits=tile, batch_log2_amps=n + 2,
+                                                                       no_dedup=1))
+    assert np.array_equal(nd.leaf_outcomes, a.leaf_outcomes)
