@@ -761,7 +761,7 @@ void run_level_kraus(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t par
     a.arity = h->plan.arities[d];
     a.g0 = (uint32_t)h->plan.bounds[d];
     a.g1 = (uint32_t)h->plan.bounds[d + 1];
-    a.n = (uint32_t)h->n_user;
+    a.n = (uint32_t)h->n_sim;   // the layout's state size (n < 4 padded, R28: the pad qubits stay |0>)
     a.n_user = h->n_user;
     a.mode = d > 0 ? 1u : 0u;
     a.leaf = d + 1 == levels ? 1u : 0u;
