@@ -256,7 +256,16 @@ Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl) {
     l.runs_off = off;
     off = align_up(off + l.cap.back() * (8ull << (n - RUN_Q)));
     l.sums_off = off;
-    off = align_up(off + l.cap.back() * (8ull << (n - l.chunk_log2)));
+    {   // chunk sums: the sampler's chunks, or (conditional leaf sampling) 2^m top-bit chunks and
+        // the stage-2 sampler's chunks of the n2-qubit states
+      uint64_t per = 8ull << (n - l.chunk_log2);
+      if (h->pp.trail.on) {
+        const int n2 = h->pp.trail.n2;
+        per = std::max<uint64_t>(per, 8ull << (n - n2));
+        per = std::max<uint64_t>(per, 8ull << (n2 - std::min(n2, 12)));
+      }
+      off = align_up(off + l.cap.back() * per);
+    }
     l.rows_off = off;   // noise rows of every instance of the shard (drawn in one launch)
     uint64_t rows = 0;
     l.rows_lvl_off.clear();

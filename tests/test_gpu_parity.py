@@ -418,8 +418,8 @@ def test_random_circuits_dedup_vs_oracle(tile, p):
         run_and_compare(n, gates, nm, shots, arities, 900 + it, opts)
 
 
-@pytest.mark.parametrize("n,tile,p,ar", [(14, 7, 0.05, [3, 2, 4]), (14, 8, 1.0, [3, 2, 4]), (12, 6, 0.002, [4, 6]),
-                                         (13, 0, 0.2, [2, 3, 4]), (20, 4, 0.01, [2, 3])])
+@pytest.mark.parametrize("n,tile,p,ar", [(14, 7, 0.05, [3, 2, 4]), (14, 8, 1.0, [3, 2, 4]), (12, 6, 0.002, [2, 2, 2, 3]),
+                                         (13, 0, 0.2, [4, 6]), (20, 4, 0.01, [2, 3, 4])])
 def test_conditional_leaf_sampling_vs_oracle(n, tile, p, ar):
     """Leaf slices ending in a single-qubit layer (QAOA mixers) are sampled top bits first
     (marginals of the top bits from the gates touching them, then the
