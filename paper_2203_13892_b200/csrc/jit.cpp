@@ -52,6 +52,8 @@ struct TqJitArgs {
   const tq_u32* tiles; const tq_u32* runsel; tq_d2* scratch; tq_u32* xlout;
   // dedup maps (launch_dedup_map) of the batch and of the parent batch, or null
   const tq_u32* rep; const tq_u32* prep;
+  // projection (variant 3) work list: leaves and their count, or null (every leaf)
+  const tq_u32* wlist; const tq_u32* wcount;
 };
 // 16-byte global load the compiler may not sink below the error-branch: the tile loads
 // are issued before the (dependent) noise-row mask load is waited on
@@ -91,6 +93,8 @@ struct HostJitArgs {   // mirrors TqJitArgs
   uint32_t* xlout;
   const uint32_t* rep;
   const uint32_t* prep;
+  const uint32_t* wlist;
+  const uint32_t* wcount;
 };
 
 std::string hexd(double v) {
@@ -1192,6 +1196,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
   if (variant == 2)   // one CTA per leaf, on the tile holding its selected run
     o << "  const tq_u32 s = (tq_u32)bid;\n  const tq_u64 t = a.tiles[s];\n  const tq_u32 rsel = a.runsel[s];\n";
+  else if (variant == 3)   // projection: every (leaf, tile), or the leaves of a work list (persistent CTAs)
+    o << "  const tq_u32 nw = a.wlist ? *a.wcount : a.batch;\n"
+      << "  for (tq_u64 w = bid; w < ((tq_u64)nw << " << pd.n_out << "); w += gridDim.x) {\n"
+      << "  const tq_u32 s = a.wlist ? a.wlist[w % nw] : (tq_u32)(w % nw);\n  const tq_u64 t = w / nw;\n";
   else
     o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
   if (variant == 3)   // the leaf's chosen top bits (the select kernel's chunk)
@@ -2118,6 +2126,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     emit_phases(fast, true, ph);
     o << "  }\n";
   }
+  if (variant == 3) o << "  __syncthreads();\n  }\n";   // the work loop (shared memory is reused)
   o << "}\n";
   g_pool = nullptr;
   coefs = pool.vals;
@@ -2397,11 +2406,12 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
                 L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes,
-                L.tiles, L.runsel, L.scratch, L.xlout, L.rep, L.prep};
+                L.tiles, L.runsel, L.scratch, L.xlout, L.rep, L.prep, L.wlist, L.wcount};
   const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore
                    : L.variant == 2 ? jp.kernel_recompute : jp.kernel_project;
   if (!kern) return (int)cudaErrorInvalidDeviceFunction;
-  const uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;
+  uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;
+  if (L.variant == 3 && L.wlist) grid = std::min<uint64_t>(grid, 4 * 148);   // persistent over the work list
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;
   static const double zero = 0.0;

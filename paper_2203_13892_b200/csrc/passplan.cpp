@@ -12,6 +12,7 @@
 // with which it shares no qubit (they commute); the Pauli error of a gate is
 // applied together with the gate, so "noise after its gate" holds.
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 
 #include "tq_internal.h"
@@ -309,6 +310,97 @@ void plan_trail(PassPlan& pp, const std::vector<LGate>& gates, const Plan& plan,
   }
   if (B.empty() || A.size() > (size_t)MAX_PASS_OPS) return;
   TrailPlan t;
+  // the fast projection's spec (ProjSpec): diagonal units before the top-bit 1q gates
+  {
+    ProjSpec& ps = t.proj;
+    ps.m = (uint32_t)m;
+    ps.n2 = (uint32_t)n2;
+    bool ok = true;
+    uint64_t touched = 0;   // top qubits that already got a 1q gate
+    std::vector<std::array<double, 8>> ug, ux;
+    std::vector<std::pair<uint32_t, uint32_t>> uqg, uqx;
+    auto cmul = [](const double* a, const double* b, double* o) {   // o = a * b (complex)
+      o[0] = a[0] * b[0] - a[1] * b[1];
+      o[1] = a[0] * b[1] + a[1] * b[0];
+    };
+    for (size_t i = 0; i < A.size() && ok;) {
+      const LGate& x = gates[A[i]];
+      size_t du = diag_unit_at(A, i, gates);
+      const bool top1q = !x.two && (int)x.q0 >= n2;
+      if (du && !top1q) {
+        // the unit's 4 diagonal entries over (bit a, bit b) by applying its gates to basis states
+        const uint32_t qa = x.q0, qb = x.two ? x.q1 : x.q0;
+        std::array<double, 8> T{};
+        for (int idx = 0; idx < 4 && ok; ++idx) {
+          if (qa == qb && (idx == 1 || idx == 2)) continue;
+          int ba = idx & 1, bb = idx >> 1;
+          double amp[2] = {1.0, 0.0};
+          for (size_t t2 = 0; t2 < du; ++t2) {
+            const LGate& g = gates[A[i + t2]];
+            if (g.op == OP_CX) {
+              const int c = g.q0 == qa ? ba : bb;
+              if (c) (g.q1 == qa ? ba : bb) ^= 1;
+            } else if (g.op == OP_CZ) {
+              if (ba && bb) amp[0] = -amp[0], amp[1] = -amp[1];
+            } else {   // 1q diagonal on qa or qb
+              const int bit = g.q0 == qa ? ba : bb;
+              const double d[2] = {g.m[bit ? 6 : 0], g.m[bit ? 7 : 1]};
+              double o[2];
+              cmul(d, amp, o);
+              amp[0] = o[0];
+              amp[1] = o[1];
+            }
+          }
+          if (ba != (idx & 1) || bb != (idx >> 1)) ok = false;   // not diagonal
+          T[2 * idx] = amp[0];
+          T[2 * idx + 1] = amp[1];
+        }
+        const bool ga = (int)qa >= n2, gb = (int)qb >= n2;
+        if (ga != gb) ok = false;                                      // couples top and low bits
+        if (ga && ((touched >> qa & 1) || (touched >> qb & 1))) ok = false;   // after a top 1q gate
+        if (ga) {
+          uqg.push_back({qa - n2, qb - n2});
+          ug.push_back(T);
+        } else {
+          uqx.push_back({qa, qb});
+          ux.push_back(T);
+        }
+        for (size_t t2 = 0; t2 < du; ++t2) {
+          if (ps.ndg >= (uint32_t)PROJ_MAX_DG) { ok = false; break; }
+          ps.dgoff[ps.ndg++] = A[i + t2] - b0;
+        }
+        i += du;
+        continue;
+      }
+      if (top1q) {   // a 1q gate on a top qubit (diagonal or not): part of U_j, in order
+        if (ps.ng >= (uint32_t)PROJ_MAX_G) { ok = false; break; }
+        ps.gbit[ps.ng] = x.q0 - n2;
+        ps.goff[ps.ng] = A[i] - b0;
+        for (int k = 0; k < 8; ++k) ps.gmat[ps.ng][k] = x.m[k];
+        ++ps.ng;
+        touched |= 1ull << x.q0;
+        ++i;
+        continue;
+      }
+      ok = false;   // a non-diagonal gate among the top qubits (e.g. CX(16, 17))
+    }
+    if (ok && m <= 10 && ug.size() + ux.size() <= (size_t)PROJ_MAX_U) {
+      ps.nug = (uint32_t)ug.size();
+      ps.nux = (uint32_t)ux.size();
+      size_t k = 0;
+      for (size_t u = 0; u < ug.size(); ++u, ++k) {
+        ps.ua[k] = uqg[u].first;
+        ps.ub[k] = uqg[u].second;
+        for (int e = 0; e < 8; ++e) ps.uT[k][e] = ug[u][e];
+      }
+      for (size_t u = 0; u < ux.size(); ++u, ++k) {
+        ps.ua[k] = uqx[u].first;
+        ps.ub[k] = uqx[u].second;
+        for (int e = 0; e < 8; ++e) ps.uT[k][e] = ux[u][e];
+      }
+      t.fast = std::getenv("TQSIM_TRAIL_FAST") == nullptr || std::getenv("TQSIM_TRAIL_FAST")[0] != '0';
+    }
+  }
   t.on = true;
   t.m = m;
   t.n2 = n2;

@@ -148,7 +148,7 @@ struct Layout {
   uint64_t map_entries = 0;
   std::vector<uint64_t> kflag_off;      // Kraus engine: per level, one path-flag byte per batch slot
   // conditional leaf sampling (pp.trail): projected states, their run sums, stage-1 outputs
-  uint64_t psi_off = 0, runs2_off = 0, hsel_off = 0, htgt_off = 0;
+  uint64_t psi_off = 0, runs2_off = 0, hsel_off = 0, htgt_off = 0, glist_off = 0;
   uint64_t sel_off = 0;                 // leaf select / recompute buffers (per leaf of a batch):
                                         // runsel u32, tile u32, xl u32, t3 f64, 8 amplitudes
   int chunk_log2 = 0;
@@ -298,6 +298,8 @@ Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl) {
       off = align_up(off + capl * 4);
       l.htgt_off = off;
       off = align_up(off + capl * 8);
+      l.glist_off = off;   // the generated projection's work list + its count
+      off = align_up(off + capl * 4 + 4);
     }
     l.sel_off = off;
     off = align_up(off + l.cap.back() * (4 + 4 + 4 + 8 + (16ull << RUN_Q)) + 4 * ALIGN);
@@ -486,13 +488,38 @@ void run_leaf_trail(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, uint64_t pare
                    h->noise.readout_p10, x.d_out, x.st, &s1),
      "trail select launch");
   mark(x, 1, d, 0, b, cnt);
-  // 3. projection onto the chosen top bits (every leaf: a shared state has per-leaf choices)
+  // 3. projection onto the chosen top bits (every leaf: a shared state has per-leaf choices):
+  //    the hand-written streaming kernel (ProjSpec), and the generated kernel for the leaves
+  //    it hands over (a Pauli inside a diagonal unit) -- or the generated one for all
   PassLaunch pb = pl;
   pb.variant = 3u;
   pb.rep = nullptr;
   pb.runsel = hsel;
   pb.scratch = psi;
   mark(x, 0, d, 100, b, cnt);
+  if (tp.fast) {
+    uint32_t* glist = reinterpret_cast<uint32_t*>(x.ws + x.L.glist_off);
+    uint32_t* gcount = glist + capl;
+    ckc(cudaMemsetAsync(gcount, 0, 4, x.st), "trail list reset");
+    TrailProjLaunch tl{};
+    tl.src = pbuf;
+    tl.prep = prep;
+    tl.child_first = b;
+    tl.parent_first = parent_first;
+    tl.arity = (uint32_t)A;
+    tl.batch = (uint32_t)cnt;
+    tl.n = (uint32_t)n;
+    tl.rows = rows;
+    tl.row_bytes = row_bytes;
+    tl.hsel = hsel;
+    tl.psi = psi;
+    tl.glist = glist;
+    tl.gcount = gcount;
+    ck(launch_trail_project(tp.proj, tl, x.st), "trail fast projection launch");
+    pb.wlist = glist;
+    pb.wcount = gcount;
+    h->stats.kernel_launches += 1;
+  }
   ck(launch_jit_pass(jt.a, tp.a, pb, x.st), "trail projection launch");
   mark(x, 0, d, 100, b, cnt);
   h->stats.pass_bytes += (parents << n) * 16 + (cnt << n2) * 16;

@@ -97,13 +97,45 @@ struct PassDesc {
                                 // (trail passes: their gates' pass bits are not in the row mask)
 };
 
+// Fast projection of the conditional leaf sampling (kernels.cu trail_project_kernel): pass A
+// = diagonal units (both qubits among the top bits, or both below) followed by 1q gates on
+// the top bits, so psi(x) = D_x(x) sum_y c[y] phi(y, x) with c[y] = prod_j U_j[sel_j][y_j]
+// * D_top(y) per leaf (a leaf with a Pauli inside a diagonal unit takes the generated kernel).
+constexpr int PROJ_MAX_G = 48;
+constexpr int PROJ_MAX_U = 24;
+constexpr int PROJ_MAX_DG = 72;
+struct ProjSpec {
+  uint32_t m, n2, ng, nug, nux, ndg;
+  uint32_t gbit[PROJ_MAX_G];        // top bit j (qubit n2 + j) of 1q gate i, slice order
+  uint32_t goff[PROJ_MAX_G];        // its slice offset (noise code)
+  double gmat[PROJ_MAX_G][8];       // its 2x2 (re, im row major)
+  uint32_t ua[PROJ_MAX_U], ub[PROJ_MAX_U];   // units: [0, nug) top-bit indices, [nug, nug+nux) qubits < n2
+  double uT[PROJ_MAX_U][8];         // phase by bit_a + 2 bit_b (complex)
+  uint32_t dgoff[PROJ_MAX_DG];      // slice offsets of every diagonal-unit gate
+};
+
 // Conditional leaf sampling through the trailing layer (passplan.cpp plan_trail)
 struct TrailPlan {
   bool on = false;
   int m = 0, n2 = 0;            // G1 = the top m qubits; stage-2 width n2 = n - m
   PassDesc a;                   // pass A over {0..2} ∪ G1: run sums (variant 1) / projection (variant 3)
   std::vector<PassDesc> b;      // stage-2 passes on the projected n2-qubit states (last: run sums)
+  bool fast = false;            // pass A fits ProjSpec: the hand-written projection
+  ProjSpec proj{};
 };
+struct TrailProjLaunch {
+  const void* src;              // parent level batch
+  const uint32_t* prep;         // parent dedup map (or null)
+  uint64_t child_first, parent_first;
+  uint32_t arity, batch, n;
+  const uint8_t* rows;
+  uint32_t row_bytes;
+  const uint32_t* hsel;         // per leaf: the chosen top bits
+  void* psi;                    // per leaf: the projected 2^n2 state
+  uint32_t* glist;              // leaves for the generated projection (a Pauli inside a unit)
+  uint32_t* gcount;
+};
+int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* stream);
 
 struct PassPlan {
   int n_sim = 0;                         // simulated width (>= RBITS)
@@ -138,6 +170,8 @@ struct PassLaunch {
   uint32_t* xlout;              // variant 1: store-address XOR per leaf
   const uint32_t* rep;          // dedup map of the batch (null: every instance computed)
   const uint32_t* prep;         // dedup map of the parent batch (fan-out reads prep[parent])
+  const uint32_t* wlist;        // variant 3 with a work list: the leaves (slots) to project
+  const uint32_t* wcount;       //   and their count (device); grid = persistent CTAs
 };
 
 // Noise rows of one level batch (row a3): per instance a row of row_bytes bytes,
