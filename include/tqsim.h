@@ -133,6 +133,9 @@ typedef struct {
   uint32_t tile_qubits;             /* K: amplitudes per gate-pass tile = 2^K (auto or options) */
   uint32_t trail_top_bits;          /* conditional leaf sampling: the leaf index's
                                        top bits selected first from marginals (0 = off) */
+  uint32_t trail_fast;              /* 1: its projection is the streaming kernel (diagonal units
+                                       + top-qubit 1q gates), 0: the generated pass kernel */
+  uint32_t reserved1;
 } tqsim_plan;
 
 /* Execution statistics of the last tqsim_execute on a handle. */

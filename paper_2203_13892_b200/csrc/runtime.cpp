@@ -940,6 +940,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     fill_plan(h->plan, c->n_qubits, h->gates.size(), h->pp.passes_total(h->inst), &h->cplan);
     h->cplan.tile_qubits = h->pp.levels.empty() || h->pp.levels[0].empty() ? 0u : (uint32_t)h->pp.levels[0][0].K;
     h->cplan.trail_top_bits = h->pp.trail.on && !h->kraus ? (uint32_t)h->pp.trail.m : 0u;
+    h->cplan.trail_fast = h->pp.trail.on && !h->kraus && h->pp.trail.fast ? 1u : 0u;
     if (need_gpu) {
       require_device();
       const size_t G = std::max<size_t>(h->gates.size(), 1);

@@ -63,7 +63,8 @@ class tqsim_plan(C.Structure):
                 ("predicted_speedup_gates", C.c_double), ("n_lowered_gates", C.c_uint64),
                 ("n_outcomes", C.c_uint64), ("node_executions", C.c_uint64),
                 ("gate_amp_updates", C.c_uint64), ("flat_gate_amp_updates", C.c_uint64),
-                ("hbm_passes", C.c_uint64), ("tile_qubits", C.c_uint32), ("trail_top_bits", C.c_uint32)]
+                ("hbm_passes", C.c_uint64), ("tile_qubits", C.c_uint32), ("trail_top_bits", C.c_uint32),
+                ("trail_fast", C.c_uint32), ("reserved1", C.c_uint32)]
 
     @property
     def arity_list(self) -> List[int]:

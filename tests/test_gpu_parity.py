@@ -450,3 +450,43 @@ def test_conditional_leaf_sampling_vs_oracle(n, tile, p, ar):
     nd = T.tqsim_run_ex(n, gates, noise, shots, ar, 21, T.default_options(tile_qubits=tile, batch_log2_amps=n + 2,
                                                                        no_dedup=1))
     assert np.array_equal(nd.leaf_outcomes, a.leaf_outcomes)
+
+
+def _fast_trail_circuit(n, m, rng):
+    """RZZ units within the top m qubits and within the rest, CZ / T / RZ / P / U and RX layers:
+    the leaf slice is diagonal units followed by top-qubit 1q gates (the streaming projection)."""
+    from workloads.generators import g1, g2
+    top, low = list(range(n - m, n)), list(range(n - m))
+    gs = [g1("h", q) for q in range(n)]
+    for _ in range(2):
+        for (a, b) in [(top[0], top[1]), (top[2], top[-1]), (low[0], low[3]), (low[2], low[5]), (top[1], top[3])]:
+            gs += [g2("cx", a, b), g1("rz", b, float(rng.uniform(0, 6))), g2("cx", a, b)]
+        gs += [g2("cz", top[0], top[2]), g1("t", low[1]), g1("rz", top[1], 0.3)]
+        gs += [g1("rx", q, float(rng.uniform(0, 3))) for q in range(n)]
+        gs += [g1("p", top[0], 0.4), g1("u", top[2], 0.1, 0.2, 0.3)]
+    return gs
+
+
+@pytest.mark.parametrize("n,tile,p,ar", [(14, 8, 0.05, [3, 2, 4]), (12, 7, 0.5, [2, 3, 4]), (18, 10, 0.002, [2, 2, 2, 3]),
+                                         (14, 8, 1.0, [2, 3, 4])])
+def test_streaming_projection_vs_oracle(n, tile, p, ar):
+    """The hand-written projection (diagonal units folded into per-leaf coefficients, top-qubit
+    gates with their keyed Paulis) and its hand-over of leaves with a Pauli inside a unit to
+    the generated kernel (p = 0.5, 1): outcomes equal the oracle's and the stored path's."""
+    rng = np.random.default_rng(n + tile)
+    gates = _fast_trail_circuit(n, tile - 3, rng)
+    nm = NoiseModel(p, min(1.0, 2 * p), 0.02, 0.03)
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    shots = int(np.prod(ar))
+    plan = T.tqsim_plan_circuit(n, gates, noise, shots, ar, opts)
+    assert plan.trail_top_bits == tile - 3 and plan.trail_fast == 1
+    a = T.tqsim_run_ex(n, gates, noise, shots, ar, 33, opts, (), leaf_debug=True)
+    b = T.tqsim_run_ex(n, gates, noise, shots, ar, 33, opts, [(len(ar) - 1, 1)])
+    ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 33)
+    for l, r in ref.leaves.items():
+        if r.flagged:
+            continue
+        assert int(a.leaf_outcomes[l]) == r.outcome, (l, int(a.leaf_outcomes[l]), r.outcome)
+        assert int(b.leaf_outcomes[l]) == r.outcome
+        assert not a.leaf_flagged[l]
