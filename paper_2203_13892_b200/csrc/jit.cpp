@@ -13,6 +13,7 @@
 //     synthesizes |0..0> (root); passes with one phase need no shared memory.
 // Sources are compiled with NVRTC for sm_100a (one program per pass, in
 // parallel host threads) and cached in-process by source text.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
@@ -68,6 +69,26 @@ __device__ __forceinline__ void tq_ld2(const tq_d2* p, tq_d2& a, tq_d2& b) {
 }
 __device__ __forceinline__ void tq_st2(tq_d2* p, const tq_d2& a, const tq_d2& b) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" :: "l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
+// TMA staging (TQSIM_TMA): tensor map by value, mbarrier + cp.async.bulk.tensor (5-D tile)
+struct __align__(64) TqTmap { unsigned long long v[16]; };
+__device__ __forceinline__ unsigned tq_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tq_mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(tq_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void tq_fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void tq_fence_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tq_tma_load(void* dst, const TqTmap* tm, unsigned long long* bar, int c0, int c1, int c2,
+                                            int c3, int c4, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(tq_smem(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+               :: "r"(tq_smem(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(tq_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void tq_mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0u;
+  while (!ok)
+    asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                 : "=r"(ok) : "r"(tq_smem(bar)), "r"(parity) : "memory");
 }
 // r *= i^q
 __device__ __forceinline__ void tq_rot(tq_d2& r, tq_u32 q) {
@@ -990,7 +1011,8 @@ uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal, boo
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs, int variant = 0,
-                     std::vector<uint32_t>* out_row = nullptr, double* fp64_out = nullptr, int proj_m = 0) {
+                     std::vector<uint32_t>* out_row = nullptr, double* fp64_out = nullptr, int proj_m = 0,
+                     const TmaGeom* tma = nullptr) {
   const int K = pd.K, T = 1 << (K - RBITS);
   const int low = std::min(LOW_Q, K);
   const bool coal = K - RBITS >= low;   // enough lane bits to keep qubits 0..2 on lanes 0..2
@@ -1110,6 +1132,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   const bool use_smem = fast.size() > 1;
   threads = T;
   smem = use_smem ? (size_t)16 << K : 0;
+  if (tma) smem = 128 + ((size_t)32 << K);   // 2 mbarriers + two tile buffers (prefetch / current)
   Gen g;
   std::ostringstream& o = g.o;
   ConstPool pool;
@@ -1189,12 +1212,61 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // 16 resident warps per SM (128 registers / thread), as many independent CTAs as fit
   const int minb = K >= 13 ? 1
                            : std::max(1, std::min(512 / std::max(T, 32), (int)((227 * 1024) / ((16 << K) + 1024))));
+  if (tma) {
+    // per-kernel work scan and TMA issue: the next computed (representative) work item, and
+    // the tensor-map coordinates of its tile (TmaGeom: runs of tile / out-of-tile qubits)
+    o << "__device__ __forceinline__ tq_u64 tq_next_item(const TqJitArgs& a, tq_u64 w, tq_u64 total) {\n"
+      << "  for (; w < total; w += gridDim.x) {\n"
+      << "    const tq_u32 s = (tq_u32)(w % a.batch);\n"
+      << "    if (!a.rep || a.rep[s] == s) return w;\n"
+      << (variant == 1 ? "    if (w / a.batch == 0) a.xlout[s] = 0u;\n" : "")
+      << "  }\n  return total;\n}\n";
+    o << "__device__ __forceinline__ void tq_issue(const TqJitArgs& a, const TqTmap* tm, tq_u64 w, tq_d2* dst,\n"
+      << "                                         unsigned long long* bar) {\n"
+      << "  const tq_u32 s = (tq_u32)(w % a.batch);\n  const tq_u64 t = w / a.batch;\n";
+    if (mode == 1)
+      o << "  tq_u64 pj = ((tq_u64)a.child_first + s) / a.arity - a.parent_first;\n  if (a.prep) pj = a.prep[pj];\n";
+    else
+      o << "  const tq_u64 pj = s;\n";
+    std::string c[5];
+    for (int dmi = 0; dmi < 5; ++dmi) c[dmi] = "0";
+    for (int dmi = 0; dmi < tma->ndims; ++dmi) {
+      if (tma->kind[dmi] == 2) c[dmi] = "(int)pj";
+      else if (tma->kind[dmi] == 0)
+        c[dmi] = "(int)((t >> " + std::to_string(tma->tbit[dmi]) + ") & " + std::to_string((1ull << tma->len[dmi]) - 1) + "ull)";
+    }
+    o << "  tq_tma_load(dst, tm, bar, " << c[0] << ", " << c[1] << ", " << c[2] << ", " << c[3] << ", " << c[4] << ", "
+      << (16u << K) << "u);\n}\n";
+  }
   o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << std::min(minb, 32) << ") "
-    << name << "(const TqJitArgs a, const TqCoef cf) {\n";
-  if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
+    << name << "(const TqJitArgs a, const TqCoef cf" << (tma ? ", const __grid_constant__ TqTmap tmap" : "") << ") {\n";
+  if (tma)
+    o << "  extern __shared__ __align__(128) unsigned char tq_sm[];\n"
+      << "  unsigned long long* const tq_bar = reinterpret_cast<unsigned long long*>(tq_sm);\n"
+      << "  tq_d2* const tq_buf0 = reinterpret_cast<tq_d2*>(tq_sm + 128);\n"
+      << "  __shared__ tq_u64 tq_next[2];\n";
+  else if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
   o << "  __shared__ tq_u32 tq_errb[" << NW << "];\n";
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
-  if (variant == 2)   // one CTA per leaf, on the tile holding its selected run
+  if (tma) {
+    // persistent CTAs: the next item's tile streams into the other buffer (TMA) while this
+    // one is computed; the current buffer doubles as the exchange tile of the phases
+    o << "  const tq_u64 tq_total = (tq_u64)a.batch << " << pd.n_out << ";\n"
+      << "  if (tid == 0u) { tq_mbar_init(tq_bar); tq_mbar_init(tq_bar + 1); tq_fence_mbar_init(); }\n"
+      << "  __syncthreads();\n"
+      << "  if (tid == 0u) {\n    const tq_u64 w0 = tq_next_item(a, bid, tq_total);\n    tq_next[0] = w0;\n"
+      << "    if (w0 < tq_total) tq_issue(a, &tmap, w0, tq_buf0, tq_bar);\n  }\n"
+      << "  __syncthreads();\n"
+      << "  tq_u64 tq_w = tq_next[0];\n  tq_u32 tq_b = 0u, tq_par0 = 0u, tq_par1 = 0u;\n"
+      << "  while (tq_w < tq_total) {\n"
+      << "  if (tid == 0u) {\n    const tq_u64 nx = tq_next_item(a, tq_w + gridDim.x, tq_total);\n"
+      << "    tq_next[tq_b ^ 1u] = nx;\n"
+      << "    if (nx < tq_total) tq_issue(a, &tmap, nx, tq_buf0 + ((tq_u64)(tq_b ^ 1u) << " << K << "), tq_bar + (tq_b ^ 1u));\n  }\n"
+      << "  tq_mbar_wait(tq_bar + tq_b, tq_b ? tq_par1 : tq_par0);\n"
+      << "  if (tq_b) tq_par1 ^= 1u; else tq_par0 ^= 1u;\n"
+      << "  const tq_u32 s = (tq_u32)(tq_w % a.batch);\n  const tq_u64 t = tq_w / a.batch;\n"
+      << "  tq_d2* const tile = tq_buf0 + ((tq_u64)tq_b << " << K << ");\n";
+  } else if (variant == 2)   // one CTA per leaf, on the tile holding its selected run
     o << "  const tq_u32 s = (tq_u32)bid;\n  const tq_u64 t = a.tiles[s];\n  const tq_u32 rsel = a.runsel[s];\n";
   else if (variant == 3)   // projection: every (leaf, tile), or the leaves of a work list (persistent CTAs)
     o << "  const tq_u32 nw = a.wlist ? *a.wcount : a.batch;\n"
@@ -1204,7 +1276,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
   if (variant == 3)   // the leaf's chosen top bits (the select kernel's chunk)
     o << "  const tq_u32 hsel = a.runsel[s];\n";
-  if (variant != 2) {
+  if (variant != 2 && !tma) {
     // An instance that shares its representative's state (dedup map, launch_dedup_map:
     // no error in its slice, same effective parent) is not computed; readers go through
     // the map.  A skipped leaf's store-address XOR is 0.
@@ -1280,6 +1352,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     offsets(fast[0].P, nullptr, goff, soff, lb, gb);
     o << "  {\n    const tq_u32 gb = " << gb << ";\n";
     const int b0 = pair_bit(goff, false);
+    if (tma) {   // the tile is in shared memory (TMA box order = tile-local index)
+      for (int k = 0; k < 16; ++k) o << "    r" << k << " = tile[(" << lb << ") | " << lo_last[k] << "u];\n";
+      if (fast.size() > 1) o << "    __syncthreads();\n";   // the buffer becomes the exchange tile
+      o << "  }\n";
+      return;
+    }
     for (int k = 0; k < 16; ++k) {
       if (mode == 0)
         o << "    r" << k << ".x = (gb + " << goff[k] << "u == 0u) ? 1.0 : 0.0; r" << k << ".y = 0.0;\n";
@@ -2127,6 +2205,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  }\n";
   }
   if (variant == 3) o << "  __syncthreads();\n  }\n";   // the work loop (shared memory is reused)
+  if (tma)   // generic-proxy writes (exchanges) before the buffer's next TMA fill
+    o << "  tq_fence_async();\n  __syncthreads();\n  tq_w = tq_next[tq_b ^ 1u];\n  tq_b ^= 1u;\n  }\n";
   o << "}\n";
   g_pool = nullptr;
   coefs = pool.vals;
@@ -2174,6 +2254,21 @@ std::string compile_to_cubin(const std::string& src, const std::string& name) {
   return cubin;
 }
 
+// TMA staging for a kernel (TQSIM_TMA: 0 off, 1 the leaf run-sum / trail passes (variant 1),
+// 2 every eligible pass): a load from a source batch (fan-out or in place), variants 0 / 1,
+// K <= 11 (two 32 KiB tile buffers), and a tile that is one 5-D tensor-map box.
+bool tma_wanted(const PassDesc& pd, int n, int mode, int variant, TmaGeom* g) {
+  static const int level = [] {
+    const char* e = std::getenv("TQSIM_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (level <= 0 || mode == 0 || pd.K > 11) return false;
+  if (variant != 0 && variant != 1) return false;
+  if (level == 1 && variant != 1 && !pd.mask_any) return false;
+  if (level == 1 && pd.mask_any && variant != 1) return false;
+  return tma_geom(pd, n, g);
+}
+
 }  // namespace
 
 std::string jit_source(const PassPlan& pp, const std::vector<LGate>& gates, size_t level,
@@ -2203,8 +2298,11 @@ void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint6
         int th;
         size_t sm;
         std::vector<double> cf;
+        TmaGeom tg;
+        const bool tw = tma_wanted(pp.levels[d][p], pp.n_sim, mode, v, &tg);
         srcs.push_back(std::string(kPrelude) + kJitTypes +
-                       gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, names.back(), th, sm, cf, v));
+                       gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, names.back(), th, sm, cf, v, nullptr,
+                                nullptr, 0, tw ? &tg : nullptr));
       }
     }
   if (pp.trail.on) {   // the conditional leaf sampling kernels (jit_build's trail jobs)
@@ -2214,8 +2312,11 @@ void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint6
       int th;
       size_t sm;
       std::vector<double> cf;
+      TmaGeom tg;
+      const bool tw = tma_wanted(tp.a, pp.n_sim, 1, v, &tg);
       srcs.push_back(std::string(kPrelude) + kJitTypes +
-                     gen_pass(tp.a, pp, gates, pp.n_sim, 1, names.back(), th, sm, cf, v, nullptr, nullptr, tp.m));
+                     gen_pass(tp.a, pp, gates, pp.n_sim, 1, names.back(), th, sm, cf, v, nullptr, nullptr, tp.m,
+                              tw ? &tg : nullptr));
     }
     for (size_t p = 0; p < tp.b.size(); ++p)
       for (int v : p + 1 == tp.b.size() ? std::vector<int>{1, 2} : std::vector<int>{0}) {
@@ -2223,10 +2324,19 @@ void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint6
         int th;
         size_t sm;
         std::vector<double> cf;
+        TmaGeom tg;
+        const bool tw = tma_wanted(tp.b[p], tp.n2, 2, v, &tg);
         srcs.push_back(std::string(kPrelude) + kJitTypes +
-                       gen_pass(tp.b[p], pp, gates, tp.n2, 2, names.back(), th, sm, cf, v));
+                       gen_pass(tp.b[p], pp, gates, tp.n2, 2, names.back(), th, sm, cf, v, nullptr, nullptr, 0,
+                                tw ? &tg : nullptr));
       }
   }
+  if (const char* dir = std::getenv("TQSIM_JIT_DUMP"))   // debugging: every generated source
+    for (size_t i = 0; i < srcs.size(); ++i)
+      if (FILE* f = std::fopen((std::string(dir) + "/" + names[i] + ".cu").c_str(), "w")) {
+        std::fwrite(srcs[i].data(), 1, srcs[i].size(), f);
+        std::fclose(f);
+      }
   std::vector<std::string> errs(srcs.size());
   std::vector<size_t> sizes(srcs.size(), 0);
   std::atomic<size_t> next{0};
@@ -2268,6 +2378,9 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
     std::vector<double> coefs;
     std::vector<uint32_t> out_row;
     double fp64 = 0.0;
+    bool tma = false;
+    TmaGeom geom;
+    int nsim = -1;
   };
   std::vector<Job> jobs;
   std::vector<std::vector<JitPass>> out(pp.levels.size());
@@ -2282,8 +2395,9 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
         j.variant = v;
         j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : "");
         const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
+        j.tma = tma_wanted(pp.levels[d][p], pp.n_sim, mode, v, &j.geom);
         std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
-                                    j.smem, j.coefs, v, &j.out_row, &j.fp64);
+                                    j.smem, j.coefs, v, &j.out_row, &j.fp64, 0, j.tma ? &j.geom : nullptr);
         j.src = std::string(kPrelude) + kJitTypes + body;
         jobs.push_back(std::move(j));
       }
@@ -2298,8 +2412,9 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
       j.p = 0;
       j.variant = v;
       j.name = "tq_trail_a_v" + std::to_string(v);
+      j.tma = tma_wanted(tp.a, pp.n_sim, 1, v, &j.geom);
       std::string body = gen_pass(tp.a, pp, gates, pp.n_sim, 1, j.name, j.threads, j.smem, j.coefs, v, &j.out_row,
-                                  &j.fp64, tp.m);
+                                  &j.fp64, tp.m, j.tma ? &j.geom : nullptr);
       j.src = std::string(kPrelude) + kJitTypes + body;
       jobs.push_back(std::move(j));
     }
@@ -2312,14 +2427,22 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
         j.p = p;
         j.variant = v;
         j.name = "tq_trail_b" + std::to_string(p) + "_v" + std::to_string(v);
+        j.tma = tma_wanted(tp.b[p], tp.n2, 2, v, &j.geom);
         std::string body = gen_pass(tp.b[p], pp, gates, tp.n2, 2, j.name, j.threads, j.smem, j.coefs, v, &j.out_row,
-                                    &j.fp64);
+                                    &j.fp64, 0, j.tma ? &j.geom : nullptr);
+        j.nsim = tp.n2;
         j.src = std::string(kPrelude) + kJitTypes + body;
         jobs.push_back(std::move(j));
       }
     }
     trail->b.assign(tp.b.size(), JitPass{});
   }
+  if (const char* dir = std::getenv("TQSIM_JIT_DUMP"))   // debugging: every generated source
+    for (const Job& j : jobs)
+      if (FILE* f = std::fopen((std::string(dir) + "/" + j.name + ".cu").c_str(), "w")) {
+        std::fwrite(j.src.data(), 1, j.src.size(), f);
+        std::fclose(f);
+      }
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<size_t> todo;
   {
@@ -2387,6 +2510,11 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
       jp.out_row = j.out_row;
       jp.fp64_per_amp = j.fp64;
     }
+    if (j.variant == 0 || j.variant == 1) {   // the TMA decision per variant (tma_wanted)
+      jp.tma_v[j.variant] = j.tma;
+      if (j.tma) jp.geom = j.geom;
+      jp.n_sim = j.nsim >= 0 ? j.nsim : pp.n_sim;
+    }
     if (j.variant == 0) {
       jp.kernel = reinterpret_cast<void*>(ck.fn);
       jp.threads = j.threads;
@@ -2402,6 +2530,88 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
 }
 
 
+
+bool tma_geom(const PassDesc& pd, int n, TmaGeom* g) {
+  TmaGeom r;
+  if (pd.K < 4 || n < 4 || pd.tile_q[0] != 0 || pd.tile_q[1] != 1 || pd.tile_q[2] != 2) return false;
+  r.kind[0] = 1;
+  r.qstart[0] = 0;
+  r.len[0] = 3;
+  r.ndims = 1;
+  int pos_out[64];
+  for (int i = 0; i < 64; ++i) pos_out[i] = -1;
+  for (int i = 0; i < pd.n_out; ++i) pos_out[pd.out_q[i]] = i;
+  for (int q = 3; q < n;) {
+    const bool in = (pd.tile_mask >> q) & 1ull;
+    int e = q;
+    while (e < n && (((pd.tile_mask >> e) & 1ull) != 0) == in && (!in || e - q < 8)) ++e;
+    if (r.ndims >= 4) return false;   // the state index needs the last dim
+    r.kind[r.ndims] = in ? 1 : 0;
+    r.qstart[r.ndims] = q;
+    r.len[r.ndims] = e - q;
+    r.tbit[r.ndims] = in ? 0 : pos_out[q];
+    ++r.ndims;
+    q = e;
+  }
+  r.kind[r.ndims] = 2;
+  ++r.ndims;
+  *g = r;
+  return true;
+}
+
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// The 5-D tensor map over `nstates` states of 2^n amplitudes at `base` with the pass's tile box.
+int encode_tile_map(const TmaGeom& g, int n, const void* base, uint64_t nstates, CUtensorMap* out) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return (int)cudaErrorNotSupported;
+  cuuint64_t dim[5], stride[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  uint64_t last_stride = 16ull << n;
+  for (int d = 0; d < 5; ++d) {
+    if (d >= g.ndims) {   // padding
+      dim[d] = 1;
+      box[d] = 1;
+      last_stride *= 2;
+      if (d > 0) stride[d - 1] = last_stride;
+      continue;
+    }
+    if (d == 0) {
+      dim[0] = 16;
+      box[0] = 16;
+      continue;
+    }
+    if (g.kind[d] == 2) {
+      dim[d] = nstates;
+      box[d] = 1;
+      stride[d - 1] = 16ull << n;
+      last_stride = (16ull << n) * nstates;
+      continue;
+    }
+    dim[d] = 1ull << g.len[d];
+    box[d] = g.kind[d] == 1 ? (1u << g.len[d]) : 1u;
+    stride[d - 1] = 16ull << g.qstart[d];
+  }
+  const CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dim, stride, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+}  // namespace
 
 int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, void* stream) {
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
@@ -2419,6 +2629,19 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
   void* args[] = {&a, const_cast<double*>(cf.empty() ? &zero : cf.data())};
   const int threads = L.variant == 3 ? jp.threads_project : jp.threads;
   const size_t smem = L.variant == 3 ? jp.smem_project : jp.smem;
+  if ((L.variant == 0 || L.variant == 1) && jp.tma_v[L.variant]) {
+    // TMA-staged persistent kernel: the tensor map of the source batch (parents / own states)
+    CUtensorMap tm;
+    const bool fan = L.src_mode == 1;
+    const uint64_t nst = fan ? ((L.child_first + L.batch - 1) / (L.arity ? L.arity : 1) - L.parent_first + 1) : L.batch;
+    const int e = encode_tile_map(jp.geom, jp.n_sim, fan ? L.src : L.dst, nst, &tm);
+    if (e) return e;
+    const uint64_t per_sm = jp.smem > 100 * 1024 ? 1 : jp.smem > 70 * 1024 ? 2 : 3;
+    const uint64_t pgrid = std::min<uint64_t>(grid, per_sm * 148);
+    void* targs[] = {&a, const_cast<double*>(cf.empty() ? &zero : cf.data()), &tm};
+    return (int)cudaLaunchKernel(kern, dim3((unsigned)pgrid), dim3(threads), targs, smem,
+                                 static_cast<cudaStream_t>(stream));
+  }
   return (int)cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), args, smem,
                                static_cast<cudaStream_t>(stream));
 }

@@ -282,6 +282,19 @@ inline bool kraus_enabled(const tqsim_noise_model& nm) {
 }
 
 // ---------------------------------------------------------------- JIT pass kernels (jit.cpp)
+// TMA staging of a pass's tiles (TQSIM_TMA, jit.cpp): the tile {0,1,2} ∪ H as one 5-D tensor-map
+// box over the source batch.  Dims in order (innermost first): qubits 0..2 as 16 doubles, then
+// runs of qubits alternately in the tile (box = 2^len) or out of it (box 1, coordinate = the
+// tile index bits tbit..tbit+len-1), padded, and the state index (coordinate = the source slot).
+struct TmaGeom {
+  int ndims = 0;
+  int kind[5] = {};     // 0 out-of-tile run, 1 in-tile run (incl. dim 0), 2 state index
+  int qstart[5] = {};   // first qubit of the run
+  int len[5] = {};      // qubits in the run
+  int tbit[5] = {};     // out-of-tile runs: first bit in the tile index t
+};
+bool tma_geom(const PassDesc& pd, int n, TmaGeom* g);
+
 struct JitPass {
   void* kernel = nullptr;   // cudaKernel_t
   void* kernel_nostore = nullptr;     // leaf-sum passes: run sums only (variant 1)
@@ -291,6 +304,9 @@ struct JitPass {
   size_t smem = 0;
   std::vector<double> coefs;      // by-value coefficient parameter (TQSIM_JIT_COEF=0 mode)
   double fp64_per_amp = 0.0;      // FP64 operations per amplitude of the fast path (cost model)
+  bool tma_v[2] = {false, false};   // kernel (v0) / kernel_nostore (v1) take a tensor map (persistent CTAs)
+  TmaGeom geom;
+  int n_sim = 0;                  // state width the kernel was generated for
   // trail pass A: the projection kernel (variant 3) and its launch parameters
   void* kernel_project = nullptr;
   int threads_project = 0;
