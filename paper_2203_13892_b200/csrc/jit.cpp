@@ -2505,14 +2505,17 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
     }
     if (j.which != 0 && j.variant == 1) {   // trail kernels without a variant 0: launch parameters
       jp.threads = j.threads;
-      jp.smem = j.smem;
+      jp.smem = j.tma ? (size_t)16 << (j.which == 1 ? pp.trail.a.K : pp.trail.b[j.p].K) : j.smem;
       jp.coefs = j.coefs;
       jp.out_row = j.out_row;
       jp.fp64_per_amp = j.fp64;
     }
     if (j.variant == 0 || j.variant == 1) {   // the TMA decision per variant (tma_wanted)
       jp.tma_v[j.variant] = j.tma;
-      if (j.tma) jp.geom = j.geom;
+      if (j.tma) {
+        jp.geom = j.geom;
+        jp.smem_tma = j.smem;
+      }
       jp.n_sim = j.nsim >= 0 ? j.nsim : pp.n_sim;
     }
     if (j.variant == 0) {
@@ -2636,10 +2639,10 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
     const uint64_t nst = fan ? ((L.child_first + L.batch - 1) / (L.arity ? L.arity : 1) - L.parent_first + 1) : L.batch;
     const int e = encode_tile_map(jp.geom, jp.n_sim, fan ? L.src : L.dst, nst, &tm);
     if (e) return e;
-    const uint64_t per_sm = jp.smem > 100 * 1024 ? 1 : jp.smem > 70 * 1024 ? 2 : 3;
+    const uint64_t per_sm = jp.smem_tma > 100 * 1024 ? 1 : jp.smem_tma > 70 * 1024 ? 2 : 3;
     const uint64_t pgrid = std::min<uint64_t>(grid, per_sm * 148);
     void* targs[] = {&a, const_cast<double*>(cf.empty() ? &zero : cf.data()), &tm};
-    return (int)cudaLaunchKernel(kern, dim3((unsigned)pgrid), dim3(threads), targs, smem,
+    return (int)cudaLaunchKernel(kern, dim3((unsigned)pgrid), dim3(threads), targs, jp.smem_tma,
                                  static_cast<cudaStream_t>(stream));
   }
   return (int)cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), args, smem,

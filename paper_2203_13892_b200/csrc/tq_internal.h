@@ -305,6 +305,7 @@ struct JitPass {
   std::vector<double> coefs;      // by-value coefficient parameter (TQSIM_JIT_COEF=0 mode)
   double fp64_per_amp = 0.0;      // FP64 operations per amplitude of the fast path (cost model)
   bool tma_v[2] = {false, false};   // kernel (v0) / kernel_nostore (v1) take a tensor map (persistent CTAs)
+  size_t smem_tma = 0;              // their dynamic shared memory (two tile buffers + mbarriers)
   TmaGeom geom;
   int n_sim = 0;                  // state width the kernel was generated for
   // trail pass A: the projection kernel (variant 3) and its launch parameters
