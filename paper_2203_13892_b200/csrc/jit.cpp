@@ -1215,11 +1215,17 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   if (tma) {
     // per-kernel work scan and TMA issue: the next computed (representative) work item, and
     // the tensor-map coordinates of its tile (TmaGeom: runs of tile / out-of-tile qubits)
+    // warp 0 scans 32 candidates (w, w + G, ...) per step: one dedup-map round trip per 32
     o << "__device__ __forceinline__ tq_u64 tq_next_item(const TqJitArgs& a, tq_u64 w, tq_u64 total) {\n"
-      << "  for (; w < total; w += gridDim.x) {\n"
-      << "    const tq_u32 s = (tq_u32)(w % a.batch);\n"
-      << "    if (!a.rep || a.rep[s] == s) return w;\n"
-      << (variant == 1 ? "    if (w / a.batch == 0) a.xlout[s] = 0u;\n" : "")
+      << "  const tq_u32 lane = threadIdx.x & 31u;\n"
+      << "  for (; w < total; w += 32ull * gridDim.x) {\n"
+      << "    const tq_u64 c = w + (tq_u64)lane * gridDim.x;\n"
+      << "    bool ok = false;\n"
+      << "    if (c < total) { const tq_u32 s = (tq_u32)(c % a.batch); ok = !a.rep || a.rep[s] == s; }\n"
+      << "    const unsigned bal = __ballot_sync(0xffffffffu, ok);\n"
+      << "    const int f = bal ? __ffs(bal) - 1 : 32;\n"
+      << (variant == 1 ? "    if (c < total && (int)lane < f && !ok && c / a.batch == 0) a.xlout[c % a.batch] = 0u;\n" : "")
+      << "    if (bal) return w + (tq_u64)f * gridDim.x;\n"
       << "  }\n  return total;\n}\n";
     o << "__device__ __forceinline__ void tq_issue(const TqJitArgs& a, const TqTmap* tm, tq_u64 w, tq_d2* dst,\n"
       << "                                         unsigned long long* bar) {\n"
@@ -1254,14 +1260,14 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const tq_u64 tq_total = (tq_u64)a.batch << " << pd.n_out << ";\n"
       << "  if (tid == 0u) { tq_mbar_init(tq_bar); tq_mbar_init(tq_bar + 1); tq_fence_mbar_init(); }\n"
       << "  __syncthreads();\n"
-      << "  if (tid == 0u) {\n    const tq_u64 w0 = tq_next_item(a, bid, tq_total);\n    tq_next[0] = w0;\n"
-      << "    if (w0 < tq_total) tq_issue(a, &tmap, w0, tq_buf0, tq_bar);\n  }\n"
+      << "  if (tid < 32u) {\n    const tq_u64 w0 = tq_next_item(a, bid, tq_total);\n"
+      << "    if (tid == 0u) { tq_next[0] = w0; if (w0 < tq_total) tq_issue(a, &tmap, w0, tq_buf0, tq_bar); }\n  }\n"
       << "  __syncthreads();\n"
       << "  tq_u64 tq_w = tq_next[0];\n  tq_u32 tq_b = 0u, tq_par0 = 0u, tq_par1 = 0u;\n"
       << "  while (tq_w < tq_total) {\n"
-      << "  if (tid == 0u) {\n    const tq_u64 nx = tq_next_item(a, tq_w + gridDim.x, tq_total);\n"
-      << "    tq_next[tq_b ^ 1u] = nx;\n"
-      << "    if (nx < tq_total) tq_issue(a, &tmap, nx, tq_buf0 + ((tq_u64)(tq_b ^ 1u) << " << K << "), tq_bar + (tq_b ^ 1u));\n  }\n"
+      << "  if (tid < 32u) {\n    const tq_u64 nx = tq_next_item(a, tq_w + gridDim.x, tq_total);\n"
+      << "    if (tid == 0u) {\n      tq_next[tq_b ^ 1u] = nx;\n"
+      << "      if (nx < tq_total) tq_issue(a, &tmap, nx, tq_buf0 + ((tq_u64)(tq_b ^ 1u) << " << K << "), tq_bar + (tq_b ^ 1u));\n    }\n  }\n"
       << "  tq_mbar_wait(tq_bar + tq_b, tq_b ? tq_par1 : tq_par0);\n"
       << "  if (tq_b) tq_par1 ^= 1u; else tq_par0 ^= 1u;\n"
       << "  const tq_u32 s = (tq_u32)(tq_w % a.batch);\n  const tq_u64 t = tq_w / a.batch;\n"
