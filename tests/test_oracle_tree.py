@@ -102,3 +102,47 @@ def test_u53_range_and_determinism():
     a = simulate_tree(5, low, fixed_plan(len(low), [2, 3]), nm, 77)
     b = simulate_tree(5, low, fixed_plan(len(low), [2, 3]), nm, 77)
     assert [a.leaves[i].outcome for i in range(6)] == [b.leaves[i].outcome for i in range(6)]
+
+
+def test_u53_is_uniform_on_the_2pow53_lattice():
+    """R9's u = ((w0 >> 5) 2^26 + (w1 >> 6)) 2^-53: every value is a multiple of 2^-53 in
+    [0, 1); its top 27 bits are w0's top 27 bits (u >= 1/2 iff w0's top bit is set, floor(u
+    2^27) == w0 >> 5), the next 26 are w1's top 26; the values pass a Kolmogorov-Smirnov test
+    for U[0, 1) (scipy.stats.kstest, 20,000 leaves)."""
+    from scipy import stats
+    from oracle.philox import philox4x32_10, seed_key
+    us = np.array([measure_uniform(l, 11) for l in range(20000)])
+    assert np.all((us >= 0) & (us < 1))
+    assert np.all(np.floor(us * 2.0 ** 53) == us * 2.0 ** 53)
+    for l in range(0, 20000, 997):
+        w0, w1, _, _ = philox4x32_10((0, l, 1, 0), seed_key(11))
+        assert int(np.floor(us[l] * 2.0 ** 27)) == w0 >> 5
+        assert int(us[l] * 2.0 ** 53) & ((1 << 26) - 1) == w1 >> 6
+    assert stats.kstest(us, "uniform").pvalue > 1e-4
+
+
+def test_readout_word_selection_and_rates():
+    """R11: bit b of leaf l flips iff word (b & 3) of Philox(ctr = (b >> 2, l, 2, 0)) * 2^-32 is
+    below p10 (bit set) / p01 (bit clear).  With p01 = p10 = p the flip of bit b equals that
+    word's threshold test (checked against the words directly for 5-qubit outcomes, both
+    values of every bit), and the per-bit flip rates over 20,000 leaves are p within 5 sigma."""
+    from oracle.philox import philox4x32_10, seed_key
+    from oracle.tree import readout_mask
+    p = 0.2
+    n = 6
+    flips = np.zeros(n)
+    L = 20000
+    for l in range(L):
+        m0 = readout_mask(0, n, l, 4, p, p)
+        m1 = readout_mask((1 << n) - 1, n, l, 4, p, p)
+        assert m0 == m1                     # symmetric p: the flips do not depend on x
+        if l < 200:
+            for b in range(n):
+                w = philox4x32_10((b >> 2, l, 2, 0), seed_key(4))[b & 3]
+                assert ((m0 >> b) & 1) == (w * 2.0 ** -32 < p)
+        flips += [(m0 >> b) & 1 for b in range(n)]
+    rate = flips / L
+    assert np.all(np.abs(rate - p) < 5 * np.sqrt(p * (1 - p) / L))
+    # asymmetric: a set bit uses p10, a clear bit p01
+    assert readout_mask(0, n, 3, 4, 1.0, 0.0) == (1 << n) - 1
+    assert readout_mask((1 << n) - 1, n, 3, 4, 1.0, 0.0) == 0
