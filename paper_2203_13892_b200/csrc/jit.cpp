@@ -2260,13 +2260,17 @@ std::string compile_to_cubin(const std::string& src, const std::string& name) {
   return cubin;
 }
 
-// TMA staging for a kernel (TQSIM_TMA: 0 off, 1 the leaf run-sum / trail passes (variant 1),
-// 2 every eligible pass): a load from a source batch (fan-out or in place), variants 0 / 1,
-// K <= 11 (two 32 KiB tile buffers), and a tile that is one 5-D tensor-map box.
+// TMA staging for a kernel (TQSIM_TMA: 0 off (default), 1 the leaf run-sum / trail passes
+// (variant 1), 2 every eligible pass): a load from a source batch (fan-out or in place),
+// variants 0 / 1, K <= 11 (two 32 KiB tile buffers), and a tile that is one 5-D tensor-map box.
+// Off by default: measured on C4 the persistent double-buffered CTAs (3 x 4 warps per SM, 64 KiB
+// each) hide the load latency (long_scoreboard 2.1 -> 0.5 stall cycles per issue) but stall at
+// the phase barriers with too few warps: the trail marginal pass 203 -> 416 ms per tree
+// (profiles/r02_tma_*).
 bool tma_wanted(const PassDesc& pd, int n, int mode, int variant, TmaGeom* g) {
   static const int level = [] {
     const char* e = std::getenv("TQSIM_TMA");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   if (level <= 0 || mode == 0 || pd.K > 11) return false;
   if (variant != 0 && variant != 1) return false;
