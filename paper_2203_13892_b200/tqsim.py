@@ -385,9 +385,12 @@ class Handle:
         n = C.c_uint64()
         args = (self.h, int(seed), rank, world, C.c_void_p(stream), C.c_void_p(d_workspace),
                 int(workspace_bytes), C.c_void_p(d_leaf_outcomes))
-        _check(lib().tqsim_profile_tree(*args, None, 0, C.byref(n)))
-        out = (tqsim_kernel_timing * max(1, n.value))()
-        _check(lib().tqsim_profile_tree(*args, out, n.value, C.byref(n)))
+        cap = 1024                                   # one tree run (re-run only if it overflows)
+        out = (tqsim_kernel_timing * cap)()
+        _check(lib().tqsim_profile_tree(*args, out, cap, C.byref(n)))
+        if n.value > cap:
+            out = (tqsim_kernel_timing * n.value)()
+            _check(lib().tqsim_profile_tree(*args, out, n.value, C.byref(n)))
         return [out[i] for i in range(n.value)]
 
     def noise_table(self, seed: int, level: int, inst_begin: int, count: int) -> np.ndarray:

@@ -25,7 +25,9 @@ def main():
     tree = json.load(open(tree_path))
     n = tree["n_qubits"]
     fam = {(f["level"], f["pass"]): f for f in tree["families"] if f["kind"] == 0}
+    leaf = max(f["level"] for f in tree["families"])
     agg = collections.defaultdict(lambda: collections.Counter())
+    names = {}
     total_ns = 0.0
     for d in ks:
         t = d.get("gpu__time_duration.sum", 0.0)
@@ -33,7 +35,20 @@ def main():
         m = re.match(r"tq_pass_l(\d+)_p(\d+)(_v(\d))?$", d["name"])
         key = ("pass", int(m.group(1)), int(m.group(2))) if m and m.group(4) != "2" else \
               ("recompute", int(m.group(1)), int(m.group(2))) if m else ("other", d["name"], 0)
+        # conditional leaf sampling: pass A = (leaf, 0), the projection = (leaf, 100),
+        # stage-2 pass p = (leaf, 101 + p) -- the families tqsim_profile_tree reports
+        mt = re.match(r"tq_trail_(a|b(\d+))_v(\d)$", d["name"])
+        if mt:
+            v = int(mt.group(3))
+            if mt.group(1) == "a":
+                key = ("pass", leaf, 0 if v == 1 else 100)
+            else:
+                key = ("pass", leaf, 101 + int(mt.group(2))) if v != 2 else ("recompute", leaf, 101 + int(mt.group(2)))
+        elif d["name"].startswith("tq::trail_project_kernel"):
+            key = ("pass", leaf, 100)
         a = agg[key]
+        names.setdefault(key, set()).add(d["name"])
+        a["kernels_per_batch"] = len(names[key])
         a["launches"] += 1
         a["ns"] += t
         a["dram"] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
@@ -52,7 +67,9 @@ def main():
         f = fam.get(key[1:]) if key[0] == "pass" else None
         if f:
             # the launch list may cover only part of the tree: compare per-launch averages
-            cover = a["launches"] / f["launches"]
+            # launches per family (the projection family is two kernels per batch)
+            nk = a["launches"] / max(1, a["kernels_per_batch"]) if a.get("kernels_per_batch") else a["launches"]
+            cover = nk / f["launches"]
             alg_cov = f["alg_bytes"] * cover
             comp_cov = f["computed_states"] * cover
             r.update({"tree_launches": f["launches"], "coverage": cover,
