@@ -1083,6 +1083,7 @@ void execute(tqsim_handle* h, uint64_t seed, uint32_t rank, uint32_t world, cuda
 // their fan-out pass read.  Reads the dedup maps back from the workspace (synchronous).
 struct BatchWork {
   uint64_t comp = 0, parents = 0;
+  uint64_t parents_all = 0;   // distinct parent states (representatives) read by ALL instances
 };
 using WorkMap = std::map<std::pair<uint32_t, uint64_t>, BatchWork>;
 
@@ -1103,17 +1104,18 @@ WorkMap computed_work(const tqsim_handle* h, const ShardRange& sr, const Layout&
     for (uint64_t b = i0; b < i1; b += L.cap[d]) {
       const uint64_t cnt = std::min(L.cap[d], i1 - b);
       BatchWork w;
-      std::vector<uint64_t> par;
+      std::vector<uint64_t> par, pall;
       for (uint64_t j = b; j < b + cnt; ++j) {
+        const uint64_t pr = d > 0 ? rep(d - 1, j / h->plan.arities[d]) : 0;
+        if (d > 0) pall.push_back(pr);
         if (cnt > 1 && rep(d, j) != j) continue;
         ++w.comp;
-        if (d > 0) {
-          const uint64_t P = j / h->plan.arities[d];
-          par.push_back(rep(d - 1, P));
-        }
+        if (d > 0) par.push_back(pr);
       }
       std::sort(par.begin(), par.end());
       w.parents = (uint64_t)(std::unique(par.begin(), par.end()) - par.begin());
+      std::sort(pall.begin(), pall.end());
+      w.parents_all = (uint64_t)(std::unique(pall.begin(), pall.end()) - pall.begin());
       out[{d, b}] = w;
       if (d + 1 < levels) {
         const uint64_t A = h->plan.arities[d + 1];
@@ -1170,9 +1172,9 @@ void fill_computed(tqsim_handle* h, const ShardRange& sr, const Layout& L, const
     st.computed_node_executions += w.comp;
     st.computed_gate_amp_updates += (w.comp * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
     if (d + 1 == h->plan.arities.size() && trail_active(h)) {
-      const uint64_t A = h->plan.arities[d], b = kv.first.second;
+      const uint64_t b = kv.first.second;
       const uint64_t cnt = std::min(L.cap[d], sr.hi[d] - b);
-      const uint64_t pall = (b + cnt - 1) / A - b / A + 1;
+      const uint64_t pall = w.parents_all;
       bytes += trail_alg_bytes(h, 0, cnt, w.comp, w.parents, pall) + trail_alg_bytes(h, 100, cnt, w.comp, w.parents, pall);
       for (size_t p = 0; p < h->pp.trail.b.size(); ++p)
         bytes += trail_alg_bytes(h, 101 + (uint32_t)p, cnt, w.comp, w.parents, pall);
@@ -1571,11 +1573,12 @@ tqsim_status tqsim_profile_tree(tqsim_handle* h, uint64_t seed, uint32_t rank, u
       const BatchWork w = it != wm.end() ? it->second : BatchWork{tg.cnt, 0};
       if (tg.kind == 0 && tg.level + 1 == h->plan.arities.size() && trail_active(h)) {   // trail kernels
         const uint64_t A = h->plan.arities[tg.level];
-        const uint64_t pall = (tg.b + tg.cnt - 1) / A - tg.b / A + 1;
+        const uint64_t pall = it != wm.end() ? w.parents_all : (tg.b + tg.cnt - 1) / A - tg.b / A + 1;
         const uint64_t comp = tg.pass == 0 ? w.comp : tg.cnt;
         k.computed_states += comp;
         k.alg_bytes += trail_alg_bytes(h, tg.pass, tg.cnt, w.comp, w.parents, pall);
-        k.nominal_bytes += trail_alg_bytes(h, tg.pass, tg.cnt, tg.cnt, pall, pall);
+        const uint64_t pnom = (tg.b + tg.cnt - 1) / A - tg.b / A + 1;
+        k.nominal_bytes += trail_alg_bytes(h, tg.pass, tg.cnt, tg.cnt, pnom, pnom);
         k.fp64_per_amp = tg.pass == 0 || tg.pass == 100 ? h->jit_trail.a.fp64_per_amp
                                                          : h->jit_trail.b[tg.pass - 101].fp64_per_amp;
         continue;
