@@ -211,17 +211,18 @@ void shard(const tqsim_plan& p, uint32_t rank, uint32_t world, uint64_t& t0, uin
 Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl);
 
 // Batch size: opts.batch_log2_amps, or by default 2^26 amplitudes per level batch -- and for
-// 18+ qubits the largest batch up to 2^30 amplitudes whose buffers take <= 45% of the
-// memory budget (room for a second workspace: tqsim_run keeps its arena): larger batches
-// hold more siblings and cousins, so more shared states are computed once (measured: C3
-// 251 -> 238 ms, C4 1.21 -> 0.94-0.99 s at 2^28-2^29; C5 shard 5.1 -> 3.9 s at 2^30, which
+// 18+ qubits the largest batch up to 2^30 amplitudes whose buffers take <= 55% of the
+// memory budget (room for a second, smaller workspace next to tqsim_run's arena): larger
+// batches hold more siblings and cousins, so more shared states are computed once (measured:
+// C3 251 -> 238 ms, C4 1.21 -> 0.94-0.99 s at 2^28-2^29 (round 1); round 2 C4 with conditional
+// leaf sampling 2^27 / 2^28 / 2^29: 738 / 685 / 648 ms; C5 shard 5.1 -> 3.9 s at 2^30, which
 // takes ~160 GB and so needs batch_log2_amps = 30 explicitly).
 Layout layout(const tqsim_handle* h, const ShardRange& sr) {
   if (h->opts.batch_log2_amps) return layout_tl(h, sr, (int)h->opts.batch_log2_amps);
   if (h->n_sim >= 18)
     for (int tl = 30; tl > 26; --tl) {
       Layout L = layout_tl(h, sr, tl);
-      if ((double)L.total <= 0.45 * (double)h->opts.mem_budget) return L;
+      if ((double)L.total <= 0.55 * (double)h->opts.mem_budget) return L;
     }
   return layout_tl(h, sr, 26);
 }
