@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--batch-log2", type=int, default=0)
+    ap.add_argument("--copy-cost", type=float, default=10.0,
+                    help="DCP first-slice length (copy cost in gates, R14); -1 = the fused fan-out's cost")
     ap.add_argument("--shard", default="", help="r/w: time only shard r of w (single-GPU experiments)")
     return ap.parse_args()
 
@@ -319,7 +321,7 @@ def main():
         first_call_s = time.perf_counter() - tc
         T.tqsim_release_run_cache()
 
-    opts = T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2)
+    opts = T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, copy_cost_gates=args.copy_cost)
     h = T.tqsim_create(n, gates, noise, shots, ar, opts)
     plan = h.plan
     N = int(plan.n_outcomes)
@@ -438,7 +440,8 @@ def main():
         del ws
         torch.cuda.empty_cache()
         h2 = T.tqsim_create(n, gates, noise, shots, ar,
-                            T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, no_dedup=1))
+                            T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, no_dedup=1,
+                                              copy_cost_gates=args.copy_cost))
         ws2 = torch.empty(h2.workspace_bytes(xr, xw), dtype=torch.uint8, device=dev)
         for i in range(1):
             h2.execute(2000 + i, xr, xw, st.cuda_stream, ws2.data_ptr(), ws2.numel(), out.data_ptr())

@@ -98,7 +98,9 @@ typedef struct {
 #define TQSIM_KRAUS_MAX_QUBITS 13
 
 typedef struct {
-  double copy_cost_gates;     /* first-slice length m = round(.) (R14); default 10 */
+  double copy_cost_gates;     /* first-slice length m = round(.) (R14); default 10;
+                                 -1 = this engine's fused fan-out cost: half the gates one HBM pass
+                                 holds, from the pass planner on the whole circuit */
   double z;                   /* Eq.4 z-score (R12); default 1.96 */
   double eps;                 /* Eq.4 margin of error; default 0.05 */
   uint64_t mem_budget_bytes;  /* HBM budget for states (P:310 memory limit, R25); default 180e9 */

@@ -934,6 +934,19 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     if (h->kraus && c->n_qubits > TQSIM_KRAUS_MAX_QUBITS)
       throw Error{TQSIM_EINVAL, "non-Pauli channels (amplitude / phase damping, thermal relaxation) run in the "
                                 "shared-memory Kraus engine: n_qubits must be <= 13"};
+    if (opts.copy_cost_gates == -1.0 && !arities) {
+      // copy cost of this engine's fused fan-out: the child's
+      // first pass reads the parent instead of its own state, so the copy adds no HBM pass; what
+      // a level boundary costs is the pass it may split, on average half a pass = half the
+      // gates one pass holds.  Gates per pass from the pass planner on the whole circuit.
+      Plan whole;
+      whole.arities = {1};
+      whole.bounds = {0, h->gates.size()};
+      const PassPlan pw = make_pass_plan(h->gates, c->n_qubits, whole, opts);
+      const double gpp = (double)h->gates.size() / (double)std::max<size_t>(1, pw.levels[0].size());
+      opts.copy_cost_gates = std::max(1.0, 0.5 * gpp);
+      h->opts.copy_cost_gates = opts.copy_cost_gates;
+    }
     h->plan = make_plan(h->gates, c->n_qubits, nm, n_shots, arities, n_levels, opts);
     h->pp = make_pass_plan(h->gates, c->n_qubits, h->plan, opts);
     h->n_sim = h->pp.n_sim;

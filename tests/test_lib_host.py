@@ -279,3 +279,22 @@ def test_kernel_generator_accepts_every_random_plan():
             for lv, k in npass.items():
                 for ps in range(k):
                     assert T.tqsim_pass_source(n, gates, noise, 24, arities, opts, lv, ps)
+
+
+def test_fused_copy_cost_first_slice():
+    """copy_cost_gates = -1: the first slice is half the gates one
+    HBM pass holds when the whole circuit is planned as one slice (the fused fan-out adds no pass;
+    a level boundary costs the pass it splits), then DCP as usual."""
+    import paper_2203_13892_b200.tqsim as T
+    from workloads import load_config
+    w = load_config("c4_qaoa24")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    recs = T.tqsim_describe_passes(n, gates, noise, 1, [1])
+    passes = len({r.pass_ for r in recs})
+    G = len(T.tqsim_lower_circuit(n, gates))
+    m = max(1, int(np.floor(max(1.0, 0.5 * G / passes) + 0.5)))
+    p = T.tqsim_plan_circuit(n, gates, noise, shots, None, T.default_options(copy_cost_gates=-1.0))
+    assert p.boundary_list[1] == m
+    assert p.boundary_list[1] != 10
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(n, gates, noise, shots, None, T.default_options(copy_cost_gates=-2.0))
