@@ -588,34 +588,71 @@ __global__ void __launch_bounds__(256) dedup_map_level_kernel(const uint8_t* __r
 // projection kernel handles it).  One complex FMA per amplitude read: HBM-bound.
 constexpr int PT = 256, PV = 2;   // threads, consecutive x per thread (one 32-byte access)
 constexpr int PNC = 4;            // children per parent handled by one CTA (arity <= PNC)
-// One CTA = one parent of the batch x one chunk of x: the parent's amplitudes are read once
-// for all its children in the batch (siblings share the parent; per-child tables).
+// One CTA = one parent of the batch x one chunk of x; parents whose states are shared (the
+// dedup map: the same representative) are handled by the first of them, which reads the shared
+// amplitudes once for all their children in the batch, PNC children per sweep over y.
 __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant__ ProjSpec sp,
                                                            const __grid_constant__ TrailProjLaunch L,
                                                            const uint64_t* __restrict__ seedp) {
   (void)seedp;
+  constexpr int KMAX = 64;
   __shared__ cd U[PNC][16][4];
   __shared__ cd coef[PNC][1 << 8];
   __shared__ int live[PNC];
+  __shared__ uint32_t kids[KMAX];
+  __shared__ int nkid, lead, more;
   const uint32_t A = L.arity;
   const uint64_t pfirst = L.child_first / A;                    // first parent index of the batch
   const uint32_t npar = (uint32_t)((L.child_first + L.batch - 1) / A - pfirst + 1);
   const uint32_t g = blockIdx.x % npar, c = blockIdx.x / npar;
   const uint64_t P = pfirst + g;
-  // the parent's children inside the batch: slots [s0, s1)
-  const uint64_t j0 = P * A > L.child_first ? P * A : L.child_first;
-  const uint64_t j1 = (P + 1) * A < L.child_first + L.batch ? (P + 1) * A : L.child_first + L.batch;
-  const uint32_t s0 = (uint32_t)(j0 - L.child_first), nc = (uint32_t)(j1 - j0);
+  auto rep_of = [&](uint64_t Q) -> uint64_t {   // the parent batch slot holding Q's state
+    const uint64_t q = Q - L.parent_first;
+    return L.prep ? L.prep[q] : q;
+  };
+  const uint64_t rp = rep_of(P);
+  if (threadIdx.x == 0) {   // the group's leader: the first parent of the batch with this state
+    int l = 1;
+    for (uint64_t Q = pfirst; Q < P && l; ++Q)
+      if (rep_of(Q) == rp) l = 0;
+    lead = l;
+  }
+  __syncthreads();
+  if (!lead) return;
+  const cd* __restrict__ src = static_cast<const cd*>(L.src) + (rp << L.n);
+  const uint32_t n2 = sp.n2;
+  const uint64_t x0 = ((uint64_t)c * PT + threadIdx.x) * PV;
+  for (uint32_t round = 0;; ++round) {
+  if (threadIdx.x == 0) {   // children (batch slots) of every parent with this state, KMAX per round
+    int k = 0, skip = (int)(round * KMAX);
+    more = 0;
+    for (uint64_t Q = P; Q < pfirst + npar; ++Q) {
+      if (rep_of(Q) != rp) continue;
+      const uint64_t j0 = Q * A > L.child_first ? Q * A : L.child_first;
+      const uint64_t j1 = (Q + 1) * A < L.child_first + L.batch ? (Q + 1) * A : L.child_first + L.batch;
+      for (uint64_t j = j0; j < j1; ++j) {
+        if (skip > 0) { --skip; continue; }
+        if (k < KMAX) kids[k++] = (uint32_t)(j - L.child_first);
+        else more = 1;
+      }
+    }
+    nkid = k;
+  }
+  __syncthreads();
+  const int nk = nkid;
+  for (int kb = 0; kb < nk; kb += PNC) {
+  const uint32_t nc = (uint32_t)min(PNC, nk - kb);
   if (threadIdx.x < nc) {   // a child with a Pauli inside a diagonal unit -> the generated kernel
-    const unsigned char* codes = L.rows + (uint64_t)(s0 + threadIdx.x) * L.row_bytes;
+    const uint32_t sl = kids[kb + threadIdx.x];
+    const unsigned char* codes = L.rows + (uint64_t)sl * L.row_bytes;
     int e = 0;
     for (uint32_t i = 0; i < sp.ndg; ++i) e |= codes[4 + sp.dgoff[i]] != 0;
     live[threadIdx.x] = !e;
-    if (e && c == 0) L.glist[atomicAdd(L.gcount, 1u)] = s0 + threadIdx.x;
+    if (e && c == 0) L.glist[atomicAdd(L.gcount, 1u)] = sl;
   }
   if (threadIdx.x < nc * sp.m) {   // U_j of child ci: the top qubit's gates with their Paulis
     const uint32_t ci = threadIdx.x / sp.m, jb = threadIdx.x % sp.m;
-    const unsigned char* codes = L.rows + (uint64_t)(s0 + ci) * L.row_bytes;
+    const unsigned char* codes = L.rows + (uint64_t)kids[kb + ci] * L.row_bytes;
     cd u[4] = {{1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {1.0, 0.0}};
     for (uint32_t i = 0; i < sp.ng; ++i) {
       if (sp.gbit[i] != jb) continue;
@@ -644,7 +681,7 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
   const uint32_t Y = 1u << sp.m;
   for (uint32_t i = threadIdx.x; i < nc * Y; i += PT) {   // c_ci[y] = prod_j U_j[sel_j][y_j] * D_top(y)
     const uint32_t ci = i / Y, y = i % Y;
-    const uint32_t sel = L.hsel[s0 + ci];
+    const uint32_t sel = L.hsel[kids[kb + ci]];
     cd v = {1.0, 0.0};
     for (uint32_t j = 0; j < sp.m; ++j) {
       const cd e = U[ci][j][2 * ((sel >> j) & 1u) + ((y >> j) & 1u)];
@@ -658,12 +695,7 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
     coef[ci][y] = v;
   }
   __syncthreads();
-  uint64_t pj = P - L.parent_first;
-  if (L.prep) pj = L.prep[pj];
-  const cd* __restrict__ src = static_cast<const cd*>(L.src) + (pj << L.n);
-  const uint32_t n2 = sp.n2;
-  const uint64_t x0 = ((uint64_t)c * PT + threadIdx.x) * PV;
-  if (x0 >= (1ull << n2)) return;
+  if (x0 < (1ull << n2)) {
   double acc[PNC][4];
 #pragma unroll
   for (int ci = 0; ci < PNC; ++ci) acc[ci][0] = acc[ci][1] = acc[ci][2] = acc[ci][3] = 0.0;
@@ -696,9 +728,15 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
         r = {r.x * e.x - r.y * e.y, r.x * e.y + r.y * e.x};
       }
     }
-    cd* dst = static_cast<cd*>(L.psi) + ((uint64_t)(s0 + ci) << n2) + x0;
+    cd* dst = static_cast<cd*>(L.psi) + ((uint64_t)kids[kb + ci] << n2) + x0;
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(r0.x), "d"(r0.y), "d"(r1.x), "d"(r1.y)
                  : "memory");
+  }
+  }
+  __syncthreads();   // the tables of the next children
+  }
+  if (!more) break;
+  __syncthreads();
   }
 }
 
