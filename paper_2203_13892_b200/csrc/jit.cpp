@@ -1209,9 +1209,14 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   if (gd.empty()) o << "0.0";
   o << "};\n";
   const int NW = std::max(1, (nops + 31) / 32);
-  // 16 resident warps per SM (128 registers / thread), as many independent CTAs as fit
+  // resident threads per SM the register budget targets (TQSIM_JIT_THREADS_PER_SM, default 512:
+  // 16 warps at <= 128 registers / thread), as many independent CTAs as fit
+  static const int tps = [] {
+    const char* e = std::getenv("TQSIM_JIT_THREADS_PER_SM");
+    return e ? std::max(128, std::atoi(e)) : 512;
+  }();
   const int minb = K >= 13 ? 1
-                           : std::max(1, std::min(512 / std::max(T, 32), (int)((227 * 1024) / ((16 << K) + 1024))));
+                           : std::max(1, std::min(tps / std::max(T, 32), (int)((227 * 1024) / ((16 << K) + 1024))));
   if (tma) {
     // per-kernel work scan and TMA issue: the next computed (representative) work item, and
     // the tensor-map coordinates of its tile (TmaGeom: runs of tile / out-of-tile qubits)

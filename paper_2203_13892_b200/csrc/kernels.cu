@@ -587,21 +587,21 @@ __global__ void __launch_bounds__(256) dedup_map_level_kernel(const uint8_t* __r
 // whose noise row has a Pauli inside a diagonal unit is appended to glist (the generated
 // projection kernel handles it).  One complex FMA per amplitude read: HBM-bound.
 constexpr int PT = 256, PV = 2;   // threads, consecutive x per thread (one 32-byte access)
-constexpr int PNC = 4;            // children per parent handled by one CTA (arity <= PNC)
+constexpr int PNC = 8;            // children handled by one CTA (arity <= PNC)
 // One CTA = one parent of the batch x one chunk of x; parents whose states are shared (the
-// dedup map: the same representative) are handled by the first of them, which reads the shared
-// amplitudes once for all their children in the batch, PNC children per sweep over y.
+// dedup map: the same representative) are taken PNC / A at a time by the first of each run of
+// them, which reads the shared amplitudes once for all (<= PNC) their children in the batch.
 __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant__ ProjSpec sp,
                                                            const __grid_constant__ TrailProjLaunch L,
                                                            const uint64_t* __restrict__ seedp) {
   (void)seedp;
-  constexpr int KMAX = 64;
   __shared__ cd U[PNC][16][4];
   __shared__ cd coef[PNC][1 << 8];
   __shared__ int live[PNC];
-  __shared__ uint32_t kids[KMAX];
-  __shared__ int nkid, lead, more;
+  __shared__ uint32_t kids[PNC];
+  __shared__ int nkid;
   const uint32_t A = L.arity;
+  const uint32_t ppc = PNC / A;                                  // parents per CTA
   const uint64_t pfirst = L.child_first / A;                    // first parent index of the batch
   const uint32_t npar = (uint32_t)((L.child_first + L.batch - 1) / A - pfirst + 1);
   const uint32_t g = blockIdx.x % npar, c = blockIdx.x / npar;
@@ -611,34 +611,27 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
     return L.prep ? L.prep[q] : q;
   };
   const uint64_t rp = rep_of(P);
-  if (threadIdx.x == 0) {   // the group's leader: the first parent of the batch with this state
-    int l = 1;
-    for (uint64_t Q = pfirst; Q < P && l; ++Q)
-      if (rep_of(Q) == rp) l = 0;
-    lead = l;
-  }
-  __syncthreads();
-  if (!lead) return;
-  const cd* __restrict__ src = static_cast<const cd*>(L.src) + (rp << L.n);
-  const uint32_t n2 = sp.n2;
-  const uint64_t x0 = ((uint64_t)c * PT + threadIdx.x) * PV;
-  for (uint32_t round = 0;; ++round) {
-  if (threadIdx.x == 0) {   // children (batch slots) of every parent with this state, KMAX per round
-    int k = 0, skip = (int)(round * KMAX);
-    more = 0;
-    for (uint64_t Q = P; Q < pfirst + npar; ++Q) {
-      if (rep_of(Q) != rp) continue;
-      const uint64_t j0 = Q * A > L.child_first ? Q * A : L.child_first;
-      const uint64_t j1 = (Q + 1) * A < L.child_first + L.batch ? (Q + 1) * A : L.child_first + L.batch;
-      for (uint64_t j = j0; j < j1; ++j) {
-        if (skip > 0) { --skip; continue; }
-        if (k < KMAX) kids[k++] = (uint32_t)(j - L.child_first);
-        else more = 1;
+  if (threadIdx.x == 0) {   // P's rank among the batch's parents with this state; every ppc-th collects
+    uint32_t r = 0;
+    for (uint64_t Q = pfirst; Q < P; ++Q) r += rep_of(Q) == rp;
+    int k = 0;
+    if (r % ppc == 0) {
+      uint32_t taken = 0;
+      for (uint64_t Q = P; Q < pfirst + npar && taken < ppc; ++Q) {
+        if (rep_of(Q) != rp) continue;
+        ++taken;
+        const uint64_t j0 = Q * A > L.child_first ? Q * A : L.child_first;
+        const uint64_t j1 = (Q + 1) * A < L.child_first + L.batch ? (Q + 1) * A : L.child_first + L.batch;
+        for (uint64_t j = j0; j < j1; ++j) kids[k++] = (uint32_t)(j - L.child_first);
       }
     }
     nkid = k;
   }
   __syncthreads();
+  if (nkid == 0) return;
+  const cd* __restrict__ src = static_cast<const cd*>(L.src) + (rp << L.n);
+  const uint32_t n2 = sp.n2;
+  const uint64_t x0 = ((uint64_t)c * PT + threadIdx.x) * PV;
   const int nk = nkid;
   for (int kb = 0; kb < nk; kb += PNC) {
   const uint32_t nc = (uint32_t)min(PNC, nk - kb);
@@ -734,9 +727,6 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
   }
   }
   __syncthreads();   // the tables of the next children
-  }
-  if (!more) break;
-  __syncthreads();
   }
 }
 
