@@ -587,97 +587,54 @@ __global__ void __launch_bounds__(256) dedup_map_level_kernel(const uint8_t* __r
 // whose noise row has a Pauli inside a diagonal unit is appended to glist (the generated
 // projection kernel handles it).  One complex FMA per amplitude read: HBM-bound.
 constexpr int PT = 256, PV = 2;   // threads, consecutive x per thread (one 32-byte access)
-constexpr int PNC = 8;            // children handled by one CTA (arity <= PNC)
-// One CTA = one parent of the batch x one chunk of x; parents whose states are shared (the
-// dedup map: the same representative) are taken PNC / A at a time by the first of each run of
-// them, which reads the shared amplitudes once for all (<= PNC) their children in the batch.
 __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant__ ProjSpec sp,
                                                            const __grid_constant__ TrailProjLaunch L,
                                                            const uint64_t* __restrict__ seedp) {
   (void)seedp;
-  __shared__ cd U[PNC][16][4];
-  __shared__ cd coef[PNC][1 << 8];
-  __shared__ int live[PNC];
-  __shared__ uint32_t kids[PNC];
-  __shared__ int nkid;
-  const uint32_t A = L.arity;
-  const uint32_t ppc = PNC / A;                                  // parents per CTA
-  const uint64_t pfirst = L.child_first / A;                    // first parent index of the batch
-  const uint32_t npar = (uint32_t)((L.child_first + L.batch - 1) / A - pfirst + 1);
-  const uint32_t g = blockIdx.x % npar, c = blockIdx.x / npar;
-  const uint64_t P = pfirst + g;
-  auto rep_of = [&](uint64_t Q) -> uint64_t {   // the parent batch slot holding Q's state
-    const uint64_t q = Q - L.parent_first;
-    return L.prep ? L.prep[q] : q;
-  };
-  const uint64_t rp = rep_of(P);
-  if (threadIdx.x == 0) {   // P's rank among the batch's parents with this state; every ppc-th collects
-    uint32_t r = 0;
-    for (uint64_t Q = pfirst; Q < P; ++Q) r += rep_of(Q) == rp;
-    int k = 0;
-    if (r % ppc == 0) {
-      uint32_t taken = 0;
-      for (uint64_t Q = P; Q < pfirst + npar && taken < ppc; ++Q) {
-        if (rep_of(Q) != rp) continue;
-        ++taken;
-        const uint64_t j0 = Q * A > L.child_first ? Q * A : L.child_first;
-        const uint64_t j1 = (Q + 1) * A < L.child_first + L.batch ? (Q + 1) * A : L.child_first + L.batch;
-        for (uint64_t j = j0; j < j1; ++j) kids[k++] = (uint32_t)(j - L.child_first);
-      }
-    }
-    nkid = k;
-  }
-  __syncthreads();
-  if (nkid == 0) return;
-  const cd* __restrict__ src = static_cast<const cd*>(L.src) + (rp << L.n);
-  const uint32_t n2 = sp.n2;
-  const uint64_t x0 = ((uint64_t)c * PT + threadIdx.x) * PV;
-  const int nk = nkid;
-  for (int kb = 0; kb < nk; kb += PNC) {
-  const uint32_t nc = (uint32_t)min(PNC, nk - kb);
-  if (threadIdx.x < nc) {   // a child with a Pauli inside a diagonal unit -> the generated kernel
-    const uint32_t sl = kids[kb + threadIdx.x];
-    const unsigned char* codes = L.rows + (uint64_t)sl * L.row_bytes;
+  __shared__ cd U[16][4];
+  __shared__ cd coef[1 << 10];
+  __shared__ int skip;
+  const uint32_t s = blockIdx.x % L.batch, c = blockIdx.x / L.batch;
+  const unsigned char* codes = L.rows + (uint64_t)s * L.row_bytes;
+  if (threadIdx.x == 0) {
     int e = 0;
     for (uint32_t i = 0; i < sp.ndg; ++i) e |= codes[4 + sp.dgoff[i]] != 0;
-    live[threadIdx.x] = !e;
-    if (e && c == 0) L.glist[atomicAdd(L.gcount, 1u)] = sl;
+    skip = e;
+    if (e && c == 0) L.glist[atomicAdd(L.gcount, 1u)] = s;
   }
-  if (threadIdx.x < nc * sp.m) {   // U_j of child ci: the top qubit's gates with their Paulis
-    const uint32_t ci = threadIdx.x / sp.m, jb = threadIdx.x % sp.m;
-    const unsigned char* codes = L.rows + (uint64_t)kids[kb + ci] * L.row_bytes;
+  if (threadIdx.x < sp.m) {   // U_j: the top qubit's gates with their Paulis, in slice order
     cd u[4] = {{1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {1.0, 0.0}};
     for (uint32_t i = 0; i < sp.ng; ++i) {
-      if (sp.gbit[i] != jb) continue;
-      cd gm[4] = {{sp.gmat[i][0], sp.gmat[i][1]}, {sp.gmat[i][2], sp.gmat[i][3]},
-                  {sp.gmat[i][4], sp.gmat[i][5]}, {sp.gmat[i][6], sp.gmat[i][7]}};
+      if (sp.gbit[i] != threadIdx.x) continue;
+      cd g[4] = {{sp.gmat[i][0], sp.gmat[i][1]}, {sp.gmat[i][2], sp.gmat[i][3]},
+                 {sp.gmat[i][4], sp.gmat[i][5]}, {sp.gmat[i][6], sp.gmat[i][7]}};
       const uint32_t code = codes[4 + sp.goff[i]];
       if (code) {   // P g: X swaps the rows, Z negates row 1, Y = [[0,-i],[i,0]]
-        const cd r0 = gm[0], r1 = gm[1], r2 = gm[2], r3 = gm[3];
-        if (code == 1) { gm[0] = r2; gm[1] = r3; gm[2] = r0; gm[3] = r1; }
+        cd r0 = g[0], r1 = g[1], r2 = g[2], r3 = g[3];
+        if (code == 1) { g[0] = r2; g[1] = r3; g[2] = r0; g[3] = r1; }
         else if (code == 2) {
-          gm[0] = {r2.y, -r2.x}; gm[1] = {r3.y, -r3.x}; gm[2] = {-r0.y, r0.x}; gm[3] = {-r1.y, r1.x};
-        } else { gm[2] = {-r2.x, -r2.y}; gm[3] = {-r3.x, -r3.y}; }
+          g[0] = {r2.y, -r2.x}; g[1] = {r3.y, -r3.x}; g[2] = {-r0.y, r0.x}; g[3] = {-r1.y, r1.x};
+        } else { g[2] = {-r2.x, -r2.y}; g[3] = {-r3.x, -r3.y}; }
       }
       cd v[4];   // u <- g u
       for (int r = 0; r < 2; ++r)
         for (int k = 0; k < 2; ++k) {
-          const cd a = gm[2 * r], b = gm[2 * r + 1], x0 = u[k], x1 = u[2 + k];
+          const cd a = g[2 * r], b = g[2 * r + 1], x0 = u[k], x1 = u[2 + k];
           v[2 * r + k] = {a.x * x0.x - a.y * x0.y + b.x * x1.x - b.y * x1.y,
                           a.x * x0.y + a.y * x0.x + b.x * x1.y + b.y * x1.x};
         }
       for (int k = 0; k < 4; ++k) u[k] = v[k];
     }
-    for (int k = 0; k < 4; ++k) U[ci][jb][k] = u[k];
+    for (int k = 0; k < 4; ++k) U[threadIdx.x][k] = u[k];
   }
   __syncthreads();
+  if (skip) return;
+  const uint32_t sel = L.hsel[s];
   const uint32_t Y = 1u << sp.m;
-  for (uint32_t i = threadIdx.x; i < nc * Y; i += PT) {   // c_ci[y] = prod_j U_j[sel_j][y_j] * D_top(y)
-    const uint32_t ci = i / Y, y = i % Y;
-    const uint32_t sel = L.hsel[kids[kb + ci]];
+  for (uint32_t y = threadIdx.x; y < Y; y += PT) {   // c[y] = prod_j U_j[sel_j][y_j] * D_top(y)
     cd v = {1.0, 0.0};
     for (uint32_t j = 0; j < sp.m; ++j) {
-      const cd e = U[ci][j][2 * ((sel >> j) & 1u) + ((y >> j) & 1u)];
+      const cd e = U[j][2 * ((sel >> j) & 1u) + ((y >> j) & 1u)];
       v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
     }
     for (uint32_t u = 0; u < sp.nug; ++u) {
@@ -685,49 +642,42 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
       const cd e = {sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
       v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
     }
-    coef[ci][y] = v;
+    coef[y] = v;
   }
   __syncthreads();
-  if (x0 < (1ull << n2)) {
-  double acc[PNC][4];
-#pragma unroll
-  for (int ci = 0; ci < PNC; ++ci) acc[ci][0] = acc[ci][1] = acc[ci][2] = acc[ci][3] = 0.0;
+  const uint64_t j = L.child_first + s;
+  uint64_t pj = j / L.arity - L.parent_first;
+  if (L.prep) pj = L.prep[pj];
+  const cd* __restrict__ src = static_cast<const cd*>(L.src) + (pj << L.n);
+  const uint32_t n2 = sp.n2;
+  const uint64_t x0 = ((uint64_t)c * PT + threadIdx.x) * PV;
+  if (x0 >= (1ull << n2)) return;
+  double a0x = 0.0, a0y = 0.0, a1x = 0.0, a1y = 0.0;
 #pragma unroll 4
   for (uint32_t y = 0; y < Y; ++y) {
     double px, py, qx, qy;
     asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
                  : "=d"(px), "=d"(py), "=d"(qx), "=d"(qy)
                  : "l"(src + (((uint64_t)y << n2) | x0)));
-#pragma unroll
-    for (int ci = 0; ci < PNC; ++ci) {
-      if ((uint32_t)ci >= nc) break;
-      const cd k = coef[ci][y];
-      acc[ci][0] = fma(k.x, px, fma(-k.y, py, acc[ci][0]));
-      acc[ci][1] = fma(k.x, py, fma(k.y, px, acc[ci][1]));
-      acc[ci][2] = fma(k.x, qx, fma(-k.y, qy, acc[ci][2]));
-      acc[ci][3] = fma(k.x, qy, fma(k.y, qx, acc[ci][3]));
+    const cd k = coef[y];
+    a0x = fma(k.x, px, fma(-k.y, py, a0x));
+    a0y = fma(k.x, py, fma(k.y, px, a0y));
+    a1x = fma(k.x, qx, fma(-k.y, qy, a1x));
+    a1y = fma(k.x, qy, fma(k.y, qx, a1y));
+  }
+  cd r0 = {a0x, a0y}, r1 = {a1x, a1y};
+  for (uint32_t u = sp.nug; u < sp.nug + sp.nux; ++u) {   // D_x: units below the top bits
+    for (int v = 0; v < PV; ++v) {
+      const uint64_t x = x0 + v;
+      const uint32_t idx = (uint32_t)((x >> sp.ua[u]) & 1u) | (uint32_t)(((x >> sp.ub[u]) & 1u) << 1);
+      const cd e = {sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
+      cd& r = v ? r1 : r0;
+      r = {r.x * e.x - r.y * e.y, r.x * e.y + r.y * e.x};
     }
   }
-#pragma unroll
-  for (int ci = 0; ci < PNC; ++ci) {
-    if ((uint32_t)ci >= nc || !live[ci]) continue;
-    cd r0 = {acc[ci][0], acc[ci][1]}, r1 = {acc[ci][2], acc[ci][3]};
-    for (uint32_t u = sp.nug; u < sp.nug + sp.nux; ++u) {   // D_x: units below the top bits
-      for (int v = 0; v < PV; ++v) {
-        const uint64_t x = x0 + v;
-        const uint32_t idx = (uint32_t)((x >> sp.ua[u]) & 1u) | (uint32_t)(((x >> sp.ub[u]) & 1u) << 1);
-        const cd e = {sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
-        cd& r = v ? r1 : r0;
-        r = {r.x * e.x - r.y * e.y, r.x * e.y + r.y * e.x};
-      }
-    }
-    cd* dst = static_cast<cd*>(L.psi) + ((uint64_t)kids[kb + ci] << n2) + x0;
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(r0.x), "d"(r0.y), "d"(r1.x), "d"(r1.y)
-                 : "memory");
-  }
-  }
-  __syncthreads();   // the tables of the next children
-  }
+  cd* dst = static_cast<cd*>(L.psi) + ((uint64_t)s << n2) + x0;
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(r0.x), "d"(r0.y), "d"(r1.x), "d"(r1.y)
+               : "memory");
 }
 
 // The run's seed in device memory: the tree's launches (a replayed CUDA graph) read it
@@ -762,10 +712,8 @@ int launch_dedup_map_level(const uint8_t* d_rows, const NoiseLevels& L, uint32_t
 }
 
 int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* stream) {
-  if (L.arity > (uint32_t)dev::PNC || spec.m > 8) return (int)cudaErrorInvalidValue;
   const uint64_t per_leaf = std::max<uint64_t>(1, (1ull << spec.n2) / (dev::PT * dev::PV));
-  const uint64_t npar = (L.child_first + L.batch - 1) / L.arity - L.child_first / L.arity + 1;
-  const uint64_t grid = per_leaf * npar;
+  const uint64_t grid = per_leaf * L.batch;
   if (grid == 0) return 0;
   dev::trail_project_kernel<<<(unsigned)grid, dev::PT, 0, static_cast<cudaStream_t>(stream)>>>(spec, L, nullptr);
   return (int)cudaGetLastError();

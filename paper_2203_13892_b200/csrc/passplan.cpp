@@ -384,7 +384,7 @@ void plan_trail(PassPlan& pp, const std::vector<LGate>& gates, const Plan& plan,
       }
       ok = false;   // a non-diagonal gate among the top qubits (e.g. CX(16, 17))
     }
-    if (ok && m <= 8 && plan.arities.back() <= 8 && ug.size() + ux.size() <= (size_t)PROJ_MAX_U) {
+    if (ok && m <= 10 && ug.size() + ux.size() <= (size_t)PROJ_MAX_U) {
       ps.nug = (uint32_t)ug.size();
       ps.nux = (uint32_t)ux.size();
       size_t k = 0;
