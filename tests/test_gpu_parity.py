@@ -490,3 +490,31 @@ def test_streaming_projection_vs_oracle(n, tile, p, ar):
         assert int(a.leaf_outcomes[l]) == r.outcome, (l, int(a.leaf_outcomes[l]), r.outcome)
         assert int(b.leaf_outcomes[l]) == r.outcome
         assert not a.leaf_flagged[l]
+
+
+@pytest.mark.parametrize("world", [3, 5])
+def test_conditional_sampling_split_level_shards(world):
+    """Conditional leaf sampling under split-level sharding (W does not divide A_0,
+    the leaf batches are clipped to the shard): serial shards add up to the single run."""
+    torch = pytest.importorskip("torch")
+    from workloads.generators import qaoa_gates, random_3_regular_edges
+    rng = np.random.default_rng(40 + world)
+    n = 14
+    gates = qaoa_gates(n, random_3_regular_edges(n, rng), [0.7, 1.1], [0.4, 0.9])
+    noise = T.noise_arg(0.01, 0.03, 0.01, 0.01)
+    opts = T.default_options(tile_qubits=7, batch_log2_amps=n + 2)
+    ar = [4, 3, 2]
+    shots = int(np.prod(ar))
+    h = T.tqsim_create(n, gates, noise, shots, ar, opts)
+    assert h.plan.trail_top_bits > 0
+    single = T.tqsim_run_ex(n, gates, noise, shots, ar, 8, opts).leaf_outcomes
+    acc = np.zeros(shots, dtype=np.int64)
+    split, lo, hi = T.tqsim_shard_levels(h.plan, 0, world)
+    assert split > 0
+    for r in range(world):
+        ws = torch.empty(h.workspace_bytes(r, world), dtype=torch.uint8, device="cuda")
+        o = torch.zeros(shots, dtype=torch.int32, device="cuda")
+        h.execute(8, r, world, torch.cuda.current_stream().cuda_stream, ws.data_ptr(), ws.numel(), o.data_ptr())
+        acc += o.cpu().numpy()
+    assert np.array_equal(acc.astype(np.uint32), single)
+    h.close()
