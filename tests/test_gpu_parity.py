@@ -518,3 +518,26 @@ def test_conditional_sampling_split_level_shards(world):
         acc += o.cpu().numpy()
     assert np.array_equal(acc.astype(np.uint32), single)
     h.close()
+
+
+def test_streaming_projection_split_level_shards():
+    """The streaming projection (clipped leaf batches, parent slots of a split shard) under
+    serial shards W = 3 equals the single run."""
+    torch = pytest.importorskip("torch")
+    n, tile, ar = 14, 8, [2, 3, 4]
+    gates = _fast_trail_circuit(n, tile - 3, np.random.default_rng(5))
+    noise = T.noise_arg(0.02, 0.05, 0.01, 0.01)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    shots = int(np.prod(ar))
+    h = T.tqsim_create(n, gates, noise, shots, ar, opts)
+    assert h.plan.trail_fast == 1
+    single = T.tqsim_run_ex(n, gates, noise, shots, ar, 12, opts).leaf_outcomes
+    acc = np.zeros(shots, dtype=np.int64)
+    assert T.tqsim_shard_levels(h.plan, 0, 3)[0] > 0
+    for r in range(3):
+        ws = torch.empty(h.workspace_bytes(r, 3), dtype=torch.uint8, device="cuda")
+        o = torch.zeros(shots, dtype=torch.int32, device="cuda")
+        h.execute(12, r, 3, torch.cuda.current_stream().cuda_stream, ws.data_ptr(), ws.numel(), o.data_ptr())
+        acc += o.cpu().numpy()
+    assert np.array_equal(acc.astype(np.uint32), single)
+    h.close()
