@@ -923,7 +923,7 @@ struct PItem {
 // phase is the store layout: when `coal` it must hold no position < low in
 // registers, so a trailing re-layout phase is added if the last group needs one.
 std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint64_t R0, bool coal,
-                                   const int* store_key) {
+                                   const int* store_key, bool runsums_only = false) {
   const int low = std::min(LOW_Q, K);
   const uint64_t lowm = (1ull << low) - 1;
   uint64_t store_low = 0;   // positions of the store's address bits 0..low-1
@@ -964,7 +964,13 @@ std::vector<PhaseSpec> plan_phases(const std::vector<PItem>& items, int K, uint6
   if (coal) {
     const uint64_t last_regs = io_with_pair(groups.size() == 1 ? R0 : groups.back().second, store_key, K);
     const bool st_ok = __builtin_popcountll(last_regs) <= RBITS && io_regs_ok(last_regs, store_key, K);
-    if (!st_ok || (groups.size() == 1 && !same_low)) groups.emplace_back(std::vector<int>(), 0);
+    // a pass that stores no state (leaf run sums / the run recompute) needs no coalesced store
+    // layout: when its last phase already holds the run's low qubits in registers, the run
+    // sums are register sums and the extra (empty) exchange phase is dropped
+    const uint64_t last_R = groups.size() == 1 ? R0 : groups.back().second;
+    const bool runs_in_regs = (last_R & store_low) == store_low && groups.size() > 1;
+    if (!(runsums_only && runs_in_regs) && (!st_ok || (groups.size() == 1 && !same_low)))
+      groups.emplace_back(std::vector<int>(), 0);
   }
   (void)lowm;
   std::vector<PhaseSpec> out;
@@ -1055,7 +1061,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     const uint64_t r0 = choose_load_regs(items, K, coal, cand >= 2);
     int skey[64];
     for (int p = 0; p < K; ++p) skey[p] = lop[pd.tile_q[p]];
-    std::vector<PhaseSpec> ph = plan_phases(items, K, r0, coal, skey);
+    std::vector<PhaseSpec> ph = plan_phases(items, K, r0, coal, skey,
+                                            pd.leaf_sums && (variant == 1 || variant == 2) &&
+                                                std::getenv("TQSIM_RUNSUM_PHASE") == nullptr);
     const double cost = fcost + 12.0 * (double)ph.size();
     if (cand == 0 || cost < best_cost) {
       best_cost = cost;
