@@ -680,6 +680,38 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
                : "memory");
 }
 
+// The computed instances (dedup representatives) of a batch, in slot order: the work list of
+// the batch's pass kernels (persistent CTAs, no empty CTAs for the shared instances).  The
+// leaf level's skipped instances get store-address XOR 0 (their representative is error-free).
+__global__ void __launch_bounds__(256) compact_reps_kernel(const uint32_t* __restrict__ rep, uint32_t cnt,
+                                                           uint32_t* __restrict__ list, uint32_t* __restrict__ count,
+                                                           uint32_t* __restrict__ xlout) {
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t c0 = 0; c0 < cnt; c0 += blockDim.x) {
+    const uint32_t s = c0 + threadIdx.x;
+    const bool keep = s < cnt && rep[s] == s;
+    if (s < cnt && !keep && xlout) xlout[s] = 0u;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    uint32_t off = base;
+    for (int i = 0; i < w; ++i) off += wsum[i];
+    if (keep) list[off + __popc(bal & ((1u << lane) - 1u))] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[i];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base;
+}
+
 // The run's seed in device memory: the tree's launches (a replayed CUDA graph) read it
 __global__ void set_seed_kernel(uint64_t* d_seed, uint64_t seed) { *d_seed = seed; }
 
@@ -716,6 +748,12 @@ int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* s
   const uint64_t grid = per_leaf * L.batch;
   if (grid == 0) return 0;
   dev::trail_project_kernel<<<(unsigned)grid, dev::PT, 0, static_cast<cudaStream_t>(stream)>>>(spec, L, nullptr);
+  return (int)cudaGetLastError();
+}
+
+int launch_compact_reps(const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
+                        void* stream) {
+  dev::compact_reps_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_rep, cnt, d_list, d_count, d_xlout);
   return (int)cudaGetLastError();
 }
 

@@ -147,6 +147,7 @@ struct Layout {
   std::vector<uint64_t> map_lvl;        // entry offset of each level's map
   uint64_t map_entries = 0;
   std::vector<uint64_t> kflag_off;      // Kraus engine: per level, one path-flag byte per batch slot
+  std::vector<uint64_t> wl_off;         // per level: the batch's work list (cap u32) + its count
   // conditional leaf sampling (pp.trail): projected states, their run sums, stage-1 outputs
   uint64_t psi_off = 0, runs2_off = 0, hsel_off = 0, htgt_off = 0, glist_off = 0;
   uint64_t sel_off = 0;                 // leaf select / recompute buffers (per leaf of a batch):
@@ -289,6 +290,11 @@ Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl) {
       l.kflag_off.push_back(off);
       off = align_up(off + (h->kraus ? l.cap[d] : 0));
     }
+    l.wl_off.clear();
+    for (size_t d = 0; d < levels; ++d) {
+      l.wl_off.push_back(off);
+      off = align_up(off + 4 * (l.cap[d] + 1));
+    }
     if (h->pp.trail.on) {
       const uint64_t capl = l.cap.back(), n2 = (uint64_t)h->pp.trail.n2;
       l.psi_off = off;
@@ -367,6 +373,8 @@ struct Exec {
   bool leaf_issued = false;
   uint64_t pcnt[64] = {};   // instances of the current batch per level
   bool dedup = false;       // dedup maps built for this tree (no state dumps asked for)
+  const uint32_t* wl = nullptr;      // the current batch's work list (compact_reps) and count
+  const uint32_t* wlc = nullptr;
   const cudaEvent_t* map_ev = nullptr;   // side-stream map chain: level d's map is ready
   bool map_waited[64] = {};
 };
@@ -472,6 +480,8 @@ void run_leaf_trail(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, uint64_t pare
   pl.runsum = runs;
   pl.xlout = xlv;
   pl.rep = rep;
+  pl.wlist = x.wl;
+  pl.wcount = x.wlc;
   mark(x, 0, d, 0, b, cnt);
   ck(launch_jit_pass(jt.a, tp.a, pl, x.st), "trail pass A launch");
   mark(x, 0, d, 0, b, cnt);
@@ -495,6 +505,8 @@ void run_leaf_trail(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, uint64_t pare
   PassLaunch pb = pl;
   pb.variant = 3u;
   pb.rep = nullptr;
+  pb.wlist = nullptr;
+  pb.wcount = nullptr;
   pb.runsel = hsel;
   pb.scratch = psi;
   mark(x, 0, d, 100, b, cnt);
@@ -528,6 +540,8 @@ void run_leaf_trail(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, uint64_t pare
   PassLaunch last{};
   for (size_t p = 0; p < tp.b.size(); ++p) {
     PassLaunch q = pl;
+    q.wlist = nullptr;
+    q.wcount = nullptr;
     q.src_mode = 2u;
     q.src = psi;
     q.dst = psi;
@@ -628,6 +642,25 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     uint32_t* xlv = reinterpret_cast<uint32_t*>(sel + 2 * align_up(4 * capl));
     double* t3 = reinterpret_cast<double*>(sel + 3 * align_up(4 * capl));
     void* scratch = sel + 3 * align_up(4 * capl) + align_up(8 * capl);
+    // the batch's computed instances as a work list: the pass kernels loop over them with
+    // persistent CTAs instead of launching an (empty) CTA per shared instance and tile
+    x.wl = x.wlc = nullptr;
+    static const bool use_wl = [] {
+      const char* e = std::getenv("TQSIM_WORKLIST");
+      return !(e && e[0] == '0');
+    }();
+    if (use_wl && x.dedup && cnt > 1) {
+      const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
+      uint32_t* wl = reinterpret_cast<uint32_t*>(x.ws + x.L.wl_off[d]);
+      uint32_t* xl0 = leaf && nostore ? reinterpret_cast<uint32_t*>(x.ws + x.L.sel_off + 2 * align_up(4 * x.L.cap.back()))
+                                      : nullptr;
+      ck(launch_compact_reps(maps + x.L.map_lvl[d] + (b - x.lvl_first[d]), (uint32_t)cnt, wl, wl + x.L.cap[d], xl0,
+                             x.st),
+         "work list launch");
+      h->stats.kernel_launches++;
+      x.wl = wl;
+      x.wlc = wl + x.L.cap[d];
+    }
     if (leaf && nostore && h->pp.trail.on) {   // conditional leaf sampling (default path)
       run_leaf_trail(x, d, b, cnt, parent_first, pbuf, buf, rows, row_bytes);
       h->stats.node_executions += cnt;
@@ -655,6 +688,8 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       pl.xlout = xlv;
       // shared states computed once (dedup maps; nobody reads a skipped slot except through
       // the maps: the next level's fan-out, the sampler, the recompute)
+      pl.wlist = x.wl;
+      pl.wcount = x.wlc;
       if (x.dedup) {
         const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
         if (cnt > 1) pl.rep = maps + x.L.map_lvl[d] + (b - x.lvl_first[d]);

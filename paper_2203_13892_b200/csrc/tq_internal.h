@@ -182,6 +182,10 @@ int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t s
                       uint32_t slice_len, uint64_t inst_first, uint32_t count, const uint64_t* d_seed,
                       double p1, double p2, uint32_t row_bytes, uint8_t* d_rows, void* stream);
 int launch_set_seed(uint64_t* d_seed, uint64_t seed, void* stream);
+// the batch's computed instances (rep[s] == s) in slot order -> list, *count; xlout (leaf level,
+// may be null) = 0 for the others
+int launch_compact_reps(const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
+                        void* stream);
 // All noise rows of a shard in one launch (one warp per instance of every level).
 struct NoiseLevel {
   uint64_t inst_first;   // global instance id of the shard's first instance at this level
