@@ -485,9 +485,10 @@ def main():
             T.tqsim_release_run_cache()
             note = ("tqsim_run per step: host circuit in (validated, hashed; the prepared plan and its "
                     "specialized kernels are reused from the library's plan cache after the first call), "
-                    "h2d = per-gate noise-class and pass tables (2 B / lowered gate) + kernel parameters, "
+                    "h2d = per-gate noise-class and pass tables (2 B / lowered gate) + the seed (the tree is a "
+                    "replayed CUDA graph: no per-kernel parameters cross PCIe), "
                     "d2h = leaf outcomes (uint32) into page-locked memory, host histogram (C)")
-            h2d = 2 * n_low + 96 * launches_per_step
+            h2d = 2 * n_low + 8
         else:
             from paper_2203_13892_b200.distributed import ShardRunner
             host = torch.empty(N, dtype=torch.int32, pin_memory=True)
