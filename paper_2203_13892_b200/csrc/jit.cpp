@@ -1287,8 +1287,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       << "  tq_d2* const tile = tq_buf0 + ((tq_u64)tq_b << " << K << ");\n";
   } else if (variant == 2)   // one CTA per leaf, on the tile holding its selected run
     o << "  const tq_u32 s = (tq_u32)bid;\n  const tq_u64 t = a.tiles[s];\n  const tq_u32 rsel = a.runsel[s];\n";
-  else   // every (instance, tile), or the instances of a work list (dedup representatives /
-         // projection hand-overs) with persistent CTAs
+  else if (variant == 0)
+    o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
+  else   // leaf run sums / projection: every (instance, tile), or the instances of a work list
+         // (dedup representatives / projection hand-overs) with persistent CTAs
     o << "  const tq_u32 nw = a.wlist ? *a.wcount : a.batch;\n"
       << "  for (tq_u64 w = bid; w < ((tq_u64)nw << " << pd.n_out << "); w += gridDim.x) {\n"
       << "  const tq_u32 s = a.wlist ? a.wlist[w % nw] : (tq_u32)(w % nw);\n  const tq_u64 t = w / nw;\n";
@@ -1300,7 +1302,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     // the map.  A skipped leaf's store-address XOR is 0.
     o << "  if (a.rep && a.rep[s] != s) {\n"
       << (variant == 1 ? "    if (t == 0 && tid == 0u) a.xlout[s] = 0u;\n" : "")
-      << (tma ? "    return;\n" : "    continue;\n")
+      << (tma || variant == 0 ? "    return;\n" : "    continue;\n")
       << "  }\n";
   }
   o << "  tq_u32 gtile = 0u, gtile_st = 0u;\n";   // the tile's out-of-tile index bits: physical / stored
@@ -2222,7 +2224,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     emit_phases(fast, true, ph);
     o << "  }\n";
   }
-  if (!tma && variant != 2) o << "  __syncthreads();\n  }\n";   // the work loop (shared memory is reused)
+  if (!tma && (variant == 1 || variant == 3)) o << "  __syncthreads();\n  }\n";   // the work loop
   if (tma)   // generic-proxy writes (exchanges) before the buffer's next TMA fill
     o << "  tq_fence_async();\n  __syncthreads();\n  tq_w = tq_next[tq_b ^ 1u];\n  tq_b ^= 1u;\n  }\n";
   o << "}\n";
@@ -2647,7 +2649,7 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
   if (!kern) return (int)cudaErrorInvalidDeviceFunction;
   uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;
   if (L.variant == 3 && L.wlist) grid = std::min<uint64_t>(grid, 4 * 148);   // persistent over the work list
-  if ((L.variant == 0 || L.variant == 1) && L.wlist) {   // persistent over the batch's representatives
+  if (L.variant == 1 && L.wlist) {   // persistent over the batch's representatives
     const uint64_t per_sm = std::max<uint64_t>(1, 512 / std::max(jp.threads, 32));
     grid = std::min<uint64_t>(grid, per_sm * 148 * 2);
   }

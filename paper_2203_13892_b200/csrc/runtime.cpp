@@ -649,7 +649,7 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       const char* e = std::getenv("TQSIM_WORKLIST");
       return !(e && e[0] == '0');
     }();
-    if (use_wl && x.dedup && cnt > 1) {
+    if (use_wl && x.dedup && cnt > 1 && leaf && nostore) {   // the leaf run-sum passes (variant 1)
       const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
       uint32_t* wl = reinterpret_cast<uint32_t*>(x.ws + x.L.wl_off[d]);
       uint32_t* xl0 = leaf && nostore ? reinterpret_cast<uint32_t*>(x.ws + x.L.sel_off + 2 * align_up(4 * x.L.cap.back()))
@@ -688,8 +688,8 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       pl.xlout = xlv;
       // shared states computed once (dedup maps; nobody reads a skipped slot except through
       // the maps: the next level's fan-out, the sampler, the recompute)
-      pl.wlist = x.wl;
-      pl.wcount = x.wlc;
+      pl.wlist = runsums_only ? x.wl : nullptr;   // only the variant-1 kernels loop over a work list
+      pl.wcount = runsums_only ? x.wlc : nullptr;
       if (x.dedup) {
         const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
         if (cnt > 1) pl.rep = maps + x.L.map_lvl[d] + (b - x.lvl_first[d]);
