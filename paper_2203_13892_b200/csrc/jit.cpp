@@ -2271,6 +2271,11 @@ std::string compile_to_cubin(const std::string& src, const std::string& name) {
   std::string cubin(n, '\0');
   nvrtcGetCUBIN(prog, &cubin[0]);
   nvrtcDestroyProgram(&prog);
+  if (const char* dir = std::getenv("TQSIM_JIT_DUMP"))   // the cubin too (cuobjdump -sass)
+    if (FILE* f = std::fopen((std::string(dir) + "/" + name + ".cubin").c_str(), "wb")) {
+      std::fwrite(cubin.data(), 1, cubin.size(), f);
+      std::fclose(f);
+    }
   return cubin;
 }
 
