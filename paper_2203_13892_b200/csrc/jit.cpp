@@ -1420,6 +1420,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     // at the end of the phase.  Exact up to fp rounding (R30).
     cplx dph[16];
     for (int k = 0; k < 16; ++k) dph[k] = cplx(1.0, 0.0);
+    double sum_scale = 1.0;   // run sums x this (variant 1, last phase; see the flush)
     auto permute = [&](auto perm) {   // new logical k <- old logical perm(k)
       int nrm[16];
       cplx nd[16];
@@ -1438,7 +1439,14 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         if (pd.tile_q[P.rpos[b]] == q) return b;
       return -1;
     };
-    bool gph_on = false;
+    bool gph_on = false, gph_decl = false;
+    // a thread-bit diagonal joins the common factor gph (declared once per phase; reset to 1
+    // after a flush folded it into the registers)
+    auto gph_begin = [&]() {
+      if (!gph_decl) o << "    double gphx = 1.0, gphy = 0.0;\n";
+      else if (!gph_on) o << "    gphx = 1.0; gphy = 0.0;\n";
+      gph_decl = gph_on = true;
+    };
     int fb_gen = 0;
     struct FBv {
       bool on = false;
@@ -1452,12 +1460,28 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     // apply pending F_b to the registers (before an op mixing bit b), then reset it
     auto fb_flush = [&](int b, int& gen) {
       if (b < 0 || !fb[b].on) return;
+      // A flush that multiplies all 16 registers also takes the pending common factor gph
+      // (a per-thread scalar: it commutes with every register op), two per-thread products
+      // instead of 16 register multiplies at the phase end.
+      const bool fold = gph_on && !fb[b].one[0] && !fb[b].one[1];
+      std::string X[2];
+      for (int v = 0; v < 2; ++v) {
+        if (fb[b].one[v]) continue;
+        X[v] = fb[b].var[v];
+        if (fold) {
+          const std::string nm = X[v] + "p";
+          o << "    const double " << nm << "r = fma(" << X[v] << "r, gphx, -" << X[v] << "i * gphy), " << nm
+            << "i = fma(" << X[v] << "r, gphy, " << X[v] << "i * gphx);\n";
+          X[v] = nm;
+        }
+      }
+      if (fold) gph_on = false;
       for (int k = 0; k < 16; ++k) {
         const int v = (k >> b) & 1;
-        if (fb[b].one[v]) continue;
-        const std::string X = fb[b].var[v], r = g.r(k);
-        o << "    { const tq_d2 x = " << r << "; " << r << ".x = fma(" << X << "r, x.x, -" << X << "i * x.y); " << r
-          << ".y = fma(" << X << "r, x.y, " << X << "i * x.x); }\n";
+        if (X[v].empty()) continue;
+        const std::string r = g.r(k);
+        o << "    { const tq_d2 x = " << r << "; " << r << ".x = fma(" << X[v] << "r, x.x, -" << X[v] << "i * x.y); " << r
+          << ".y = fma(" << X[v] << "r, x.y, " << X[v] << "i * x.x); }\n";
       }
       ++gen;
       fb[b] = FBv();
@@ -1625,10 +1649,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
               sel_r = sel(false);
               sel_i = sel(true);
             }
-            if (!gph_on) {
-              o << "    double gphx = 1.0, gphy = 0.0;\n";
-              gph_on = true;
-            }
+            gph_begin();
             oo << "      { const double fr = " << sel_r << ", fi = " << sel_i << ";\n"
                << "        const double tx = fma(gphx, fr, -gphy * fi); gphy = fma(gphx, fi, gphy * fr); gphx = tx; }\n";
             o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
@@ -1939,10 +1960,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
               return "(" + B + " ? (" + A + " ? " + val(entry(1, 1), im) + " : " + val(entry(0, 1), im) + ") : (" +
                      A + " ? " + val(entry(1, 0), im) + " : " + val(entry(0, 0), im) + "))";
             };
-            if (!gph_on) {
-              o << "    double gphx = 1.0, gphy = 0.0;\n";
-              gph_on = true;
-            }
+            gph_begin();
             oo << "      { const double fr = " << sel(false) << ", fi = " << sel(true) << ";\n"
                << "        const double tx = fma(gphx, fr, -gphy * fi); gphy = fma(gphx, fi, gphy * fr); gphx = tx; }\n";
             o << "    {\n" << pool.decl.str() << oo.str() << "    }\n";
@@ -2057,6 +2075,17 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       }
       std::ostringstream oo;
       pool.begin_op();
+      // run sums only (variant 1): a modulus common to the 16 registers scales the sums
+      // (one multiply per stored sum) instead of every amplitude
+      if (mag_only && variant == 1 && pd.leaf_sums) {
+        const double s0 = std::abs(dph[0]);
+        bool uni = true;
+        for (int k = 1; k < 16; ++k) uni &= std::abs(dph[k]) == s0;
+        if (uni && s0 != 1.0) {
+          sum_scale = s0 * s0;
+          for (int k = 0; k < 16; ++k) dph[k] = cplx(1.0, 0.0);
+        }
+      }
       for (int k = 0; k < 16; ++k) {
         const cplx d = mag_only ? snap(cplx(std::abs(dph[k]), 0.0)) : dph[k];
         if (d == cplx(1.0, 0.0)) continue;
@@ -2186,7 +2215,8 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         o << "};\n";
         for (size_t j = 0; j < v.size(); ++j)
           o << "    a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + (((gbs ^ ROFF[rbase + " << j << "u])" << xl
-            << ") >> " << RUN_Q << ")] = " << v[j] << ";\n";
+            << ") >> " << RUN_Q << ")] = " << v[j] << (sum_scale != 1.0 ? " * " + hexd(sum_scale) : std::string())
+            << ";\n";
       }
     } else {
       o << "    const tq_u32 sbs = tq_swz(" << lbs << ");\n";
