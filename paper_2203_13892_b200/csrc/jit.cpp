@@ -1398,6 +1398,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   else
     o << "  const bool errs = (emask >> " << std::min<uint32_t>(pd.pass_index, 31) << ") & 1u;\n";
 
+  bool sc_used = false;   // a fast phase scaled the run sums by the run-time tq_sc
   auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors, int ph_only) {
   const int nph = (int)specs.size();
   for (int ph = 0; ph < nph; ++ph) {
@@ -2075,6 +2076,38 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       }
       std::ostringstream oo;
       pool.begin_op();
+      // run sums only (variant 1), an earlier phase of the fast path: when no later op of
+      // the pass mixes this phase's register qubits (only diagonal ops touch them), the
+      // pending per-register phases are unobservable in |a|^2 -- only their modulus is kept,
+      // as a run-time factor of the sums when common to the 16 registers
+      if (!last && !with_errors && variant == 1 && pd.leaf_sums) {
+        uint64_t mixed = 0;
+        std::function<void(const FOp&)> mq = [&](const FOp& f) {
+          if (f.kind != FOp::DIAG && f.kind != FOp::NOP) {
+            if (f.qa >= 0) mixed |= 1ull << f.qa;
+            if (f.qb >= 0) mixed |= 1ull << f.qb;
+          }
+          for (const FOp& c : f.comps) mq(c);
+        };
+        for (int p2 = ph + 1; p2 < nph; ++p2)
+          for (int it : specs[p2].items) mq(fops[it]);
+        bool hidden = true;
+        for (int b = 0; b < RBITS; ++b) hidden &= !((mixed >> pd.tile_q[P.rpos[b]]) & 1ull);
+        if (hidden) {
+          const double s0 = std::abs(dph[0]);
+          bool uni = true;
+          for (int k = 1; k < 16; ++k) uni &= std::abs(dph[k]) == s0;
+          if (uni) {
+            if (s0 != 1.0) {
+              o << "    tq_sc *= " << hexd(s0 * s0) << ";\n";
+              sc_used = true;
+            }
+            for (int k = 0; k < 16; ++k) dph[k] = cplx(1.0, 0.0);
+          } else {
+            for (int k = 0; k < 16; ++k) dph[k] = snap(cplx(std::abs(dph[k]), 0.0));
+          }
+        }
+      }
       // run sums only (variant 1): a modulus common to the 16 registers scales the sums
       // (one multiply per stored sum) instead of every amplitude
       if (mag_only && variant == 1 && pd.leaf_sums) {
@@ -2216,6 +2249,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         for (size_t j = 0; j < v.size(); ++j)
           o << "    a.runsum[((tq_u64)s << " << (n - RUN_Q) << ") + (((gbs ^ ROFF[rbase + " << j << "u])" << xl
             << ") >> " << RUN_Q << ")] = " << v[j] << (sum_scale != 1.0 ? " * " + hexd(sum_scale) : std::string())
+            << (sc_used ? " * tq_sc" : "")
             << ";\n";
       }
     } else {
@@ -2238,6 +2272,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   for (int w = 0; w < NW; ++w) o << "    eb" << w << " = tq_errb[" << w << "];\n";
   o << "  }\n";
   o << "  tq_u32 fx = 0u, fz = 0u, fk = 0u;\n";
+  if (variant == 1 && pd.leaf_sums) o << "  double tq_sc = 1.0;\n";   // run-sum factor (see the flush)
   for (int ph = 0; ph < (int)fast.size(); ++ph) {
     std::vector<uint32_t> pm(NW, 0u);   // error sites of the phase's ops
     std::function<void(const FOp&)> mark = [&](const FOp& f) {
