@@ -9,6 +9,7 @@
 //                   "the final outcome is sampled", reading R9), then readout
 //                   flips (R11).
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "tq_device_common.cuh"
 #include "tq_internal.h"
@@ -680,6 +681,120 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
                : "memory");
 }
 
+// The same projection for sibling pairs (leaf arity 2, the DCP plans' leaf level): one CTA
+// per (parent, chunk of x) reads the parent's amplitudes once for both children -- half the
+// L2->SM traffic of one CTA per leaf -- with 8 row loads in flight per thread.
+constexpr int QT = 256, QV = 2;
+__global__ void __launch_bounds__(QT) trail_project_pair_kernel(const __grid_constant__ ProjSpec sp,
+                                                                const __grid_constant__ TrailProjLaunch L) {
+  extern __shared__ cd pcoef[];   // [2][2^m]
+  __shared__ cd U[2][16][4];
+  __shared__ int live[2];
+  const uint64_t pfirst = L.child_first / 2;
+  const uint32_t npar = (uint32_t)((L.child_first + L.batch - 1) / 2 - pfirst + 1);
+  const uint32_t g = blockIdx.x % npar, c = blockIdx.x / npar;
+  const uint64_t P = pfirst + g;
+  const uint64_t j0 = P * 2 > L.child_first ? P * 2 : L.child_first;
+  const uint64_t j1 = P * 2 + 2 < L.child_first + L.batch ? P * 2 + 2 : L.child_first + L.batch;
+  const uint32_t nc = (uint32_t)(j1 - j0), s0 = (uint32_t)(j0 - L.child_first);
+  if (threadIdx.x < nc) {   // a child with a Pauli inside a diagonal unit -> the generated kernel
+    const uint32_t sl = s0 + threadIdx.x;
+    const unsigned char* codes = L.rows + (uint64_t)sl * L.row_bytes;
+    int e = 0;
+    for (uint32_t i = 0; i < sp.ndg; ++i) e |= codes[4 + sp.dgoff[i]] != 0;
+    live[threadIdx.x] = !e;
+    if (e && c == 0) L.glist[atomicAdd(L.gcount, 1u)] = sl;
+  }
+  if (threadIdx.x < nc * sp.m) {   // U_j of child ci: the top qubit's gates with their Paulis
+    const uint32_t ci = threadIdx.x / sp.m, jb = threadIdx.x % sp.m;
+    const unsigned char* codes = L.rows + (uint64_t)(s0 + ci) * L.row_bytes;
+    cd u[4] = {{1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {1.0, 0.0}};
+    for (uint32_t i = 0; i < sp.ng; ++i) {
+      if (sp.gbit[i] != jb) continue;
+      cd gm[4] = {{sp.gmat[i][0], sp.gmat[i][1]}, {sp.gmat[i][2], sp.gmat[i][3]},
+                  {sp.gmat[i][4], sp.gmat[i][5]}, {sp.gmat[i][6], sp.gmat[i][7]}};
+      const uint32_t code = codes[4 + sp.goff[i]];
+      if (code) {   // P g: X swaps the rows, Z negates row 1, Y = [[0,-i],[i,0]]
+        const cd r0 = gm[0], r1 = gm[1], r2 = gm[2], r3 = gm[3];
+        if (code == 1) { gm[0] = r2; gm[1] = r3; gm[2] = r0; gm[3] = r1; }
+        else if (code == 2) {
+          gm[0] = {r2.y, -r2.x}; gm[1] = {r3.y, -r3.x}; gm[2] = {-r0.y, r0.x}; gm[3] = {-r1.y, r1.x};
+        } else { gm[2] = {-r2.x, -r2.y}; gm[3] = {-r3.x, -r3.y}; }
+      }
+      cd v[4];   // u <- g u
+      for (int r = 0; r < 2; ++r)
+        for (int k = 0; k < 2; ++k) {
+          const cd a = gm[2 * r], b = gm[2 * r + 1], x0 = u[k], x1 = u[2 + k];
+          v[2 * r + k] = {a.x * x0.x - a.y * x0.y + b.x * x1.x - b.y * x1.y,
+                          a.x * x0.y + a.y * x0.x + b.x * x1.y + b.y * x1.x};
+        }
+      for (int k = 0; k < 4; ++k) u[k] = v[k];
+    }
+    for (int k = 0; k < 4; ++k) U[ci][jb][k] = u[k];
+  }
+  __syncthreads();
+  const uint32_t Y = 1u << sp.m;
+  for (uint32_t i = threadIdx.x; i < 2 * Y; i += QT) {   // c_ci[y] = prod_j U_j[sel_j][y_j] * D_top(y)
+    const uint32_t ci = i / Y, y = i % Y;
+    cd v = {0.0, 0.0};
+    if (ci < nc) {
+      const uint32_t sel = L.hsel[s0 + ci];
+      v = {1.0, 0.0};
+      for (uint32_t j = 0; j < sp.m; ++j) {
+        const cd e = U[ci][j][2 * ((sel >> j) & 1u) + ((y >> j) & 1u)];
+        v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
+      }
+      for (uint32_t u = 0; u < sp.nug; ++u) {
+        const uint32_t idx = ((y >> sp.ua[u]) & 1u) | (((y >> sp.ub[u]) & 1u) << 1);
+        const cd e = {sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
+        v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
+      }
+    }
+    pcoef[i] = v;
+  }
+  __syncthreads();
+  if (!live[0] && (nc < 2 || !live[1])) return;
+  uint64_t pj = P - L.parent_first;
+  if (L.prep) pj = L.prep[pj];
+  const cd* __restrict__ src = static_cast<const cd*>(L.src) + (pj << L.n);
+  const uint32_t n2 = sp.n2;
+  const uint64_t x0 = ((uint64_t)c * QT + threadIdx.x) * QV;
+  if (x0 >= (1ull << n2)) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+#pragma unroll 8
+  for (uint32_t y = 0; y < Y; ++y) {
+    double px, py, qx, qy;
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(px), "=d"(py), "=d"(qx), "=d"(qy)
+                 : "l"(src + (((uint64_t)y << n2) | x0)));
+    const cd k = pcoef[y], h = pcoef[Y + y];
+    a0 = fma(k.x, px, fma(-k.y, py, a0));
+    a1 = fma(k.x, py, fma(k.y, px, a1));
+    a2 = fma(k.x, qx, fma(-k.y, qy, a2));
+    a3 = fma(k.x, qy, fma(k.y, qx, a3));
+    b0 = fma(h.x, px, fma(-h.y, py, b0));
+    b1 = fma(h.x, py, fma(h.y, px, b1));
+    b2 = fma(h.x, qx, fma(-h.y, qy, b2));
+    b3 = fma(h.x, qy, fma(h.y, qx, b3));
+  }
+  for (uint32_t ci = 0; ci < nc; ++ci) {
+    if (!live[ci]) continue;
+    cd r0 = ci ? cd{b0, b1} : cd{a0, a1}, r1 = ci ? cd{b2, b3} : cd{a2, a3};
+    for (uint32_t u = sp.nug; u < sp.nug + sp.nux; ++u) {   // D_x: units below the top bits
+      for (int v = 0; v < QV; ++v) {
+        const uint64_t x = x0 + v;
+        const uint32_t idx = (uint32_t)((x >> sp.ua[u]) & 1u) | (uint32_t)(((x >> sp.ub[u]) & 1u) << 1);
+        const cd e = {sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
+        cd& r = v ? r1 : r0;
+        r = {r.x * e.x - r.y * e.y, r.x * e.y + r.y * e.x};
+      }
+    }
+    cd* dst = static_cast<cd*>(L.psi) + ((uint64_t)(s0 + ci) << n2) + x0;
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(r0.x), "d"(r0.y), "d"(r1.x), "d"(r1.y)
+                 : "memory");
+  }
+}
+
 // The computed instances (dedup representatives) of a batch, in slot order: the work list of
 // the batch's pass kernels (persistent CTAs, no empty CTAs for the shared instances).  The
 // leaf level's skipped instances get store-address XOR 0 (their representative is error-free).
@@ -744,6 +859,19 @@ int launch_dedup_map_level(const uint8_t* d_rows, const NoiseLevels& L, uint32_t
 }
 
 int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* stream) {
+  static const bool pair = [] {
+    const char* e = std::getenv("TQSIM_PROJ_PAIR");   // 0: one CTA per leaf also for arity 2
+    return !(e && e[0] == '0');
+  }();
+  if (pair && L.arity == 2) {
+    const uint64_t per_par = std::max<uint64_t>(1, (1ull << spec.n2) / (dev::QT * dev::QV));
+    const uint64_t npar = L.batch ? (L.child_first + L.batch - 1) / 2 - L.child_first / 2 + 1 : 0;
+    const uint64_t grid = per_par * npar;
+    if (grid == 0) return 0;
+    const size_t smem = (size_t)2 * sizeof(double) * 2 << spec.m;
+    dev::trail_project_pair_kernel<<<(unsigned)grid, dev::QT, smem, static_cast<cudaStream_t>(stream)>>>(spec, L);
+    return (int)cudaGetLastError();
+  }
   const uint64_t per_leaf = std::max<uint64_t>(1, (1ull << spec.n2) / (dev::PT * dev::PV));
   const uint64_t grid = per_leaf * L.batch;
   if (grid == 0) return 0;
