@@ -685,8 +685,13 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
 // per (parent, chunk of x) reads the parent's amplitudes once for both children -- half the
 // L2->SM traffic of one CTA per leaf -- with 8 row loads in flight per thread.
 constexpr int QT = 256, QV = 2;
+__device__ __forceinline__ void tq_bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __global__ void __launch_bounds__(QT) trail_project_pair_kernel(const __grid_constant__ ProjSpec sp,
-                                                                const __grid_constant__ TrailProjLaunch L) {
+                                                                const __grid_constant__ TrailProjLaunch L,
+                                                                uint32_t pf) {
   extern __shared__ cd pcoef[];   // [2][2^m]
   __shared__ cd U[2][16][4];
   __shared__ int live[2];
@@ -694,6 +699,18 @@ __global__ void __launch_bounds__(QT) trail_project_pair_kernel(const __grid_con
   const uint32_t npar = (uint32_t)((L.child_first + L.batch - 1) / 2 - pfirst + 1);
   const uint32_t g = blockIdx.x % npar, c = blockIdx.x / npar;
   const uint64_t P = pfirst + g;
+  // the CTA's rows: 2^m rows of (2^n2 amplitudes apart), its chunk of QT * QV of each; with
+  // pf > 0 one thread streams the rows pf ahead into L2 (bulk prefetch: no registers held)
+  const uint64_t xb = (uint64_t)c * QT * QV;
+  const uint32_t rbytes = (uint32_t)(16 * ((1ull << sp.n2) - xb < (uint64_t)QT * QV ? (1ull << sp.n2) - xb
+                                                                                    : (uint64_t)QT * QV));
+  const cd* psrc = nullptr;
+  if (pf && threadIdx.x == 0 && xb < (1ull << sp.n2)) {
+    uint64_t pq = P - L.parent_first;
+    if (L.prep) pq = L.prep[pq];
+    psrc = static_cast<const cd*>(L.src) + (pq << L.n) + xb;
+    for (uint32_t y = 0; y < pf && y < (1u << sp.m); ++y) tq_bulk_prefetch_l2(psrc + ((uint64_t)y << sp.n2), rbytes);
+  }
   const uint64_t j0 = P * 2 > L.child_first ? P * 2 : L.child_first;
   const uint64_t j1 = P * 2 + 2 < L.child_first + L.batch ? P * 2 + 2 : L.child_first + L.batch;
   const uint32_t nc = (uint32_t)(j1 - j0), s0 = (uint32_t)(j0 - L.child_first);
@@ -761,21 +778,33 @@ __global__ void __launch_bounds__(QT) trail_project_pair_kernel(const __grid_con
   const uint64_t x0 = ((uint64_t)c * QT + threadIdx.x) * QV;
   if (x0 >= (1ull << n2)) return;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
-#pragma unroll 8
-  for (uint32_t y = 0; y < Y; ++y) {
-    double px, py, qx, qy;
-    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-                 : "=d"(px), "=d"(py), "=d"(qx), "=d"(qy)
-                 : "l"(src + (((uint64_t)y << n2) | x0)));
-    const cd k = pcoef[y], h = pcoef[Y + y];
-    a0 = fma(k.x, px, fma(-k.y, py, a0));
-    a1 = fma(k.x, py, fma(k.y, px, a1));
-    a2 = fma(k.x, qx, fma(-k.y, qy, a2));
-    a3 = fma(k.x, qy, fma(k.y, qx, a3));
-    b0 = fma(h.x, px, fma(-h.y, py, b0));
-    b1 = fma(h.x, py, fma(h.y, px, b1));
-    b2 = fma(h.x, qx, fma(-h.y, qy, b2));
-    b3 = fma(h.x, qy, fma(h.y, qx, b3));
+  // QR rows per step: every load of the step issued before the first use (QR x 32 B in flight)
+  constexpr uint32_t QR = 8;
+  const char* rp = reinterpret_cast<const char*>(src + x0);   // row y at rp + y * rstride
+  const uint64_t rstride = (uint64_t)16 << n2;
+  for (uint32_t y0 = 0; y0 < Y; y0 += QR) {
+    if (psrc)
+      for (uint32_t y = y0 + pf; y < y0 + pf + QR && y < Y; ++y) tq_bulk_prefetch_l2(psrc + ((uint64_t)y << n2), rbytes);
+    double px[QR], py[QR], qx[QR], qy[QR];
+#pragma unroll
+    for (uint32_t i = 0; i < QR; ++i) {   // (Y is a multiple of QR: the launcher checks m >= 3)
+      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(px[i]), "=d"(py[i]), "=d"(qx[i]), "=d"(qy[i])
+                   : "l"(rp));
+      rp += rstride;
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < QR; ++i) {
+      const cd k = pcoef[y0 + i], h = pcoef[Y + y0 + i];
+      a0 = fma(k.x, px[i], fma(-k.y, py[i], a0));
+      a1 = fma(k.x, py[i], fma(k.y, px[i], a1));
+      a2 = fma(k.x, qx[i], fma(-k.y, qy[i], a2));
+      a3 = fma(k.x, qy[i], fma(k.y, qx[i], a3));
+      b0 = fma(h.x, px[i], fma(-h.y, py[i], b0));
+      b1 = fma(h.x, py[i], fma(h.y, px[i], b1));
+      b2 = fma(h.x, qx[i], fma(-h.y, qy[i], b2));
+      b3 = fma(h.x, qy[i], fma(h.y, qx[i], b3));
+    }
   }
   for (uint32_t ci = 0; ci < nc; ++ci) {
     if (!live[ci]) continue;
@@ -863,13 +892,18 @@ int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* s
     const char* e = std::getenv("TQSIM_PROJ_PAIR");   // 0: one CTA per leaf also for arity 2
     return !(e && e[0] == '0');
   }();
-  if (pair && L.arity == 2) {
+  if (pair && L.arity == 2 && spec.m >= 3) {
     const uint64_t per_par = std::max<uint64_t>(1, (1ull << spec.n2) / (dev::QT * dev::QV));
     const uint64_t npar = L.batch ? (L.child_first + L.batch - 1) / 2 - L.child_first / 2 + 1 : 0;
     const uint64_t grid = per_par * npar;
     if (grid == 0) return 0;
     const size_t smem = (size_t)2 * sizeof(double) * 2 << spec.m;
-    dev::trail_project_pair_kernel<<<(unsigned)grid, dev::QT, smem, static_cast<cudaStream_t>(stream)>>>(spec, L);
+    static const uint32_t pf = [] {   // rows prefetched ahead into L2 (0 = off)
+      const char* e = std::getenv("TQSIM_PROJ_PF");
+      return e ? (uint32_t)std::atoi(e) : 0u;
+    }();
+    dev::trail_project_pair_kernel<<<(unsigned)grid, dev::QT, smem, static_cast<cudaStream_t>(stream)>>>(spec, L,
+                                                                                                        pf);
     return (int)cudaGetLastError();
   }
   const uint64_t per_leaf = std::max<uint64_t>(1, (1ull << spec.n2) / (dev::PT * dev::PV));
