@@ -689,7 +689,8 @@ __device__ __forceinline__ void tq_bulk_prefetch_l2(const void* p, uint32_t byte
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-__global__ void __launch_bounds__(QT) trail_project_pair_kernel(const __grid_constant__ ProjSpec sp,
+template <int MINB>
+__global__ void __launch_bounds__(QT, MINB) trail_project_pair_kernel(const __grid_constant__ ProjSpec sp,
                                                                 const __grid_constant__ TrailProjLaunch L,
                                                                 uint32_t pf) {
   extern __shared__ cd pcoef[];   // [2][2^m]
@@ -902,8 +903,14 @@ int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* s
       const char* e = std::getenv("TQSIM_PROJ_PF");
       return e ? (uint32_t)std::atoi(e) : 0u;
     }();
-    dev::trail_project_pair_kernel<<<(unsigned)grid, dev::QT, smem, static_cast<cudaStream_t>(stream)>>>(spec, L,
-                                                                                                        pf);
+    static const int minb = [] {   // resident CTAs per SM the register budget targets
+      const char* e = std::getenv("TQSIM_PROJ_MINB");
+      return e ? std::atoi(e) : 3;
+    }();
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (minb >= 5) dev::trail_project_pair_kernel<5><<<(unsigned)grid, dev::QT, smem, st>>>(spec, L, pf);
+    else if (minb == 4) dev::trail_project_pair_kernel<4><<<(unsigned)grid, dev::QT, smem, st>>>(spec, L, pf);
+    else dev::trail_project_pair_kernel<3><<<(unsigned)grid, dev::QT, smem, st>>>(spec, L, pf);
     return (int)cudaGetLastError();
   }
   const uint64_t per_leaf = std::max<uint64_t>(1, (1ull << spec.n2) / (dev::PT * dev::PV));
