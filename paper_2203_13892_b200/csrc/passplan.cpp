@@ -445,8 +445,13 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
                                (uint32_t)pi, d + 2 == plan.bounds.size() && pi + 1 == passes.size()));
     pp.levels.push_back(std::move(lvl));
   }
-  if (const char* e = std::getenv("TQSIM_TRAIL"); !(e && e[0] == '0'))
-    plan_trail(pp, gates, plan, n, K, low);
+  if (const char* e = std::getenv("TQSIM_TRAIL"); !(e && e[0] == '0')) {
+    // pass A's tile: the low qubits 0..tlow-1 (contiguous runs of 2^tlow amplitudes) and the
+    // top m = K - tlow qubits (TQSIM_TRAIL_LOW, default LOW_Q)
+    int tlow = low;
+    if (const char* t = std::getenv("TQSIM_TRAIL_LOW")) tlow = std::max(low, std::min(K - 1, std::atoi(t)));
+    plan_trail(pp, gates, plan, n, K, tlow);
+  }
   return pp;
 }
 }  // namespace
