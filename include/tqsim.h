@@ -112,7 +112,9 @@ typedef struct {
                                  state equals an earlier instance's of its batch shares that
                                  instance's computed state (bit-identical);
                                  1 = every node instance of the tree is computed */
-  uint32_t reserved;          /* 0 */
+  uint32_t trail_low;         /* conditional leaf sampling: the marginal pass's tile =
+                                 qubits 0..trail_low-1 + the top K - trail_low qubits (3..K-1);
+                                 0 = auto (4 when K >= 10, else 3) */
 } tqsim_options;
 
 /* The tree plan (§3.1): level d executes lowered gates

@@ -149,12 +149,13 @@ uint64_t PassPlan::passes_total(const std::vector<uint64_t>& inst) const {
 }
 
 namespace {
-PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan, int K);
+PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan, int K,
+                          uint32_t trail_low);
 }
 
 PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan,
                         const Options& o) {
-  if (o.tile_qubits) return make_pass_plan_k(gates, n_qubits, plan, (int)o.tile_qubits);
+  if (o.tile_qubits) return make_pass_plan_k(gates, n_qubits, plan, (int)o.tile_qubits, o.trail_low);
   // Auto tile width (measured on B200): 2^11-amplitude tiles (4 CTAs x
   // 4 warps per SM) hide HBM latency ~10% better than 2^12 tiles (2 CTAs x 8 warps) but
   // may need more HBM passes; pick the smaller  sum_d instances_d * passes_d / eta_K.
@@ -162,7 +163,7 @@ PassPlan make_pass_plan(const std::vector<LGate>& gates, uint32_t n_qubits, cons
   PassPlan best;
   double best_cost = 0.0;
   for (int K : {12, 11}) {
-    PassPlan pp = make_pass_plan_k(gates, n_qubits, plan, K);
+    PassPlan pp = make_pass_plan_k(gates, n_qubits, plan, K, o.trail_low);
     const double eta = K == 11 ? 1.10 : 1.0;
     const double cost = (double)pp.passes_total(inst) / eta;
     if (best.levels.empty() || cost < best_cost) {
@@ -420,7 +421,8 @@ void plan_trail(PassPlan& pp, const std::vector<LGate>& gates, const Plan& plan,
   pp.trail = std::move(t);
 }
 
-PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan, int K) {
+PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, const Plan& plan, int K,
+                          uint32_t trail_low) {
   PassPlan pp;
   const int n = std::max<int>((int)n_qubits, RBITS);
   pp.n_sim = n;
@@ -447,10 +449,11 @@ PassPlan make_pass_plan_k(const std::vector<LGate>& gates, uint32_t n_qubits, co
   }
   if (const char* e = std::getenv("TQSIM_TRAIL"); !(e && e[0] == '0')) {
     // pass A's tile: the low qubits 0..tlow-1 (contiguous runs of 2^tlow amplitudes) and the
-    // top m = K - tlow qubits (TQSIM_TRAIL_LOW, default LOW_Q)
-    int tlow = low;
-    if (const char* t = std::getenv("TQSIM_TRAIL_LOW")) tlow = std::max(low, std::min(K - 1, std::atoi(t)));
-    plan_trail(pp, gates, plan, n, K, tlow);
+    // top m = K - tlow qubits.  Auto: 4 low qubits for K >= 10 -- one top qubit fewer to
+    // rotate per amplitude in the marginal pass and 256-byte runs (C4: 185 -> 165 ms per tree
+    // for that pass, the stage-2 passes unchanged; 5 low qubits add a stage-2 pass)
+    const int tlow = trail_low ? std::min<int>(K - 1, (int)trail_low) : (K >= 10 ? LOW_Q + 1 : LOW_Q);
+    plan_trail(pp, gates, plan, n, K, std::max(low, tlow));
   }
   return pp;
 }

@@ -34,7 +34,7 @@ std::vector<LGate> lower(const tqsim_circuit* c);
 struct Options {
   double copy_cost_gates = 10.0, z = 1.96, eps = 0.05;
   uint64_t mem_budget = 180000000000ull;
-  uint32_t topup = 0, tile_qubits = 0, batch_log2_amps = 0, profile = 0, no_dedup = 0;
+  uint32_t topup = 0, tile_qubits = 0, batch_log2_amps = 0, profile = 0, no_dedup = 0, trail_low = 0;
 };
 Options options_from(const tqsim_options* o);
 

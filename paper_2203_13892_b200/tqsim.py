@@ -53,7 +53,7 @@ class tqsim_options(C.Structure):
     _fields_ = [("copy_cost_gates", C.c_double), ("z", C.c_double), ("eps", C.c_double),
                 ("mem_budget_bytes", C.c_uint64), ("topup", C.c_uint32),
                 ("tile_qubits", C.c_uint32), ("batch_log2_amps", C.c_uint32),
-                ("profile", C.c_uint32), ("no_dedup", C.c_uint32), ("reserved", C.c_uint32)]
+                ("profile", C.c_uint32), ("no_dedup", C.c_uint32), ("trail_low", C.c_uint32)]
 
 
 class tqsim_plan(C.Structure):

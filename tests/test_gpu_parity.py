@@ -467,20 +467,24 @@ def _fast_trail_circuit(n, m, rng):
     return gs
 
 
-@pytest.mark.parametrize("n,tile,p,ar", [(14, 8, 0.05, [3, 2, 4]), (12, 7, 0.5, [2, 3, 4]), (18, 10, 0.002, [2, 2, 2, 3]),
-                                         (14, 8, 1.0, [2, 3, 4])])
-def test_streaming_projection_vs_oracle(n, tile, p, ar):
+@pytest.mark.parametrize("n,tile,p,ar,tl", [(14, 8, 0.05, [3, 2, 4], 3), (12, 7, 0.5, [2, 3, 4], 3),
+                                            (18, 10, 0.002, [2, 2, 2, 3], 3), (14, 8, 1.0, [2, 3, 4], 3),
+                                            (14, 8, 0.05, [3, 2, 4], 4), (18, 10, 0.01, [2, 2, 2, 3], 4),
+                                            (16, 11, 0.5, [2, 3, 4], 5), (14, 8, 0.05, [3, 4, 2], 3),
+                                            (18, 10, 0.3, [2, 3, 2], 4), (13, 9, 0.02, [3, 5, 2], 3)])
+def test_streaming_projection_vs_oracle(n, tile, p, ar, tl):
     """The hand-written projection (diagonal units folded into per-leaf coefficients, top-qubit
     gates with their keyed Paulis) and its hand-over of leaves with a Pauli inside a unit to
-    the generated kernel (p = 0.5, 1): outcomes equal the oracle's and the stored path's."""
+    the generated kernel (p = 0.5, 1): outcomes equal the oracle's and the stored path's.
+    tl = options.trail_low: the marginal pass's tile holds qubits 0..tl-1 and the top tile - tl."""
     rng = np.random.default_rng(n + tile)
-    gates = _fast_trail_circuit(n, tile - 3, rng)
+    gates = _fast_trail_circuit(n, tile - tl, rng)
     nm = NoiseModel(p, min(1.0, 2 * p), 0.02, 0.03)
     noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
-    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2, trail_low=tl)
     shots = int(np.prod(ar))
     plan = T.tqsim_plan_circuit(n, gates, noise, shots, ar, opts)
-    assert plan.trail_top_bits == tile - 3 and plan.trail_fast == 1
+    assert plan.trail_top_bits == tile - tl and plan.trail_fast == 1
     a = T.tqsim_run_ex(n, gates, noise, shots, ar, 33, opts, (), leaf_debug=True)
     b = T.tqsim_run_ex(n, gates, noise, shots, ar, 33, opts, [(len(ar) - 1, 1)])
     ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 33)
@@ -520,24 +524,26 @@ def test_conditional_sampling_split_level_shards(world):
     h.close()
 
 
-def test_streaming_projection_split_level_shards():
-    """The streaming projection (clipped leaf batches, parent slots of a split shard) under
-    serial shards W = 3 equals the single run."""
+@pytest.mark.parametrize("ar,world,blog", [([2, 3, 4], 3, 2), ([3, 5, 2], 3, 2), ([2, 7, 2], 5, 1)])
+def test_streaming_projection_split_level_shards(ar, world, blog):
+    """The streaming projection (clipped leaf batches, parent slots of a split shard; leaf
+    arity 2: the sibling-pair kernel, batches of 2 or 4 leaves that may cut a pair) under
+    serial shards equals the single run."""
     torch = pytest.importorskip("torch")
-    n, tile, ar = 14, 8, [2, 3, 4]
+    n, tile = 14, 8
     gates = _fast_trail_circuit(n, tile - 3, np.random.default_rng(5))
     noise = T.noise_arg(0.02, 0.05, 0.01, 0.01)
-    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 2)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + blog, trail_low=3)
     shots = int(np.prod(ar))
     h = T.tqsim_create(n, gates, noise, shots, ar, opts)
     assert h.plan.trail_fast == 1
     single = T.tqsim_run_ex(n, gates, noise, shots, ar, 12, opts).leaf_outcomes
     acc = np.zeros(shots, dtype=np.int64)
-    assert T.tqsim_shard_levels(h.plan, 0, 3)[0] > 0
-    for r in range(3):
-        ws = torch.empty(h.workspace_bytes(r, 3), dtype=torch.uint8, device="cuda")
+    assert T.tqsim_shard_levels(h.plan, 0, world)[0] > 0
+    for r in range(world):
+        ws = torch.empty(h.workspace_bytes(r, world), dtype=torch.uint8, device="cuda")
         o = torch.zeros(shots, dtype=torch.int32, device="cuda")
-        h.execute(12, r, 3, torch.cuda.current_stream().cuda_stream, ws.data_ptr(), ws.numel(), o.data_ptr())
+        h.execute(12, r, world, torch.cuda.current_stream().cuda_stream, ws.data_ptr(), ws.numel(), o.data_ptr())
         acc += o.cpu().numpy()
     assert np.array_equal(acc.astype(np.uint32), single)
     h.close()
