@@ -524,7 +524,7 @@ def test_conditional_sampling_split_level_shards(world):
     h.close()
 
 
-@pytest.mark.parametrize("ar,world,blog", [([2, 3, 4], 3, 2), ([3, 5, 2], 3, 2), ([2, 7, 2], 5, 1)])
+@pytest.mark.parametrize("ar,world,blog", [([2, 3, 4], 3, 2), ([3, 5, 2], 2, 2), ([2, 7, 2], 5, 1)])
 def test_streaming_projection_split_level_shards(ar, world, blog):
     """The streaming projection (clipped leaf batches, parent slots of a split shard; leaf
     arity 2: the sibling-pair kernel, batches of 2 or 4 leaves that may cut a pair) under
