@@ -1018,7 +1018,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs, int variant = 0,
                      std::vector<uint32_t>* out_row = nullptr, double* fp64_out = nullptr, int proj_m = 0,
-                     const TmaGeom* tma = nullptr) {
+                     const TmaGeom* tma = nullptr, bool clean = false) {
   const int K = pd.K, T = 1 << (K - RBITS);
   const int low = std::min(LOW_Q, K);
   const bool coal = K - RBITS >= low;   // enough lane bits to keep qubits 0..2 on lanes 0..2
@@ -2264,6 +2264,9 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // across phases; both leave the tile in the same canonical shared-memory layout).
   // bitmap of the pass ops whose gate drew an error
   for (int w = 0; w < NW; ++w) o << "  tq_u32 eb" << w << " = 0u;\n";
+  // clean: the kernel of the work-list items whose pass drew no error (compact_reps_kernel
+  // classifies them): the fast code only -- a third of the instructions, no frame state
+  if (!clean) {
   o << "  if (errs) {\n";
   o << "    if (tid < " << NW << "u) tq_errb[tid] = 0u;\n    __syncthreads();\n";
   o << "    for (tq_u32 li = tid; li < " << nops << "u; li += " << T << "u)\n"
@@ -2271,6 +2274,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   o << "    __syncthreads();\n";
   for (int w = 0; w < NW; ++w) o << "    eb" << w << " = tq_errb[" << w << "];\n";
   o << "  }\n";
+  }
   o << "  tq_u32 fx = 0u, fz = 0u, fk = 0u;\n";
   if (variant == 1 && pd.leaf_sums) o << "  double tq_sc = 1.0;\n";   // run-sum factor (see the flush)
   for (int ph = 0; ph < (int)fast.size(); ++ph) {
@@ -2280,6 +2284,10 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       for (const ErrSite& es : f.sites) pm[es.local >> 5] |= 1u << (es.local & 31);
     };
     for (int it : fast[ph].items) mark(fops[it]);
+    if (clean) {
+      emit_phases(fast, false, ph);
+      continue;
+    }
     o << "  if ((fx | fz | fk) == 0u";
     for (int w = 0; w < NW; ++w)
       if (pm[w]) o << " && !(eb" << w << " & " << pm[w] << "u)";
@@ -2385,32 +2393,35 @@ void jit_compile_only(const PassPlan& pp, const std::vector<LGate>& gates, uint6
   std::vector<std::string> srcs, names;
   for (size_t d = 0; d < pp.levels.size(); ++d)
     for (size_t p = 0; p < pp.levels[d].size(); ++p) {
-      const int nvar = pp.levels[d][p].leaf_sums ? 3 : 1;
-      for (int v = 0; v < nvar; ++v) {
-        names.push_back("tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : ""));
+      const int nvar = pp.levels[d][p].leaf_sums ? 4 : 1;
+      for (int vv = 0; vv < nvar; ++vv) {   // (3: the clean variant-1 kernel)
+        const int v = vv == 3 ? 1 : vv;
+        names.push_back("tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : "") +
+                        (vv == 3 ? "c" : ""));
         const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
         int th;
         size_t sm;
         std::vector<double> cf;
         TmaGeom tg;
-        const bool tw = tma_wanted(pp.levels[d][p], pp.n_sim, mode, v, &tg);
+        const bool tw = vv != 3 && tma_wanted(pp.levels[d][p], pp.n_sim, mode, v, &tg);
         srcs.push_back(std::string(kPrelude) + kJitTypes +
                        gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, names.back(), th, sm, cf, v, nullptr,
-                                nullptr, 0, tw ? &tg : nullptr));
+                                nullptr, 0, tw ? &tg : nullptr, vv == 3));
       }
     }
   if (pp.trail.on) {   // the conditional leaf sampling kernels (jit_build's trail jobs)
     const TrailPlan& tp = pp.trail;
-    for (int v : {1, 3}) {
-      names.push_back("tq_trail_a_v" + std::to_string(v));
+    for (int vv : {1, 3, 4}) {   // (4: the clean variant-1 kernel)
+      const int v = vv == 4 ? 1 : vv;
+      names.push_back("tq_trail_a_v" + std::to_string(v) + (vv == 4 ? "c" : ""));
       int th;
       size_t sm;
       std::vector<double> cf;
       TmaGeom tg;
-      const bool tw = tma_wanted(tp.a, pp.n_sim, 1, v, &tg);
+      const bool tw = vv != 4 && tma_wanted(tp.a, pp.n_sim, 1, v, &tg);
       srcs.push_back(std::string(kPrelude) + kJitTypes +
                      gen_pass(tp.a, pp, gates, pp.n_sim, 1, names.back(), th, sm, cf, v, nullptr, nullptr, tp.m,
-                              tw ? &tg : nullptr));
+                              tw ? &tg : nullptr, vv == 4));
     }
     for (size_t p = 0; p < tp.b.size(); ++p)
       for (int v : p + 1 == tp.b.size() ? std::vector<int>{1, 2} : std::vector<int>{0}) {
@@ -2464,6 +2475,7 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
     size_t d, p;
     int which = 0;   // 0 level pass, 1 trail pass A, 2 trail stage-2 pass p
     int variant;
+    bool clean = false;   // variant 1 for the items without an error (JitPass::kernel_clean)
     std::string name, src;
     int threads;
     size_t smem;
@@ -2481,17 +2493,21 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
   for (size_t d = 0; d < pp.levels.size(); ++d) {
     out[d].resize(pp.levels[d].size());
     for (size_t p = 0; p < pp.levels[d].size(); ++p) {
-      const int nvar = pp.levels[d][p].leaf_sums ? 3 : 1;
-      for (int v = 0; v < nvar; ++v) {
+      const int nvar = pp.levels[d][p].leaf_sums ? 4 : 1;
+      for (int vv = 0; vv < nvar; ++vv) {
         Job j;
         j.d = d;
         j.p = p;
+        const int v = vv == 3 ? 1 : vv;
         j.variant = v;
-        j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : "");
+        j.clean = vv == 3;
+        j.name = "tq_pass_l" + std::to_string(d) + "_p" + std::to_string(p) + (v ? "_v" + std::to_string(v) : "") +
+                 (j.clean ? "c" : "");
         const int mode = p > 0 ? 2 : (d == 0 ? 0 : 1);
-        j.tma = tma_wanted(pp.levels[d][p], pp.n_sim, mode, v, &j.geom);
+        j.tma = !j.clean && tma_wanted(pp.levels[d][p], pp.n_sim, mode, v, &j.geom);
         std::string body = gen_pass(pp.levels[d][p], pp, gates, pp.n_sim, mode, j.name, j.threads,
-                                    j.smem, j.coefs, v, &j.out_row, &j.fp64, 0, j.tma ? &j.geom : nullptr);
+                                    j.smem, j.coefs, v, &j.out_row, &j.fp64, 0, j.tma ? &j.geom : nullptr,
+                                    j.clean);
         j.src = std::string(kPrelude) + kJitTypes + body;
         jobs.push_back(std::move(j));
       }
@@ -2499,16 +2515,18 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
   }
   if (trail && pp.trail.on) {   // conditional leaf sampling (passplan.cpp plan_trail)
     const TrailPlan& tp = pp.trail;
-    for (int v : {1, 3}) {       // pass A: run sums (marginals) / projection onto the chosen top bits
+    for (int vv : {1, 3, 4}) {   // pass A: run sums (marginals; 4: clean) / projection onto the chosen top bits
       Job j;
       j.which = 1;
       j.d = pp.levels.size() - 1;
       j.p = 0;
+      const int v = vv == 4 ? 1 : vv;
       j.variant = v;
-      j.name = "tq_trail_a_v" + std::to_string(v);
-      j.tma = tma_wanted(tp.a, pp.n_sim, 1, v, &j.geom);
+      j.clean = vv == 4;
+      j.name = "tq_trail_a_v" + std::to_string(v) + (j.clean ? "c" : "");
+      j.tma = !j.clean && tma_wanted(tp.a, pp.n_sim, 1, v, &j.geom);
       std::string body = gen_pass(tp.a, pp, gates, pp.n_sim, 1, j.name, j.threads, j.smem, j.coefs, v, &j.out_row,
-                                  &j.fp64, tp.m, j.tma ? &j.geom : nullptr);
+                                  &j.fp64, tp.m, j.tma ? &j.geom : nullptr, j.clean);
       j.src = std::string(kPrelude) + kJitTypes + body;
       jobs.push_back(std::move(j));
     }
@@ -2590,6 +2608,10 @@ std::vector<std::vector<JitPass>> jit_build(const PassPlan& pp, const std::vecto
   for (Job& j : jobs) {
     const CompiledKernel& ck = g_cache.at(j.src);
     JitPass& jp = j.which == 0 ? out[j.d][j.p] : j.which == 1 ? trail->a : trail->b[j.p];
+    if (j.clean) {   // same launch geometry as the variant-1 kernel (same tile, threads, smem)
+      jp.kernel_clean = reinterpret_cast<void*>(ck.fn);
+      continue;
+    }
     if (j.variant == 3) {   // trail projection: its own launch parameters
       jp.kernel_project = reinterpret_cast<void*>(ck.fn);
       jp.threads_project = j.threads;
@@ -2714,7 +2736,8 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
   HostJitArgs a{L.src, L.dst, L.seed, L.p1, L.p2, L.child_first, L.parent_first,
                 L.arity ? L.arity : 1u, L.batch, static_cast<double*>(L.runsum), L.rows, L.row_bytes,
                 L.tiles, L.runsel, L.scratch, L.xlout, L.rep, L.prep, L.wlist, L.wcount};
-  const void* kern = L.variant == 0 ? jp.kernel : L.variant == 1 ? jp.kernel_nostore
+  const void* kern = L.variant == 0 ? jp.kernel
+                   : L.variant == 1 ? (L.clean ? jp.kernel_clean : jp.kernel_nostore)
                    : L.variant == 2 ? jp.kernel_recompute : jp.kernel_project;
   if (!kern) return (int)cudaErrorInvalidDeviceFunction;
   uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;
@@ -2730,7 +2753,7 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
   void* args[] = {&a, const_cast<double*>(cf.empty() ? &zero : cf.data())};
   const int threads = L.variant == 3 ? jp.threads_project : jp.threads;
   const size_t smem = L.variant == 3 ? jp.smem_project : jp.smem;
-  if ((L.variant == 0 || L.variant == 1) && jp.tma_v[L.variant]) {
+  if ((L.variant == 0 || L.variant == 1) && jp.tma_v[L.variant] && !L.clean) {
     // TMA-staged persistent kernel: the tensor map of the source batch (parents / own states)
     CUtensorMap tm;
     const bool fan = L.src_mode == 1;

@@ -828,33 +828,52 @@ __global__ void __launch_bounds__(QT, MINB) trail_project_pair_kernel(const __gr
 // The computed instances (dedup representatives) of a batch, in slot order: the work list of
 // the batch's pass kernels (persistent CTAs, no empty CTAs for the shared instances).  The
 // leaf level's skipped instances get store-address XOR 0 (their representative is error-free).
+// With rows: the representatives whose noise row has no error in the pass (emask bits of the
+// row's pass bitmask) go to list, the others to list2 (the clean kernel / the full kernel).
 __global__ void __launch_bounds__(256) compact_reps_kernel(const uint32_t* __restrict__ rep, uint32_t cnt,
                                                            uint32_t* __restrict__ list, uint32_t* __restrict__ count,
-                                                           uint32_t* __restrict__ xlout) {
-  __shared__ uint32_t wsum[8];
-  __shared__ uint32_t base;
-  if (threadIdx.x == 0) base = 0;
+                                                           uint32_t* __restrict__ xlout,
+                                                           const uint8_t* __restrict__ rows, uint32_t row_bytes,
+                                                           uint32_t emask, uint32_t* __restrict__ list2,
+                                                           uint32_t* __restrict__ count2) {
+  __shared__ uint32_t wsum[2][8];
+  __shared__ uint32_t base[2];
+  if (threadIdx.x < 2) base[threadIdx.x] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (uint32_t c0 = 0; c0 < cnt; c0 += blockDim.x) {
     const uint32_t s = c0 + threadIdx.x;
-    const bool keep = s < cnt && rep[s] == s;
+    const bool keep = s < cnt && (!rep || rep[s] == s);
     if (s < cnt && !keep && xlout) xlout[s] = 0u;
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) wsum[w] = __popc(bal);
+    bool err = false;
+    if (keep && rows) err = (*reinterpret_cast<const uint32_t*>(rows + (uint64_t)s * row_bytes) & emask) != 0u;
+    const bool k0 = keep && !err, k1 = keep && err;
+    const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+    if (lane == 0) {
+      wsum[0][w] = __popc(b0);
+      wsum[1][w] = __popc(b1);
+    }
     __syncthreads();
-    uint32_t off = base;
-    for (int i = 0; i < w; ++i) off += wsum[i];
-    if (keep) list[off + __popc(bal & ((1u << lane) - 1u))] = s;
+    uint32_t o0 = base[0], o1 = base[1];
+    for (int i = 0; i < w; ++i) {
+      o0 += wsum[0][i];
+      o1 += wsum[1][i];
+    }
+    const unsigned below = (1u << lane) - 1u;
+    if (k0) list[o0 + __popc(b0 & below)] = s;
+    if (k1) list2[o1 + __popc(b1 & below)] = s;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 2) {
       uint32_t t = 0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[i];
-      base += t;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[threadIdx.x][i];
+      base[threadIdx.x] += t;
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *count = base;
+  if (threadIdx.x == 0) {
+    *count = base[0];
+    if (count2) *count2 = base[1];
+  }
 }
 
 // The run's seed in device memory: the tree's launches (a replayed CUDA graph) read it
@@ -921,8 +940,11 @@ int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* s
 }
 
 int launch_compact_reps(const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
+                        const uint8_t* d_rows, uint32_t row_bytes, uint32_t emask, uint32_t* d_list2, uint32_t* d_count2,
                         void* stream) {
-  dev::compact_reps_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_rep, cnt, d_list, d_count, d_xlout);
+  dev::compact_reps_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_rep, cnt, d_list, d_count, d_xlout,
+                                                                             d_rows, row_bytes, emask, d_list2,
+                                                                             d_count2);
   return (int)cudaGetLastError();
 }
 

@@ -293,7 +293,7 @@ Layout layout_tl(const tqsim_handle* h, const ShardRange& sr, int tl) {
     l.wl_off.clear();
     for (size_t d = 0; d < levels; ++d) {
       l.wl_off.push_back(off);
-      off = align_up(off + 4 * (l.cap[d] + 1));
+      off = align_up(off + 4 * (2 * l.cap[d] + 2));   // two lists (clean, with errors) + counts
     }
     if (h->pp.trail.on) {
       const uint64_t capl = l.cap.back(), n2 = (uint64_t)h->pp.trail.n2;
@@ -373,8 +373,10 @@ struct Exec {
   bool leaf_issued = false;
   uint64_t pcnt[64] = {};   // instances of the current batch per level
   bool dedup = false;       // dedup maps built for this tree (no state dumps asked for)
-  const uint32_t* wl = nullptr;      // the current batch's work list (compact_reps) and count
-  const uint32_t* wlc = nullptr;
+  const uint32_t* wl = nullptr;      // the current batch's work list (compact_reps) and count:
+  const uint32_t* wlc = nullptr;     //   the computed instances whose variant-1 pass drew no error,
+  const uint32_t* wl2 = nullptr;     //   and (wl2, wlc2) those with an error (null: wl holds all)
+  const uint32_t* wlc2 = nullptr;
   const cudaEvent_t* map_ev = nullptr;   // side-stream map chain: level d's map is ready
   bool map_waited[64] = {};
 };
@@ -483,6 +485,15 @@ void run_leaf_trail(Exec& x, uint32_t d, uint64_t b, uint64_t cnt, uint64_t pare
   pl.wlist = x.wl;
   pl.wcount = x.wlc;
   mark(x, 0, d, 0, b, cnt);
+  if (x.wl2 && jt.a.kernel_clean) {   // the marginals of the clean leaves, then of those with errors
+    pl.clean = 1u;
+    ck(launch_jit_pass(jt.a, tp.a, pl, x.st), "trail pass A launch (clean)");
+    pl.clean = 0u;
+    pl.wlist = x.wl2;
+    pl.wcount = x.wlc2;
+    h->stats.kernel_launches++;
+    h->stats.pass_launches++;
+  }
   ck(launch_jit_pass(jt.a, tp.a, pl, x.st), "trail pass A launch");
   mark(x, 0, d, 0, b, cnt);
   h->stats.pass_bytes += (cnt << n) * 1 + (parents << n) * 16;
@@ -644,22 +655,35 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
     void* scratch = sel + 3 * align_up(4 * capl) + align_up(8 * capl);
     // the batch's computed instances as a work list: the pass kernels loop over them with
     // persistent CTAs instead of launching an (empty) CTA per shared instance and tile
-    x.wl = x.wlc = nullptr;
+    x.wl = x.wlc = x.wl2 = x.wlc2 = nullptr;
     static const bool use_wl = [] {
       const char* e = std::getenv("TQSIM_WORKLIST");
+      return !(e && e[0] == '0');
+    }();
+    static const bool split_clean = [] {   // 0: one variant-1 kernel (with the careful code) for all
+      const char* e = std::getenv("TQSIM_CLEAN_SPLIT");
       return !(e && e[0] == '0');
     }();
     if (use_wl && x.dedup && cnt > 1 && leaf && nostore) {   // the leaf run-sum passes (variant 1)
       const uint32_t* maps = reinterpret_cast<const uint32_t*>(x.ws + x.L.map_off);
       uint32_t* wl = reinterpret_cast<uint32_t*>(x.ws + x.L.wl_off[d]);
+      const uint64_t c = x.L.cap[d];
       uint32_t* xl0 = leaf && nostore ? reinterpret_cast<uint32_t*>(x.ws + x.L.sel_off + 2 * align_up(4 * x.L.cap.back()))
                                       : nullptr;
-      ck(launch_compact_reps(maps + x.L.map_lvl[d] + (b - x.lvl_first[d]), (uint32_t)cnt, wl, wl + x.L.cap[d], xl0,
+      // the variant-1 pass's error bits of the noise row: the trail's marginal pass takes the
+      // careful code on any error of the slice (mask_any), a level pass on its own bit
+      const uint32_t em = h->pp.trail.on ? ~0u : 1u << std::min<size_t>(passes.size() - 1, 31);
+      ck(launch_compact_reps(maps + x.L.map_lvl[d] + (b - x.lvl_first[d]), (uint32_t)cnt, wl, wl + c, xl0,
+                             split_clean ? rows : nullptr, row_bytes, em, wl + c + 1, split_clean ? wl + 2 * c + 1 : nullptr,
                              x.st),
          "work list launch");
       h->stats.kernel_launches++;
       x.wl = wl;
-      x.wlc = wl + x.L.cap[d];
+      x.wlc = wl + c;
+      if (split_clean) {
+        x.wl2 = wl + c + 1;
+        x.wlc2 = wl + 2 * c + 1;
+      }
     }
     if (leaf && nostore && h->pp.trail.on) {   // conditional leaf sampling (default path)
       run_leaf_trail(x, d, b, cnt, parent_first, pbuf, buf, rows, row_bytes);
@@ -696,6 +720,15 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
         if (d > 0 && x.pcnt[d - 1] > 1) pl.prep = maps + x.L.map_lvl[d - 1] + (parent_first - x.lvl_first[d - 1]);
       }
       mark(x, 0, d, (uint32_t)p, b, cnt);
+      if (runsums_only && x.wl2 && h->jit[d][p].kernel_clean) {   // clean items, then those with errors
+        pl.clean = 1u;
+        ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch (clean)");
+        pl.clean = 0u;
+        pl.wlist = x.wl2;
+        pl.wcount = x.wlc2;
+        h->stats.kernel_launches++;
+        h->stats.pass_launches++;
+      }
       ck(launch_jit_pass(h->jit[d][p], passes[p], pl, x.st), "gate pass launch");
       mark(x, 0, d, (uint32_t)p, b, cnt);
       h->stats.kernel_launches++;

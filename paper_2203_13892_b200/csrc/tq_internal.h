@@ -172,6 +172,8 @@ struct PassLaunch {
   const uint32_t* prep;         // dedup map of the parent batch (fan-out reads prep[parent])
   const uint32_t* wlist;        // variant 3 with a work list: the leaves (slots) to project
   const uint32_t* wcount;       //   and their count (device); grid = persistent CTAs
+  uint32_t clean;               // variant 1: the work list holds only items without an error in
+                                //   the pass (the fast-code kernel, JitPass::kernel_clean)
 };
 
 // Noise rows of one level batch (row a3): per instance a row of row_bytes bytes,
@@ -185,6 +187,7 @@ int launch_set_seed(uint64_t* d_seed, uint64_t seed, void* stream);
 // the batch's computed instances (rep[s] == s) in slot order -> list, *count; xlout (leaf level,
 // may be null) = 0 for the others
 int launch_compact_reps(const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
+                        const uint8_t* d_rows, uint32_t row_bytes, uint32_t emask, uint32_t* d_list2, uint32_t* d_count2,
                         void* stream);
 // All noise rows of a shard in one launch (one warp per instance of every level).
 struct NoiseLevel {
@@ -303,6 +306,7 @@ struct JitPass {
   void* kernel = nullptr;   // cudaKernel_t
   void* kernel_nostore = nullptr;     // leaf-sum passes: run sums only (variant 1)
   void* kernel_recompute = nullptr;   // leaf-sum passes: one tile per leaf, 8 amps (variant 2)
+  void* kernel_clean = nullptr;       // variant 1 for work-list items whose pass drew no error
   std::vector<uint32_t> out_row;   // per out-of-tile qubit: stored-address bits whose parity is its bit
   int threads = 0;
   size_t smem = 0;
