@@ -32,19 +32,19 @@ def main():
     for d in ks:
         t = d.get("gpu__time_duration.sum", 0.0)
         total_ns += t
-        m = re.match(r"tq_pass_l(\d+)_p(\d+)(_v(\d))?$", d["name"])
+        m = re.match(r"tq_pass_l(\d+)_p(\d+)(_v(\d))?c?$", d["name"])
         key = ("pass", int(m.group(1)), int(m.group(2))) if m and m.group(4) != "2" else \
               ("recompute", int(m.group(1)), int(m.group(2))) if m else ("other", d["name"], 0)
         # conditional leaf sampling: pass A = (leaf, 0), the projection = (leaf, 100),
         # stage-2 pass p = (leaf, 101 + p) -- the families tqsim_profile_tree reports
-        mt = re.match(r"tq_trail_(a|b(\d+))_v(\d)$", d["name"])
+        mt = re.match(r"tq_trail_(a|b(\d+))_v(\d)c?$", d["name"])
         if mt:
             v = int(mt.group(3))
             if mt.group(1) == "a":
                 key = ("pass", leaf, 0 if v == 1 else 100)
             else:
                 key = ("pass", leaf, 101 + int(mt.group(2))) if v != 2 else ("recompute", leaf, 101 + int(mt.group(2)))
-        elif d["name"].startswith("tq::trail_project_kernel"):
+        elif "trail_project" in d["name"]:
             key = ("pass", leaf, 100)
         a = agg[key]
         names.setdefault(key, set()).add(d["name"])
