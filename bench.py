@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--batch-log2", type=int, default=0)
     ap.add_argument("--copy-cost", type=float, default=10.0,
                     help="DCP first-slice length (copy cost in gates, R14); -1 = the fused fan-out's cost")
+    ap.add_argument("--small-tree", type=int, default=0,
+                    help="options.small_tree: 0 auto, 1 on (n <= 10), 2 off (DESIGN.md §6.4)")
     ap.add_argument("--shard", default="", help="r/w: time only shard r of w (single-GPU experiments)")
     return ap.parse_args()
 
@@ -321,7 +323,8 @@ def main():
         first_call_s = time.perf_counter() - tc
         T.tqsim_release_run_cache()
 
-    opts = T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, copy_cost_gates=args.copy_cost)
+    opts = T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, copy_cost_gates=args.copy_cost,
+                             small_tree=args.small_tree)
     h = T.tqsim_create(n, gates, noise, shots, ar, opts)
     plan = h.plan
     N = int(plan.n_outcomes)
@@ -534,7 +537,7 @@ def main():
             "config": {"workload": w.name, "n_qubits": n, "shots": shots, "outcomes": N,
                        "outcomes_per_step": step_outcomes,
                        "shard": args.shard or None,
-                       "arities": plan.arity_list, "lowered_gates": int(plan.n_lowered_gates),
+                       "arities": plan.arity_list, "small_tree": int(plan.small_tree), "lowered_gates": int(plan.n_lowered_gates),
                        "tile_qubits": int(plan.tile_qubits),
                        "l2": "inputs larger than L2 (state batches >= 1 GiB per launch group)",
                        "parallelism": "tree sharding x%d (tqsim_shard_levels)" % world},

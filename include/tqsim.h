@@ -97,6 +97,12 @@ typedef struct {
 
 #define TQSIM_KRAUS_MAX_QUBITS 13
 
+/* Small-state tree (SURVEY §8(a) kernel notes): a circuit of at most this
+ * many qubits (Pauli noise only) may run the whole tree as ONE kernel -- one warp per leaf,
+ * the state in shared memory, the root-to-leaf path recomputed with the inherited keys
+ * (identical noise draws and outcomes to the tree; §3, R7). */
+#define TQSIM_SMALL_MAX_QUBITS 10
+
 typedef struct {
   double copy_cost_gates;     /* first-slice length m = round(.) (R14); default 10;
                                  -1 = this engine's fused fan-out cost: half the gates one HBM pass
@@ -115,6 +121,10 @@ typedef struct {
   uint32_t trail_low;         /* conditional leaf sampling: the marginal pass's tile =
                                  qubits 0..trail_low-1 + the top K - trail_low qubits (3..K-1);
                                  0 = auto (4 when K >= 10, else 3) */
+  uint32_t small_tree;        /* small-state tree kernel (n_qubits <= TQSIM_SMALL_MAX_QUBITS, Pauli
+                                 noise, no state dumps): 0 = auto (when the per-leaf recompute is
+                                 cheap: n_outcomes * lowered gates * 2^max(n,5) <= 2^24), 1 = on
+                                 whenever eligible, 2 = off (the general tree engine) */
 } tqsim_options;
 
 /* The tree plan (§3.1): level d executes lowered gates
@@ -139,7 +149,7 @@ typedef struct {
                                        top bits selected first from marginals (0 = off) */
   uint32_t trail_fast;              /* 1: its projection is the streaming kernel (diagonal units
                                        + top-qubit 1q gates), 0: the generated pass kernel */
-  uint32_t reserved1;
+  uint32_t small_tree;              /* 1: the tree runs as the small-state kernel (options.small_tree) */
 } tqsim_plan;
 
 /* Execution statistics of the last tqsim_execute on a handle. */

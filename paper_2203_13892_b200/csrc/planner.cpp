@@ -30,8 +30,9 @@ Options options_from(const tqsim_options* o) {
   r.profile = o->profile;
   r.no_dedup = o->no_dedup;
   r.trail_low = o->trail_low;
+  r.small_tree = o->small_tree;
   if (!(r.copy_cost_gates >= 0 || r.copy_cost_gates == -1.0) || !(r.z > 0) || !(r.eps > 0) || r.topup > 1 ||
-      r.no_dedup > 1 || (r.trail_low != 0 && (r.trail_low < 3 || r.trail_low > MAX_K - 1)) ||
+      r.no_dedup > 1 || r.small_tree > 2 || (r.trail_low != 0 && (r.trail_low < 3 || r.trail_low > MAX_K - 1)) ||
       (r.tile_qubits != 0 && (r.tile_qubits < RBITS || r.tile_qubits > MAX_K)) ||
       r.batch_log2_amps > 40)
     throw Error{TQSIM_EINVAL, "invalid tqsim_options"};

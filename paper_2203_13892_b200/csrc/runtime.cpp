@@ -72,7 +72,9 @@ struct tqsim_handle {
   bool tag_launches = false;
   // Kraus engine (non-Pauli channels, kraus.cu): the lowered gate table in HBM
   bool kraus = false;
-  tq::KGate* d_kgates = nullptr;
+  tq::KGate* d_kgates = nullptr;   // also read by the small-state tree kernel (small.cu)
+  // small-state tree (small.cu): the whole tree as one kernel, one warp per leaf
+  bool small = false;
 };
 
 namespace tq {
@@ -909,8 +911,51 @@ void run_level_kraus(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t par
   }
 }
 
+// Small-state tree (small.cu): every leaf of the shard in one launch, one warp per leaf
+// recomputing its root-to-leaf path with the inherited keys (the tree's own noise draws).
+void run_small_tree(Exec& x) {
+  tqsim_handle* h = x.h;
+  const uint32_t L = (uint32_t)h->plan.arities.size();
+  SmallTreeArgs a{};
+  a.gates = h->d_kgates;
+  a.leaf_first = x.lvl_first[L - 1];
+  a.leaf_count = x.lvl_end[L - 1] - x.lvl_first[L - 1];
+  a.levels = L;
+  a.n = (uint32_t)std::max(h->n_sim, 5);   // >= one amplitude per lane; pad qubits stay |0> (R28)
+  a.n_user = h->n_user;
+  for (uint32_t d = 0; d < L; ++d) a.arity[d] = h->plan.arities[d];
+  for (uint32_t d = 0; d <= L; ++d) a.bounds[d] = (uint32_t)h->plan.bounds[d];
+  a.seedp = h->d_seed;
+  a.p1 = h->noise.p1;
+  a.p2 = h->noise.p2;
+  a.p01 = h->noise.readout_p01;
+  a.p10 = h->noise.readout_p10;
+  a.out = x.d_out;
+  a.dbg_u = h->d_dbg_u;
+  a.dbg_total = h->d_dbg_total;
+  a.dbg_flag = h->d_dbg_flag;
+  mark(x, 0, L - 1, 0, a.leaf_first, a.leaf_count);
+  ck(launch_small_tree(a, x.st), "small tree launch");
+  mark(x, 0, L - 1, 0, a.leaf_first, a.leaf_count);
+  h->stats.kernel_launches++;
+  h->stats.pass_launches++;
+  uint64_t nodes = 0, gamps = 0;
+  for (uint32_t d = 0; d < L; ++d) {   // the tree's nominal work over the shard (as run_level counts it)
+    const uint64_t cnt = x.lvl_end[d] - x.lvl_first[d];
+    nodes += cnt;
+    gamps += (cnt * (h->plan.bounds[d + 1] - h->plan.bounds[d])) << h->n_user;
+  }
+  h->stats.node_executions += nodes;
+  h->stats.gate_amp_updates += gamps;
+  h->stats.leaves += a.leaf_count;
+}
+
 // Every noise row of the shard (all levels) in one launch, then the tree.
 void run_tree(Exec& x) {
+  if (x.h->small && !(x.h->debug && x.h->debug->n_dumps)) {
+    run_small_tree(x);
+    return;
+  }
   if (x.h->kraus) {
     run_level_kraus(x, 0, x.lvl_first[0], x.lvl_end[0], 0);
     return;
@@ -1023,6 +1068,18 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     h->cplan.tile_qubits = h->pp.levels.empty() || h->pp.levels[0].empty() ? 0u : (uint32_t)h->pp.levels[0][0].K;
     h->cplan.trail_top_bits = h->pp.trail.on && !h->kraus ? (uint32_t)h->pp.trail.m : 0u;
     h->cplan.trail_fast = h->pp.trail.on && !h->kraus && h->pp.trail.fast ? 1u : 0u;
+    {   // small-state tree: eligible for narrow Pauli-noise circuits; auto when
+        // the per-leaf recompute (n_outcomes x lowered gates x 2^n) stays small
+      const double flat = (double)h->cplan.n_outcomes * (double)h->gates.size() *
+                          (double)(1ull << std::max(h->n_sim, 5));
+      const char* env = std::getenv("TQSIM_SMALL");   // "0": auto never picks it (explicit 1 still does)
+      // auto: only where the whole tree is a few microseconds of work (measured crossover
+      // 2^23..2^25 amplitude-gate updates, profiles/r02_small_tree_sweep.jsonl)
+      const bool auto_ok = !(env && env[0] == '0') && flat <= 16777216.0;
+      h->small = !h->kraus && h->n_user <= (uint32_t)TQSIM_SMALL_MAX_QUBITS && opts.small_tree != 2 &&
+                 (opts.small_tree == 1 || auto_ok);
+      h->cplan.small_tree = h->small ? 1u : 0u;
+    }
     if (need_gpu) {
       require_device();
       const size_t G = std::max<size_t>(h->gates.size(), 1);
@@ -1037,7 +1094,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
             h->h_tables[G + h->pp.ops[oi].gate] = (uint8_t)std::min<uint32_t>(pd.pass_index, 31);
       upload_gate_tables(h, nullptr);
       ckc(cudaStreamSynchronize(nullptr), "upload gate tables");
-      if (h->kraus) {   // the Kraus engine reads the lowered gates from HBM (kraus.cu)
+      if (h->kraus || h->small) {   // the Kraus engine / small tree read the lowered gates from HBM
         std::vector<KGate> kg(h->gates.size());
         for (size_t g = 0; g < h->gates.size(); ++g) {
           const LGate& l = h->gates[g];
@@ -1050,8 +1107,10 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
         ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_kgates), sizeof(KGate) * std::max<size_t>(kg.size(), 1)),
             "cudaMalloc kraus gates");
         ckc(cudaMemcpy(h->d_kgates, kg.data(), sizeof(KGate) * kg.size(), cudaMemcpyHostToDevice), "kraus gates");
-      } else {
+      }
+      if (!h->kraus) {
         // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
+        // (small-state handles too: state dumps run the general tree)
         h->jit = jit_build(h->pp, h->gates, &h->compile_s, &h->jit_trail);
       }
 
@@ -1243,6 +1302,14 @@ bool trail_active(const tqsim_handle* h) { return h->pp.trail.on && !(h->debug &
 
 void fill_computed(tqsim_handle* h, const ShardRange& sr, const Layout& L, const char* ws) {
   const bool dumps = h->debug && h->debug->n_dumps;
+  if (h->small && !dumps) {   // small-state tree: every leaf recomputes its whole path, no HBM states
+    const size_t Lv = h->plan.arities.size();
+    const uint64_t leaves = sr.empty() ? 0 : sr.hi[Lv - 1] - sr.lo[Lv - 1];
+    h->stats.computed_node_executions = leaves * Lv;
+    h->stats.computed_gate_amp_updates = (leaves * h->plan.bounds[Lv]) << h->n_user;
+    h->stats.computed_pass_bytes = 0;
+    return;
+  }
   const bool dedup = !dumps && !h->opts.no_dedup && !h->kraus;
   const WorkMap wm = computed_work(h, sr, L, ws, dedup);
   tqsim_stats& st = h->stats;
@@ -1634,7 +1701,7 @@ tqsim_status tqsim_profile_tree(tqsim_handle* h, uint64_t seed, uint32_t rank, u
     execute(h, seed, rank, world, st, d_workspace, workspace_bytes, d_leaf_outcomes);   // synchronizes
     const ShardRange sr = shard_levels(h->cplan, rank, world);
     const Layout lay = layout(h, sr);
-    const bool dedup = !(h->debug && h->debug->n_dumps) && !h->opts.no_dedup && !h->kraus;
+    const bool dedup = !(h->debug && h->debug->n_dumps) && !h->opts.no_dedup && !h->kraus && !h->small;
     const WorkMap wm = computed_work(h, sr, lay, static_cast<const char*>(d_workspace), dedup);
     fill_computed(h, sr, lay, static_cast<const char*>(d_workspace));
     std::map<std::tuple<int, uint32_t, uint32_t>, tqsim_kernel_timing> agg;

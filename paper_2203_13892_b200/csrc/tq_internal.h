@@ -34,7 +34,7 @@ std::vector<LGate> lower(const tqsim_circuit* c);
 struct Options {
   double copy_cost_gates = 10.0, z = 1.96, eps = 0.05;
   uint64_t mem_budget = 180000000000ull;
-  uint32_t topup = 0, tile_qubits = 0, batch_log2_amps = 0, profile = 0, no_dedup = 0, trail_low = 0;
+  uint32_t topup = 0, tile_qubits = 0, batch_log2_amps = 0, profile = 0, no_dedup = 0, trail_low = 0, small_tree = 0;
 };
 Options options_from(const tqsim_options* o);
 
@@ -284,6 +284,24 @@ struct KrausArgs {
   uint8_t* dbg_flag;
 };
 int launch_kraus_slice(const KrausArgs& a, uint32_t batch, void* stream);
+
+// Small-state tree (small.cu): one warp per leaf recomputes its root-to-leaf
+// path with the inherited keys, the state in shared memory (n_sim <= TQSIM_SMALL_MAX_QUBITS).
+constexpr int SMALL_TREE_WARPS = 4;   // warps (leaves) per CTA
+struct SmallTreeArgs {
+  const KGate* gates;
+  uint64_t leaf_first, leaf_count;      // the shard's leaf range
+  uint32_t levels, n, n_user, reserved;
+  uint32_t arity[TQSIM_MAX_LEVELS];
+  uint32_t bounds[TQSIM_MAX_LEVELS + 1];
+  const uint64_t* seedp;
+  double p1, p2, p01, p10;
+  uint32_t* out;
+  double* dbg_u;
+  double* dbg_total;
+  uint8_t* dbg_flag;
+};
+int launch_small_tree(const SmallTreeArgs& a, void* stream);
 inline bool kraus_enabled(const tqsim_noise_model& nm) {
   return nm.amp_damping > 0.0 || nm.phase_damping > 0.0 || nm.t1 > 0.0;
 }

@@ -53,7 +53,8 @@ class tqsim_options(C.Structure):
     _fields_ = [("copy_cost_gates", C.c_double), ("z", C.c_double), ("eps", C.c_double),
                 ("mem_budget_bytes", C.c_uint64), ("topup", C.c_uint32),
                 ("tile_qubits", C.c_uint32), ("batch_log2_amps", C.c_uint32),
-                ("profile", C.c_uint32), ("no_dedup", C.c_uint32), ("trail_low", C.c_uint32)]
+                ("profile", C.c_uint32), ("no_dedup", C.c_uint32), ("trail_low", C.c_uint32),
+                ("small_tree", C.c_uint32)]
 
 
 class tqsim_plan(C.Structure):
@@ -64,7 +65,7 @@ class tqsim_plan(C.Structure):
                 ("n_outcomes", C.c_uint64), ("node_executions", C.c_uint64),
                 ("gate_amp_updates", C.c_uint64), ("flat_gate_amp_updates", C.c_uint64),
                 ("hbm_passes", C.c_uint64), ("tile_qubits", C.c_uint32), ("trail_top_bits", C.c_uint32),
-                ("trail_fast", C.c_uint32), ("reserved1", C.c_uint32)]
+                ("trail_fast", C.c_uint32), ("small_tree", C.c_uint32)]
 
     @property
     def arity_list(self) -> List[int]:

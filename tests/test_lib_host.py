@@ -298,3 +298,31 @@ def test_fused_copy_cost_first_slice():
     assert p.boundary_list[1] != 10
     with pytest.raises(T.TqsimError):
         T.tqsim_plan_circuit(n, gates, noise, shots, None, T.default_options(copy_cost_gates=-2.0))
+
+
+def test_small_tree_choice_host(monkeypatch):
+    """Host-side choice of the small-state tree kernel (options.small_tree):
+    auto for C1 (n_outcomes x gates x 2^5 = 2.0e6 <= 2^24), never for C2 (15 qubits), above 10
+    qubits, with a non-Pauli channel, or with small_tree = 2; TQSIM_SMALL=0 only stops auto."""
+    monkeypatch.delenv("TQSIM_SMALL", raising=False)
+    w = load_config("c1_qft5")
+    n, gates, noise, shots, ar = T.workload_args(w)
+    assert T.tqsim_plan_circuit(n, gates, noise, shots, ar).small_tree == 1
+    assert T.tqsim_plan_circuit(n, gates, noise, shots, ar, T.default_options(small_tree=2)).small_tree == 0
+    w2 = load_config("c2_qft15")
+    n2, g2, noise2, s2, ar2 = T.workload_args(w2)
+    assert T.tqsim_plan_circuit(n2, g2, noise2, s2, ar2, T.default_options(small_tree=1)).small_tree == 0
+    rng = np.random.default_rng(3)
+    g10 = random_circuit(10, 60, rng)
+    # 88 lowered gates x 2^10: 2^24 / 90,112 = 186 outcomes -- 100 shots auto, 1,000 not
+    assert T.tqsim_plan_circuit(10, g10, noise, 100, [10, 10]).small_tree == 1
+    assert T.tqsim_plan_circuit(10, g10, noise, 1000, [10, 100]).small_tree == 0
+    assert T.tqsim_plan_circuit(10, g10, noise, 1000, [10, 100], T.default_options(small_tree=1)).small_tree == 1
+    kn = T.noise_arg(0.01, 0.02, 0.0, 0.0, amp_damping=0.01)
+    assert T.tqsim_plan_circuit(6, random_circuit(6, 20, rng), kn, 100, [10, 10],
+                                T.default_options(small_tree=1)).small_tree == 0
+    monkeypatch.setenv("TQSIM_SMALL", "0")
+    assert T.tqsim_plan_circuit(n, gates, noise, shots, ar).small_tree == 0
+    assert T.tqsim_plan_circuit(n, gates, noise, shots, ar, T.default_options(small_tree=1)).small_tree == 1
+    with pytest.raises(T.TqsimError):
+        T.tqsim_plan_circuit(n, gates, noise, shots, ar, T.default_options(small_tree=3))
