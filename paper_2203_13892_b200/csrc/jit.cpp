@@ -1137,6 +1137,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       }
     }
   }
+  // TQSIM_NEXT_PF=1: persistent run-sum / projection loops prefetch the next item's tile into L2
+  static const bool next_pf_env = [] {
+    const char* e = std::getenv("TQSIM_NEXT_PF");
+    return e && e[0] == '1';
+  }();
+  const bool next_pf = next_pf_env && !tma;
   const bool use_smem = fast.size() > 1;
   threads = T;
   smem = use_smem ? (size_t)16 << K : 0;
@@ -1265,7 +1271,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       << "  tq_d2* const tq_buf0 = reinterpret_cast<tq_d2*>(tq_sm + 128);\n"
       << "  __shared__ tq_u64 tq_next[2];\n";
   else if (use_smem) o << "  extern __shared__ tq_d2 tile[];\n";
-  o << "  __shared__ tq_u32 tq_errb[" << NW << "];\n";
+  o << "  __shared__ tq_u32 tq_errb[" << std::max(1, T / 32) << "][" << NW << "];   // per warp: the eb words\n";
   o << "  const tq_u32 tid = threadIdx.x;\n  const tq_u64 bid = blockIdx.x;\n";
   if (tma) {
     // persistent CTAs: the next item's tile streams into the other buffer (TMA) while this
@@ -1291,17 +1297,39 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const tq_u32 s = (tq_u32)(bid % a.batch);\n  const tq_u64 t = bid / a.batch;\n";
   else   // leaf run sums / projection: every (instance, tile), or the instances of a work list
          // (dedup representatives / projection hand-overs) with persistent CTAs
+  {
+    // the next item's index (and, fan-out, its parent slot) is loaded one item ahead, so the
+    // dependent index loads (work list -> parent map -> tile) do not stall each item's start
     o << "  const tq_u32 nw = a.wlist ? *a.wcount : a.batch;\n"
-      << "  for (tq_u64 w = bid; w < ((tq_u64)nw << " << pd.n_out << "); w += gridDim.x) {\n"
-      << "  const tq_u32 s = a.wlist ? a.wlist[w % nw] : (tq_u32)(w % nw);\n  const tq_u64 t = w / nw;\n";
+      << "  const tq_u64 tq_tot = (tq_u64)nw << " << pd.n_out << ";\n"
+      << "  const tq_u32 tq_gm = nw ? (tq_u32)(gridDim.x % nw) : 0u;\n"
+      << "  const tq_u64 tq_gd = nw ? gridDim.x / nw : 0ull;\n"
+      << "  tq_u32 tq_i = nw ? (tq_u32)(bid % nw) : 0u;\n  tq_u64 tq_t = nw ? bid / nw : 0ull;\n"
+      << "  tq_u32 tq_snx = 0u;\n"
+      << "  if (bid < tq_tot) tq_snx = a.wlist ? a.wlist[tq_i] : tq_i;\n";
+    if (mode == 1)
+      o << "  tq_u64 tq_pnx = ((tq_u64)a.child_first + tq_snx) / a.arity - a.parent_first;\n"
+        << "  if (a.prep && bid < tq_tot) tq_pnx = a.prep[tq_pnx];\n";
+    o << "  for (tq_u64 w = bid; w < tq_tot; w += gridDim.x) {\n"
+      << "  const tq_u32 s = tq_snx;\n  const tq_u64 t = tq_t;\n";
+    if (mode == 1) o << "  const tq_u64 tq_pcur = tq_pnx;\n";
+    o << "  tq_i += tq_gm;\n  tq_t += tq_gd;\n  if (tq_i >= nw) { tq_i -= nw; ++tq_t; }\n"   // w + gridDim.x
+      << "  const tq_u64 tq_wn = w + gridDim.x;\n"
+      << "  if (tq_wn < tq_tot) tq_snx = a.wlist ? a.wlist[tq_i] : tq_i;\n";
+  }
   if (variant == 3)   // the leaf's chosen top bits (the select kernel's chunk)
     o << "  const tq_u32 hsel = a.runsel[s];\n";
   if (variant != 2 && !tma) {
     // An instance that shares its representative's state (dedup map, launch_dedup_map:
     // no error in its slice, same effective parent) is not computed; readers go through
     // the map.  A skipped leaf's store-address XOR is 0.
-    o << "  if (a.rep && a.rep[s] != s) {\n"
+    // (a variant-1 work list holds representatives only: compact_reps_kernel)
+    o << (variant == 1 ? "  if (!a.wlist && a.rep && a.rep[s] != s) {\n" : "  if (a.rep && a.rep[s] != s) {\n")
       << (variant == 1 ? "    if (t == 0 && tid == 0u) a.xlout[s] = 0u;\n" : "")
+      << ((variant == 1 || variant == 3) && mode == 1   // keep the look-ahead parent slot current
+              ? "    if (tq_wn < tq_tot) {\n      tq_pnx = ((tq_u64)a.child_first + tq_snx) / a.arity - a.parent_first;\n"
+                "      if (a.prep) tq_pnx = a.prep[tq_pnx];\n    }\n"
+              : "")
       << (tma || variant == 0 ? "    return;\n" : "    continue;\n")
       << "  }\n";
   }
@@ -1310,7 +1338,11 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  gtile |= (tq_u32)((t >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << "; gtile_st ^= (0u - (tq_u32)((t >> "
       << i << ") & 1ull)) & " << pcol[pd.out_q[i]] << "u;\n";
   o << "  tq_d2* __restrict__ dst = a.dst + ((tq_u64)s << " << n << ");\n";
-  if (mode == 1)   // fan-out src: the parent, or (skipped duplicate parent) its representative
+  const bool ahead = (variant == 1 || variant == 3) && !tma;   // the loop above loads indices ahead
+  if (mode == 1 && ahead)
+    o << "  const tq_u64 pj = tq_pcur;\n"
+      << "  const tq_d2* __restrict__ src = a.src + (pj << " << n << ");\n";
+  else if (mode == 1)   // fan-out src: the parent, or (skipped duplicate parent) its representative
     o << "  tq_u64 pj = ((tq_u64)a.child_first + s) / a.arity - a.parent_first;\n"
       << "  if (a.prep) pj = a.prep[pj];\n"
       << "  const tq_d2* __restrict__ src = a.src + (pj << " << n << ");\n";
@@ -1387,8 +1419,34 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
         o << "    tq_ld2(src + (gb + " << goff[k] << "u), r" << k << ", r" << (k | 1 << b0) << ");\n";
     }
     o << "  }\n";
+    if (next_pf && (variant == 1 || variant == 3) && mode != 0) {
+      // persistent loop: the CTA's NEXT work item's tile is prefetched into L2 while this one is
+      // computed (no registers held; its loads then wait on L2, not HBM)
+      o << "  {\n    const tq_u64 wn = w + gridDim.x;\n"
+        << "    if (wn < ((tq_u64)nw << " << pd.n_out << ")) {\n"
+        << "      const tq_u32 sn = a.wlist ? a.wlist[wn % nw] : (tq_u32)(wn % nw);\n"
+        << "      const tq_u64 tn = wn / nw;\n      tq_u32 gtn = 0u;\n";
+      for (int i = 0; i < pd.n_out; ++i)
+        o << "      gtn |= (tq_u32)((tn >> " << i << ") & 1ull) << " << (int)pd.out_q[i] << ";\n";
+      if (mode == 1)
+        o << "      tq_u64 pjn = ((tq_u64)a.child_first + sn) / a.arity - a.parent_first;\n"
+          << "      if (a.prep) pjn = a.prep[pjn];\n"
+          << "      const tq_d2* srcn = a.src + (pjn << " << n << ");\n";
+      else
+        o << "      const tq_d2* srcn = a.dst + ((tq_u64)sn << " << n << ");\n";
+      o << "      const tq_u32 gbn = gtn" << gb.substr(5) << ";\n";
+      for (int k = 0; k < 16; ++k) {
+        if (b0 >= 0 && (k >> b0 & 1)) continue;
+        o << "      asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(srcn + (gbn + " << goff[k] << "u)));\n";
+      }
+      o << "    }\n  }\n";
+    }
   };
   emit_load();
+  if (mode == 1 && ahead)   // the next item's parent slot (its index arrived during the tile loads)
+    o << "  if (tq_wn < tq_tot) {\n"
+      << "    tq_pnx = ((tq_u64)a.child_first + tq_snx) / a.arity - a.parent_first;\n"
+      << "    if (a.prep) tq_pnx = a.prep[tq_pnx];\n  }\n";
   // noise row of the instance (launch_noise_rows): error-free instances (the common
   // case) run the fused fast path, the others apply each keyed Pauli after its gate
   o << "  const unsigned char* __restrict__ codes = a.rows + (tq_u64)s * " << CROW << "u;\n";
@@ -2016,7 +2074,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
           o << "    if (" << cond.str() << ") {\n";
           o << "      for (tq_u32 si = " << so << "u; si < " << so + f.sites.size() << "u; ++si) {\n";
           o << "        const tq_u32 li = SITES[si];\n";
-          o << "        if (!((tq_errb[li >> 5] >> (li & 31u)) & 1u)) continue;\n";
+          o << "        if (!((tq_errb[tid >> 5][li >> 5] >> (li & 31u)) & 1u)) continue;\n";
           o << "        const tq_u32 c = codes[4u + GOFF[li]];\n";
           o << "        const tq_u32 wx = __ldg(ERRX + li * 16u + c), wz = __ldg(ERRZ + li * 16u + c);\n";
           o << "        if (!(wz & 0x80000000u)) {\n"
@@ -2267,13 +2325,24 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   // clean: the kernel of the work-list items whose pass drew no error (compact_reps_kernel
   // classifies them): the fast code only -- a third of the instructions, no frame state
   if (!clean) {
-  o << "  if (errs) {\n";
-  o << "    if (tid < " << NW << "u) tq_errb[tid] = 0u;\n    __syncthreads();\n";
-  o << "    for (tq_u32 li = tid; li < " << nops << "u; li += " << T << "u)\n"
-    << "      if (codes[4u + GOFF[li]] != 0) atomicOr(&tq_errb[li >> 5], 1u << (li & 31u));\n";
-  o << "    __syncthreads();\n";
-  for (int w = 0; w < NW; ++w) o << "    eb" << w << " = tq_errb[" << w << "];\n";
-  o << "  }\n";
+  // every warp builds the bitmap itself (one ballot per 32 ops; no block barrier)
+  // (CTAs of fewer than 32 threads: the T lanes cover a word's 32 ops in turn)
+  {
+    const int L = std::min(T, 32);
+    char mk[16];
+    std::snprintf(mk, sizeof mk, "0x%xu", L >= 32 ? 0xffffffffu : (1u << L) - 1u);
+    o << "  if (errs) {\n";
+    for (int w = 0; w < NW; ++w)
+      o << "    { tq_u32 m = 0u;\n"
+        << "      for (tq_u32 l = tid & 31u; l < 32u; l += " << L << "u) {\n"
+        << "        const tq_u32 li = " << 32 * w << "u + l;\n"
+        << "        if (li < " << nops << "u && codes[4u + GOFF[li]] != 0) m |= 1u << l;\n      }\n"
+        << "      eb" << w << " = __reduce_or_sync(" << mk << ", m); }\n";
+    o << "    if ((tid & 31u) == 0u) {\n";
+    for (int w = 0; w < NW; ++w) o << "      tq_errb[tid >> 5][" << w << "] = eb" << w << ";\n";
+    o << "    }\n    __syncwarp(" << mk << ");\n";
+    o << "  }\n";
+  }
   }
   o << "  tq_u32 fx = 0u, fz = 0u, fk = 0u;\n";
   if (variant == 1 && pd.leaf_sums) o << "  double tq_sc = 1.0;\n";   // run-sum factor (see the flush)
