@@ -1457,7 +1457,30 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  const bool errs = (emask >> " << std::min<uint32_t>(pd.pass_index, 31) << ") & 1u;\n";
 
   bool sc_used = false;   // a fast phase scaled the run sums by the run-time tq_sc
+  // TQSIM_FRAME_FLUSH=1: careful phases flush the Pauli frame into the exchange tile (see the
+  // phase store).  Off by default: measured slower (C2 1.94 -> 2.01 ms, C4 trail pass 154 ->
+  // 159 ms per tree; profiles/r02_ab_frame_flush.txt) -- the flush costs more than the fast
+  // phases it enables; parity-tested on (the full GPU suite passed with it on)
+  static const bool flush_frame = [] {
+    const char* e = std::getenv("TQSIM_FRAME_FLUSH");
+    return e && e[0] == '1';
+  }();
   auto emit_phases = [&](const std::vector<PhaseSpec>& specs, bool with_errors, int ph_only) {
+  // amap_upto[ph]: an absorbed CX (store-map op) among the ops of phases 0..ph
+  std::vector<char> amap_upto(specs.size(), 0);
+  {
+    std::function<bool(const FOp&)> has_amap = [&](const FOp& f) {
+      if (f.kind == FOp::AMAP) return true;
+      for (const FOp& c : f.comps)
+        if (has_amap(c)) return true;
+      return false;
+    };
+    bool seen = false;
+    for (size_t q = 0; q < specs.size(); ++q) {
+      for (int it : specs[q].items) seen = seen || has_amap(fops[it]);
+      amap_upto[q] = seen;
+    }
+  }
   const int nph = (int)specs.size();
   for (int ph = 0; ph < nph; ++ph) {
     if (ph != ph_only) continue;
@@ -2312,7 +2335,27 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
       }
     } else {
       o << "    const tq_u32 sbs = tq_swz(" << lbs << ");\n";
-      for (int k = 0; k < 16; ++k) o << "    tile[sbs ^ " << soff[k] << "u] = " << g.r(k) << ";\n";
+      std::string sx;
+      if (with_errors && flush_frame && !amap_upto[ph]) {
+        // Frame flush at the exchange: the true state i^fk X^fx Z^fz psi_s is written to the
+        // tile explicitly (amplitude at physical index i -> i ^ fx, times i^fk (-1)^popc(fz & i);
+        // X only on tile qubits -- an off-tile X keeps the frame), so the next phases start
+        // from a trivial frame and run the fast code unless they draw an error themselves.
+        // Exact: the frame is a signed permutation.  Not after an absorbed CX (the frame then
+        // acts after the deferred store map).
+        uint32_t tmask = 0;
+        for (int p = 0; p < K; ++p) tmask |= 1u << pd.tile_q[p];
+        o << "    tq_u32 tq_sxw = 0u;\n"
+          << "    if ((fx & " << ~tmask << "u) == 0u && (fx | fz | fk) != 0u) {\n"
+          << "      const tq_u32 tq_zt = __popc(fz & (" << gbs << "));\n";
+        for (int k = 0; k < 16; ++k)
+          o << "      tq_rot(" << g.r(k) << ", fk + ((tq_zt + __popc(fz & " << goff[k] << "u)) << 1));\n";
+        o << "      tq_u32 tq_xt = 0u;\n";
+        for (int p = 0; p < K; ++p) o << "      tq_xt |= ((fx >> " << (int)pd.tile_q[p] << ") & 1u) << " << p << ";\n";
+        o << "      tq_sxw = tq_swz(tq_xt);\n      fx = 0u; fz = 0u; fk = 0u;\n    }\n";
+        sx = " ^ tq_sxw";
+      }
+      for (int k = 0; k < 16; ++k) o << "    tile[sbs ^ " << soff[k] << "u" << sx << "] = " << g.r(k) << ";\n";
     }
     o << "  }\n";
   }
