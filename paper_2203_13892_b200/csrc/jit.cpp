@@ -1014,6 +1014,25 @@ uint64_t choose_load_regs(const std::vector<PItem>& items, int K, bool coal, boo
 // variant (leaf-sum passes only): 0 = store the state (and run sums); 1 = run sums only,
 // no state store, the instance's store-address frame XOR to xlout; 2 = recompute one
 // tile per leaf (tiles[s]) and store only the 8 amplitudes of run runsel[s] to scratch.
+// resident threads per SM the register budget targets (TQSIM_JIT_THREADS_PER_SM, default 512:
+// 16 warps at <= 128 registers / thread), as many independent CTAs as fit; the clean
+// (error-free work item) kernels carry no Pauli-frame state and take their own target
+// (TQSIM_JIT_CLEAN_THREADS_PER_SM, default the same).  The __launch_bounds__ minimum of a
+// K-qubit-tile kernel of T threads, and the resident CTAs persistent grids are sized by.
+int jit_ctas_per_sm(int K, int T, bool clean) {
+  static const int tps = [] {
+    const char* e = std::getenv("TQSIM_JIT_THREADS_PER_SM");
+    return e ? std::max(128, std::atoi(e)) : 512;
+  }();
+  static const int tps_clean = [] {
+    const char* e = std::getenv("TQSIM_JIT_CLEAN_THREADS_PER_SM");
+    return e ? std::max(128, std::atoi(e)) : tps;
+  }();
+  return K >= 13 ? 1
+                 : std::max(1, std::min((clean ? tps_clean : tps) / std::max(T, 32),
+                                        (int)((227 * 1024) / ((16 << K) + 1024))));
+}
+
 std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<LGate>& gates,
                      int n, int mode, const std::string& name, int& threads, size_t& smem,
                      std::vector<double>& coefs, int variant = 0,
@@ -1223,14 +1242,7 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   if (gd.empty()) o << "0.0";
   o << "};\n";
   const int NW = std::max(1, (nops + 31) / 32);
-  // resident threads per SM the register budget targets (TQSIM_JIT_THREADS_PER_SM, default 512:
-  // 16 warps at <= 128 registers / thread), as many independent CTAs as fit
-  static const int tps = [] {
-    const char* e = std::getenv("TQSIM_JIT_THREADS_PER_SM");
-    return e ? std::max(128, std::atoi(e)) : 512;
-  }();
-  const int minb = K >= 13 ? 1
-                           : std::max(1, std::min(tps / std::max(T, 32), (int)((227 * 1024) / ((16 << K) + 1024))));
+  const int minb = jit_ctas_per_sm(K, T, clean);
   if (tma) {
     // per-kernel work scan and TMA issue: the next computed (representative) work item, and
     // the tensor-map coordinates of its tile (TmaGeom: runs of tile / out-of-tile qubits)
@@ -2855,7 +2867,7 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
   uint64_t grid = L.variant == 2 ? (uint64_t)L.batch : (uint64_t)L.batch << pd.n_out;
   if (L.variant == 3 && L.wlist) grid = std::min<uint64_t>(grid, 4 * 148);   // persistent over the work list
   if (L.variant == 1 && L.wlist) {   // persistent over the batch's representatives
-    const uint64_t per_sm = std::max<uint64_t>(1, 512 / std::max(jp.threads, 32));
+    const uint64_t per_sm = (uint64_t)jit_ctas_per_sm(pd.K, (int)jp.threads, L.clean != 0);
     grid = std::min<uint64_t>(grid, per_sm * 148 * 2);
   }
   if (grid == 0) return 0;
