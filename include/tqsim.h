@@ -167,8 +167,9 @@ typedef struct {
   uint64_t noise_launches;          /* noise-row kernels (one per level batch) */
   double noise_ms;                  /* sum of noise-row launch durations (profile=1 only) */
   /* Work actually executed (error-free duplicates skipped, options.no_dedup = 0).  Filled by
-   * tqsim_profile_tree and by tqsim_run_ex / tqsim_run (which synchronize); tqsim_execute
-   * (asynchronous) leaves them 0. */
+   * tqsim_profile_tree, and by tqsim_run_ex when it is given a tqsim_debug or options.profile = 1
+   * (the dedup maps are read back: a synchronous D2H + host walk); tqsim_run (the hot call) and
+   * tqsim_execute (asynchronous) leave them 0. */
   uint64_t computed_node_executions;
   uint64_t computed_gate_amp_updates;
   uint64_t computed_pass_bytes;     /* algorithmic bytes of the computed instances' passes */

@@ -1836,7 +1836,8 @@ tqsim_status tqsim_run_ex(const tqsim_circuit* c, const tqsim_noise_model* nm, u
       }
       h->d_dbg_u = h->d_dbg_total = nullptr;
       h->d_dbg_flag = nullptr;
-      fill_computed(h, sr, lay, base);   // work executed (dedup representatives), maps read back
+      if (debug || h->opts.profile)   // work executed (dedup representatives): maps read back
+        fill_computed(h, sr, lay, base);
       h->debug = nullptr;
       const double wall =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();

@@ -88,7 +88,7 @@ def test_full_tree_default_path(cfg, tag):
     plain = T.tqsim_run(n, gates, noise, shots, ar, w.seed)           # the north_star call
     assert np.array_equal(plain.leaf_outcomes, res.leaf_outcomes)
     # every instance computed (no shared states): the same outcomes
-    nd = T.tqsim_run_ex(n, gates, noise, shots, ar, w.seed, T.default_options(no_dedup=1))
+    nd = T.tqsim_run_ex(n, gates, noise, shots, ar, w.seed, T.default_options(no_dedup=1), leaf_debug=True)
     assert np.array_equal(nd.leaf_outcomes, res.leaf_outcomes)
     assert nd.stats.computed_node_executions == res.plan.node_executions
     assert res.stats.computed_node_executions < res.plan.node_executions
