@@ -1,4 +1,4 @@
-O=gpurun_out/r02b_full; mkdir -p $O
+O=gpurun_out/${1:-r02b_full}; mkdir -p $O
 nvidia-smi > $O/smi.txt 2>&1
 ( time timeout 2400 python -m pytest tests -m gpu -x -q --durations=25 ) > $O/pytest.log 2>&1; echo "pytest_rc=$?" >> $O/pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke_rc=$?" >> $O/smoke.log
