@@ -700,7 +700,10 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
         bestP = P;
         bs1 = s1;
       } else if (allow_swap && s1 >= 0 && is_swap(P) &&
-                 (!has_map || ((phys_of[s0] < LOW_Q) == (phys_of[s1] < LOW_Q)))) {
+                 // with store maps only high-high relabelings: a low-low one could carry a
+                 // mapped logical qubit (2 above the leaf level) onto physical 0 / 1, whose
+                 // address bits a map must not move (map_ok below)
+                 (!has_map || (phys_of[s0] >= LOW_Q && phys_of[s1] >= LOW_Q))) {
         best_swap = j;
         sw1 = s1;
       }

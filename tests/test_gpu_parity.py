@@ -547,3 +547,19 @@ def test_streaming_projection_split_level_shards(ar, world, blog):
         acc += o.cpu().numpy()
     assert np.array_equal(acc.astype(np.uint32), single)
     h.close()
+
+
+@pytest.mark.parametrize("p", [0.05, 1.0])
+def test_relabel_with_store_map_case_vs_oracle(p):
+    """The stress-run case of a low-low SWAP relabeling next to an absorbed SWAP(7, 2) in a first
+    pass (tests/golden/stress_relabel_map_case.json): outcomes and state dumps equal the oracle's."""
+    import json
+    import os
+    from tq_testutil import ROOT
+    d = json.load(open(os.path.join(ROOT, "tests", "golden", "stress_relabel_map_case.json")))
+    gates = [tuple(g) for g in d["gates"]]
+    opts = T.default_options(tile_qubits=d["tile_qubits"])
+    run_and_compare(d["n_qubits"], gates, NoiseModel(p, p, 0.02, 0.03), int(np.prod(d["arities"])), d["arities"],
+                    d["seed"] % (1 << 40), opts, dumps=[(0, 1), (1, 5), (2, 17)])
+    run_and_compare(d["n_qubits"], gates, NoiseModel(p, p, 0.02, 0.03), int(np.prod(d["arities"])), d["arities"],
+                    d["seed"] % (1 << 40), opts)

@@ -326,3 +326,28 @@ def test_small_tree_choice_host(monkeypatch):
     assert T.tqsim_plan_circuit(n, gates, noise, shots, ar, T.default_options(small_tree=1)).small_tree == 1
     with pytest.raises(T.TqsimError):
         T.tqsim_plan_circuit(n, gates, noise, shots, ar, T.default_options(small_tree=3))
+
+
+def test_relabel_with_store_map_regression():
+    """A first pass holding both a low-low SWAP (a relabeling of physical qubits 0 and 2) and an
+    absorbed SWAP(7, 2) (store-map CX gates on logical qubit 2): every pass kernel of the plan
+    generates (before the fix the relabeling carried the mapped qubit onto physical 0 and the
+    generator raised TQSIM_EINTERNAL).  Case from scripts/stress_parity.py (fixture: inputs only)."""
+    import json
+    d = json.load(open(os.path.join(ROOT, "tests", "golden", "stress_relabel_map_case.json")))
+    gates = [tuple(g) for g in d["gates"]]
+    n, ar = d["n_qubits"], d["arities"]
+    noise = T.noise_arg(0.05, 0.1)
+    opts = T.default_options(tile_qubits=d["tile_qubits"])
+    plan = T.tqsim_plan_circuit(n, gates, noise, int(np.prod(ar)), ar, opts)
+    for lv in range(plan.n_levels):
+        p = 0
+        while True:
+            try:
+                src = T.tqsim_pass_source(n, gates, noise, int(np.prod(ar)), ar, opts, lv, p)
+            except T.TqsimError as e:
+                assert "out of range" in str(e), (lv, p, str(e))
+                break
+            assert "__global__" in src
+            p += 1
+        assert p >= 1
