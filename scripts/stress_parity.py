@@ -22,7 +22,45 @@ from workloads import qft_gates, random_circuit  # noqa: E402
 from workloads.generators import qaoa_gates, random_3_regular_edges  # noqa: E402
 
 
+def kraus_case(rng, k):
+    """Non-Pauli channels (the shared-memory Kraus engine) vs oracle/kraus.py."""
+    from oracle import kraus as K
+    n = int(rng.integers(1, 10))
+    gates = random_circuit(n, int(rng.integers(10, 60)), rng)
+    if not gates:
+        gates = random_circuit(n, 5, rng, kinds=["h", "rx"])
+    L = int(rng.integers(1, 4))
+    ar = [int(rng.integers(1, 5)) for _ in range(L)]
+    shots = int(np.prod(ar))
+    ad = float(rng.choice([0.0, 0.02, 0.2]))
+    pdp = float(rng.choice([0.0, 0.02, 0.2]))
+    t1 = float(rng.choice([0.0, 50e-6]))
+    km = K.KrausModel(amp_damping=ad, phase_damping=pdp, t1=t1, t2=70e-6 if t1 else 0.0,
+                      gate_time_1q=5e-6 if t1 else 0.0, gate_time_2q=30e-6 if t1 else 0.0)
+    if not km.enabled:
+        km = K.KrausModel(amp_damping=0.05)
+    p = float(rng.choice([0.0, 0.01, 0.1]))
+    nm = NoiseModel(p, 2 * p, float(rng.choice([0.0, 0.02])), 0.0)
+    seed = int(rng.integers(0, 2 ** 40))
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10, km.amp_damping, km.phase_damping, km.t1,
+                        km.t2, km.gate_time_1q, km.gate_time_2q)
+    res = T.tqsim_run_ex(n, gates, noise, shots, ar, seed, None, leaf_debug=True)
+    plan = Plan(res.plan.arity_list, res.plan.boundary_list)
+    ref = K.simulate_tree(n, OG.lower(gates), plan, nm, km, seed)
+    bad, flagged = [], 0
+    for l, r in ref.leaves.items():
+        if r.flagged:
+            flagged += 1
+            continue
+        if int(res.leaf_outcomes[l]) != r.outcome:
+            bad.append(l)
+    return {"case": k, "kind": "kraus", "n": n, "arities": ar, "p": p, "ad": ad, "pd": pdp, "t1": t1, "seed": seed,
+            "leaves": len(ref.leaves), "flagged": flagged, "bad": bad[:8], "ok": not bad}
+
+
 def one_case(rng, k):
+    if rng.random() < 0.15:
+        return kraus_case(rng, k)
     kind = rng.choice(["random", "qaoa", "qft"], p=[0.6, 0.3, 0.1])
     n = int(rng.integers(4, 15))
     if kind == "qaoa" and n % 2:
