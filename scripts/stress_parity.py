@@ -3,7 +3,7 @@ default path (dedup, work lists, conditional leaf sampling, small-state tree) ag
 oracle's tree DFS; every non-flagged leaf outcome must match.  Test infrastructure (imports
 oracle/), not part of the product.
 
-    python scripts/stress_parity.py [seconds] [seed] > gpurun_out/stress.jsonl
+    python scripts/stress_parity.py [seconds] [seed] [nmin nmax] > gpurun_out/stress.jsonl
 """
 import json
 import os
@@ -58,11 +58,14 @@ def kraus_case(rng, k):
             "leaves": len(ref.leaves), "flagged": flagged, "bad": bad[:8], "ok": not bad}
 
 
+NMIN, NMAX = 4, 15   # qubit range of the Pauli cases (argv 3, 4)
+
+
 def one_case(rng, k):
-    if rng.random() < 0.15:
+    if NMAX <= 15 and rng.random() < 0.15:
         return kraus_case(rng, k)
     kind = rng.choice(["random", "qaoa", "qft"], p=[0.6, 0.3, 0.1])
-    n = int(rng.integers(4, 15))
+    n = int(rng.integers(NMIN, NMAX))
     if kind == "qaoa" and n % 2:
         n += 1
     if kind == "random":
@@ -102,6 +105,9 @@ def one_case(rng, k):
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+    global NMIN, NMAX
+    if len(sys.argv) > 4:
+        NMIN, NMAX = int(sys.argv[3]), int(sys.argv[4])
     t0 = time.time()
     k = nbad = 0
     while time.time() - t0 < budget:
