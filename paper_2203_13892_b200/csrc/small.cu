@@ -197,6 +197,7 @@ int launch_small_tree(const SmallTreeArgs& a, void* stream) {
     attr = true;
   }
   const uint64_t blocks = (a.leaf_count + SMALL_TREE_WARPS - 1) / SMALL_TREE_WARPS;
+  if (blocks > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;
   dev::small_tree_kernel<<<(unsigned)blocks, SMALL_TREE_WARPS * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
   return (int)cudaGetLastError();
 }
