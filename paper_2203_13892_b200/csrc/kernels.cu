@@ -830,13 +830,14 @@ __global__ void __launch_bounds__(QT, MINB) trail_project_pair_kernel(const __gr
 // leaf level's skipped instances get store-address XOR 0 (their representative is error-free).
 // With rows: the representatives whose noise row has no error in the pass (emask bits of the
 // row's pass bitmask) go to list, the others to list2 (the clean kernel / the full kernel).
-__global__ void __launch_bounds__(256) compact_reps_kernel(const uint32_t* __restrict__ rep, uint32_t cnt,
+constexpr int CR_T = 1024;   // one CTA: a C2 leaf batch (2,048 slots) in two rounds
+__global__ void __launch_bounds__(CR_T) compact_reps_kernel(const uint32_t* __restrict__ rep, uint32_t cnt,
                                                            uint32_t* __restrict__ list, uint32_t* __restrict__ count,
                                                            uint32_t* __restrict__ xlout,
                                                            const uint8_t* __restrict__ rows, uint32_t row_bytes,
                                                            uint32_t emask, uint32_t* __restrict__ list2,
                                                            uint32_t* __restrict__ count2) {
-  __shared__ uint32_t wsum[2][8];
+  __shared__ uint32_t wsum[2][CR_T / 32];
   __shared__ uint32_t base[2];
   if (threadIdx.x < 2) base[threadIdx.x] = 0;
   __syncthreads();
@@ -942,7 +943,7 @@ int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* s
 int launch_compact_reps(const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
                         const uint8_t* d_rows, uint32_t row_bytes, uint32_t emask, uint32_t* d_list2, uint32_t* d_count2,
                         void* stream) {
-  dev::compact_reps_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_rep, cnt, d_list, d_count, d_xlout,
+  dev::compact_reps_kernel<<<1, dev::CR_T, 0, static_cast<cudaStream_t>(stream)>>>(d_rep, cnt, d_list, d_count, d_xlout,
                                                                              d_rows, row_bytes, emask, d_list2,
                                                                              d_count2);
   return (int)cudaGetLastError();
