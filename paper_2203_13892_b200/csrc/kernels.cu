@@ -519,7 +519,14 @@ __device__ __forceinline__ void dedup_map_level(const uint8_t* __restrict__ rows
   {
     const NoiseLevel& lv = L.lv[d];
     const uint8_t* rw = rows + lv.rows_off;
-    auto em = [&](uint64_t j) { return *reinterpret_cast<const uint32_t*>(rw + (j - lv.inst_first) * lv.row_bytes); };
+    // em(j) != 0: instance j drew an error that makes it "not error-free" (lv.err_sel: only those gates)
+    auto em = [&](uint64_t j) -> uint32_t {
+      const uint8_t* row = rw + (j - lv.inst_first) * lv.row_bytes;
+      if (!lv.err_sel) return *reinterpret_cast<const uint32_t*>(row);
+      for (uint32_t t = 0; t < lv.slice_len; ++t)
+        if (lv.err_sel[t] && row[4 + t]) return 1u;
+      return 0u;
+    };
     const uint64_t A = lv.arity;
     for (uint64_t idx = idx0; idx < lv.count; idx += stride) {
       const uint64_t j = lv.inst_first + idx;
@@ -831,7 +838,8 @@ __global__ void __launch_bounds__(QT, MINB) trail_project_pair_kernel(const __gr
 // With rows: the representatives whose noise row has no error in the pass (emask bits of the
 // row's pass bitmask) go to list, the others to list2 (the clean kernel / the full kernel).
 constexpr int CR_T = 1024;   // one CTA: a C2 leaf batch (2,048 slots) in two rounds
-__global__ void __launch_bounds__(CR_T) compact_reps_kernel(const uint32_t* __restrict__ rep, uint32_t cnt,
+__global__ void __launch_bounds__(CR_T) compact_reps_kernel(const uint8_t* __restrict__ err_sel, uint32_t slice_len,
+                                                           const uint32_t* __restrict__ rep, uint32_t cnt,
                                                            uint32_t* __restrict__ list, uint32_t* __restrict__ count,
                                                            uint32_t* __restrict__ xlout,
                                                            const uint8_t* __restrict__ rows, uint32_t row_bytes,
@@ -847,7 +855,14 @@ __global__ void __launch_bounds__(CR_T) compact_reps_kernel(const uint32_t* __re
     const bool keep = s < cnt && (!rep || rep[s] == s);
     if (s < cnt && !keep && xlout) xlout[s] = 0u;
     bool err = false;
-    if (keep && rows) err = (*reinterpret_cast<const uint32_t*>(rows + (uint64_t)s * row_bytes) & emask) != 0u;
+    if (keep && rows) {
+      const uint8_t* row = rows + (uint64_t)s * row_bytes;
+      if (err_sel) {   // only the selected gates' errors (the trail's pass A)
+        for (uint32_t t = 0; t < slice_len && !err; ++t) err = err_sel[t] && row[4 + t];
+      } else {
+        err = (*reinterpret_cast<const uint32_t*>(row) & emask) != 0u;
+      }
+    }
     const bool k0 = keep && !err, k1 = keep && err;
     const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
     if (lane == 0) {
@@ -940,10 +955,12 @@ int launch_trail_project(const ProjSpec& spec, const TrailProjLaunch& L, void* s
   return (int)cudaGetLastError();
 }
 
-int launch_compact_reps(const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
+int launch_compact_reps(const uint8_t* d_err_sel, uint32_t slice_len,
+                        const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
                         const uint8_t* d_rows, uint32_t row_bytes, uint32_t emask, uint32_t* d_list2, uint32_t* d_count2,
                         void* stream) {
-  dev::compact_reps_kernel<<<1, dev::CR_T, 0, static_cast<cudaStream_t>(stream)>>>(d_rep, cnt, d_list, d_count, d_xlout,
+  dev::compact_reps_kernel<<<1, dev::CR_T, 0, static_cast<cudaStream_t>(stream)>>>(d_err_sel, slice_len, d_rep, cnt,
+                                                                             d_list, d_count, d_xlout,
                                                                              d_rows, row_bytes, emask, d_list2,
                                                                              d_count2);
   return (int)cudaGetLastError();

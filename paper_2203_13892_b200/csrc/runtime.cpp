@@ -75,6 +75,9 @@ struct tqsim_handle {
   tq::KGate* d_kgates = nullptr;   // also read by the small-state tree kernel (small.cu)
   // small-state tree (small.cu): the whole tree as one kernel, one warp per leaf
   bool small = false;
+  // conditional leaf sampling: a byte per leaf-slice gate, 1 = in pass A (the gates whose errors
+  // change the marginals; NoiseLevel::err_sel of the leaf level's dedup map)
+  uint8_t* d_trail_asel = nullptr;
 };
 
 namespace tq {
@@ -675,7 +678,10 @@ void run_level(Exec& x, uint32_t d, uint64_t i0, uint64_t i1, uint64_t parent_fi
       // the variant-1 pass's error bits of the noise row: the trail's marginal pass takes the
       // careful code on any error of the slice (mask_any), a level pass on its own bit
       const uint32_t em = h->pp.trail.on ? ~0u : 1u << std::min<size_t>(passes.size() - 1, 31);
-      ck(launch_compact_reps(maps + x.L.map_lvl[d] + (b - x.lvl_first[d]), (uint32_t)cnt, wl, wl + c, xl0,
+      const bool asel = h->pp.trail.on && h->d_trail_asel;   // (nostore: the trail is active)
+      ck(launch_compact_reps(asel ? h->d_trail_asel : nullptr,
+                             (uint32_t)(h->plan.bounds[d + 1] - h->plan.bounds[d]),
+                             maps + x.L.map_lvl[d] + (b - x.lvl_first[d]), (uint32_t)cnt, wl, wl + c, xl0,
                              split_clean ? rows : nullptr, row_bytes, em, wl + c + 1, split_clean ? wl + 2 * c + 1 : nullptr,
                              x.st),
          "work list launch");
@@ -976,6 +982,7 @@ void run_tree(Exec& x) {
     lv.map_off = x.L.map_lvl[d];
     lv.cap = x.L.cap[d];
     lv.arity = h->plan.arities[d];
+    lv.err_sel = d + 1 == levels && h->pp.trail.on ? h->d_trail_asel : nullptr;   // (dumps: no maps)
     total += lv.count;
   }
   NL.n_levels = (uint32_t)levels;
@@ -1107,6 +1114,15 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
         ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_kgates), sizeof(KGate) * std::max<size_t>(kg.size(), 1)),
             "cudaMalloc kraus gates");
         ckc(cudaMemcpy(h->d_kgates, kg.data(), sizeof(KGate) * kg.size(), cudaMemcpyHostToDevice), "kraus gates");
+      }
+      if (h->pp.trail.on && !h->kraus) {   // pass A's gates within the leaf slice
+        const size_t L = h->plan.arities.size();
+        const uint64_t b0 = h->plan.bounds[L - 1], len = h->plan.bounds[L] - b0;
+        std::vector<uint8_t> asel(std::max<uint64_t>(len, 1), 0);
+        const PassDesc& pa = h->pp.trail.a;
+        for (uint32_t oi = pa.op_begin; oi < pa.op_end; ++oi) asel.at(h->pp.ops[oi].gate - b0) = 1;
+        ckc(cudaMalloc(reinterpret_cast<void**>(&h->d_trail_asel), asel.size()), "cudaMalloc trail asel");
+        ckc(cudaMemcpy(h->d_trail_asel, asel.data(), asel.size(), cudaMemcpyHostToDevice), "trail asel");
       }
       if (!h->kraus) {
         // gate tables (gate sequence, qubit positions, matrices) become code + constant banks
@@ -1536,6 +1552,7 @@ void tqsim_destroy(tqsim_handle* h) {
   if (h->d_pass_of) cudaFree(h->d_pass_of);
   if (h->d_seed) cudaFree(h->d_seed);
   if (h->d_kgates) cudaFree(h->d_kgates);
+  if (h->d_trail_asel) cudaFree(h->d_trail_asel);
   if (h->h_tables_pinned) cudaFreeHost(h->h_tables_pinned);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);

@@ -186,7 +186,8 @@ int launch_noise_rows(const uint8_t* d_two, const uint8_t* d_pass_of, uint32_t s
 int launch_set_seed(uint64_t* d_seed, uint64_t seed, void* stream);
 // the batch's computed instances (rep[s] == s) in slot order -> list, *count; xlout (leaf level,
 // may be null) = 0 for the others
-int launch_compact_reps(const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
+int launch_compact_reps(const uint8_t* d_err_sel, uint32_t slice_len,   // d_err_sel: as NoiseLevel::err_sel
+                        const uint32_t* d_rep, uint32_t cnt, uint32_t* d_list, uint32_t* d_count, uint32_t* d_xlout,
                         const uint8_t* d_rows, uint32_t row_bytes, uint32_t emask, uint32_t* d_list2, uint32_t* d_count2,
                         void* stream);
 // All noise rows of a shard in one launch (one warp per instance of every level).
@@ -200,6 +201,10 @@ struct NoiseLevel {
   uint64_t map_off;
   uint64_t cap;
   uint32_t arity, pad2;
+  // which gates' errors make an instance "not error-free" for the dedup map: null = any gate
+  // of the slice (the row's pass bitmask); else a byte per slice gate (the conditional-sampling
+  // leaf level: only pass A's gates -- the marginals are of pass A's state)
+  const uint8_t* err_sel;
 };
 constexpr int NOISE_MAX_LEVELS = 64;
 struct NoiseLevels {

@@ -563,3 +563,29 @@ def test_relabel_with_store_map_case_vs_oracle(p):
                     d["seed"] % (1 << 40), opts, dumps=[(0, 1), (1, 5), (2, 17)])
     run_and_compare(d["n_qubits"], gates, NoiseModel(p, p, 0.02, 0.03), int(np.prod(d["arities"])), d["arities"],
                     d["seed"] % (1 << 40), opts)
+
+
+@pytest.mark.parametrize("n,tile,ar", [(14, 8, [2, 4, 6]), (16, 10, [3, 2, 8]), (12, 7, [2, 2, 2, 5])])
+def test_conditional_sampling_b_only_errors_share_marginals(n, tile, ar):
+    """Leaves whose errors all fall in the stage-2 gates B share their representative's marginals
+    (the dedup map of the conditional-sampling leaf level counts pass A's gates only, DESIGN.md
+    §6.2): noise on 1q gates only (p2 = 0), so many leaves draw errors only on the low-qubit RX
+    layer.  Outcomes equal the oracle's, and the run with every instance computed."""
+    from workloads.generators import qaoa_gates, random_3_regular_edges
+    rng = np.random.default_rng(3 * n + tile)
+    gates = qaoa_gates(n, random_3_regular_edges(n, rng), list(rng.uniform(0, 3, 2)), list(rng.uniform(0, 3, 2)))
+    nm = NoiseModel(0.03, 0.0, 0.02, 0.0)
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 4)
+    shots = int(np.prod(ar))
+    a = T.tqsim_run_ex(n, gates, noise, shots, ar, 5, opts, (), leaf_debug=True)
+    assert a.plan.trail_top_bits > 0
+    ref = simulate_tree(n, OG.lower(gates), oracle_plan_of(a.plan), nm, 5)
+    for l, r in ref.leaves.items():
+        assert a.leaf_u[l] == r.u
+        if not r.flagged:
+            assert int(a.leaf_outcomes[l]) == r.outcome, (l, int(a.leaf_outcomes[l]), r.outcome)
+    nd = T.tqsim_run_ex(n, gates, noise, shots, ar, 5, T.default_options(tile_qubits=tile, batch_log2_amps=n + 4,
+                                                                      no_dedup=1), leaf_debug=True)
+    assert np.array_equal(nd.leaf_outcomes, a.leaf_outcomes)
+    assert a.stats.computed_node_executions < nd.stats.computed_node_executions
