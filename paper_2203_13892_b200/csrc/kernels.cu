@@ -588,6 +588,87 @@ __global__ void __launch_bounds__(256) dedup_map_level_kernel(const uint8_t* __r
                   rep, pos);
 }
 
+// A leaf whose Pauli falls inside a diagonal unit on the TOP bits keeps the streaming
+// projection: the unit with its Paulis is monomial, U|idx> = D[idx] |idx ^ flip> (a Pauli pushed
+// through CX / diagonal gates stays a Pauli), idx = bit ua + 2 bit ub of the top index.  Applied
+// to the gates' basis states in slice order; returns the flip as a mask over the top bits.
+// (Units on the low bits would move the rows read: those leaves go to the generated kernel.)
+__device__ __forceinline__ void proj_pauli(uint32_t c, int& b, cd& amp) {
+  if (c == 1u) {
+    b ^= 1;
+  } else if (c == 2u) {   // Y|0> = i|1>, Y|1> = -i|0>
+    amp = b ? cd{amp.y, -amp.x} : cd{-amp.y, amp.x};
+    b ^= 1;
+  } else if (c == 3u && b) {
+    amp = {-amp.x, -amp.y};
+  }
+}
+__device__ uint32_t proj_unit_eff(const ProjSpec& sp, uint32_t u, const unsigned char* codes, cd* D) {
+  const bool one = sp.ua[u] == sp.ub[u];
+  uint32_t xm = 0;
+  for (int idx = 0; idx < 4; ++idx) {
+    if (one && (idx == 1 || idx == 2)) {
+      D[idx] = {0.0, 0.0};
+      continue;
+    }
+    int ba = idx & 1, bb = idx >> 1;
+    cd amp = {1.0, 0.0};
+    for (uint32_t g = 0; g < sp.ugn[u]; ++g) {
+      const uint32_t k = sp.ugk[u][g], code = codes[4 + sp.ugoff[u][g]];
+      uint32_t pa = 0, pb = 0;
+      if (k <= 1u) {   // 1q diagonal
+        const double* d = sp.ugd[u][g];
+        const cd e = (k == 0u ? ba : bb) ? cd{d[2], d[3]} : cd{d[0], d[1]};
+        amp = {amp.x * e.x - amp.y * e.y, amp.x * e.y + amp.y * e.x};
+        (k == 0u ? pa : pb) = code;
+      } else {         // CX(ua -> ub) / CZ(ua, ub), then the Pauli pair (q0 = code >> 2 on ua)
+        if (k == 2u) {
+          if (ba) bb ^= 1;
+        } else if (ba && bb) {
+          amp = {-amp.x, -amp.y};
+        }
+        pa = code >> 2;
+        pb = code & 3u;
+      }
+      proj_pauli(pa, ba, amp);
+      if (one) bb = ba;
+      proj_pauli(pb, bb, amp);
+      if (one) ba = bb;
+    }
+    const int f = idx ^ (ba | (bb << 1));
+    if (f & 1) xm |= 1u << sp.ua[u];
+    if (f & 2) xm |= 1u << sp.ub[u];
+    D[idx] = amp;
+  }
+  return xm;
+}
+__device__ __forceinline__ bool proj_unit_erred(const ProjSpec& sp, uint32_t u, const unsigned char* codes) {
+  bool e = false;
+  for (uint32_t g = 0; g < sp.ugn[u]; ++g) e |= codes[4 + sp.ugoff[u][g]] != 0;
+  return e;
+}
+// c[y] = prod_j U_j[sel_j][cur_j] * (the units' factors along the walk cur: y -> y ^ flips),
+// E/X/on: the leaf's effective operators of the erred top units (else the planned tables)
+__device__ __forceinline__ cd proj_coef(const ProjSpec& sp, const cd (*U)[4], uint32_t sel, uint32_t y,
+                                        const cd (*E)[4], const uint32_t* X, const uint8_t* on) {
+  uint32_t cur = y;
+  for (uint32_t u = 0; u < sp.nug; ++u)
+    if (on[u]) cur ^= X[u];
+  cd v = {1.0, 0.0};
+  for (uint32_t j = 0; j < sp.m; ++j) {
+    const cd e = U[j][2 * ((sel >> j) & 1u) + ((cur >> j) & 1u)];
+    v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
+  }
+  cur = y;
+  for (uint32_t u = 0; u < sp.nug; ++u) {
+    const uint32_t idx = ((cur >> sp.ua[u]) & 1u) | (((cur >> sp.ub[u]) & 1u) << 1);
+    const cd e = on[u] ? E[u][idx] : cd{sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
+    v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
+    if (on[u]) cur ^= X[u];
+  }
+  return v;
+}
+
 // Conditional leaf sampling, projection onto the chosen top bits for pass A
 // = diagonal units then 1q gates on the top bits (ProjSpec): per leaf s with top bits sel,
 //   psi_s(x) = D_x(x) * sum_y c_s[y] * phi(y 2^n2 + x),  c_s[y] = prod_j U_j[sel_j][y_j] * D_top(y),
@@ -601,14 +682,22 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
   (void)seedp;
   __shared__ cd U[16][4];
   __shared__ cd coef[1 << 10];
+  __shared__ cd UE[PROJ_MAX_U][4];
+  __shared__ uint32_t UX[PROJ_MAX_U];
+  __shared__ uint8_t UON[PROJ_MAX_U];
   __shared__ int skip;
   const uint32_t s = blockIdx.x % L.batch, c = blockIdx.x / L.batch;
   const unsigned char* codes = L.rows + (uint64_t)s * L.row_bytes;
-  if (threadIdx.x == 0) {
-    int e = 0;
-    for (uint32_t i = 0; i < sp.ndg; ++i) e |= codes[4 + sp.dgoff[i]] != 0;
+  if (threadIdx.x == 0) {   // a Pauli inside a low-bit unit: the generated kernel
+    bool e = false;
+    for (uint32_t u = sp.nug; u < sp.nug + sp.nux; ++u) e |= proj_unit_erred(sp, u, codes);
     skip = e;
     if (e && c == 0) L.glist[atomicAdd(L.gcount, 1u)] = s;
+  }
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + sp.nug) {   // the top units under this leaf's Paulis
+    const uint32_t u = threadIdx.x - 32;
+    UON[u] = proj_unit_erred(sp, u, codes);
+    UX[u] = UON[u] ? proj_unit_eff(sp, u, codes, UE[u]) : 0u;
   }
   if (threadIdx.x < sp.m) {   // U_j: the top qubit's gates with their Paulis, in slice order
     cd u[4] = {{1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {1.0, 0.0}};
@@ -639,19 +728,8 @@ __global__ void __launch_bounds__(PT) trail_project_kernel(const __grid_constant
   if (skip) return;
   const uint32_t sel = L.hsel[s];
   const uint32_t Y = 1u << sp.m;
-  for (uint32_t y = threadIdx.x; y < Y; y += PT) {   // c[y] = prod_j U_j[sel_j][y_j] * D_top(y)
-    cd v = {1.0, 0.0};
-    for (uint32_t j = 0; j < sp.m; ++j) {
-      const cd e = U[j][2 * ((sel >> j) & 1u) + ((y >> j) & 1u)];
-      v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
-    }
-    for (uint32_t u = 0; u < sp.nug; ++u) {
-      const uint32_t idx = ((y >> sp.ua[u]) & 1u) | (((y >> sp.ub[u]) & 1u) << 1);
-      const cd e = {sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
-      v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
-    }
-    coef[y] = v;
-  }
+  for (uint32_t y = threadIdx.x; y < Y; y += PT)   // c[y] = prod_j U_j[sel_j][y_j] * D_top(y)
+    coef[y] = proj_coef(sp, U, sel, y, UE, UX, UON);
   __syncthreads();
   const uint64_t j = L.child_first + s;
   uint64_t pj = j / L.arity - L.parent_first;
@@ -702,6 +780,9 @@ __global__ void __launch_bounds__(QT, MINB) trail_project_pair_kernel(const __gr
                                                                 uint32_t pf) {
   extern __shared__ cd pcoef[];   // [2][2^m]
   __shared__ cd U[2][16][4];
+  __shared__ cd UE[2][PROJ_MAX_U][4];
+  __shared__ uint32_t UX[2][PROJ_MAX_U];
+  __shared__ uint8_t UON[2][PROJ_MAX_U];
   __shared__ int live[2];
   const uint64_t pfirst = L.child_first / 2;
   const uint32_t npar = (uint32_t)((L.child_first + L.batch - 1) / 2 - pfirst + 1);
@@ -722,13 +803,19 @@ __global__ void __launch_bounds__(QT, MINB) trail_project_pair_kernel(const __gr
   const uint64_t j0 = P * 2 > L.child_first ? P * 2 : L.child_first;
   const uint64_t j1 = P * 2 + 2 < L.child_first + L.batch ? P * 2 + 2 : L.child_first + L.batch;
   const uint32_t nc = (uint32_t)(j1 - j0), s0 = (uint32_t)(j0 - L.child_first);
-  if (threadIdx.x < nc) {   // a child with a Pauli inside a diagonal unit -> the generated kernel
+  if (threadIdx.x < nc) {   // a child with a Pauli inside a low-bit unit -> the generated kernel
     const uint32_t sl = s0 + threadIdx.x;
     const unsigned char* codes = L.rows + (uint64_t)sl * L.row_bytes;
-    int e = 0;
-    for (uint32_t i = 0; i < sp.ndg; ++i) e |= codes[4 + sp.dgoff[i]] != 0;
+    bool e = false;
+    for (uint32_t u = sp.nug; u < sp.nug + sp.nux; ++u) e |= proj_unit_erred(sp, u, codes);
     live[threadIdx.x] = !e;
     if (e && c == 0) L.glist[atomicAdd(L.gcount, 1u)] = sl;
+  }
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + nc * sp.nug) {   // top units under each child's Paulis
+    const uint32_t ci = (threadIdx.x - 64) / sp.nug, u = (threadIdx.x - 64) % sp.nug;
+    const unsigned char* codes = L.rows + (uint64_t)(s0 + ci) * L.row_bytes;
+    UON[ci][u] = proj_unit_erred(sp, u, codes);
+    UX[ci][u] = UON[ci][u] ? proj_unit_eff(sp, u, codes, UE[ci][u]) : 0u;
   }
   if (threadIdx.x < nc * sp.m) {   // U_j of child ci: the top qubit's gates with their Paulis
     const uint32_t ci = threadIdx.x / sp.m, jb = threadIdx.x % sp.m;
@@ -762,19 +849,7 @@ __global__ void __launch_bounds__(QT, MINB) trail_project_pair_kernel(const __gr
   for (uint32_t i = threadIdx.x; i < 2 * Y; i += QT) {   // c_ci[y] = prod_j U_j[sel_j][y_j] * D_top(y)
     const uint32_t ci = i / Y, y = i % Y;
     cd v = {0.0, 0.0};
-    if (ci < nc) {
-      const uint32_t sel = L.hsel[s0 + ci];
-      v = {1.0, 0.0};
-      for (uint32_t j = 0; j < sp.m; ++j) {
-        const cd e = U[ci][j][2 * ((sel >> j) & 1u) + ((y >> j) & 1u)];
-        v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
-      }
-      for (uint32_t u = 0; u < sp.nug; ++u) {
-        const uint32_t idx = ((y >> sp.ua[u]) & 1u) | (((y >> sp.ub[u]) & 1u) << 1);
-        const cd e = {sp.uT[u][2 * idx], sp.uT[u][2 * idx + 1]};
-        v = {v.x * e.x - v.y * e.y, v.x * e.y + v.y * e.x};
-      }
-    }
+    if (ci < nc) v = proj_coef(sp, U[ci], L.hsel[s0 + ci], y, UE[ci], UX[ci], UON[ci]);
     pcoef[i] = v;
   }
   __syncthreads();

@@ -320,6 +320,12 @@ void plan_trail(PassPlan& pp, const std::vector<LGate>& gates, const Plan& plan,
     uint64_t touched = 0;   // top qubits that already got a 1q gate
     std::vector<std::array<double, 8>> ug, ux;
     std::vector<std::pair<uint32_t, uint32_t>> uqg, uqx;
+    struct UnitGates {   // the unit's gates (ProjSpec::ugn / ugk / ugoff / ugd)
+      uint8_t n = 0, k[3] = {0, 0, 0};
+      uint32_t off[3] = {0, 0, 0};
+      double d[3][4] = {};
+    };
+    std::vector<UnitGates> ugg, ugx;
     auto cmul = [](const double* a, const double* b, double* o) {   // o = a * b (complex)
       o[0] = a[0] * b[0] - a[1] * b[1];
       o[1] = a[0] * b[1] + a[1] * b[0];
@@ -356,15 +362,33 @@ void plan_trail(PassPlan& pp, const std::vector<LGate>& gates, const Plan& plan,
           T[2 * idx] = amp[0];
           T[2 * idx + 1] = amp[1];
         }
+        UnitGates ugs;
+        ugs.n = (uint8_t)du;
+        for (size_t t2 = 0; t2 < du && t2 < 3; ++t2) {
+          const LGate& g = gates[A[i + t2]];
+          ugs.off[t2] = A[i + t2] - b0;
+          if (g.op == OP_CX) ugs.k[t2] = 2;
+          else if (g.op == OP_CZ) ugs.k[t2] = 3;
+          else {
+            ugs.k[t2] = g.q0 == qa ? 0 : 1;
+            ugs.d[t2][0] = g.m[0];
+            ugs.d[t2][1] = g.m[1];
+            ugs.d[t2][2] = g.m[6];
+            ugs.d[t2][3] = g.m[7];
+          }
+        }
+        if (du > 3) ok = false;
         const bool ga = (int)qa >= n2, gb = (int)qb >= n2;
         if (ga != gb) ok = false;                                      // couples top and low bits
         if (ga && ((touched >> qa & 1) || (touched >> qb & 1))) ok = false;   // after a top 1q gate
         if (ga) {
           uqg.push_back({qa - n2, qb - n2});
           ug.push_back(T);
+          ugg.push_back(ugs);
         } else {
           uqx.push_back({qa, qb});
           ux.push_back(T);
+          ugx.push_back(ugs);
         }
         for (size_t t2 = 0; t2 < du; ++t2) {
           if (ps.ndg >= (uint32_t)PROJ_MAX_DG) { ok = false; break; }
@@ -389,15 +413,25 @@ void plan_trail(PassPlan& pp, const std::vector<LGate>& gates, const Plan& plan,
       ps.nug = (uint32_t)ug.size();
       ps.nux = (uint32_t)ux.size();
       size_t k = 0;
+      auto put_gates = [&](size_t kk, const UnitGates& s) {
+        ps.ugn[kk] = s.n;
+        for (int t2 = 0; t2 < 3; ++t2) {
+          ps.ugk[kk][t2] = s.k[t2];
+          ps.ugoff[kk][t2] = s.off[t2];
+          for (int e = 0; e < 4; ++e) ps.ugd[kk][t2][e] = s.d[t2][e];
+        }
+      };
       for (size_t u = 0; u < ug.size(); ++u, ++k) {
         ps.ua[k] = uqg[u].first;
         ps.ub[k] = uqg[u].second;
         for (int e = 0; e < 8; ++e) ps.uT[k][e] = ug[u][e];
+        put_gates(k, ugg[u]);
       }
       for (size_t u = 0; u < ux.size(); ++u, ++k) {
         ps.ua[k] = uqx[u].first;
         ps.ub[k] = uqx[u].second;
         for (int e = 0; e < 8; ++e) ps.uT[k][e] = ux[u][e];
+        put_gates(k, ugx[u]);
       }
       t.fast = std::getenv("TQSIM_TRAIL_FAST") == nullptr || std::getenv("TQSIM_TRAIL_FAST")[0] != '0';
     }

@@ -112,6 +112,12 @@ struct ProjSpec {
   uint32_t ua[PROJ_MAX_U], ub[PROJ_MAX_U];   // units: [0, nug) top-bit indices, [nug, nug+nux) qubits < n2
   double uT[PROJ_MAX_U][8];         // phase by bit_a + 2 bit_b (complex)
   uint32_t dgoff[PROJ_MAX_DG];      // slice offsets of every diagonal-unit gate
+  // each unit's gates (1, or 3 for CX.D.CX), for its effective operator under a leaf's Paulis:
+  // kind 0 = 1q diagonal on ua, 1 = 1q diagonal on ub, 2 = CX(ua -> ub), 3 = CZ(ua, ub)
+  uint8_t ugn[PROJ_MAX_U];
+  uint8_t ugk[PROJ_MAX_U][3];
+  uint32_t ugoff[PROJ_MAX_U][3];    // slice offsets (noise codes)
+  double ugd[PROJ_MAX_U][3][4];     // kind 0/1: diag(d0, d1) as (re, im, re, im)
 };
 
 // Conditional leaf sampling through the trailing layer (passplan.cpp plan_trail)

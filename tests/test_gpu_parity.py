@@ -589,3 +589,41 @@ def test_conditional_sampling_b_only_errors_share_marginals(n, tile, ar):
                                                                       no_dedup=1), leaf_debug=True)
     assert np.array_equal(nd.leaf_outcomes, a.leaf_outcomes)
     assert a.stats.computed_node_executions < nd.stats.computed_node_executions
+
+
+@pytest.mark.parametrize("n,tile,p,ar,tl", [(14, 8, 0.2, [8, 8], 3), (16, 10, 0.1, [8, 8], 4),
+                                            (12, 7, 0.6, [4, 16], 3)])
+def test_streaming_projection_top_unit_paulis_vs_oracle(n, tile, p, ar, tl):
+    """Paulis inside diagonal units on the TOP bits stay in the streaming projection (the unit
+    with its Paulis is monomial: per-leaf effective diagonal + top-bit flips, kernels.cu
+    proj_unit_eff); the leaf slice's units are all on the top bits, so no leaf is handed over.
+    Outcomes equal the oracle's and the stored-state path's."""
+    from workloads.generators import g1, g2
+    rng = np.random.default_rng(n + tile)
+    m = tile - tl
+    top = list(range(n - m, n))
+    suffix = []   # the leaf slice: top units (CX.RZ.CX, CZ), low gates, the RX layer
+    for (a, b) in [(top[0], top[1]), (top[2], top[-1]), (top[1], top[3]), (top[-1], top[0])]:
+        suffix += [g2("cx", a, b), g1("rz", b, float(rng.uniform(0, 6))), g2("cx", a, b)]
+    suffix += [g2("cz", top[0], top[2]), g1("t", 1), g2("cx", 0, 2)]
+    suffix += [g1("rx", q, float(rng.uniform(0, 3))) for q in range(n)]
+    prefix = [g1("h", q) for q in range(n)]   # as many lowered gates: the first slice of a 2-level plan
+    while len(OG.lower(prefix)) < len(OG.lower(suffix)):
+        q = int(rng.integers(0, n - 1))
+        prefix += [g1("ry", q, float(rng.uniform(0, 3))), g2("cx", q, q + 1)]
+    while len(OG.lower(prefix)) > len(OG.lower(suffix)):
+        prefix = prefix[:-1]
+    gs = prefix + suffix
+    nm = NoiseModel(p, p, 0.02, 0.03)
+    noise = T.noise_arg(nm.p1, nm.p2, nm.readout_p01, nm.readout_p10)
+    opts = T.default_options(tile_qubits=tile, batch_log2_amps=n + 3, trail_low=tl)
+    shots = int(np.prod(ar))
+    a = T.tqsim_run_ex(n, gs, noise, shots, ar, 17, opts, (), leaf_debug=True)
+    assert a.plan.trail_top_bits > 0 and a.plan.trail_fast == 1
+    b = T.tqsim_run_ex(n, gs, noise, shots, ar, 17, opts, [(len(ar) - 1, 0)])            # stored path
+    ref = simulate_tree(n, OG.lower(gs), oracle_plan_of(a.plan), nm, 17)
+    for l, r in ref.leaves.items():
+        if r.flagged:
+            continue
+        assert int(a.leaf_outcomes[l]) == r.outcome, (l, int(a.leaf_outcomes[l]), r.outcome)
+        assert int(b.leaf_outcomes[l]) == r.outcome
