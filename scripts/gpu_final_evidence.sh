@@ -3,10 +3,12 @@
 # of the top families, one --set full capture of the C4 top kernel.   bash scripts/gpu_final_evidence.sh TAG
 TAG=$1; O=gpurun_out/$TAG; mkdir -p $O
 nvidia-smi > $O/smi.txt 2>&1
+timeout 2400 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo "pytest_rc=$?" >> $O/pytest.log
+timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > $O/smoke.log 2>&1; echo "smoke_rc=$?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err; echo "rc=$?" >> $O/bench_c4.err
 timeout 600 python bench.py --config c2_qft15 > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 900 python bench.py --config c3_brick20 --steps 5 > $O/bench_c3.json 2> $O/bench_c3.err
-timeout 900 python bench.py --config c5_hea28 --shard 0/16 --steps 3 --no-e2e --no-dedup-steps 0 --cpu-budget 10 > $O/bench_c5s.json 2> $O/bench_c5s.err
+timeout 900 python bench.py --config c5_hea28 --shard 0/16 --steps 3 --no-e2e --no-dedup-steps 0 --no-cpu > $O/bench_c5s.json 2> $O/bench_c5s.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > $O/bench_ref.json 2> $O/bench_ref.err
 bash scripts/ncu_ll.sh c4_qaoa24 $TAG/c4ll
 bash scripts/ncu_fp64.sh c4_qaoa24 $TAG/c4fp "tq_trail_a_v1|tq_pass_l[5-8]" 400
