@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup-steps", type=int, default=2,
                     help="also time this many steps with options.no_dedup=1 (0 = skip)")
+    ap.add_argument("--flat-shots", type=int, default=0,
+                    help="time the flat baseline on this many shots (0 = auto: all for n <= 16, else "
+                         "min(shots, 1024); -1 = skip)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--batch-log2", type=int, default=0)
@@ -473,6 +476,43 @@ def main():
         del ws2
         torch.cuda.empty_cache()
 
+    # the paper's baseline: every shot simulated on its own (the flat plan (F),
+    # options.no_dedup = 1), timed on F shots of the same circuit and noise; flat work is
+    # linear in shots, so ms per N shots = ms(F) * N / F
+    flat = None
+    if args.flat_shots >= 0 and not shard_w and world == 1:
+        F = args.flat_shots or (N if n <= 16 else min(N, 1024))
+        try:
+            del ws
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        h3 = T.tqsim_create(n, gates, noise, F, [F],
+                            T.default_options(tile_qubits=args.tile, batch_log2_amps=args.batch_log2, no_dedup=1))
+        assert list(h3.plan.arity_list) == [F]
+        ws3 = torch.empty(h3.workspace_bytes(0, 1), dtype=torch.uint8, device=dev)
+        out3 = torch.zeros(F, dtype=torch.int32, device=dev)
+        h3.execute(3000, 0, 1, st.cuda_stream, ws3.data_ptr(), ws3.numel(), out3.data_ptr())
+        torch.cuda.synchronize(dev)
+        fsteps = 2
+        e0.record(st)
+        for i in range(fsteps):
+            h3.execute(3100 + i, 0, 1, st.cuda_stream, ws3.data_ptr(), ws3.numel(), out3.data_ptr())
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        ms3 = e0.elapsed_time(e1) / fsteps
+        per_n = ms3 * N / F
+        flat = {"shots_timed": F, "ms_per_timed_step": ms3, "ms_per_n_shots": per_n,
+                "shots_per_s": F / (ms3 * 1e-3), "steps": fsteps,
+                "speedup_tree_vs_flat": per_n / ms_step,
+                "speedup_tree_no_dedup_vs_flat": (per_n / no_dedup["ms_per_step"]) if no_dedup else None,
+                "note": "flat plan (F) with options.no_dedup = 1: each shot runs the whole circuit on its own "
+                        "state (the paper's baseline); ms_per_n_shots scales the F-shot time to this config's "
+                        "%d shots (flat work is linear in shots)" % N}
+        h3.close()
+        del ws3, out3
+        torch.cuda.empty_cache()
+
     # end to end through the public API with HOST buffers
     e2e = None
     if not args.no_e2e and not args.shard:
@@ -549,6 +589,7 @@ def main():
                              "computed",
             "tree_vs_flat_gate_ratio": plan.flat_gate_amp_updates / plan.gate_amp_updates,
             "no_dedup": no_dedup,
+            "flat": flat,
             "roofline": roofline,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
