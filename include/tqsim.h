@@ -87,15 +87,16 @@ typedef struct {
  * 1 - exp(-2t/t2 + t/t1), t = gate_time_1q / gate_time_2q, requires t2 <= 2 t1),
  * amplitude damping (amp_damping = gamma) and phase damping (phase_damping = lambda),
  * each unravelled as a keyed quantum trajectory (R34-R35).  Any of them enabled selects
- * the Kraus engine: the state of every trajectory resident in one CTA's shared memory,
- * n_qubits <= 13 (TQSIM_EINVAL otherwise).  0 = off. */
+ * the Kraus engine: the state of every trajectory resident in shared memory -- one CTA's
+ * for n_qubits <= 13, a thread-block cluster of 2^(n-13) CTAs (distributed shared memory)
+ * for 14..16; n_qubits <= 16 (TQSIM_EINVAL otherwise).  0 = off. */
 typedef struct {
   double p1, p2, readout_p01, readout_p10;
   double amp_damping, phase_damping;
   double t1, t2, gate_time_1q, gate_time_2q;   /* seconds */
 } tqsim_noise_model;
 
-#define TQSIM_KRAUS_MAX_QUBITS 13
+#define TQSIM_KRAUS_MAX_QUBITS 16
 
 /* Small-state tree (SURVEY §8(a) kernel notes): a circuit of at most this
  * many qubits (Pauli noise only) may run the whole tree as ONE kernel -- one warp per leaf,

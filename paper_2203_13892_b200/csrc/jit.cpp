@@ -1315,12 +1315,28 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
   {
     // the next item's index (and, fan-out, its parent slot) is loaded one item ahead, so the
     // dependent index loads (work list -> parent map -> tile) do not stall each item's start
+    // item order: tile-major (w = i + nw t: concurrent CTAs take the same tile of many
+    // instances) or instance-major (w = t + 2^n_out i: concurrent CTAs sweep consecutive
+    // tiles of few instances).  Instance-major for states of <= 256 tiles (C2's leaf pass
+    // 0.90 -> 0.86 ms per tree; neutral on C3/C4: profiles/r02_ab_item_order.txt);
+    // TQSIM_ITEM_ORDER=0/1 forces one.
+    static const int order_env = [] {
+      const char* e = std::getenv("TQSIM_ITEM_ORDER");
+      return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool inst_major = order_env >= 0 ? order_env == 1 : pd.n_out <= 8;
     o << "  const tq_u32 nw = a.wlist ? *a.wcount : a.batch;\n"
-      << "  const tq_u64 tq_tot = (tq_u64)nw << " << pd.n_out << ";\n"
-      << "  const tq_u32 tq_gm = nw ? (tq_u32)(gridDim.x % nw) : 0u;\n"
-      << "  const tq_u64 tq_gd = nw ? gridDim.x / nw : 0ull;\n"
-      << "  tq_u32 tq_i = nw ? (tq_u32)(bid % nw) : 0u;\n  tq_u64 tq_t = nw ? bid / nw : 0ull;\n"
-      << "  tq_u32 tq_snx = 0u;\n"
+      << "  const tq_u64 tq_tot = (tq_u64)nw << " << pd.n_out << ";\n";
+    if (inst_major)
+      o << "  const tq_u32 tq_gm = (tq_u32)(gridDim.x >> " << pd.n_out << ");\n"
+        << "  const tq_u64 tq_gd = gridDim.x & " << ((1ull << pd.n_out) - 1) << "ull;\n"
+        << "  tq_u32 tq_i = (tq_u32)(bid >> " << pd.n_out << ");\n  tq_u64 tq_t = bid & " << ((1ull << pd.n_out) - 1)
+        << "ull;\n";
+    else
+      o << "  const tq_u32 tq_gm = nw ? (tq_u32)(gridDim.x % nw) : 0u;\n"
+        << "  const tq_u64 tq_gd = nw ? gridDim.x / nw : 0ull;\n"
+        << "  tq_u32 tq_i = nw ? (tq_u32)(bid % nw) : 0u;\n  tq_u64 tq_t = nw ? bid / nw : 0ull;\n";
+    o << "  tq_u32 tq_snx = 0u;\n"
       << "  if (bid < tq_tot) tq_snx = a.wlist ? a.wlist[tq_i] : tq_i;\n";
     if (mode == 1)
       o << "  tq_u64 tq_pnx = ((tq_u64)a.child_first + tq_snx) / a.arity - a.parent_first;\n"
@@ -1328,8 +1344,12 @@ std::string gen_pass(const PassDesc& pd, const PassPlan& pp, const std::vector<L
     o << "  for (tq_u64 w = bid; w < tq_tot; w += gridDim.x) {\n"
       << "  const tq_u32 s = tq_snx;\n  const tq_u64 t = tq_t;\n";
     if (mode == 1) o << "  const tq_u64 tq_pcur = tq_pnx;\n";
-    o << "  tq_i += tq_gm;\n  tq_t += tq_gd;\n  if (tq_i >= nw) { tq_i -= nw; ++tq_t; }\n"   // w + gridDim.x
-      << "  const tq_u64 tq_wn = w + gridDim.x;\n"
+    if (inst_major)
+      o << "  tq_i += tq_gm;\n  tq_t += tq_gd;\n  if (tq_t >= " << (1ull << pd.n_out) << "ull) { tq_t -= "
+        << (1ull << pd.n_out) << "ull; ++tq_i; }\n";   // w + gridDim.x
+    else
+      o << "  tq_i += tq_gm;\n  tq_t += tq_gd;\n  if (tq_i >= nw) { tq_i -= nw; ++tq_t; }\n";   // w + gridDim.x
+    o << "  const tq_u64 tq_wn = w + gridDim.x;\n"
       << "  if (tq_wn < tq_tot) tq_snx = a.wlist ? a.wlist[tq_i] : tq_i;\n";
   }
   if (variant == 3)   // the leaf's chosen top bits (the select kernel's chunk)
@@ -2871,7 +2891,13 @@ int launch_jit_pass(const JitPass& jp, const PassDesc& pd, const PassLaunch& L, 
   if (L.variant == 3 && L.wlist) grid = std::min<uint64_t>(grid, 4 * 148);   // persistent over the work list
   if (L.variant == 1 && L.wlist) {   // persistent over the batch's representatives
     const uint64_t per_sm = (uint64_t)jit_ctas_per_sm(pd.K, (int)jp.threads, L.clean != 0);
-    grid = std::min<uint64_t>(grid, per_sm * 148 * 2);
+    // TQSIM_PERSIST_WAVES: CTAs per resident slot (1 / 2 / 4: C4's marginal pass 148.6 /
+    // 145.5 / 142.8 ms per tree, C2 neutral: profiles/r02_ab_item_order.txt)
+    static const uint64_t waves = [] {
+      const char* e = std::getenv("TQSIM_PERSIST_WAVES");
+      return (uint64_t)(e ? std::max(1, std::atoi(e)) : 4);
+    }();
+    grid = std::min<uint64_t>(grid, per_sm * 148 * waves);
   }
   if (grid == 0) return 0;
   if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidConfiguration;

@@ -20,6 +20,7 @@
 //   4. psi <- (M_0 (x) M_1) psi
 // and at the end store the state for the children (HBM), or, at a leaf, sample it in place
 // (block scan of |a|^2, smallest x with C(x) > u*total, R9; readout flips, R11).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "tq_device_common.cuh"
@@ -106,12 +107,15 @@ struct KrausShared {
 };
 
 // Joint |a|^2 table over (bit q0, bit q1): tbl[b0 + 2 b1].  Fixed-order block reduction.
-__device__ __forceinline__ void k_joint_table(const kd2* psi, int n, int q0, int q1, KrausShared& sh) {
+// (goff: the global index of psi[0] -- a cluster CTA's slice, see kraus_cluster_kernel)
+__device__ __forceinline__ void k_joint_table(const kd2* psi, int n, int q0, int q1, KrausShared& sh,
+                                              uint32_t goff = 0u) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const uint32_t N = 1u << n;
   for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
     const kd2 a = psi[i];
-    const uint32_t k = ((i >> q0) & 1u) | (((i >> q1) & 1u) << 1);
+    const uint32_t gi = goff | i;
+    const uint32_t k = ((gi >> q0) & 1u) | (((gi >> q1) & 1u) << 1);
     const double p = a.x * a.x + a.y * a.y;
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[t] += (k == (uint32_t)t) ? p : 0.0;
@@ -334,6 +338,243 @@ __global__ void __launch_bounds__(KT) kraus_slice_kernel(const __grid_constant__
   if (a.dbg_flag) a.dbg_flag[leaf] = (uint8_t)flag;
 }
 
+// ---------------------------------------------------------------------------------------
+// Widths 14..16: the state is spread over a thread-block CLUSTER of CL = 2^(n-13) CTAs, each
+// holding a 2^13-amplitude slice (128 KiB) in its shared memory; global index i lives in rank
+// i >> 13 at slot i & (2^13 - 1).  Gates on the slice's qubits stay in the CTA; gates on the
+// top qubits pair amplitudes across CTAs through distributed shared memory (DSMEM,
+// map_shared_rank).  Every gate / Kraus sweep enumerates its pairs globally, CTA r taking the
+// r-th contiguous share (for a slice qubit that share is exactly its own slice), with a
+// cluster barrier between sweeps.  The joint table: each CTA reduces its slice, then every CTA
+// sums the CL partial tables in rank order, so all CTAs hold the same table and take the same
+// R33 decisions.  The leaf sample: per-CTA totals summed in rank order, the CTA whose range
+// holds u * total finishes the search (R9, R11) -- the same rules as kraus_slice_kernel.
+constexpr int KCQ = 13;   // qubits per CTA slice
+
+struct KrausClusterShared {
+  KrausShared k;
+  double tsum[4];
+  double ctot;
+  int found;
+  kd2* rp[8];   // every rank's slice (generic DSMEM addresses)
+};
+
+__device__ __forceinline__ kd2* kc_at(const KrausClusterShared& sh, uint32_t i) {
+  return sh.rp[i >> KCQ] + (i & ((1u << KCQ) - 1u));
+}
+
+// psi <- m psi on qubit q over the cluster's state (pairs p of CTA rank: [rank per, (rank+1) per))
+__device__ __forceinline__ void kc_apply_1q(const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL, int q,
+                                            const kd2 m0, const kd2 m1, const kd2 m2, const kd2 m3) {
+  const uint32_t per = (1u << (n - 1)) / CL, lowm = (1u << q) - 1u;
+  for (uint32_t p = rank * per + threadIdx.x; p < (rank + 1) * per; p += blockDim.x) {
+    const uint32_t i0 = ((p >> q) << (q + 1)) | (p & lowm), i1 = i0 | (1u << q);
+    kd2* A = kc_at(sh, i0);
+    kd2* B = kc_at(sh, i1);
+    const kd2 a = *A, b = *B;
+    *A = kadd(kmul(m0, a), kmul(m1, b));
+    *B = kadd(kmul(m2, a), kmul(m3, b));
+  }
+}
+
+__device__ __forceinline__ void kc_apply_real(const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL, int q,
+                                              double a00, double a01, double a10, double a11) {
+  const uint32_t per = (1u << (n - 1)) / CL, lowm = (1u << q) - 1u;
+  for (uint32_t p = rank * per + threadIdx.x; p < (rank + 1) * per; p += blockDim.x) {
+    const uint32_t i0 = ((p >> q) << (q + 1)) | (p & lowm), i1 = i0 | (1u << q);
+    kd2* A = kc_at(sh, i0);
+    kd2* B = kc_at(sh, i1);
+    const kd2 a = *A, b = *B;
+    *A = kd2{a00 * a.x + a01 * b.x, a00 * a.y + a01 * b.y};
+    *B = kd2{a10 * a.x + a11 * b.x, a10 * a.y + a11 * b.y};
+  }
+}
+
+__device__ __forceinline__ void kc_apply_2q(const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL, bool cx,
+                                            int c, int t) {
+  const uint32_t per = (1u << (n - 2)) / CL;
+  const int lo = c < t ? c : t, hi = c < t ? t : c;
+  for (uint32_t p = rank * per + threadIdx.x; p < (rank + 1) * per; p += blockDim.x) {
+    const uint32_t b = k_insert2(p, lo, hi) | (1u << c), b1 = b | (1u << t);
+    if (cx) {
+      kd2* A = kc_at(sh, b);
+      kd2* B = kc_at(sh, b1);
+      const kd2 v = *A;
+      *A = *B;
+      *B = v;
+    } else {
+      kd2* B = kc_at(sh, b1);
+      *B = kd2{-B->x, -B->y};
+    }
+  }
+}
+
+__global__ void __launch_bounds__(KT) kraus_cluster_kernel(const __grid_constant__ KrausArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ kd2 psi[];
+  __shared__ KrausClusterShared sh;
+  const int n = (int)a.n;
+  const uint32_t CL = 1u << (n - KCQ), L = 1u << KCQ;
+  const uint32_t rank = cl.block_rank();
+  const uint32_t goff = rank << KCQ;
+  const uint32_t s = blockIdx.x / CL;
+  const uint64_t j = a.child_first + s;
+  const uint64_t seed = *a.seedp;
+  const kd2* __restrict__ gsrc = reinterpret_cast<const kd2*>(a.src);
+  if (threadIdx.x < CL) sh.rp[threadIdx.x] = cl.map_shared_rank(psi, (int)threadIdx.x);
+  if (threadIdx.x == 0) sh.k.flag = 0u;
+  uint64_t pj = 0;
+  if (a.mode == 1) {   // fan-out: this rank's slice of the parent's state
+    pj = j / a.arity - a.parent_first;
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) psi[i] = gsrc[(pj << n) + goff + i];
+  } else {             // |0..0> at the root
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) psi[i] = kd2{(goff | i) == 0 ? 1.0 : 0.0, 0.0};
+  }
+  if (threadIdx.x == 0 && a.mode == 1 && a.src_flag) sh.k.flag = a.src_flag[pj];
+  cl.sync();
+  const KGate* __restrict__ G = a.gates;
+  for (uint32_t g = a.g0; g < a.g1; ++g) {
+    const KGate gt = G[g];
+    const bool two = gt.two != 0;
+    const uint32_t code = tq_noise_code(g, j, seed, two ? a.p2 : a.p1, two);
+    if (!two) {
+      kd2 m[4] = {kd2{gt.m[0], gt.m[1]}, kd2{gt.m[2], gt.m[3]}, kd2{gt.m[4], gt.m[5]}, kd2{gt.m[6], gt.m[7]}};
+      if (code) {
+        kd2 p[4];
+        k_pauli(code, p);
+        const kd2 r0 = kadd(kmul(p[0], m[0]), kmul(p[1], m[2])), r1 = kadd(kmul(p[0], m[1]), kmul(p[1], m[3]));
+        const kd2 r2 = kadd(kmul(p[2], m[0]), kmul(p[3], m[2])), r3 = kadd(kmul(p[2], m[1]), kmul(p[3], m[3]));
+        m[0] = r0; m[1] = r1; m[2] = r2; m[3] = r3;
+      }
+      kc_apply_1q(sh, n, rank, CL, (int)gt.q0, m[0], m[1], m[2], m[3]);
+    } else {
+      kc_apply_2q(sh, n, rank, CL, gt.op == OP_CX, (int)gt.q0, (int)gt.q1);
+      if (code) {
+        kd2 p[4];
+        if (code >> 2) {
+          cl.sync();
+          k_pauli(code >> 2, p);
+          kc_apply_1q(sh, n, rank, CL, (int)gt.q0, p[0], p[1], p[2], p[3]);
+        }
+        if (code & 3u) {
+          cl.sync();
+          k_pauli(code & 3u, p);
+          kc_apply_1q(sh, n, rank, CL, (int)gt.q1, p[0], p[1], p[2], p[3]);
+        }
+      }
+    }
+    cl.sync();
+    // the gate's Kraus channels (R33): this slice's partial table, the cluster's sum in rank
+    // order (identical in every CTA), the decisions, one sweep per qubit
+    k_joint_table(psi, KCQ, (int)gt.q0, two ? (int)gt.q1 : (int)gt.q0, sh.k, goff);
+    cl.sync();
+    if (threadIdx.x < 4) {
+      double t = 0.0;
+      for (uint32_t r = 0; r < CL; ++r) t += cl.map_shared_rank(&sh.k.tbl[0], (int)r)[threadIdx.x];
+      sh.tsum[threadIdx.x] = t;
+    }
+    cl.sync();   // every rank has read every partial table
+    if (threadIdx.x < 4) sh.k.tbl[threadIdx.x] = sh.tsum[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) k_decide(a, g, j, seed, two, sh.k);
+    __syncthreads();
+    kc_apply_real(sh, n, rank, CL, (int)gt.q0, sh.k.M[0][0], sh.k.M[0][1], sh.k.M[0][2], sh.k.M[0][3]);
+    if (two) {
+      cl.sync();
+      kc_apply_real(sh, n, rank, CL, (int)gt.q1, sh.k.M[1][0], sh.k.M[1][1], sh.k.M[1][2], sh.k.M[1][3]);
+    }
+    cl.sync();
+  }
+  if (!a.leaf || a.store_leaf) {
+    kd2* __restrict__ dst = reinterpret_cast<kd2*>(a.dst) + ((uint64_t)s << n) + goff;
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) dst[i] = psi[i];
+    if (threadIdx.x == 0 && rank == 0 && a.dst_flag) a.dst_flag[s] = (uint8_t)sh.k.flag;
+  }
+  if (a.leaf) {
+    // leaf (§2.3, R9): thread t of rank r owns global amplitudes goff + [t C, (t+1) C)
+    const uint32_t T = blockDim.x, C = L / T;
+    const uint32_t c0 = threadIdx.x * C, c1 = c0 + C;
+    double loc = 0.0;
+    for (uint32_t i = c0; i < c1; ++i) loc += psi[i].x * psi[i].x + psi[i].y * psi[i].y;
+    double incl = loc;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) sh.k.scan[w] = incl;
+    if (threadIdx.x == 0) sh.k.pick = (int)T;
+    __syncthreads();
+    double before = 0.0, ctot = 0.0;
+    for (int v = 0; v < (int)(T >> 5); ++v) {
+      if (v < w) before += sh.k.scan[v];
+      ctot += sh.k.scan[v];
+    }
+    if (threadIdx.x == 0) sh.ctot = ctot;
+    cl.sync();
+    double rbefore = 0.0, total = 0.0;
+    for (uint32_t r = 0; r < CL; ++r) {
+      const double v = *cl.map_shared_rank(&sh.ctot, (int)r);
+      if (r < rank) rbefore += v;
+      total += v;
+    }
+    incl += rbefore + before;
+    const uint64_t leaf = j;
+    const double u = tq_measure_uniform(leaf, seed);
+    const double target = u * total;
+    if (incl > target) atomicMin(&sh.k.pick, (int)threadIdx.x);   // this rank's first chunk past it
+    __syncthreads();
+    if (threadIdx.x == 0) sh.found = sh.k.pick < (int)T ? 1 : 0;
+    cl.sync();
+    uint32_t win = CL;   // the first rank holding the target
+    for (uint32_t r = CL; r-- > 0;)
+      if (*cl.map_shared_rank(&sh.found, (int)r)) win = r;
+    uint32_t flag = sh.k.flag;
+    int pick = sh.k.pick;
+    if (win == CL) {   // rounding: the target at the very top -> the last chunk of the last rank
+      win = CL - 1;
+      pick = (int)T - 1;
+      flag = 1u;
+    }
+    if (rank == win && (int)threadIdx.x == pick) {
+      double c = incl - loc, cb = c, ca = c;
+      int x = -1, lastnz = -1;
+      for (uint32_t i = c0; i < c1; ++i) {
+        const double p = psi[i].x * psi[i].x + psi[i].y * psi[i].y;
+        if (p > 0.0) lastnz = (int)(goff | i);
+        if (x < 0) cb = c;
+        c += p;
+        if (x < 0 && c > target) {
+          x = (int)(goff | i);
+          ca = c;
+        }
+      }
+      if (x < 0) {
+        x = lastnz >= 0 ? lastnz : (int)(goff | c0);
+        flag = 1u;
+      } else if (target - cb < 1e-9 || ca - target < 1e-9) {
+        flag = 1u;
+      }
+      uint32_t mask = 0;
+      if (a.p01 > 0.0 || a.p10 > 0.0) {
+        tq_w4 rw = {0, 0, 0, 0};
+        for (uint32_t b = 0; b < a.n_user; ++b) {
+          if ((b & 3u) == 0) rw = tq_philox_keyed(b >> 2, leaf, 2u, seed);
+          const uint32_t wv = (b & 3u) == 0 ? rw.x : (b & 3u) == 1 ? rw.y : (b & 3u) == 2 ? rw.z : rw.w;
+          const double p = (((uint32_t)x >> b) & 1u) ? a.p10 : a.p01;
+          if ((double)wv * 0x1p-32 < p) mask |= 1u << b;
+        }
+      }
+      a.out[leaf] = (uint32_t)x ^ mask;
+      if (a.dbg_u) a.dbg_u[leaf] = u;
+      if (a.dbg_total) a.dbg_total[leaf] = total;
+      if (a.dbg_flag) a.dbg_flag[leaf] = (uint8_t)flag;
+    }
+  }
+  cl.sync();   // no CTA leaves while another may still read its shared memory
+}
+
 }  // namespace dev
 
 int launch_kraus_slice(const KrausArgs& a, uint32_t batch, void* stream) {
@@ -342,12 +583,38 @@ int launch_kraus_slice(const KrausArgs& a, uint32_t batch, void* stream) {
   static bool attr = false;
   if (!attr) {
     const cudaError_t e = cudaFuncSetAttribute(dev::kraus_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)((size_t)16 << TQSIM_KRAUS_MAX_QUBITS));
+                                               (int)((size_t)16 << dev::KCQ));
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
-  dev::kraus_slice_kernel<<<batch, dev::KT, smem, static_cast<cudaStream_t>(stream)>>>(a);
-  return (int)cudaGetLastError();
+  if (a.n <= (uint32_t)dev::KCQ) {
+    dev::kraus_slice_kernel<<<batch, dev::KT, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    return (int)cudaGetLastError();
+  }
+  // 14..16 qubits: one cluster of 2^(n-13) CTAs per instance (state in distributed shared memory)
+  const size_t csmem = (size_t)16 << dev::KCQ;
+  static bool cattr = false;
+  if (!cattr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(dev::kraus_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+    if (e != cudaSuccess) return (int)e;
+    cattr = true;
+  }
+  const uint32_t CL = 1u << (a.n - dev::KCQ);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(batch * CL);
+  cfg.blockDim = dim3(dev::KT);
+  cfg.dynamicSmemBytes = csmem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::kraus_cluster_kernel, a);
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
 }  // namespace tq

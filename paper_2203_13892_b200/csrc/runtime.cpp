@@ -1053,7 +1053,7 @@ tqsim_handle* create_handle(const tqsim_circuit* c, const tqsim_noise_model* nm,
     h->kraus = kraus_enabled(*nm);
     if (h->kraus && c->n_qubits > TQSIM_KRAUS_MAX_QUBITS)
       throw Error{TQSIM_EINVAL, "non-Pauli channels (amplitude / phase damping, thermal relaxation) run in the "
-                                "shared-memory Kraus engine: n_qubits must be <= 13"};
+                                "shared-memory Kraus engine: n_qubits must be <= 16"};
     if (opts.copy_cost_gates == -1.0 && !arities) {
       // copy cost of this engine's fused fan-out: the child's
       // first pass reads the parent instead of its own state, so the copy adds no HBM pass; what

@@ -5,7 +5,7 @@ TAG=$1; ENVKV=$2; shift 2
 O=gpurun_out/$TAG; mkdir -p $O
 for c in "$@"; do
   for e in "" "$ENVKV"; do
-    env $e timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu --no-e2e --no-dedup-steps 0 > $O/b.json 2> $O/b.err
+    env $e timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu --no-e2e --no-dedup-steps 0 --flat-shots -1 > $O/b.json 2> $O/b.err
     python - "$c" "${e:-base}" $O/b.json >> $O/ab.txt <<'PY'
 import json, sys
 d = json.loads([l for l in open(sys.argv[3]) if l.startswith("{")][-1])

@@ -97,8 +97,31 @@ def test_max_width_13_and_width_check():
     dep, ro, km = table2_models(5.0)["AD"]
     run_compare(n, gates, dep, ro, km, 12, [3, 4], 3, dumps=[(1, 11)])
     with pytest.raises(T.TqsimError) as e:
-        T.tqsim_run(14, qft_gates(14), noise_of(dep, ro, km), 8, [8], 0)
+        T.tqsim_run(17, qft_gates(17), noise_of(dep, ro, km), 8, [8], 0)
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("n", [14, 15, 16])
+def test_cluster_engine_widths_14_to_16(n):
+    """Widths 14..16 run in the cluster kernel (the state over 2^(n-13) CTAs' shared memory,
+    gates on the top qubits through DSMEM): random circuits that touch the top qubits, every
+    Table 2 channel at 20x rates, a (3, 4) tree -- dumped amplitudes, outcomes, histogram vs
+    the oracle."""
+    rng = np.random.default_rng(100 + n)
+    gates = random_circuit(n, 40, rng)
+    gates += [("cx", n - 1, 0, 0.0, 0.0, 0.0), ("h", n - 2, -1, 0.0, 0.0, 0.0), ("cz", n - 2, n - 1, 0.0, 0.0, 0.0),
+              ("rx", n - 1, -1, 0.7, 0.0, 0.0), ("cx", 3, n - 1, 0.0, 0.0, 0.0)]
+    dep, ro, km = table2_models(20.0)["ALL"]
+    run_compare(n, gates, dep, ro, km, 12, [3, 4], 11, dumps=[(0, 1), (1, 7)])
+
+
+def test_qft15_all_channels_paper_rates_cluster():
+    """C2's circuit (QFT-15, BASELINE configs[1]) under ALL at the paper's rates through the
+    cluster engine (4 CTAs per trajectory): 20 shots on a (4, 5) tree, the full oracle tree."""
+    n = 15
+    gates = [("h", q, -1, 0.0, 0.0, 0.0) for q in range(n)] + qft_gates(n)
+    dep, ro, km = table2_models(1.0)["ALL"]
+    run_compare(n, gates, dep, ro, km, 20, [4, 5], 5, dumps=[(0, 2), (1, 17)])
 
 
 def test_vanishing_damping_equals_pauli_engine():
