@@ -367,6 +367,7 @@ __device__ __forceinline__ kd2* kc_at(const KrausClusterShared& sh, uint32_t i) 
 __device__ __forceinline__ void kc_apply_1q(const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL, int q,
                                             const kd2 m0, const kd2 m1, const kd2 m2, const kd2 m3) {
   const uint32_t per = (1u << (n - 1)) / CL, lowm = (1u << q) - 1u;
+#pragma unroll 4
   for (uint32_t p = rank * per + threadIdx.x; p < (rank + 1) * per; p += blockDim.x) {
     const uint32_t i0 = ((p >> q) << (q + 1)) | (p & lowm), i1 = i0 | (1u << q);
     kd2* A = kc_at(sh, i0);
@@ -380,6 +381,7 @@ __device__ __forceinline__ void kc_apply_1q(const KrausClusterShared& sh, int n,
 __device__ __forceinline__ void kc_apply_real(const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL, int q,
                                               double a00, double a01, double a10, double a11) {
   const uint32_t per = (1u << (n - 1)) / CL, lowm = (1u << q) - 1u;
+#pragma unroll 4
   for (uint32_t p = rank * per + threadIdx.x; p < (rank + 1) * per; p += blockDim.x) {
     const uint32_t i0 = ((p >> q) << (q + 1)) | (p & lowm), i1 = i0 | (1u << q);
     kd2* A = kc_at(sh, i0);
@@ -406,6 +408,36 @@ __device__ __forceinline__ void kc_apply_2q(const KrausClusterShared& sh, int n,
       kd2* B = kc_at(sh, b1);
       *B = kd2{-B->x, -B->y};
     }
+  }
+}
+
+// Dispatch: a sweep on a slice qubit (< 13) touches only the CTA's own slice -- the
+// single-CTA sweeps on psi (plain shared-memory accesses); a top qubit goes through DSMEM.
+__device__ __forceinline__ void kc_1q(kd2* psi, const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL, int q,
+                                      const kd2 m0, const kd2 m1, const kd2 m2, const kd2 m3) {
+  if (q < KCQ) k_apply_1q(psi, KCQ, q, m0, m1, m2, m3);
+  else kc_apply_1q(sh, n, rank, CL, q, m0, m1, m2, m3);
+}
+
+__device__ __forceinline__ void kc_real(kd2* psi, const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL,
+                                        int q, double a00, double a01, double a10, double a11) {
+  if (q < KCQ) k_apply_real(psi, KCQ, q, a00, a01, a10, a11);
+  else kc_apply_real(sh, n, rank, CL, q, a00, a01, a10, a11);
+}
+
+// CX / CZ: local unless the CX target is a top qubit.  A top control selects whole CTAs (the
+// target flip is then a local X: exact, 0 a + 1 b = b); CZ is diagonal (a sign per amplitude).
+__device__ __forceinline__ void kc_2q(kd2* psi, const KrausClusterShared& sh, int n, uint32_t rank, uint32_t CL,
+                                      uint32_t goff, bool cx, int c, int t) {
+  if (!cx) {
+    const uint32_t m = (1u << c) | (1u << t);
+    for (uint32_t i = threadIdx.x; i < (1u << KCQ); i += blockDim.x)
+      if (((goff | i) & m) == m) psi[i] = kd2{-psi[i].x, -psi[i].y};
+  } else if (t < KCQ) {
+    if (c < KCQ) k_apply_cx(psi, KCQ, c, t);
+    else if ((goff >> c) & 1u) k_apply_real(psi, KCQ, t, 0.0, 1.0, 1.0, 0.0);
+  } else {
+    kc_apply_2q(sh, n, rank, CL, true, c, t);
   }
 }
 
@@ -447,20 +479,20 @@ __global__ void __launch_bounds__(KT) kraus_cluster_kernel(const __grid_constant
         const kd2 r2 = kadd(kmul(p[2], m[0]), kmul(p[3], m[2])), r3 = kadd(kmul(p[2], m[1]), kmul(p[3], m[3]));
         m[0] = r0; m[1] = r1; m[2] = r2; m[3] = r3;
       }
-      kc_apply_1q(sh, n, rank, CL, (int)gt.q0, m[0], m[1], m[2], m[3]);
+      kc_1q(psi, sh, n, rank, CL, (int)gt.q0, m[0], m[1], m[2], m[3]);
     } else {
-      kc_apply_2q(sh, n, rank, CL, gt.op == OP_CX, (int)gt.q0, (int)gt.q1);
+      kc_2q(psi, sh, n, rank, CL, goff, gt.op == OP_CX, (int)gt.q0, (int)gt.q1);
       if (code) {
         kd2 p[4];
         if (code >> 2) {
           cl.sync();
           k_pauli(code >> 2, p);
-          kc_apply_1q(sh, n, rank, CL, (int)gt.q0, p[0], p[1], p[2], p[3]);
+          kc_1q(psi, sh, n, rank, CL, (int)gt.q0, p[0], p[1], p[2], p[3]);
         }
         if (code & 3u) {
           cl.sync();
           k_pauli(code & 3u, p);
-          kc_apply_1q(sh, n, rank, CL, (int)gt.q1, p[0], p[1], p[2], p[3]);
+          kc_1q(psi, sh, n, rank, CL, (int)gt.q1, p[0], p[1], p[2], p[3]);
         }
       }
     }
@@ -479,10 +511,10 @@ __global__ void __launch_bounds__(KT) kraus_cluster_kernel(const __grid_constant
     __syncthreads();
     if (threadIdx.x == 0) k_decide(a, g, j, seed, two, sh.k);
     __syncthreads();
-    kc_apply_real(sh, n, rank, CL, (int)gt.q0, sh.k.M[0][0], sh.k.M[0][1], sh.k.M[0][2], sh.k.M[0][3]);
+    kc_real(psi, sh, n, rank, CL, (int)gt.q0, sh.k.M[0][0], sh.k.M[0][1], sh.k.M[0][2], sh.k.M[0][3]);
     if (two) {
       cl.sync();
-      kc_apply_real(sh, n, rank, CL, (int)gt.q1, sh.k.M[1][0], sh.k.M[1][1], sh.k.M[1][2], sh.k.M[1][3]);
+      kc_real(psi, sh, n, rank, CL, (int)gt.q1, sh.k.M[1][0], sh.k.M[1][1], sh.k.M[1][2], sh.k.M[1][3]);
     }
     cl.sync();
   }

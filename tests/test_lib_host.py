@@ -13,7 +13,7 @@ from oracle import gates as OG
 from oracle.planner import dcp_plan, fixed_plan
 from oracle.tree import NoiseModel, error_rates
 from tq_testutil import ROOT
-from workloads import config_names, load_config, random_circuit
+from workloads import config_names, load_config, qft_gates, random_circuit
 
 HAVE_GPU = False
 try:
@@ -351,3 +351,16 @@ def test_relabel_with_store_map_regression():
             assert "__global__" in src
             p += 1
         assert p >= 1
+
+
+def test_kraus_width_limit_host():
+    """The Kraus engine's width limit (include/tqsim.h TQSIM_KRAUS_MAX_QUBITS = 16: one CTA up
+    to 13 qubits, a thread-block cluster of 2^(n-13) CTAs for 14..16): 16 plans, 17 is
+    TQSIM_EINVAL; the same widths without non-Pauli channels are not limited."""
+    kn = T.noise_arg(1e-3, 1e-2, 0.0, 0.0, amp_damping=0.01)
+    for n in (13, 14, 16):
+        assert T.tqsim_plan_circuit(n, qft_gates(n), kn, 32, [4, 8]).n_outcomes == 32
+    with pytest.raises(T.TqsimError) as e:
+        T.tqsim_plan_circuit(17, qft_gates(17), kn, 32, [4, 8])
+    assert e.value.status == 2
+    assert T.tqsim_plan_circuit(17, qft_gates(17), T.noise_arg(1e-3, 1e-2), 32, [4, 8]).n_outcomes == 32
