@@ -25,7 +25,7 @@ from workloads.generators import qaoa_gates, random_3_regular_edges  # noqa: E40
 def kraus_case(rng, k):
     """Non-Pauli channels (the shared-memory Kraus engine) vs oracle/kraus.py."""
     from oracle import kraus as K
-    n = int(rng.integers(1, 10))
+    n = int(rng.integers(KN[0], KN[1] + 1))
     gates = random_circuit(n, int(rng.integers(10, 60)), rng)
     if not gates:
         gates = random_circuit(n, 5, rng, kinds=["h", "rx"])
@@ -59,10 +59,16 @@ def kraus_case(rng, k):
 
 
 NMIN, NMAX = 4, 15   # qubit range of the Pauli cases (argv 3, 4)
+# STRESS_KRAUS_N="lo,hi": Kraus cases only, n in [lo, hi] (10-13: one CTA, 14-16: the cluster engine)
+KN = (1, 9)
+KRAUS_ONLY = False
+if os.environ.get("STRESS_KRAUS_N"):
+    KN = tuple(int(x) for x in os.environ["STRESS_KRAUS_N"].split(","))
+    KRAUS_ONLY = True
 
 
 def one_case(rng, k):
-    if NMAX <= 15 and rng.random() < 0.15:
+    if KRAUS_ONLY or (NMAX <= 15 and rng.random() < 0.15):
         return kraus_case(rng, k)
     kind = rng.choice(["random", "qaoa", "qft"], p=[0.6, 0.3, 0.1])
     n = int(rng.integers(NMIN, NMAX))
