@@ -292,6 +292,19 @@ struct M4 {
         if (i != j && a[i][j] != cplx(0, 0)) return false;
     return true;
   }
+  // a permutation times a diagonal (decompose()'s 1e-12 threshold): one entry per column
+  // and per row
+  bool monomial() const {
+    int rows = 0;
+    for (int j = 0; j < 4; ++j) {
+      int cnt = 0, r0 = -1;
+      for (int i = 0; i < 4; ++i)
+        if (std::abs(a[i][j]) > 1e-12) ++cnt, r0 = i;
+      if (cnt != 1) return false;
+      rows |= 1 << r0;
+    }
+    return rows == 15;
+  }
 };
 
 M4 op_matrix(const LGate& g, int s0, int s1) {
@@ -675,6 +688,19 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
     int bs1 = s1, sw1 = -1;
     int jmax = i, cost = gate_cost(g0), gens = cost >= 4 ? 1 : 0;
     M4 Pmax = P;
+    // A run [i, j] is fused into one DIAG / NOP op only if every error of its gates can be
+    // pushed to the run's end as a monomial (make_sites): the product R_t of the gates after
+    // each t must itself be monomial.  (H Tdg T H is the identity, but X after Tdg pushed
+    // through T H is (Z - Y)/sqrt 2: such a run is left to the single-gate ops.)
+    auto sites_monomial = [&](int j, int S1) {
+      const int slot1 = S1 >= 0 ? S1 : (s0 == 0 ? 1 : 0);
+      M4 R = M4::id();
+      for (int t = j; t > i; --t) {
+        R = R.mul(op_matrix(lg_of(t), s0, slot1));
+        if (!R.monomial()) return false;
+      }
+      return true;
+    };
     for (int j = i + 1; j < n && j < i + 12; ++j) {
       const LGate& gj = lg_of(j);
       if (is_map(j) || (!restricted && off_tile(gj))) break;
@@ -696,10 +722,12 @@ std::vector<FOp> fuse_fast_ops(const PassDesc& pd, const PassPlan& pp,
       cost += gate_cost(gj);
       gens += gate_cost(gj) >= 4 ? 1 : 0;
       if (P.diagonal()) {
-        best = j;
-        bestP = P;
-        bs1 = s1;
-      } else if (allow_swap && s1 >= 0 && is_swap(P) &&
+        if (restricted || sites_monomial(j, s1)) {
+          best = j;
+          bestP = P;
+          bs1 = s1;
+        }
+      } else if (allow_swap && s1 >= 0 && is_swap(P) && sites_monomial(j, s1) &&
                  // with store maps only high-high relabelings: a low-low one could carry a
                  // mapped logical qubit (2 above the leaf level) onto physical 0 / 1, whose
                  // address bits a map must not move (map_ok below)

@@ -627,3 +627,24 @@ def test_streaming_projection_top_unit_paulis_vs_oracle(n, tile, p, ar, tl):
             continue
         assert int(a.leaf_outcomes[l]) == r.outcome, (l, int(a.leaf_outcomes[l]), r.outcome)
         assert int(b.leaf_outcomes[l]) == r.outcome
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [1.0, 0.2])
+def test_nonmonomial_suffix_run_case_vs_oracle(p):
+    """The stress-run case of a run H Tdg T H (product 1, suffix products not monomial;
+    tests/golden/stress_nonmonomial_run_case.json): outcomes equal the oracle's, with and without
+    dedup, and so do those of the minimal circuit."""
+    import json
+    import os
+    from tq_testutil import ROOT
+    d = json.load(open(os.path.join(ROOT, "tests", "golden", "stress_nonmonomial_run_case.json")))
+    gates = [tuple(g) for g in d["gates"]]
+    ar = d["arities"]
+    for nd in (0, 1):
+        opts = T.default_options(trail_low=4, batch_log2_amps=9, no_dedup=nd)
+        run_and_compare(d["n_qubits"], gates, NoiseModel(p, min(1.0, 2 * p), 0.02, 0.03), int(np.prod(ar)), ar,
+                        d["seed"] % (1 << 40), opts)
+    mini = [("h", 1, -1, 0.0, 0.0, 0.0), ("tdg", 1, -1, 0.0, 0.0, 0.0), ("t", 1, -1, 0.0, 0.0, 0.0),
+            ("h", 1, -1, 0.0, 0.0, 0.0), ("cx", 0, 1, 0.0, 0.0, 0.0), ("ry", 2, -1, 0.7, 0.0, 0.0)]
+    run_and_compare(4, mini, NoiseModel(p, p, 0.0, 0.0), 24, [2, 3, 4], 5, T.default_options(small_tree=0))

@@ -364,3 +364,23 @@ def test_kraus_width_limit_host():
         T.tqsim_plan_circuit(17, qft_gates(17), kn, 32, [4, 8])
     assert e.value.status == 2
     assert T.tqsim_plan_circuit(17, qft_gates(17), T.noise_arg(1e-3, 1e-2), 32, [4, 8]).n_outcomes == 32
+
+
+def test_nonmonomial_suffix_run_regression():
+    """A run of single-qubit gates whose product is diagonal (H Tdg T H = 1) but whose suffix
+    products are not monomial (an error after Tdg pushed through T H is (Z - Y)/sqrt 2) must not be
+    fused into one DIAG / NOP op: every pass kernel of the plan generates and compiles (before the
+    fix the generator raised TQSIM_EINTERNAL 'not an X-type permutation').  Case from
+    scripts/stress_parity.py (fixture: inputs only)."""
+    import json
+    d = json.load(open(os.path.join(ROOT, "tests", "golden", "stress_nonmonomial_run_case.json")))
+    gates = [tuple(g) for g in d["gates"]]
+    n, ar = d["n_qubits"], d["arities"]
+    for p in (1.0, 0.2):
+        k, _, _ = T.tqsim_compile_passes(n, gates, T.noise_arg(p, p), int(np.prod(ar)), ar,
+                                         T.default_options(trail_low=4, batch_log2_amps=9))
+        assert k > 0
+    mini = [("h", 1, -1, 0.0, 0.0, 0.0), ("tdg", 1, -1, 0.0, 0.0, 0.0), ("t", 1, -1, 0.0, 0.0, 0.0),
+            ("h", 1, -1, 0.0, 0.0, 0.0), ("cx", 0, 1, 0.0, 0.0, 0.0), ("ry", 2, -1, 0.7, 0.0, 0.0)]
+    k, _, _ = T.tqsim_compile_passes(4, mini, T.noise_arg(0.3, 0.3), 6, [2, 3])
+    assert k > 0
